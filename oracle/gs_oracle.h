@@ -1,0 +1,170 @@
+/*
+ * gs_oracle.h — TEST INFRASTRUCTURE ONLY (the parity checker, never the product).
+ *
+ * Plain-C restatement of the GreenLLM decision-engine hot path of the
+ * reference `greensim` library (/root/reference/proj), plus the plain-data
+ * types shared with the reference shim (ref_capi.cpp, compiled into
+ * oracle/_ref/). Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.
+ *
+ * Parity of this restatement is pinned two ways (tests/test_oracle_*.py):
+ *   1. the reference's own golden values, and
+ *   2. element-wise equality against oracle/_ref/libgreensim_ref.so, i.e. the
+ *      reference sources compiled unmodified from /root/reference.
+ *
+ * All arithmetic is IEEE binary64, round-to-nearest, evaluated in the
+ * reference's operation order; the library is compiled with
+ * -ffp-contract=off so that no FMA contraction can change a bit.
+ */
+#ifndef GS_ORACLE_H
+#define GS_ORACLE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* greensim::GpuProfile minus the name (gpu_model.hpp:16-87). */
+typedef struct gso_profile {
+  double f_min_mhz, f_max_mhz, step_mhz, f_ref_mhz;                 /* FrequencyGrid   :16-28 */
+  double lat_a, lat_b, lat_c, lat_f_ref_mhz;                         /* LatencyModel    :32-39 */
+  double dec_alpha0_ms, dec_alpha1_ms, dec_beta0_ms, dec_beta1_ms,   /* DecodeStepModel :45-53 */
+      dec_f_ref_mhz;
+  double k3, k2, k1, k0, p_idle_w;                                   /* PowerModel      :57-67 */
+} gso_profile;
+
+/* greensim::QueueOptimizerConfig (prefill_opt.hpp:61-68). */
+typedef struct gso_qopt_cfg {
+  double resolve_period_ms, margin_prefill, min_budget_ms, first_token_allowance_ms;
+} gso_qopt_cfg;
+
+/* greensim::DecodeCtlConfig (decode_ctl.hpp:13-29). */
+typedef struct gso_ctl_cfg {
+  double tslo_ms, margin_decode, fine_period_ms, coarse_period_ms, adapt_period_s;
+  double step_mhz, max_step_mhz;
+  int32_t hysteresis_count, tbt_window_tokens;
+  double bias_threshold, tps_scale, upper_margin, lower_margin;
+} gso_ctl_cfg;
+
+/* greensim::DecisionRecord (decode_ctl.hpp:95-105) with the action string as an enum. */
+enum {
+  GSO_ACT_HOLD = 0, GSO_ACT_UP = 1, GSO_ACT_DOWN = 2,
+  GSO_ACT_COARSE_HOLD = 3, GSO_ACT_COARSE_PENDING = 4, GSO_ACT_COARSE_COMMIT = 5,
+  GSO_ACT_ADAPT_UP = 6, GSO_ACT_ADAPT_DOWN = 7
+};
+typedef struct gso_decision {
+  double tick_ms, tps, p95_tbt_ms, band_lo, band_hi, command_mhz;
+  int32_t worker, bucket, action, pad_;
+} gso_decision;
+
+/* One TPS-bucketed band table (decode_ctl.hpp:39-64), SoA. */
+typedef struct gso_band_table {
+  int32_t n;
+  const double* tps_lo;
+  const double* tps_hi;
+  const double* f_opt_mhz;
+} gso_band_table;
+
+/*
+ * Raw decode telemetry of one decode worker (what Sim feeds the windows,
+ * simkernel.cpp:365-393): step-end events sorted by time; event j emitted
+ * tokens[j] tokens at t_ms[j] and recorded gaps[gap_off[j] .. gap_off[j+1])
+ * into the TBT ring in that order.
+ */
+typedef struct gso_telemetry {
+  int64_t n_events;
+  const double* t_ms;
+  const int32_t* tokens;
+  const int64_t* gap_off; /* n_events + 1 */
+  const double* gaps;
+} gso_telemetry;
+
+/* ---------------- prefill objective (prefill_opt.cpp) ---------------- */
+int gso_profile_validate(const gso_profile* p);                  /* gpu_model.cpp:80-87; 0 ok */
+int gso_grid_size(const gso_profile* p);                         /* gpu_model.cpp:24-26 */
+double gso_grid_at(const gso_profile* p, int i);                 /* gpu_model.cpp:28 */
+double gso_active_power_w(const gso_profile* p, double f);       /* gpu_model.hpp:64 */
+double gso_t_ref_total_ms(const gso_profile* p, int64_t n, const int32_t* prompt,
+                          const double* wf /* NULL = all 1.0 */); /* prefill_opt.cpp:9-14 */
+/* energy_total (prefill_opt.cpp:22-31); returns 0 ok, -1 ModelError. */
+int gso_energy_total(const gso_profile* p, int64_t n, const int32_t* prompt, const double* wf,
+                     double f, double window_ms, double* active_j, double* idle_j,
+                     double* total_j, int* feasible);
+double gso_energy_closed_form(const gso_profile* p, int64_t n, const int32_t* prompt,
+                              const double* wf, double f, double window_ms); /* :33-43 */
+/* select_frequency (prefill_opt.cpp:45-56): returns grid index of the choice or -1 (nullopt). */
+int gso_select_frequency(const gso_profile* p, int64_t n, const int32_t* prompt, const double* wf,
+                         double window_ms, double* f_out, double* e_out);
+/* select on a precomputed T_ref (same bits as the batch form; used for binned cells). */
+int gso_select_frequency_t(const gso_profile* p, double t_ref, double window_ms, double* f_out,
+                           double* e_out);
+/* queue_optimizer_tick for one non-empty class queue (prefill_opt.cpp:63-80). */
+void gso_queue_tick_one(const gso_profile* p, const gso_qopt_cfg* cfg, int64_t n,
+                        const int32_t* prompt, const double* deadline, const double* wf,
+                        double now_ms, double* f_out, double* window_out, int* infeasible_out,
+                        int* f_idx_out, double* e_out);
+
+/* ---------------- routing (router.cpp) ---------------- */
+int gso_classify(int n_thr, const int32_t* thresholds, int32_t prompt); /* router.cpp:26-31 */
+/* Offline binning convention: window k = [k*W, (k+1)*W), class = classify().
+ * Per cell (window-major, class-minor): count, T_ref (arrival order), min deadline,
+ * and the stable FIFO order of request indices (Dispatcher, router.cpp:37-43). */
+int gso_route_bin(int64_t n_req, const int64_t* arrival_ms, const int32_t* prompt, int n_thr,
+                  const int32_t* thresholds, int64_t window_ms, int64_t w0, int64_t n_windows,
+                  int n_profiles, const gso_profile* profiles, double ttft_sm_ms, double ttft_l_ms,
+                  double first_token_allowance_ms, uint8_t* cls_out, uint32_t* cell_count,
+                  double* cell_t_ref /* [n_profiles][cells] */, double* cell_min_deadline,
+                  int64_t* fifo_out /* n_req or NULL */);
+
+/* ---------------- decode control (decode_ctl.cpp, metrics.cpp) ---------------- */
+double gso_quantile(int64_t n, const double* samples, double q);         /* metrics.cpp:11-19 */
+int gso_decode_steady_state(const gso_profile* p, double tps, double f, int max_batch,
+                            double* batch, double* tbt_ms);               /* decode_ctl.cpp:28-50 */
+/* build_band_table (decode_ctl.cpp:76-111); returns 0 ok, -1 ModelError. */
+int gso_build_band_table(const gso_profile* p, int n_levels, const double* levels, double t_slo_ms,
+                         int workers, int max_batch, double* tps_lo, double* tps_hi,
+                         double* f_opt, uint8_t* feasible);
+int gso_ctl_cfg_validate(const gso_ctl_cfg* c);                           /* decode_ctl.cpp:12-26 */
+
+/*
+ * Window statistics of one telemetry stream as Sim's ticks observe them
+ * (simkernel.cpp:441-458; decode_ctl.cpp:113-128): the P95 at every fine tick and
+ * the TPS at every coarse tick up to t_end_ms inclusive.
+ */
+int64_t gso_n_ticks(double period_ms, double t_end_ms);
+void gso_window_series(const gso_telemetry* tel, int tbt_capacity, double fine_period_ms,
+                       double coarse_period_ms, double t_end_ms, uint8_t* fine_has,
+                       double* fine_p95, double* coarse_tps);
+
+/*
+ * Open-loop controller replay of one worker: the DecodeController composed with the
+ * windows exactly as Sim's fine/coarse/adapt ticks do. Writes up to cap records and
+ * returns the record count (or -1 on ModelError). Two drivers: from raw telemetry,
+ * and from precomputed window series.
+ */
+int64_t gso_replay_telemetry(const gso_ctl_cfg* cfg, const gso_band_table* table, double f_min,
+                             double f_max, int worker, const gso_telemetry* tel, double t_end_ms,
+                             gso_decision* out, int64_t cap);
+int64_t gso_replay_series(const gso_ctl_cfg* cfg, const gso_band_table* table, double f_min,
+                          double f_max, int worker, const uint8_t* fine_has,
+                          const double* fine_p95, const double* coarse_tps, double t_end_ms,
+                          gso_decision* out, int64_t cap);
+
+/* 64-bit trajectory digest (FNV-1a over the record fields). */
+uint64_t gso_digest_records(const gso_decision* recs, int64_t n);
+
+/* ---------------- trace generators (trace.cpp, rng.hpp) ---------------- */
+int64_t gso_gen_poisson_trace(double qps, int64_t duration_ms, double prompt_mean_short,
+                              double prompt_mean_long, double long_fraction, double output_mean,
+                              uint64_t seed, int64_t cap, int64_t* arrival, int32_t* prompt,
+                              int32_t* output);
+int64_t gso_gen_sinusoid_decode_trace(double tps_mean, double tps_amp, double period_ms,
+                                      int64_t duration_ms, uint64_t seed, int64_t cap,
+                                      int64_t* arrival, int32_t* prompt, int32_t* output);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
