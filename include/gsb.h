@@ -1,0 +1,295 @@
+/*
+ * gsb.h — C ABI of the B200-native GreenLLM decision engine (libgsb.so).
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or torch types.
+ * Every compute entry point runs hand-written sm_100a CUDA kernels on caller-owned
+ * DEVICE buffers on the caller's stream (`stream` is a cudaStream_t; NULL means the
+ * context's own stream). There is no CPU fallback: a call on a host without a usable
+ * B200 returns GSB_CUDA_ERROR.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   include/greensim/gpu_model.hpp:16-87    FrequencyGrid / LatencyModel / DecodeStepModel /
+ *                                           PowerModel / GpuProfile (+ validate())
+ *   include/greensim/router.hpp:19-56       RoutingConfig, classify(), Dispatcher
+ *   include/greensim/prefill_opt.hpp:13-88  PrefillBatch::t_ref_total_ms, busy_time_ms,
+ *                                           energy_total, select_frequency,
+ *                                           QueueOptimizerConfig, queue_optimizer_tick
+ *   include/greensim/decode_ctl.hpp:13-165  DecodeCtlConfig, decode_steady_state,
+ *                                           build_band_table, TpsWindow, TbtWindow,
+ *                                           DecodeController, DecisionRecord
+ *   include/greensim/metrics.hpp:14-16      quantile (nearest rank, the TBT-window P95)
+ *
+ * Error behaviour mirrors the reference's typed exceptions: ModelError -> GSB_MODEL_ERROR,
+ * RouterError -> GSB_ROUTER_ERROR, TraceError -> GSB_TRACE_ERROR; gsb_last_error() holds
+ * the message. Infeasibility is a value, not an error (prefill_opt.hpp:55-57,79).
+ *
+ * Threading: a context is single-owner (one per host thread), like DecodeController
+ * (SPEC.md:435). Distinct contexts may run concurrently.
+ */
+#ifndef GSB_H
+#define GSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSB_ABI_VERSION 1
+#define GSB_MAX_PROFILES 4   /* profiles evaluated in one prefill pass */
+#define GSB_MAX_GRID 256     /* clock grid points per profile (81 for 210..1410/15) */
+#define GSB_MAX_CLASSES 8    /* length classes (<= 7 routing thresholds) */
+#define GSB_MAX_BUCKETS 32   /* TPS buckets per band table */
+#define GSB_MAX_TBT_WINDOW 256
+
+typedef enum gsb_status {
+  GSB_OK = 0,
+  GSB_MODEL_ERROR = 1,  /* greensim::ModelError  (gpu_model.hpp:11-13) */
+  GSB_ROUTER_ERROR = 2, /* greensim::RouterError (router.hpp:13-15) */
+  GSB_TRACE_ERROR = 3,  /* greensim::TraceError  (trace.hpp:36-40) */
+  GSB_CUDA_ERROR = 4,
+  GSB_INVALID_ARGUMENT = 5
+} gsb_status;
+
+typedef struct gsb_ctx gsb_ctx;
+
+/* greensim::GpuProfile minus its name; same field order as gpu_model.hpp:16-87. */
+typedef struct gsb_profile {
+  double f_min_mhz, f_max_mhz, step_mhz, f_ref_mhz;                 /* FrequencyGrid   */
+  double lat_a, lat_b, lat_c, lat_f_ref_mhz;                         /* LatencyModel    */
+  double dec_alpha0_ms, dec_alpha1_ms, dec_beta0_ms, dec_beta1_ms,   /* DecodeStepModel */
+      dec_f_ref_mhz;
+  double k3, k2, k1, k0, p_idle_w;                                   /* PowerModel      */
+} gsb_profile;
+
+/* greensim::QueueOptimizerConfig (prefill_opt.hpp:61-68). */
+typedef struct gsb_qopt_cfg {
+  double resolve_period_ms, margin_prefill, min_budget_ms, first_token_allowance_ms;
+} gsb_qopt_cfg;
+
+/* greensim::DecodeCtlConfig (decode_ctl.hpp:13-29). */
+typedef struct gsb_ctl_cfg {
+  double tslo_ms, margin_decode, fine_period_ms, coarse_period_ms, adapt_period_s;
+  double step_mhz, max_step_mhz;
+  int32_t hysteresis_count, tbt_window_tokens;
+  double bias_threshold, tps_scale, upper_margin, lower_margin;
+} gsb_ctl_cfg;
+
+/* greensim::DecisionRecord (decode_ctl.hpp:95-105); action is an enum instead of a string:
+ * 0 hold, 1 up, 2 down, 3 coarse_hold, 4 coarse_pending, 5 coarse_commit, 6 adapt_up,
+ * 7 adapt_down. */
+typedef struct gsb_decision {
+  double tick_ms, tps, p95_tbt_ms, band_lo, band_hi, command_mhz;
+  int32_t worker, bucket, action, pad_;
+} gsb_decision;
+
+/* ---------------------------------------------------------------- context */
+const char* gsb_version(void);
+const char* gsb_status_string(int status);
+int gsb_ctx_create(int device, gsb_ctx** out);
+void gsb_ctx_destroy(gsb_ctx* ctx);
+const char* gsb_last_error(const gsb_ctx* ctx);
+void* gsb_ctx_stream(gsb_ctx* ctx); /* the context's own cudaStream_t */
+int gsb_synchronize(gsb_ctx* ctx);
+
+/* GpuProfile::validate (gpu_model.cpp:80-87), host-side; GSB_MODEL_ERROR + message. */
+int gsb_profile_validate(const gsb_profile* p, char* msg, size_t msg_cap);
+/* DecodeCtlConfig::validate (decode_ctl.cpp:12-26). */
+int gsb_ctl_cfg_validate(const gsb_ctl_cfg* c, char* msg, size_t msg_cap);
+
+/* Installs the profile set used by the prefill kernels (validated; per-clock tables of
+ * f_i, 1/f_i and P(f_i) are built once here, gpu_model.cpp:24-28, gpu_model.hpp:64). */
+int gsb_set_profiles(gsb_ctx* ctx, int n_profiles, const gsb_profile* profiles);
+
+/* ---------------------------------------------------------------- K1: route + bin */
+/* Routing / binning configuration. Offline window convention: window k of
+ * the pass covers [(w0+k)*window_ms, (w0+k+1)*window_ms); jobs of a cell are the requests
+ * of that class arriving in the window, in arrival order (Dispatcher FIFO, router.cpp:37-43). */
+typedef struct gsb_route_cfg {
+  int32_t n_thresholds;                 /* RoutingConfig::thresholds (router.hpp:19-29) */
+  int32_t thresholds[GSB_MAX_CLASSES - 1];
+  int32_t enabled;                      /* RoutingConfig::enabled; 0 -> one queue */
+  int32_t slo_boundary_tokens;          /* SM/L boundary, 1024 (simkernel.cpp:258-260) */
+  int64_t window_ms, w0, n_windows;
+  double ttft_sm_ms, ttft_l_ms;         /* SloConfig (simkernel.hpp:53-62) */
+  double first_token_allowance_ms;      /* QueueOptimizerConfig (prefill_opt.hpp:66-67) */
+} gsb_route_cfg;
+
+/* RoutingConfig::validate (router.cpp:7-24) for n_prefill_workers / worker_map. */
+int gsb_routing_validate(const gsb_route_cfg* cfg, int n_prefill_workers,
+                         const int32_t* worker_map, char* msg, size_t msg_cap);
+
+/* Window start indices: bounds[k] = first request with arrival >= (w0+k)*window_ms,
+ * k = 0..n_windows (arrival must be non-decreasing, trace.cpp:109-111). */
+int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
+                      const int64_t* d_arrival_ms, int64_t* d_bounds, void* stream);
+
+/* classify() per request (router.cpp:26-31) and, per cell = window*C + class:
+ *   d_count[cell]        jobs in the cell
+ *   d_t_ref[p*cells+cell] PrefillBatch::t_ref_total_ms over the cell's FIFO for profile p
+ *                        (prefill_opt.cpp:9-14, left-to-right, bit-exact)
+ *   d_min_deadline[cell] min_j (arrival_j + TTFT(SM/L)) - allowance (simkernel.cpp:499-501);
+ *                        optional (NULL)
+ * d_bounds from gsb_window_bounds. C = n_thresholds + 1 (or 1 when routing is disabled). */
+int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
+                  const int64_t* d_arrival_ms, const int32_t* d_prompt, const int64_t* d_bounds,
+                  uint8_t* d_class, uint32_t* d_count, double* d_t_ref, double* d_min_deadline,
+                  void* stream);
+
+/* Dispatcher queue contents: stable per-cell FIFO of request indices (cell-major), i.e.
+ * Dispatcher::queue(q) of every window (router.cpp:37-43). d_cell_off[cells+1] receives
+ * the exclusive prefix of d_count. */
+int gsb_fifo_order(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
+                   const uint8_t* d_class, const int64_t* d_bounds, const uint32_t* d_count,
+                   int64_t* d_cell_off, int64_t* d_fifo, void* stream);
+
+/* ---------------------------------------------------------------- K2: prefill objective */
+typedef enum gsb_window_mode {
+  GSB_FIXED_WINDOW = 0,    /* D = fixed_window_ms for every cell (select_frequency) */
+  GSB_DEADLINE_SLACK = 1,  /* D = max(margin * (min_deadline - now), min_budget), now =
+                              window start; queue_optimizer_tick, prefill_opt.cpp:63-67 */
+  GSB_PER_CELL_WINDOW = 2  /* D = d_window[cell] */
+} gsb_window_mode;
+
+typedef struct gsb_select_cfg {
+  int32_t mode;             /* gsb_window_mode */
+  int32_t n_classes;        /* C of the cell layout (DEADLINE_SLACK: cell -> window) */
+  double fixed_window_ms;   /* GSB_FIXED_WINDOW */
+  int64_t w0, window_ms;    /* GSB_DEADLINE_SLACK: now = (w0 + cell / C) * window_ms */
+  gsb_qopt_cfg qopt;
+} gsb_select_cfg;
+
+/* Exhaustive window-energy argmin for every (cell, profile) over the profile's clock grid:
+ * energy_total (prefill_opt.cpp:22-31) at every grid clock, feasible iff busy <= D,
+ * ascending scan with strict '<' (lowest clock on ties, prefill_opt.cpp:45-56).
+ * Outputs per (p, cell) at index p*n_cells + cell:
+ *   d_f_idx   grid index of the choice; -1 = nothing feasible (nullopt; a queue tick pins
+ *             f_max with infeasible=true, prefill_opt.cpp:75-78); -2 = empty cell (no command)
+ *   d_energy  energy_j of the choice (FrequencyChoice::energy_j), 0 otherwise
+ * d_window (optional) receives / supplies the budget D per cell (PrefillFreqCommand::window_ms).
+ * d_count may be NULL (all cells non-empty). */
+int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                       const double* d_t_ref, const uint32_t* d_count,
+                       const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
+                       double* d_energy, void* stream);
+
+/* Ragged explicit batches (the reference's own call shape): batch b has jobs
+ * [d_off[b], d_off[b+1]) with prompt tokens, work_fraction (NULL = 1.0) and, for
+ * DEADLINE_SLACK, absolute deadlines and a per-batch now. Mode FIXED/PER_CELL uses
+ * d_window[b] (PER_CELL) or cfg->fixed_window_ms. T_ref is the left-to-right sum of
+ * wf*((a*L+b)*L+c) (prefill_opt.cpp:9-14). One profile (index `profile`). */
+int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int64_t n_batches,
+                       const int64_t* d_off, const int32_t* d_prompt, const double* d_wf,
+                       const double* d_deadline, const double* d_now, double* d_window,
+                       int16_t* d_f_idx, double* d_energy, double* d_t_ref_out, void* stream);
+
+/* busy_time_ms + energy_total at one given clock per batch (prefill_opt.cpp:16-31): full
+ * breakdown. d_feasible[b] = 2 marks the reference's ModelError (empty batch or off-grid
+ * clock, prefill_opt.cpp:17-18). */
+int gsb_energy_batches(gsb_ctx* ctx, int profile, int64_t n_batches, const int64_t* d_off,
+                       const int32_t* d_prompt, const double* d_wf, const double* d_f_mhz,
+                       const double* d_window, double* d_busy, double* d_active, double* d_idle,
+                       double* d_total, uint8_t* d_feasible, void* stream);
+
+/* Per (profile, class) summary of a K2 pass for the end-of-run reductions:
+ * n_cmd, n_infeasible, n_empty, sum_energy (fixed-shape tree order, deterministic),
+ * and the argmin cell (min energy, then lowest cell index). */
+typedef struct gsb_class_summary {
+  int64_t n_cmd, n_infeasible, n_empty;
+  double sum_energy_j;
+  double min_energy_j;
+  int64_t argmin_cell;
+} gsb_class_summary;
+int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_cells,
+                        const int16_t* d_f_idx, const double* d_energy,
+                        gsb_class_summary* d_out /* [n_profiles*n_classes] */, void* stream);
+
+/* ---------------------------------------------------------------- K3/K4: decode control */
+/* Raw decode telemetry of S streams (one decode worker each), CSR layout:
+ * events of stream s are [d_ev_off[s], d_ev_off[s+1]) sorted by time; event j emitted
+ * d_tokens[j] tokens at d_t_ms[j] and recorded gaps [d_gap_off[j], d_gap_off[j+1]) into the
+ * TBT ring in that order (simkernel.cpp:365-393). */
+typedef struct gsb_telemetry {
+  int64_t n_streams;
+  const int64_t* d_ev_off;  /* [S+1] */
+  const double* d_t_ms;     /* [E] */
+  const int32_t* d_tokens;  /* [E] */
+  const int64_t* d_gap_off; /* [E+1] (global gap indices) */
+  const double* d_gaps;     /* [G] */
+} gsb_telemetry;
+
+/* Window statistics as Sim's ticks observe them (simkernel.cpp:441-458): the TbtWindow
+ * P95 (nearest rank over the last `tbt_capacity` gaps, decode_ctl.cpp:120-128,
+ * metrics.cpp:11-19) at every fine tick and the TpsWindow rate (decode_ctl.cpp:113-118,
+ * window = coarse period) at every coarse tick, ticks up to t_end_ms inclusive.
+ * Outputs [S][n_fine] and [S][n_coarse] where n_* = gsb_n_ticks(period, t_end_ms). */
+int64_t gsb_n_ticks(double period_ms, double t_end_ms);
+int gsb_window_series(gsb_ctx* ctx, const gsb_telemetry* tel, int tbt_capacity,
+                      double fine_period_ms, double coarse_period_ms, double t_end_ms,
+                      uint8_t* d_fine_has, double* d_fine_p95, double* d_coarse_tps,
+                      void* stream);
+
+/* Band tables for T (profile, t_slo, workers, max_batch) tuples on n_levels ascending
+ * TPS levels (build_band_table, decode_ctl.cpp:76-111). Outputs [T][n_levels]. */
+int gsb_build_band_tables(gsb_ctx* ctx, int64_t n_tables, const gsb_profile* d_profiles,
+                          const int32_t* d_profile_of, const double* d_t_slo_ms,
+                          const int32_t* d_workers, const int32_t* d_max_batch, int n_levels,
+                          const double* d_levels, double* d_tps_lo, double* d_tps_hi,
+                          double* d_f_opt, uint8_t* d_feasible, void* stream);
+
+/* Open-loop DecodeController replay (decode_ctl.cpp:130-228) of N trajectories, one GPU
+ * lane each, composed with the window series of stream d_stream_of[n] exactly as Sim's
+ * fine/coarse/adapt ticks (simkernel.cpp:243-248,441-464; tie order coarse < adapt < fine).
+ * Band table d_table_of[n] of the [T][n_buckets] tables (tps_hi, f_opt), clamped to
+ * [f_min, f_max] of the grid. Per trajectory outputs:
+ *   d_digest[n]  word-wise FNV-1a over (command, band_lo, band_hi, action|bucket<<32)
+ *                of every DecisionRecord in log order
+ *   d_n_rec[n]   number of DecisionRecords
+ *   d_counts[n*8] per-action counts (optional)
+ *   d_mean_cmd[n] mean fine-tick command in MHz, left-to-right sum / count (optional)
+ *   d_records / rec_cap: full DecisionRecords, rec_cap per trajectory (optional)
+ * The series' fine/coarse periods must equal every cfg's (checked on host). */
+typedef struct gsb_replay_args {
+  int64_t n_traj;
+  const gsb_ctl_cfg* d_cfg;      /* [N] */
+  const int32_t* d_table_of;     /* [N] */
+  const int32_t* d_stream_of;    /* [N] */
+  const int32_t* d_worker;       /* [N] DecisionRecord::worker */
+  int32_t n_buckets;             /* per table */
+  const double* d_tps_hi;        /* [T][n_buckets] */
+  const double* d_f_opt;         /* [T][n_buckets] */
+  double f_min_mhz, f_max_mhz;
+  double fine_period_ms, coarse_period_ms, t_end_ms;
+  const uint8_t* d_fine_has;     /* [S][n_fine] */
+  const double* d_fine_p95;      /* [S][n_fine] */
+  const double* d_coarse_tps;    /* [S][n_coarse] */
+  uint64_t* d_digest;
+  int64_t* d_n_rec;
+  int32_t* d_counts;             /* optional */
+  double* d_mean_cmd;            /* optional */
+  gsb_decision* d_records;       /* optional */
+  int64_t rec_cap;
+} gsb_replay_args;
+int gsb_decode_replay(gsb_ctx* ctx, const gsb_replay_args* a, void* stream);
+
+/* Host-side validation of a replay batch (band tables + configs), host pointers. */
+int gsb_replay_validate(const gsb_ctl_cfg* cfgs, int64_t n, int32_t n_buckets,
+                        const double* tps_lo, const double* tps_hi, int64_t n_tables,
+                        char* msg, size_t msg_cap);
+
+/* ---------------------------------------------------------------- microbenchmarks */
+/* FP64 pipe peak probe: n_threads lanes each run `iters` independent DFMA chains;
+ * returns the DFMA count in *d_out-sized work (used by bench.py for the roofline). */
+int gsb_fp64_probe(gsb_ctx* ctx, int64_t n_threads, int iters, double* d_sink, void* stream);
+
+/* Self-test of the correctly-rounded division used by K2/K3:
+ * per_divisor random dividends for every clock of profile 0 and for 1000; writes the count
+ * of results that differ in any bit from IEEE division to *d_mismatches. */
+int gsb_selftest_division(gsb_ctx* ctx, int64_t per_divisor, uint64_t seed,
+                          unsigned long long* d_mismatches, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSB_H */

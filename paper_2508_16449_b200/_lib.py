@@ -1,0 +1,131 @@
+"""ctypes binding of libgsb.so (include/gsb.h). Fails loudly when the library is missing:
+there is no CPU fallback anywhere in this package."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libgsb.so")
+
+_d, _i32, _i64, _u64, _p = C.c_double, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+
+GSB_MAX_PROFILES = 4
+GSB_MAX_GRID = 256
+GSB_MAX_CLASSES = 8
+GSB_MAX_BUCKETS = 32
+GSB_MAX_TBT_WINDOW = 256
+
+OK, MODEL_ERROR, ROUTER_ERROR, TRACE_ERROR, CUDA_ERROR, INVALID_ARGUMENT = range(6)
+FIXED_WINDOW, DEADLINE_SLACK, PER_CELL_WINDOW = range(3)
+
+
+class CProfile(C.Structure):
+    _fields_ = [(n, _d) for n in (
+        "f_min_mhz", "f_max_mhz", "step_mhz", "f_ref_mhz",
+        "lat_a", "lat_b", "lat_c", "lat_f_ref_mhz",
+        "dec_alpha0_ms", "dec_alpha1_ms", "dec_beta0_ms", "dec_beta1_ms", "dec_f_ref_mhz",
+        "k3", "k2", "k1", "k0", "p_idle_w")]
+
+
+class CQoptCfg(C.Structure):
+    _fields_ = [("resolve_period_ms", _d), ("margin_prefill", _d), ("min_budget_ms", _d),
+                ("first_token_allowance_ms", _d)]
+
+
+class CCtlCfg(C.Structure):
+    _fields_ = [("tslo_ms", _d), ("margin_decode", _d), ("fine_period_ms", _d),
+                ("coarse_period_ms", _d), ("adapt_period_s", _d), ("step_mhz", _d),
+                ("max_step_mhz", _d), ("hysteresis_count", _i32), ("tbt_window_tokens", _i32),
+                ("bias_threshold", _d), ("tps_scale", _d), ("upper_margin", _d),
+                ("lower_margin", _d)]
+
+
+class CRouteCfg(C.Structure):
+    _fields_ = [("n_thresholds", _i32), ("thresholds", _i32 * (GSB_MAX_CLASSES - 1)),
+                ("enabled", _i32), ("slo_boundary_tokens", _i32), ("window_ms", _i64),
+                ("w0", _i64), ("n_windows", _i64), ("ttft_sm_ms", _d), ("ttft_l_ms", _d),
+                ("first_token_allowance_ms", _d)]
+
+
+class CSelectCfg(C.Structure):
+    _fields_ = [("mode", _i32), ("n_classes", _i32), ("fixed_window_ms", _d), ("w0", _i64),
+                ("window_ms", _i64), ("qopt", CQoptCfg)]
+
+
+class CClassSummary(C.Structure):
+    _fields_ = [("n_cmd", _i64), ("n_infeasible", _i64), ("n_empty", _i64),
+                ("sum_energy_j", _d), ("min_energy_j", _d), ("argmin_cell", _i64)]
+
+
+class CTelemetry(C.Structure):
+    _fields_ = [("n_streams", _i64), ("d_ev_off", _p), ("d_t_ms", _p), ("d_tokens", _p),
+                ("d_gap_off", _p), ("d_gaps", _p)]
+
+
+class CReplayArgs(C.Structure):
+    _fields_ = [("n_traj", _i64), ("d_cfg", _p), ("d_table_of", _p), ("d_stream_of", _p),
+                ("d_worker", _p), ("n_buckets", _i32), ("d_tps_hi", _p), ("d_f_opt", _p),
+                ("f_min_mhz", _d), ("f_max_mhz", _d), ("fine_period_ms", _d),
+                ("coarse_period_ms", _d), ("t_end_ms", _d), ("d_fine_has", _p),
+                ("d_fine_p95", _p), ("d_coarse_tps", _p), ("d_digest", _p), ("d_n_rec", _p),
+                ("d_counts", _p), ("d_mean_cmd", _p), ("d_records", _p), ("rec_cap", _i64)]
+
+
+# every symbol include/gsb.h declares (checked by tests/test_boundary.py)
+EXPORTS = (
+    "gsb_version", "gsb_status_string", "gsb_ctx_create", "gsb_ctx_destroy", "gsb_last_error",
+    "gsb_ctx_stream", "gsb_synchronize", "gsb_profile_validate", "gsb_ctl_cfg_validate",
+    "gsb_set_profiles", "gsb_routing_validate", "gsb_window_bounds", "gsb_route_bin",
+    "gsb_fifo_order", "gsb_prefill_select", "gsb_select_batches", "gsb_energy_batches",
+    "gsb_prefill_summary", "gsb_n_ticks", "gsb_window_series", "gsb_build_band_tables",
+    "gsb_decode_replay", "gsb_replay_validate", "gsb_fp64_probe", "gsb_selftest_division",
+)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libgsb.so once and declare every prototype. Raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build the sm_100a library first "
+                          f"(python -c 'import __graft_entry__ as g; g.build()')")
+    L = C.CDLL(path)
+    P = C.POINTER
+    L.gsb_version.restype = C.c_char_p
+    L.gsb_status_string.argtypes = [C.c_int]
+    L.gsb_status_string.restype = C.c_char_p
+    L.gsb_ctx_create.argtypes = [C.c_int, P(_p)]
+    L.gsb_ctx_destroy.argtypes = [_p]
+    L.gsb_ctx_destroy.restype = None
+    L.gsb_last_error.argtypes = [_p]
+    L.gsb_last_error.restype = C.c_char_p
+    L.gsb_ctx_stream.argtypes = [_p]
+    L.gsb_ctx_stream.restype = _p
+    L.gsb_synchronize.argtypes = [_p]
+    L.gsb_profile_validate.argtypes = [P(CProfile), C.c_char_p, C.c_size_t]
+    L.gsb_ctl_cfg_validate.argtypes = [P(CCtlCfg), C.c_char_p, C.c_size_t]
+    L.gsb_set_profiles.argtypes = [_p, C.c_int, _p]
+    L.gsb_routing_validate.argtypes = [P(CRouteCfg), C.c_int, _p, C.c_char_p, C.c_size_t]
+    L.gsb_window_bounds.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p]
+    L.gsb_route_bin.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_fifo_order.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p]
+    L.gsb_prefill_select.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_select_batches.argtypes = [_p, P(CSelectCfg), C.c_int, _i64, _p, _p, _p, _p, _p, _p,
+                                     _p, _p, _p, _p]
+    L.gsb_energy_batches.argtypes = [_p, C.c_int, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_prefill_summary.argtypes = [_p, C.c_int, C.c_int, _i64, _p, _p, _p, _p]
+    L.gsb_n_ticks.argtypes = [_d, _d]
+    L.gsb_n_ticks.restype = _i64
+    L.gsb_window_series.argtypes = [_p, P(CTelemetry), C.c_int, _d, _d, _d, _p, _p, _p, _p]
+    L.gsb_build_band_tables.argtypes = [_p, _i64, _p, _p, _p, _p, _p, C.c_int, _p, _p, _p, _p,
+                                        _p, _p]
+    L.gsb_decode_replay.argtypes = [_p, P(CReplayArgs), _p]
+    L.gsb_replay_validate.argtypes = [_p, _i64, _i32, _p, _p, _i64, C.c_char_p, C.c_size_t]
+    L.gsb_fp64_probe.argtypes = [_p, _i64, C.c_int, _p, _p]
+    L.gsb_selftest_division.argtypes = [_p, _i64, _u64, _p, _p]
+    _lib = L
+    return L

@@ -1,0 +1,765 @@
+"""Python host mirror of the reference's decision-engine interface over libgsb.so.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/greensim:
+  gpu_model.hpp   FrequencyGrid, LatencyModel, DecodeStepModel, PowerModel, GpuProfile
+  prefill_opt.hpp PrefillJob, PrefillBatch, EnergyBreakdown, FrequencyChoice,
+                  QueueOptimizerConfig, ClassQueueSnapshot, PrefillFreqCommand,
+                  busy_time_ms, energy_total, select_frequency, queue_optimizer_tick
+  router.hpp      RoutingConfig, classify, Dispatcher
+  decode_ctl.hpp  DecodeCtlConfig, BandBucket, FreqBandTable, build_band_table,
+                  DecisionRecord
+Every computation runs in the sm_100a kernels behind include/gsb.h on the chosen CUDA
+device; this module only marshals arguments (torch is used for device memory and
+streams). ModelError / RouterError are raised from the C status codes exactly where the
+reference throws.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+class ModelError(RuntimeError):
+    """greensim::ModelError (gpu_model.hpp:11-13)."""
+
+
+class RouterError(RuntimeError):
+    """greensim::RouterError (router.hpp:13-15)."""
+
+
+class TraceError(RuntimeError):
+    """greensim::TraceError (trace.hpp:36-40)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRORS = {L.MODEL_ERROR: ModelError, L.ROUTER_ERROR: RouterError, L.TRACE_ERROR: TraceError,
+           L.CUDA_ERROR: CudaError, L.INVALID_ARGUMENT: ValueError}
+
+
+# ------------------------------------------------------------------ gpu_model.hpp
+@dataclass
+class FrequencyGrid:
+    f_min_mhz: float = 210.0
+    f_max_mhz: float = 1410.0
+    step_mhz: float = 15.0
+    f_ref_mhz: float = 1410.0
+
+    def size(self) -> int:  # gpu_model.cpp:24-26
+        return int(round((self.f_max_mhz - self.f_min_mhz) / self.step_mhz)) + 1
+
+    def at(self, i: int) -> float:  # gpu_model.cpp:28
+        return self.f_min_mhz + self.step_mhz * float(i)
+
+    def frequencies(self) -> list:
+        return [self.at(i) for i in range(self.size())]
+
+    def on_grid(self, f: float) -> bool:  # gpu_model.cpp:18-22
+        if f < self.f_min_mhz - 1e-9 or f > self.f_max_mhz + 1e-9:
+            return False
+        k = (f - self.f_min_mhz) / self.step_mhz
+        return abs(k - round(k)) < 1e-9
+
+
+@dataclass
+class LatencyModel:
+    a: float = 0.0
+    b: float = 0.0
+    c: float = 0.0
+    f_ref_mhz: float = 1410.0
+
+
+@dataclass
+class DecodeStepModel:
+    alpha0_ms: float = 0.0
+    alpha1_ms: float = 0.0
+    beta0_ms: float = 0.0
+    beta1_ms: float = 0.0
+    f_ref_mhz: float = 1410.0
+
+
+@dataclass
+class PowerModel:
+    k3: float = 0.0
+    k2: float = 0.0
+    k1: float = 0.0
+    k0: float = 0.0
+    p_idle_w: float = 0.0
+
+
+@dataclass
+class GpuProfile:
+    name: str = "default"
+    grid: FrequencyGrid = field(default_factory=FrequencyGrid)
+    prefill: LatencyModel = field(default_factory=LatencyModel)
+    decode: DecodeStepModel = field(default_factory=DecodeStepModel)
+    power: PowerModel = field(default_factory=PowerModel)
+
+    @staticmethod
+    def default_profile() -> "GpuProfile":
+        """GpuProfile::default_profile (gpu_model.cpp:121-130): synth-a100-40g."""
+        p = GpuProfile("synth-a100-40g", FrequencyGrid(210.0, 1410.0, 15.0, 1410.0),
+                       LatencyModel(2.0e-5, 0.12, 8.0, 1410.0),
+                       DecodeStepModel(14.5, 0.1, 9.0, 0.135, 1410.0),
+                       PowerModel(1.6e-7, -1.0e-4, 0.05, 216.5, 15.0))
+        p.validate()
+        return p
+
+    def to_c(self) -> L.CProfile:
+        g, a, d, w = self.grid, self.prefill, self.decode, self.power
+        return L.CProfile(g.f_min_mhz, g.f_max_mhz, g.step_mhz, g.f_ref_mhz, a.a, a.b, a.c,
+                          a.f_ref_mhz, d.alpha0_ms, d.alpha1_ms, d.beta0_ms, d.beta1_ms,
+                          d.f_ref_mhz, w.k3, w.k2, w.k1, w.k0, w.p_idle_w)
+
+    def key(self) -> tuple:
+        c = self.to_c()
+        return tuple(getattr(c, n) for n, _ in c._fields_)
+
+    def validate(self) -> None:
+        """GpuProfile::validate (gpu_model.cpp:80-87); raises ModelError."""
+        msg = C.create_string_buffer(256)
+        rc = L.load().gsb_profile_validate(C.byref(self.to_c()), msg, 256)
+        if rc != L.OK:
+            raise ModelError(msg.value.decode())
+
+    @staticmethod
+    def from_json(path: str) -> "GpuProfile":
+        """Profile JSON schema of proj/profiles/*.json (io.hpp:14-19)."""
+        with open(path) as fh:
+            j = json.load(fh)
+        p = GpuProfile(j.get("name", "default"),
+                       FrequencyGrid(**{k: float(v) for k, v in j["grid"].items()}),
+                       LatencyModel(**{k: float(v) for k, v in j["prefill_latency"].items()}),
+                       DecodeStepModel(**{k: float(v) for k, v in j["decode_step"].items()}),
+                       PowerModel(**{k: float(v) for k, v in j["power"].items()}))
+        p.validate()
+        return p
+
+    def to_json(self) -> dict:
+        g, a, d, w = self.grid, self.prefill, self.decode, self.power
+        return {"name": self.name,
+                "grid": {"f_min_mhz": g.f_min_mhz, "f_max_mhz": g.f_max_mhz,
+                         "step_mhz": g.step_mhz, "f_ref_mhz": g.f_ref_mhz},
+                "prefill_latency": {"a": a.a, "b": a.b, "c": a.c, "f_ref_mhz": a.f_ref_mhz},
+                "decode_step": {"alpha0_ms": d.alpha0_ms, "alpha1_ms": d.alpha1_ms,
+                                "beta0_ms": d.beta0_ms, "beta1_ms": d.beta1_ms,
+                                "f_ref_mhz": d.f_ref_mhz},
+                "power": {"k3": w.k3, "k2": w.k2, "k1": w.k1, "k0": w.k0,
+                          "p_idle_w": w.p_idle_w}}
+
+
+# ------------------------------------------------------------------ prefill_opt.hpp
+@dataclass
+class PrefillJob:
+    request_id: int = 0
+    prompt_tokens: int = 0
+    deadline_ms: float = 0.0
+    work_fraction: float = 1.0
+
+
+@dataclass
+class PrefillBatch:
+    jobs: list = field(default_factory=list)
+
+
+@dataclass
+class EnergyBreakdown:
+    active_j: float = 0.0
+    idle_j: float = 0.0
+    total_j: float = 0.0
+    feasible: bool = True
+
+
+@dataclass
+class FrequencyChoice:
+    f_mhz: float = 0.0
+    energy_j: float = 0.0
+
+
+@dataclass
+class QueueOptimizerConfig:
+    resolve_period_ms: float = 100.0
+    margin_prefill: float = 0.95
+    min_budget_ms: float = 100.0
+    first_token_allowance_ms: float = 100.0
+
+    def to_c(self) -> L.CQoptCfg:
+        return L.CQoptCfg(self.resolve_period_ms, self.margin_prefill, self.min_budget_ms,
+                          self.first_token_allowance_ms)
+
+
+@dataclass
+class ClassQueueSnapshot:
+    class_id: int = 0
+    batch: PrefillBatch = field(default_factory=PrefillBatch)
+
+
+@dataclass
+class PrefillFreqCommand:
+    class_id: int = 0
+    f_mhz: float = 0.0
+    window_ms: float = 0.0
+    infeasible: bool = False
+
+
+# ------------------------------------------------------------------ router.hpp
+@dataclass
+class RoutingConfig:
+    enabled: bool = True
+    thresholds: list = field(default_factory=lambda: [1024])
+    worker_map: list = field(default_factory=lambda: [0, 1])
+
+    def n_classes(self) -> int:
+        return len(self.thresholds) + 1
+
+    def validate(self, n_prefill_workers: int) -> None:
+        """RoutingConfig::validate (router.cpp:7-24); raises RouterError."""
+        wm = np.ascontiguousarray(self.worker_map[:n_prefill_workers] if len(self.worker_map)
+                                  >= n_prefill_workers else self.worker_map, np.int32)
+        msg = C.create_string_buffer(256)
+        cfg = _route_cfg(self, 1, 0, 1)
+        if self.enabled and len(self.worker_map) != n_prefill_workers:
+            raise RouterError("routing: worker_map must name a class per prefill worker")
+        if len(self.thresholds) > L.GSB_MAX_CLASSES - 1:
+            raise RouterError("routing: more than 7 thresholds")
+        rc = L.load().gsb_routing_validate(C.byref(cfg), n_prefill_workers,
+                                           wm.ctypes.data_as(C.c_void_p), msg, 256)
+        if rc != L.OK:
+            raise RouterError(msg.value.decode())
+
+
+@dataclass
+class SloConfig:
+    """greensim::SloConfig (simkernel.hpp:53-62)."""
+    ttft_sm_ms: float = 400.0
+    ttft_l_ms: float = 2000.0
+    tbt_p95_ms: float = 100.0
+
+
+def _route_cfg(rc: RoutingConfig, window_ms: int, w0: int, n_windows: int,
+               slo: SloConfig = SloConfig(), allowance: float = 100.0) -> L.CRouteCfg:
+    c = L.CRouteCfg()
+    thr = list(rc.thresholds)
+    c.n_thresholds = len(thr)
+    for i, t in enumerate(thr[:L.GSB_MAX_CLASSES - 1]):
+        c.thresholds[i] = int(t)
+    c.enabled = 1 if rc.enabled else 0
+    c.slo_boundary_tokens = 1024
+    c.window_ms, c.w0, c.n_windows = int(window_ms), int(w0), int(n_windows)
+    c.ttft_sm_ms, c.ttft_l_ms = slo.ttft_sm_ms, slo.ttft_l_ms
+    c.first_token_allowance_ms = allowance
+    return c
+
+
+# ------------------------------------------------------------------ decode_ctl.hpp
+@dataclass
+class DecodeCtlConfig:
+    tslo_ms: float = 100.0
+    margin_decode: float = 0.95
+    fine_period_ms: float = 20.0
+    coarse_period_ms: float = 200.0
+    adapt_period_s: float = 6.0
+    step_mhz: float = 15.0
+    max_step_mhz: float = 30.0
+    hysteresis_count: int = 3
+    bias_threshold: float = 0.8
+    tbt_window_tokens: int = 256
+    tps_scale: float = 4.0
+    upper_margin: float = 1.0
+    lower_margin: float = 0.65
+
+    def to_c(self) -> L.CCtlCfg:
+        return L.CCtlCfg(self.tslo_ms, self.margin_decode, self.fine_period_ms,
+                         self.coarse_period_ms, self.adapt_period_s, self.step_mhz,
+                         self.max_step_mhz, int(self.hysteresis_count),
+                         int(self.tbt_window_tokens), self.bias_threshold, self.tps_scale,
+                         self.upper_margin, self.lower_margin)
+
+    def validate(self) -> None:
+        """DecodeCtlConfig::validate (decode_ctl.cpp:12-26); raises ModelError."""
+        msg = C.create_string_buffer(256)
+        if L.load().gsb_ctl_cfg_validate(C.byref(self.to_c()), msg, 256) != L.OK:
+            raise ModelError(msg.value.decode())
+
+
+@dataclass
+class BandBucket:
+    tps_lo: float = 0.0
+    tps_hi: float = 0.0
+    f_opt_mhz: float = 0.0
+    feasible: bool = True
+
+
+@dataclass
+class FreqBandTable:
+    buckets: list = field(default_factory=list)
+
+    def bucket_index(self, tps: float) -> int:  # decode_ctl.cpp:47-51
+        for i, b in enumerate(self.buckets):
+            if tps <= b.tps_hi:
+                return i
+        return len(self.buckets) - 1
+
+    def band(self, bucket: int, grid: FrequencyGrid, step_mhz: float):  # :52-57
+        f = self.buckets[bucket].f_opt_mhz
+        lo, hi = f - step_mhz, f + step_mhz
+        return (lo if grid.f_min_mhz < lo else grid.f_min_mhz,
+                grid.f_max_mhz if grid.f_max_mhz < hi else hi)
+
+
+ACTIONS = ("hold", "up", "down", "coarse_hold", "coarse_pending", "coarse_commit", "adapt_up",
+           "adapt_down")
+
+DECISION_DTYPE = np.dtype([("tick_ms", "<f8"), ("tps", "<f8"), ("p95_tbt_ms", "<f8"),
+                           ("band_lo", "<f8"), ("band_hi", "<f8"), ("command_mhz", "<f8"),
+                           ("worker", "<i4"), ("bucket", "<i4"), ("action", "<i4"),
+                           ("pad_", "<i4")])
+
+CTL_DTYPE = np.dtype([("tslo_ms", "<f8"), ("margin_decode", "<f8"), ("fine_period_ms", "<f8"),
+                      ("coarse_period_ms", "<f8"), ("adapt_period_s", "<f8"),
+                      ("step_mhz", "<f8"), ("max_step_mhz", "<f8"),
+                      ("hysteresis_count", "<i4"), ("tbt_window_tokens", "<i4"),
+                      ("bias_threshold", "<f8"), ("tps_scale", "<f8"),
+                      ("upper_margin", "<f8"), ("lower_margin", "<f8")])
+assert CTL_DTYPE.itemsize == C.sizeof(L.CCtlCfg)
+
+
+def ctl_cfg_array(cfgs: Sequence[DecodeCtlConfig]) -> np.ndarray:
+    a = np.zeros(len(cfgs), CTL_DTYPE)
+    for i, c in enumerate(cfgs):
+        a[i] = (c.tslo_ms, c.margin_decode, c.fine_period_ms, c.coarse_period_ms,
+                c.adapt_period_s, c.step_mhz, c.max_step_mhz, c.hysteresis_count,
+                c.tbt_window_tokens, c.bias_threshold, c.tps_scale, c.upper_margin,
+                c.lower_margin)
+    return a
+
+
+# ------------------------------------------------------------------ results
+@dataclass
+class RouteResult:
+    """K1 output (device tensors). cells are window-major, class-minor."""
+    n_classes: int
+    n_windows: int
+    window_ms: int
+    w0: int
+    bounds: torch.Tensor          # i64 [n_windows+1]
+    cls: torch.Tensor             # u8  [n_req]   queue assignment per request
+    count: torch.Tensor           # i32 (u32 bits) [cells]
+    t_ref: torch.Tensor           # f64 [P, cells]
+    min_deadline: Optional[torch.Tensor]   # f64 [cells]
+    cell_off: Optional[torch.Tensor] = None  # i64 [cells+1]
+    fifo: Optional[torch.Tensor] = None      # i64 [n_req] cell-major FIFO order
+
+    @property
+    def n_cells(self) -> int:
+        return self.n_windows * self.n_classes
+
+
+@dataclass
+class SelectResult:
+    """K2 output (device tensors) per (profile, cell)."""
+    f_idx: torch.Tensor           # i16 [P, cells]; -1 infeasible, -2 empty
+    energy_j: torch.Tensor        # f64 [P, cells]
+    window_ms: torch.Tensor       # f64 [cells]
+
+
+@dataclass
+class Telemetry:
+    """Raw decode telemetry of S streams, CSR (include/gsb.h gsb_telemetry)."""
+    ev_off: np.ndarray   # i64 [S+1]
+    t_ms: np.ndarray     # f64 [E]
+    tokens: np.ndarray   # i32 [E]
+    gap_off: np.ndarray  # i64 [E+1]
+    gaps: np.ndarray     # f64 [G]
+
+    @property
+    def n_streams(self) -> int:
+        return len(self.ev_off) - 1
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    raise TypeError(type(t))
+
+
+class Engine:
+    """One libgsb context on one CUDA device (single owner, like the reference's objects)."""
+
+    def __init__(self, device: int = 0, profiles: Optional[Sequence[GpuProfile]] = None):
+        self.lib = L.load()
+        self.device = torch.device("cuda", device)
+        torch.cuda.init()
+        h = C.c_void_p()
+        rc = self.lib.gsb_ctx_create(device, C.byref(h))
+        if rc != L.OK:
+            raise CudaError(f"gsb_ctx_create({device}) failed: "
+                            f"{self.lib.gsb_status_string(rc).decode()} (needs an sm_100 GPU)")
+        self.ctx = h
+        self.profiles: list = []
+        self.set_profiles(profiles or [GpuProfile.default_profile()])
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.gsb_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- plumbing
+    def _check(self, rc: int):
+        if rc != L.OK:
+            msg = self.lib.gsb_last_error(self.ctx).decode()
+            raise _ERRORS.get(rc, RuntimeError)(msg)
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _dev(self, a, dtype) -> torch.Tensor:
+        if isinstance(a, torch.Tensor):
+            return a.to(self.device, dtype).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(a), device=self.device).to(dtype).contiguous()
+
+    def _empty(self, shape, dtype) -> torch.Tensor:
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    def set_profiles(self, profiles: Sequence[GpuProfile]) -> None:
+        arr = (L.CProfile * len(profiles))(*[p.to_c() for p in profiles])
+        self._check(self.lib.gsb_set_profiles(self.ctx, len(profiles), C.cast(arr, C.c_void_p)))
+        self.profiles = list(profiles)
+
+    def _profile_index(self, profile: GpuProfile) -> int:
+        for i, p in enumerate(self.profiles):
+            if p.key() == profile.key():
+                return i
+        self.set_profiles([profile])
+        return 0
+
+    # ---------------------------------------------------------------- K1
+    def window_bounds(self, arrival: torch.Tensor, rc: RoutingConfig, window_ms: int, w0: int,
+                      n_windows: int) -> torch.Tensor:
+        cfg = _route_cfg(rc, window_ms, w0, n_windows)
+        bounds = self._empty(n_windows + 1, torch.int64)
+        self._check(self.lib.gsb_window_bounds(self.ctx, C.byref(cfg), arrival.numel(),
+                                               _ptr(arrival), _ptr(bounds), self.stream()))
+        return bounds
+
+    def route_bin(self, arrival, prompt, routing: RoutingConfig, window_ms: int, w0: int = 0,
+                  n_windows: Optional[int] = None, want_deadline: bool = False,
+                  want_fifo: bool = False, slo: SloConfig = SloConfig(),
+                  allowance_ms: float = 100.0, out: Optional[RouteResult] = None) -> RouteResult:
+        """K1: classify every request (router.cpp:26-31) and bin the trace into
+        (window, class) cells with the reference-order T_ref per profile."""
+        arrival = self._dev(arrival, torch.int64)
+        prompt = self._dev(prompt, torch.int32)
+        n = arrival.numel()
+        if n_windows is None:
+            last = int(arrival[-1].item()) if n else 0
+            n_windows = max(1, last // window_ms - w0 + 1)
+        Cn = routing.n_classes() if routing.enabled else 1
+        cells = n_windows * Cn
+        cfg = _route_cfg(routing, window_ms, w0, n_windows, slo, allowance_ms)
+        P = len(self.profiles)
+        if out is None:
+            out = RouteResult(Cn, n_windows, window_ms, w0, self._empty(n_windows + 1, torch.int64),
+                              self._empty(n, torch.uint8), self._empty(cells, torch.int32),
+                              self._empty((P, cells), torch.float64),
+                              self._empty(cells, torch.float64) if want_deadline else None)
+        s = self.stream()
+        self._check(self.lib.gsb_window_bounds(self.ctx, C.byref(cfg), n, _ptr(arrival),
+                                               _ptr(out.bounds), s))
+        self._check(self.lib.gsb_route_bin(self.ctx, C.byref(cfg), n, _ptr(arrival), _ptr(prompt),
+                                           _ptr(out.bounds), _ptr(out.cls), _ptr(out.count),
+                                           _ptr(out.t_ref), _ptr(out.min_deadline), s))
+        if want_fifo:
+            out.cell_off = self._empty(cells + 1, torch.int64)
+            out.fifo = self._empty(n, torch.int64)
+            self._check(self.lib.gsb_fifo_order(self.ctx, C.byref(cfg), n, _ptr(out.cls),
+                                                _ptr(out.bounds), _ptr(out.count),
+                                                _ptr(out.cell_off), _ptr(out.fifo), s))
+        return out
+
+    # ---------------------------------------------------------------- K2
+    def prefill_select(self, rr: RouteResult, mode: int = L.FIXED_WINDOW,
+                       fixed_window_ms: float = 0.0,
+                       qopt: QueueOptimizerConfig = QueueOptimizerConfig(),
+                       window: Optional[torch.Tensor] = None,
+                       out: Optional[SelectResult] = None) -> SelectResult:
+        """K2: energy_total at every (cell, profile, clock) + deterministic argmin."""
+        cfg = L.CSelectCfg(mode, rr.n_classes, fixed_window_ms, rr.w0, rr.window_ms, qopt.to_c())
+        P, cells = len(self.profiles), rr.n_cells
+        if out is None:
+            out = SelectResult(self._empty((P, cells), torch.int16),
+                               self._empty((P, cells), torch.float64),
+                               window if window is not None else self._empty(cells, torch.float64))
+        self._check(self.lib.gsb_prefill_select(self.ctx, C.byref(cfg), cells, _ptr(rr.t_ref),
+                                                _ptr(rr.count), _ptr(rr.min_deadline),
+                                                _ptr(out.window_ms), _ptr(out.f_idx),
+                                                _ptr(out.energy_j), self.stream()))
+        return out
+
+    def prefill_summary(self, sel: SelectResult, n_classes: int) -> np.ndarray:
+        P, cells = sel.f_idx.shape
+        out = self._empty((P * n_classes, C.sizeof(L.CClassSummary)), torch.uint8)
+        self._check(self.lib.gsb_prefill_summary(self.ctx, P, n_classes, cells, _ptr(sel.f_idx),
+                                                 _ptr(sel.energy_j), _ptr(out), self.stream()))
+        host = out.cpu().numpy()
+        dt = np.dtype([("n_cmd", "<i8"), ("n_infeasible", "<i8"), ("n_empty", "<i8"),
+                       ("sum_energy_j", "<f8"), ("min_energy_j", "<f8"), ("argmin_cell", "<i8")])
+        return host.view(dt).reshape(P, n_classes)
+
+    # ---------------------------------------------------------------- ragged batches
+    def select_batches(self, off, prompt, windows=None, profile: Optional[GpuProfile] = None,
+                       wf=None, mode: int = L.PER_CELL_WINDOW, fixed_window_ms: float = 0.0,
+                       deadline=None, now=None,
+                       qopt: QueueOptimizerConfig = QueueOptimizerConfig()):
+        """select_frequency / queue_optimizer_tick over CSR batches. Returns device tensors
+        (f_idx i16, energy f64, window f64, t_ref f64)."""
+        pi = 0 if profile is None else self._profile_index(profile)
+        off = self._dev(off, torch.int64)
+        nb = off.numel() - 1
+        prompt = self._dev(prompt, torch.int32)
+        wf_t = None if wf is None else self._dev(wf, torch.float64)
+        dl = None if deadline is None else self._dev(deadline, torch.float64)
+        nw = None if now is None else self._dev(now, torch.float64)
+        win = self._dev(windows, torch.float64) if windows is not None else self._empty(nb, torch.float64)
+        f_idx = self._empty(nb, torch.int16)
+        energy = self._empty(nb, torch.float64)
+        t_ref = self._empty(nb, torch.float64)
+        cfg = L.CSelectCfg(mode, 1, fixed_window_ms, 0, 1, qopt.to_c())
+        self._check(self.lib.gsb_select_batches(self.ctx, C.byref(cfg), pi, nb, _ptr(off),
+                                                _ptr(prompt), _ptr(wf_t), _ptr(dl), _ptr(nw),
+                                                _ptr(win), _ptr(f_idx), _ptr(energy),
+                                                _ptr(t_ref), self.stream()))
+        return f_idx, energy, win, t_ref
+
+    def energy_batches(self, off, prompt, f_mhz, windows, profile: Optional[GpuProfile] = None,
+                       wf=None):
+        pi = 0 if profile is None else self._profile_index(profile)
+        off = self._dev(off, torch.int64)
+        nb = off.numel() - 1
+        prompt = self._dev(prompt, torch.int32)
+        wf_t = None if wf is None else self._dev(wf, torch.float64)
+        f = self._dev(f_mhz, torch.float64)
+        w = self._dev(windows, torch.float64)
+        outs = [self._empty(nb, torch.float64) for _ in range(4)]
+        feas = self._empty(nb, torch.uint8)
+        self._check(self.lib.gsb_energy_batches(self.ctx, pi, nb, _ptr(off), _ptr(prompt),
+                                                _ptr(wf_t), _ptr(f), _ptr(w), *[_ptr(o) for o in outs],
+                                                _ptr(feas), self.stream()))
+        return (*outs, feas)
+
+    # ---------------------------------------------------------------- reference-named calls
+    @staticmethod
+    def _batch_arrays(batch: PrefillBatch):
+        p = np.array([j.prompt_tokens for j in batch.jobs], np.int32)
+        wf = np.array([j.work_fraction for j in batch.jobs], np.float64)
+        dl = np.array([j.deadline_ms for j in batch.jobs], np.float64)
+        return p, wf, dl
+
+    def select_frequency(self, batch: PrefillBatch, window_ms: float,
+                         profile: GpuProfile) -> Optional[FrequencyChoice]:
+        """select_frequency (prefill_opt.cpp:45-56) on the GPU."""
+        if not batch.jobs:
+            raise ModelError("busy_time: empty batch")
+        p, wf, _ = self._batch_arrays(batch)
+        f_idx, e, _, _ = self.select_batches([0, len(p)], p, [window_ms], profile, wf)
+        i = int(f_idx[0].item())
+        if i < 0:
+            return None
+        return FrequencyChoice(profile.grid.at(i), float(e[0].item()))
+
+    def energy_total(self, batch: PrefillBatch, f: float, window_ms: float,
+                     profile: GpuProfile) -> EnergyBreakdown:
+        """energy_total (prefill_opt.cpp:22-31) on the GPU; ModelError as the reference."""
+        if not batch.jobs:
+            raise ModelError("busy_time: empty batch")
+        if not profile.grid.on_grid(f):
+            raise ModelError("busy_time: frequency off grid")
+        p, wf, _ = self._batch_arrays(batch)
+        busy, a, i, t, feas = self.energy_batches([0, len(p)], p, [f], [window_ms], profile, wf)
+        if int(feas[0].item()) >= 2:
+            raise ModelError("busy_time: frequency off grid")
+        return EnergyBreakdown(float(a[0].item()), float(i[0].item()), float(t[0].item()),
+                               bool(feas[0].item()))
+
+    def busy_time_ms(self, batch: PrefillBatch, f: float, profile: GpuProfile) -> float:
+        """busy_time_ms (prefill_opt.cpp:16-20)."""
+        if not batch.jobs:
+            raise ModelError("busy_time: empty batch")
+        if not profile.grid.on_grid(f):
+            raise ModelError("busy_time: frequency off grid")
+        p, wf, _ = self._batch_arrays(batch)
+        busy, *_ = self.energy_batches([0, len(p)], p, [f], [math.inf], profile, wf)
+        return float(busy[0].item())
+
+    def t_ref_total_ms(self, batch: PrefillBatch, profile: GpuProfile) -> float:
+        p, wf, _ = self._batch_arrays(batch)
+        *_, t = self.select_batches([0, len(p)], p, [0.0], profile, wf)
+        return float(t[0].item())
+
+    def queue_optimizer_tick(self, queues: Sequence[ClassQueueSnapshot], now_ms: float,
+                             cfg: QueueOptimizerConfig, profile: GpuProfile) -> list:
+        """queue_optimizer_tick (prefill_opt.cpp:58-82): one GPU batch per non-empty queue."""
+        live = [q for q in queues if q.batch.jobs]
+        if not live:
+            return []
+        off = np.zeros(len(live) + 1, np.int64)
+        ps, wfs, dls = [], [], []
+        for i, q in enumerate(live):
+            p, wf, dl = self._batch_arrays(q.batch)
+            ps.append(p), wfs.append(wf), dls.append(dl)
+            off[i + 1] = off[i] + len(p)
+        f_idx, _, win, _ = self.select_batches(
+            off, np.concatenate(ps), None, profile, np.concatenate(wfs), L.DEADLINE_SLACK, 0.0,
+            np.concatenate(dls), np.full(len(live), now_ms), cfg)
+        f_idx = f_idx.cpu().numpy()
+        win = win.cpu().numpy()
+        out = []
+        for i, q in enumerate(live):
+            fi = int(f_idx[i])
+            out.append(PrefillFreqCommand(q.class_id,
+                                          profile.grid.at(fi) if fi >= 0 else profile.grid.f_max_mhz,
+                                          float(win[i]), fi < 0))
+        return out
+
+    def classify_many(self, routing: RoutingConfig, prompts) -> np.ndarray:
+        """classify (router.cpp:26-31) for a vector of prompts, on the GPU (K1 with one window)."""
+        prompts = np.ascontiguousarray(prompts, np.int32)
+        rr = self.route_bin(np.zeros(len(prompts), np.int64), prompts, routing, 1, 0, 1)
+        return rr.cls.cpu().numpy().astype(np.int64)
+
+    def classify(self, routing: RoutingConfig, prompt_tokens: int) -> int:
+        return int(self.classify_many(routing, [prompt_tokens])[0])
+
+    # ---------------------------------------------------------------- decode (K3/K4)
+    def telemetry_to_device(self, tel: Telemetry):
+        d = [self._dev(tel.ev_off, torch.int64), self._dev(tel.t_ms, torch.float64),
+             self._dev(tel.tokens, torch.int32), self._dev(tel.gap_off, torch.int64),
+             self._dev(tel.gaps, torch.float64)]
+        c = L.CTelemetry(tel.n_streams, *[_ptr(x) for x in d])
+        return c, d
+
+    def window_series(self, tel: Telemetry, capacity: int, fine_ms: float, coarse_ms: float,
+                      t_end_ms: float, dev=None):
+        """K3a: P95 per fine tick, TPS per coarse tick, per stream (device tensors)."""
+        c, keep = dev if dev is not None else self.telemetry_to_device(tel)
+        nf = self.lib.gsb_n_ticks(fine_ms, t_end_ms)
+        nc = self.lib.gsb_n_ticks(coarse_ms, t_end_ms)
+        S = tel.n_streams
+        has = self._empty((S, nf), torch.uint8)
+        p95 = self._empty((S, nf), torch.float64)
+        tps = self._empty((S, nc), torch.float64)
+        self._check(self.lib.gsb_window_series(self.ctx, C.byref(c), capacity, fine_ms, coarse_ms,
+                                               t_end_ms, _ptr(has), _ptr(p95), _ptr(tps),
+                                               self.stream()))
+        return has, p95, tps
+
+    def build_band_tables(self, profiles: Sequence[GpuProfile], profile_of, t_slo_ms, workers,
+                          max_batch, levels):
+        """K4: build_band_table (decode_ctl.cpp:76-111) for many tuples; raises ModelError
+        on invalid levels like the reference."""
+        lv = np.ascontiguousarray(levels, np.float64)
+        if len(lv) == 0:
+            raise ModelError("band table: need at least one TPS level")
+        if np.any(lv[:-1] >= lv[1:]):
+            raise ModelError("band table: levels must be ascending")
+        wk = np.ascontiguousarray(workers, np.int32)
+        mb = np.ascontiguousarray(max_batch, np.int32)
+        if np.any(wk < 1) or np.any(mb < 1):
+            raise ModelError("band table: bad pool shape")
+        T = len(profile_of)
+        parr = np.frombuffer(b"".join(bytes(p.to_c()) for p in profiles), np.uint8)
+        dp = self._dev(parr, torch.uint8)
+        outs = [self._empty((T, len(lv)), torch.float64) for _ in range(3)]
+        feas = self._empty((T, len(lv)), torch.uint8)
+        self._check(self.lib.gsb_build_band_tables(
+            self.ctx, T, _ptr(dp), _ptr(self._dev(profile_of, torch.int32)),
+            _ptr(self._dev(t_slo_ms, torch.float64)), _ptr(self._dev(wk, torch.int32)),
+            _ptr(self._dev(mb, torch.int32)), len(lv), _ptr(self._dev(lv, torch.float64)),
+            *[_ptr(o) for o in outs], _ptr(feas), self.stream()))
+        torch.cuda.current_stream(self.device).synchronize()
+        return (*outs, feas)
+
+    def build_band_table(self, profile: GpuProfile, tps_levels, t_slo_ms: float,
+                         decode_workers: int, max_batch: int = 64) -> FreqBandTable:
+        lo, hi, fo, fe = self.build_band_tables([profile], [0], [t_slo_ms], [decode_workers],
+                                                [max_batch], tps_levels)
+        lo, hi, fo, fe = (x.cpu().numpy()[0] for x in (lo, hi, fo, fe))
+        return FreqBandTable([BandBucket(float(a), float(b), float(c), bool(d))
+                              for a, b, c, d in zip(lo, hi, fo, fe)])
+
+    def decode_replay(self, cfgs: Sequence[DecodeCtlConfig] | np.ndarray, table_of, stream_of,
+                      worker, tps_lo, tps_hi, f_opt, grid: FrequencyGrid, fine_has, fine_p95,
+                      coarse_tps, t_end_ms: float, rec_cap: int = 0, want_counts: bool = True,
+                      validate: bool = True):
+        """K3b: DecodeController replay, one lane per trajectory. Returns dict of device
+        tensors: digest (i64 bits of u64), n_rec, counts [N,8], mean_cmd, records."""
+        cfg_arr = cfgs if isinstance(cfgs, np.ndarray) else ctl_cfg_array(cfgs)
+        N = len(cfg_arr)
+        tps_lo_h = np.ascontiguousarray(tps_lo.cpu().numpy() if isinstance(tps_lo, torch.Tensor)
+                                        else tps_lo, np.float64)
+        tps_hi_h = np.ascontiguousarray(tps_hi.cpu().numpy() if isinstance(tps_hi, torch.Tensor)
+                                        else tps_hi, np.float64)
+        T, NB = tps_hi_h.reshape(-1, tps_hi_h.shape[-1]).shape
+        fine_ms = float(cfg_arr["fine_period_ms"][0])
+        coarse_ms = float(cfg_arr["coarse_period_ms"][0])
+        if validate:
+            msg = C.create_string_buffer(256)
+            rc = self.lib.gsb_replay_validate(cfg_arr.ctypes.data_as(C.c_void_p), N, NB,
+                                              tps_lo_h.ctypes.data_as(C.c_void_p),
+                                              tps_hi_h.ctypes.data_as(C.c_void_p), T, msg, 256)
+            if rc != L.OK:
+                raise ModelError(msg.value.decode())
+            if np.any(cfg_arr["fine_period_ms"] != fine_ms) or np.any(
+                    cfg_arr["coarse_period_ms"] != coarse_ms):
+                raise ValueError("decode_replay: all trajectories must share the series periods")
+        dcfg = self._dev(cfg_arr.view(np.uint8), torch.uint8)
+        keep = [dcfg, self._dev(table_of, torch.int32), self._dev(stream_of, torch.int32),
+                self._dev(worker, torch.int32), self._dev(tps_hi_h, torch.float64),
+                self._dev(f_opt, torch.float64)]
+        out = {"digest": self._empty(N, torch.int64), "n_rec": self._empty(N, torch.int64),
+               "counts": self._empty((N, 8), torch.int32) if want_counts else None,
+               "mean_cmd": self._empty(N, torch.float64),
+               "records": (self._empty((N, rec_cap, DECISION_DTYPE.itemsize), torch.uint8)
+                           if rec_cap else None)}
+        a = L.CReplayArgs(N, *[_ptr(x) for x in keep[:4]], NB, _ptr(keep[4]), _ptr(keep[5]),
+                          grid.f_min_mhz, grid.f_max_mhz, fine_ms, coarse_ms, t_end_ms,
+                          _ptr(fine_has), _ptr(fine_p95), _ptr(coarse_tps), _ptr(out["digest"]),
+                          _ptr(out["n_rec"]), _ptr(out["counts"]), _ptr(out["mean_cmd"]),
+                          _ptr(out["records"]), rec_cap)
+        self._check(self.lib.gsb_decode_replay(self.ctx, C.byref(a), self.stream()))
+        out["_keep"] = keep
+        return out
+
+    def selftest_division(self, per_divisor: int, seed: int = 12345) -> int:
+        bad = self._empty(1, torch.int64)
+        self._check(self.lib.gsb_selftest_division(self.ctx, per_divisor, seed, _ptr(bad),
+                                                   self.stream()))
+        return int(bad.item())
+
+    def fp64_probe(self, n_threads: int, iters: int):
+        sink = self._empty(1, torch.float64)
+        self._check(self.lib.gsb_fp64_probe(self.ctx, n_threads, iters, _ptr(sink), self.stream()))
+        return sink
+
+
+def records_from_bytes(t: torch.Tensor, n: int) -> np.ndarray:
+    """Decode one trajectory's record slab (uint8 [cap, 64]) into DecisionRecord rows."""
+    return t[:n].cpu().numpy().reshape(-1).view(DECISION_DTYPE)

@@ -1,0 +1,426 @@
+"""GPU parity: the sm_100a kernels behind include/gsb.h against the CPU oracle
+(oracle/gs_oracle.c) and the unmodified reference build (oracle/_ref). Bit-exact for every
+integer output, chosen clock and energy; run with `pytest -m gpu` on a B200."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import (Profile, TelemetryArrays, band_table, default_ctl_cfg,
+                           default_qopt_cfg)
+
+pytestmark = pytest.mark.gpu
+
+LEVELS = np.arange(200.0, 3000.0 + 1e-9, 200.0)
+
+
+def u64(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def _api():
+    from paper_2508_16449_b200 import api
+    return api
+
+
+def synth_profiles(api):
+    """default + 3 synthetic variants (synth-* profiles, validated)."""
+    base = api.GpuProfile.default_profile()
+    out = [base]
+    for i, (ls, ps) in enumerate([(1.6, 1.25), (0.7, 0.8), (2.5, 1.6)]):
+        p = api.GpuProfile(f"synth-{i}", base.grid,
+                           api.LatencyModel(base.prefill.a * ls, base.prefill.b * ls,
+                                            base.prefill.c * ls, 1410.0),
+                           base.decode,
+                           api.PowerModel(base.power.k3 * ps, base.power.k2 * ps,
+                                          base.power.k1 * ps, base.power.k0 * ps,
+                                          base.power.p_idle_w * ps))
+        p.validate()
+        out.append(p)
+    return out
+
+
+def to_oracle(p) -> Profile:
+    return Profile(*p.key())
+
+
+@pytest.fixture(scope="module")
+def eng(gsb):
+    return gsb
+
+
+def test_library_is_native_and_on_b200(eng):
+    name = torch.cuda.get_device_name(0)
+    cap = torch.cuda.get_device_capability(0)
+    assert cap[0] == 10, (name, cap)
+    assert eng.lib.gsb_version().startswith(b"gsb")
+
+
+def test_fast_division_equals_ieee(eng):
+    """div_pre (precomputed reciprocal + 2 FMA) == IEEE division for every grid clock and
+    1000, over random dividends across the exponent range and near-midpoint hard cases."""
+    bad = eng.selftest_division(1 << 22)
+    assert bad == 0
+
+
+@pytest.mark.parametrize("thr,P,qps,wms", [
+    ([512, 1024], 1, 5.0, 60_000),
+    ([256, 512, 1024, 2048], 2, 3.0, 60_000),
+    ([128, 256, 512, 768, 1024, 2048, 4096], 4, 8.0, 30_000),
+    ([1024], 3, 20.0, 1_000),
+])
+def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms):
+    api = _api()
+    profs = synth_profiles(api)[:P]
+    eng.set_profiles(profs)
+    a, p, _ = restate.gen_poisson_trace(qps, 1_800_000, 768.0, 3072.0, 0.15, 128.0, seed=len(thr))
+    nw = int(a[-1] // wms) + 1
+    rr = eng.route_bin(a, p, api.RoutingConfig(True, thr, list(range(len(thr) + 1))), wms, 0, nw,
+                       want_deadline=True, want_fifo=True)
+    torch.cuda.synchronize()
+    cls, cnt, tref, mdl, fifo = restate.route_bin(a, p, thr, wms, 0, nw,
+                                                  [to_oracle(x) for x in profs])
+    np.testing.assert_array_equal(rr.cls.cpu().numpy(), cls)
+    np.testing.assert_array_equal(rr.count.cpu().numpy().view(np.uint32), cnt)
+    np.testing.assert_array_equal(u64(rr.t_ref.cpu().numpy()), u64(tref))
+    np.testing.assert_array_equal(u64(rr.min_deadline.cpu().numpy()), u64(mdl))
+    np.testing.assert_array_equal(rr.fifo.cpu().numpy(), fifo)
+    eng.set_profiles([api.GpuProfile.default_profile()])
+
+
+def test_route_bin_edges(eng, restate):
+    """empty windows, a window offset (w0), requests outside the range, routing disabled."""
+    api = _api()
+    eng.set_profiles([api.GpuProfile.default_profile()])
+    a = np.array([0, 5, 5, 70_000, 70_001, 250_000, 250_000, 250_001], np.int64)
+    p = np.array([10, 1024, 1025, 4096, 1, 600, 2000, 3], np.int32)
+    prof = to_oracle(api.GpuProfile.default_profile())
+    for thr, enabled in (([1024], True), ([1024], False)):
+        rr = eng.route_bin(a, p, api.RoutingConfig(enabled, thr, [0, 1]), 60_000, 1, 4,
+                           want_deadline=True, want_fifo=True)
+        torch.cuda.synchronize()
+        got_cnt = rr.count.cpu().numpy().view(np.uint32)
+        o = restate.route_bin(a, p, thr if enabled else [], 60_000, 1, 4, [prof])
+        np.testing.assert_array_equal(got_cnt, o[1])
+        np.testing.assert_array_equal(u64(rr.t_ref.cpu().numpy()), u64(o[2]))
+        inside = slice(3, 8)
+        np.testing.assert_array_equal(rr.cls.cpu().numpy()[inside], o[0][inside])
+
+
+@pytest.mark.parametrize("mode", ["fixed", "slack"])
+def test_prefill_select_matches_oracle(eng, restate, mode):
+    api = _api()
+    profs = synth_profiles(api)
+    eng.set_profiles(profs)
+    thr = [256, 512, 1024, 2048]
+    a, p, _ = restate.gen_poisson_trace(6.0, 3_600_000, 1024.0, 6144.0, 0.35, 32.0, seed=5)
+    wms = 60_000
+    nw = int(a[-1] // wms) + 1
+    rr = eng.route_bin(a, p, api.RoutingConfig(True, thr, list(range(5))), wms, 0, nw,
+                       want_deadline=True)
+    qcfg = api.QueueOptimizerConfig()
+    if mode == "fixed":
+        sel = eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=0.95 * wms)
+    else:
+        sel = eng.prefill_select(rr, api.L.DEADLINE_SLACK, qopt=qcfg)
+    torch.cuda.synchronize()
+    cls, cnt, tref, mdl, _ = restate.route_bin(a, p, thr, wms, 0, nw, [to_oracle(x) for x in profs],
+                                               fifo=False)
+    fi = sel.f_idx.cpu().numpy()
+    en = sel.energy_j.cpu().numpy()
+    win = sel.window_ms.cpu().numpy()
+    n_inf = 0
+    for pi, pr in enumerate(profs):
+        op = to_oracle(pr)
+        for c in range(len(cnt)):
+            if cnt[c] == 0:
+                assert fi[pi, c] == -2
+                continue
+            if mode == "fixed":
+                W = 0.95 * wms
+            else:
+                now = float((c // 5) * wms)
+                slack = mdl[c] - now
+                W = max(qcfg.margin_prefill * slack, qcfg.min_budget_ms) \
+                    if not (qcfg.margin_prefill * slack < qcfg.min_budget_ms) else qcfg.min_budget_ms
+                W = qcfg.min_budget_ms if qcfg.margin_prefill * slack < qcfg.min_budget_ms \
+                    else qcfg.margin_prefill * slack
+                assert u64(win[c]) == u64(W)
+            r = restate.select_t(op, tref[pi, c], W)
+            if r is None:
+                n_inf += 1
+                assert fi[pi, c] == -1
+            else:
+                assert fi[pi, c] == r[0] and u64(en[pi, c]) == u64(r[2]), (pi, c)
+    assert n_inf > 0  # the long classes are over-subscribed: infeasible cells exercised
+    eng.set_profiles([api.GpuProfile.default_profile()])
+
+
+def test_rounding_driven_argmin_probes_on_gpu(eng):
+    api = _api()
+    prof = api.GpuProfile.default_profile()
+    b = api.PrefillBatch([api.PrefillJob(0, 1024)])
+    for D, f, e in [(1e12, 975.0, 15000000066.645506), (1e15, 975.0, 15000000000066.645),
+                    (1e17, 945.0, 1500000000000066.8), (1e20, 390.0, 1.5e18),
+                    (1e300, 210.0, 1.5e298)]:
+        ch = eng.select_frequency(b, D, prof)
+        assert ch.f_mhz == f and ch.energy_j == e
+    batch = api.PrefillBatch([api.PrefillJob(i, L) for i, L in enumerate([512, 700, 300, 2048])])
+    assert eng.select_frequency(batch, 100.0, prof) is None
+    ch = eng.select_frequency(batch, 1000.0, prof)
+    assert (ch.f_mhz, ch.energy_j) == (975.0, 260.74498153855995)
+    ch = eng.select_frequency(batch, 57000.0, prof)
+    assert (ch.f_mhz, ch.energy_j) == (975.0, 1100.74498153856)
+    # frozen 313.803221 J case (proj/tests/test_prefill_opt.cpp:67-83)
+    p2 = api.GpuProfile("t", prof.grid, api.LatencyModel(0.0, 1.0, 0.0, 1410.0), prof.decode,
+                        api.PowerModel(1e-9, 0.0, 0.1, 50.0, 60.0))
+    e = eng.energy_total(api.PrefillBatch([api.PrefillJob(0, 1000)]), 1410.0, 3000.0, p2)
+    assert e.feasible and abs(e.total_j - 313.803221) / 313.803221 < 1e-9
+    with pytest.raises(api.ModelError):
+        eng.energy_total(api.PrefillBatch([]), 1410.0, 3000.0, prof)
+    with pytest.raises(api.ModelError):
+        eng.energy_total(batch, 1411.0, 3000.0, prof)
+    eng.set_profiles([prof])
+
+
+def test_acceptance_batches_vs_reference(eng, ref, prof):
+    """acceptance check 2 shape (acceptance_main.cpp:149-188) + running jobs + random power
+    shapes: GPU select/energy == the reference library, bit for bit."""
+    api = _api()
+    rng = np.random.default_rng(2)
+    gp = api.GpuProfile.default_profile()
+    for shape in range(4):
+        if shape:
+            gp = api.GpuProfile("r", gp.grid, api.LatencyModel(1e-6 + 1e-4 * rng.random(),
+                                                              0.5 * rng.random(), 20 * rng.random(),
+                                                              1410.0), gp.decode,
+                                api.PowerModel(1e-8 + 4e-7 * rng.random(), -2e-4 * rng.random(),
+                                               0.2 * rng.random(), 50 + 400 * rng.random(),
+                                               80.0 * rng.random() + 1e-3))
+            try:
+                gp.validate()
+            except api.ModelError:
+                continue
+        op = to_oracle(gp)
+        nb = 1000
+        sizes = rng.integers(1, 7, nb)
+        off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        prompts = rng.integers(16, 6000, off[-1]).astype(np.int32)
+        wf = np.where(rng.random(off[-1]) < 0.2, rng.random(off[-1]), 1.0)
+        win = np.where(np.arange(nb) % 10 == 9, 0.5 + 30 * rng.random(nb), 10 + 4000 * rng.random(nb))
+        f_idx, en, _, tr = eng.select_batches(off, prompts, win, gp, wf)
+        grid = np.array(gp.grid.frequencies())
+        fsel = grid[rng.integers(0, len(grid), nb)]
+        busy, act, idl, tot, feas = eng.energy_batches(off, prompts, fsel, win, gp, wf)
+        torch.cuda.synchronize()
+        fi, en, tr = f_idx.cpu().numpy(), en.cpu().numpy(), tr.cpu().numpy()
+        act, idl, tot, feas = act.cpu().numpy(), idl.cpu().numpy(), tot.cpu().numpy(), feas.cpu().numpy()
+        rf, re_, found = ref.select_many(op, off, prompts, win, wf)
+        n_inf = 0
+        for b in range(nb):
+            s, e = off[b], off[b + 1]
+            assert u64(tr[b]) == u64(ref.t_ref(op, prompts[s:e], wf[s:e]))
+            if not found[b]:
+                n_inf += 1
+                assert fi[b] == -1
+            else:
+                assert grid[fi[b]] == rf[b] and u64(en[b]) == u64(re_[b]), b
+            ra = ref.energy_total(op, prompts[s:e], fsel[b], win[b], wf[s:e])
+            assert (act[b], idl[b], tot[b], bool(feas[b])) == ra, b
+        assert n_inf > 0
+
+
+def test_online_snapshots_reproduce_reference_commands(eng, ref, prof):
+    """C1: the reference simulator's own optimizer snapshots (greenllm, Alibaba-shaped 1 h,
+    3 classes; captured at simkernel.cpp:487) replayed on the GPU give the reference's
+    PrefillFreqCommands exactly (clock, window, infeasible flag)."""
+    api = _api()
+    a, p, o = ref.gen_poisson_trace(5.0, 3_600_000, seed=7)
+    r = ref.run_capture(a, p, o, prof, "greenllm", thresholds=(512, 1024), worker_map=(0, 1, 2))
+    off = r["snap_off"]
+    nonempty = np.diff(off) > 0
+    idx = np.nonzero(nonempty)[0]
+    # CSR over the non-empty snapshots
+    sizes = np.diff(off)[idx]
+    noff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    sel = np.concatenate([np.arange(off[i], off[i + 1]) for i in idx])
+    gp = api.GpuProfile.default_profile()
+    f_idx, en, win, _ = eng.select_batches(noff, r["job_prompt"][sel], None, gp, r["job_wf"][sel],
+                                           api.L.DEADLINE_SLACK, 0.0, r["job_deadline"][sel],
+                                           r["snap_now"][idx], api.QueueOptimizerConfig())
+    torch.cuda.synchronize()
+    fi = f_idx.cpu().numpy()
+    win = win.cpu().numpy()
+    f = np.where(fi >= 0, 210.0 + 15.0 * fi, 1410.0)
+    assert len(idx) == len(r["cmd_f"]) and len(idx) > 30_000
+    np.testing.assert_array_equal(r["snap_class"][idx], r["cmd_class"])
+    np.testing.assert_array_equal(f, r["cmd_f"])
+    np.testing.assert_array_equal(u64(win), u64(r["cmd_window"]))
+    np.testing.assert_array_equal((fi < 0).astype(np.uint8), r["cmd_infeasible"])
+    assert r["cmd_infeasible"].sum() > 1000
+
+
+def test_band_tables_vs_reference(eng, ref):
+    api = _api()
+    rng = np.random.default_rng(3)
+    base = api.GpuProfile.default_profile()
+    profs, t_slo, workers = [], [], []
+    for i in range(64):
+        d = base.decode
+        p = api.GpuProfile("b", base.grid, base.prefill,
+                           api.DecodeStepModel(d.alpha0_ms * (0.5 + rng.random()), d.alpha1_ms,
+                                               d.beta0_ms, d.beta1_ms * (0.5 + rng.random()),
+                                               1410.0), base.power)
+        profs.append(p)
+        t_slo.append(40 + 120 * rng.random())
+        workers.append(int(rng.integers(1, 9)))
+    lo, hi, fo, fe = eng.build_band_tables(profs, np.arange(64), t_slo, workers, [64] * 64, LEVELS)
+    lo, hi, fo, fe = (x.cpu().numpy() for x in (lo, hi, fo, fe))
+    for i in range(64):
+        want = ref.band_table(to_oracle(profs[i]), LEVELS, t_slo[i], workers[i], 64)
+        np.testing.assert_array_equal(u64(lo[i]), u64(want[0]))
+        np.testing.assert_array_equal(u64(hi[i]), u64(want[1]))
+        np.testing.assert_array_equal(fo[i], want[2])
+        np.testing.assert_array_equal(fe[i].astype(bool), want[3])
+    t = eng.build_band_table(base, LEVELS, 95.0, 4, 64)
+    assert [b.f_opt_mhz for b in t.buckets] == [210, 210, 210, 210, 225, 240, 255, 270, 285, 300,
+                                                315, 315, 330, 360, 390]
+    with pytest.raises(api.ModelError):
+        eng.build_band_table(base, [200.0, 200.0], 95.0, 4, 64)
+
+
+def _telemetry(rng, S, t_end, rate_hz=200.0):
+    offs, ts, toks, goffs, gaps = [0], [], [], [0], []
+    for s in range(S):
+        n = int(t_end / 1000.0 * rate_hz * (0.5 + rng.random()))
+        t = np.sort(rng.uniform(0.0, t_end, n))
+        k = rng.integers(0, n, n // 10)
+        t[k] = np.round(t[k] / 20.0) * 20.0  # events exactly on tick times
+        t = np.sort(t)
+        ts.append(t)
+        toks.append(rng.integers(1, 12, n).astype(np.int32))
+        ng = rng.integers(0, 12, n)
+        for g in ng:
+            goffs.append(goffs[-1] + int(g))
+        gaps.append(rng.gamma(4.0, 20.0, int(ng.sum())))
+        offs.append(offs[-1] + n)
+    api = _api()
+    return api.Telemetry(np.array(offs, np.int64), np.concatenate(ts), np.concatenate(toks),
+                         np.array(goffs, np.int64), np.concatenate(gaps))
+
+
+def _stream_arrays(tel, s):
+    e0, e1 = tel.ev_off[s], tel.ev_off[s + 1]
+    goff = tel.gap_off[e0:e1 + 1]
+    return TelemetryArrays(tel.t_ms[e0:e1].copy(), tel.tokens[e0:e1].copy(),
+                           (goff - goff[0]).astype(np.int64), tel.gaps[goff[0]:goff[-1]].copy())
+
+
+@pytest.mark.parametrize("cap", [1, 16, 256])
+def test_window_series_matches_oracle(eng, restate, cap):
+    rng = np.random.default_rng(cap)
+    tel = _telemetry(rng, 6, 12_000.0)
+    has, p95, tps = eng.window_series(tel, cap, 20.0, 200.0, 12_000.0)
+    torch.cuda.synchronize()
+    for s in range(tel.n_streams):
+        h, p, t = restate.window_series(_stream_arrays(tel, s), cap, 20.0, 200.0, 12_000.0)
+        np.testing.assert_array_equal(has[s].cpu().numpy(), h)
+        np.testing.assert_array_equal(u64(p95[s].cpu().numpy()), u64(p))
+        np.testing.assert_array_equal(u64(tps[s].cpu().numpy()), u64(t))
+
+
+def test_decode_replay_matches_oracle_full_records(eng, restate):
+    """Param sweep (hysteresis x step x TBT target) on shared telemetry: every DecisionRecord
+    bit-identical to the restated DecodeController driven exactly like Sim."""
+    api = _api()
+    rng = np.random.default_rng(9)
+    t_end = 30_000.0
+    tel = _telemetry(rng, 4, t_end)
+    gp = api.GpuProfile.default_profile()
+    cfgs, table_of, stream_of, worker = [], [], [], []
+    tslos = [60.0, 95.0, 130.0]
+    for h in (1, 3, 5):
+        for st in (15.0, 30.0):
+            for ti, ts in enumerate(tslos):
+                for s in range(4):
+                    cfgs.append(api.DecodeCtlConfig(tslo_ms=ts, step_mhz=st,
+                                                    max_step_mhz=max(30.0, st),
+                                                    hysteresis_count=h))
+                    table_of.append(ti)
+                    stream_of.append(s)
+                    worker.append(s)
+    lo, hi, fo, fe = eng.build_band_tables([gp], [0] * 3, [t * 0.95 for t in tslos], [4] * 3,
+                                           [64] * 3, LEVELS)
+    has, p95, tps = eng.window_series(tel, 256, 20.0, 200.0, t_end)
+    cap = 2048
+    out = eng.decode_replay(cfgs, table_of, stream_of, worker, lo, hi, fo, gp.grid, has, p95, tps,
+                            t_end, rec_cap=cap)
+    torch.cuda.synchronize()
+    lo_h, hi_h, fo_h = (x.cpu().numpy() for x in (lo, hi, fo))
+    nrec = out["n_rec"].cpu().numpy()
+    dig = out["digest"].cpu().numpy().view(np.uint64)
+    recs = out["records"].cpu().numpy()
+    for n, c in enumerate(cfgs):
+        oc = default_ctl_cfg(tslo_ms=c.tslo_ms, step_mhz=c.step_mhz, max_step_mhz=c.max_step_mhz,
+                             hysteresis_count=c.hysteresis_count)
+        tb = band_table(lo_h[table_of[n]], hi_h[table_of[n]], fo_h[table_of[n]])
+        want = restate.replay_telemetry(oc, tb, 210.0, 1410.0, worker[n],
+                                        _stream_arrays(tel, stream_of[n]), t_end)
+        assert nrec[n] == len(want)
+        assert dig[n] == restate.digest(want)
+        got = recs[n, :min(cap, len(want))].reshape(-1).view(want.dtype)
+        assert (got == want[:cap]).all(), n
+
+
+def test_decode_replay_reproduces_reference_closed_loop_run(eng, ref, prof):
+    """The reference simulator's own controllers (greenllm, sinusoid decode load): their
+    captured per-tick inputs replayed on the GPU give the reference's decision log."""
+    api = _api()
+    a, p, o = ref.gen_sinusoid_decode_trace(1500.0, 1000.0, 120000.0, 150000, 11)
+    r = ref.run_capture(a, p, o, prof, "greenllm")
+    gp = api.GpuProfile.default_profile()
+    cfg = api.DecodeCtlConfig()
+    lo, hi, fo, fe = eng.build_band_tables([gp], [0], [cfg.tslo_ms * cfg.margin_decode], [4], [64],
+                                           LEVELS)
+    t_end = float(r["fine_t"][-1])
+    nf = eng.lib.gsb_n_ticks(20.0, t_end)
+    nc = eng.lib.gsb_n_ticks(200.0, t_end)
+    has = np.zeros((4, nf), np.uint8)
+    p95 = np.zeros((4, nf))
+    tps = np.zeros((4, nc))
+    for w in range(4):
+        m, mc = r["fine_worker"] == w, r["coarse_worker"] == w
+        has[w], p95[w], tps[w] = r["fine_has"][m], r["fine_p95"][m], r["coarse_tps"][mc]
+    dev = lambda x, dt: torch.as_tensor(x, device="cuda").to(dt)
+    out = eng.decode_replay([cfg] * 4, [0] * 4, range(4), range(4), lo, hi, fo, gp.grid,
+                            dev(has, torch.uint8), dev(p95, torch.float64),
+                            dev(tps, torch.float64), t_end, rec_cap=12_000)
+    torch.cuda.synchronize()
+    dec = r["decisions"]
+    recs = out["records"].cpu().numpy()
+    for w in range(4):
+        want = dec[dec["worker"] == w]
+        n = int(out["n_rec"][w].item())
+        assert n == len(want)
+        got = recs[w, :n].reshape(-1).view(want.dtype)
+        assert (got == want).all()
+
+
+def test_summary_is_deterministic_and_exact_counts(eng, restate):
+    api = _api()
+    eng.set_profiles([api.GpuProfile.default_profile()])
+    a, p, _ = restate.gen_poisson_trace(5.0, 7_200_000, seed=3)
+    rr = eng.route_bin(a, p, api.RoutingConfig(True, [512, 1024], [0, 1, 2]), 60_000)
+    sel = eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=0.95 * 60_000)
+    s1 = eng.prefill_summary(sel, 3)
+    s2 = eng.prefill_summary(sel, 3)
+    assert s1.tobytes() == s2.tobytes()
+    fi = sel.f_idx.cpu().numpy()[0].reshape(-1, 3)
+    en = sel.energy_j.cpu().numpy()[0].reshape(-1, 3)
+    for c in range(3):
+        assert s1[0, c]["n_empty"] == (fi[:, c] == -2).sum()
+        assert s1[0, c]["n_infeasible"] == (fi[:, c] == -1).sum()
+        e = en[fi[:, c] >= 0, c]
+        assert abs(s1[0, c]["sum_energy_j"] - e.sum()) <= 1e-9 * abs(e.sum())
+        assert s1[0, c]["min_energy_j"] == e.min()
