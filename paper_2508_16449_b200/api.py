@@ -429,12 +429,19 @@ class Engine:
             raise _ERRORS.get(rc, RuntimeError)(msg)
 
     def stream(self) -> int:
-        return torch.cuda.current_stream(self.device).cuda_stream
+        """The caller's current torch stream as a cudaStream_t. torch's legacy default stream
+        has handle 0, which the C ABI reads as "the context's own stream"; pass
+        cudaStreamLegacy (1) instead so the kernels stay ordered after torch's copies."""
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        return s if s else 1
 
     def _dev(self, a, dtype) -> torch.Tensor:
         if isinstance(a, torch.Tensor):
             return a.to(self.device, dtype).contiguous()
-        return torch.as_tensor(np.ascontiguousarray(a), device=self.device).to(dtype).contiguous()
+        a = np.ascontiguousarray(a)
+        if not a.flags.writeable:
+            a = a.copy()
+        return torch.as_tensor(a, device=self.device).to(dtype).contiguous()
 
     def _empty(self, shape, dtype) -> torch.Tensor:
         return torch.empty(shape, dtype=dtype, device=self.device)
@@ -689,11 +696,14 @@ class Engine:
         dp = self._dev(parr, torch.uint8)
         outs = [self._empty((T, len(lv)), torch.float64) for _ in range(3)]
         feas = self._empty((T, len(lv)), torch.uint8)
+        # inputs must stay referenced until the launch is enqueued: a freed temporary's
+        # block can be handed to the next _dev() copy before the kernel reads it
+        ins = [self._dev(profile_of, torch.int32), self._dev(t_slo_ms, torch.float64),
+               self._dev(wk, torch.int32), self._dev(mb, torch.int32),
+               self._dev(lv, torch.float64)]
         self._check(self.lib.gsb_build_band_tables(
-            self.ctx, T, _ptr(dp), _ptr(self._dev(profile_of, torch.int32)),
-            _ptr(self._dev(t_slo_ms, torch.float64)), _ptr(self._dev(wk, torch.int32)),
-            _ptr(self._dev(mb, torch.int32)), len(lv), _ptr(self._dev(lv, torch.float64)),
-            *[_ptr(o) for o in outs], _ptr(feas), self.stream()))
+            self.ctx, T, _ptr(dp), _ptr(ins[0]), _ptr(ins[1]), _ptr(ins[2]), _ptr(ins[3]),
+            len(lv), _ptr(ins[4]), *[_ptr(o) for o in outs], _ptr(feas), self.stream()))
         torch.cuda.current_stream(self.device).synchronize()
         return (*outs, feas)
 

@@ -178,6 +178,10 @@ __device__ __forceinline__ int argmin_clock(const double* s_f, const double* s_r
     const double idle = gsb::div_pre_fast(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0, gsb::kRcp1000);
     const double e = __dadd_rn(active, idle);
     const bool take = (busy <= W) && (best < 0 || e < be);
+#ifdef GSB_DEBUG_ARGMIN
+    printf("i=%d f=%.1f busy=%a act=%a idle=%a e=%a be=%a take=%d\n", i, f, busy, active, idle, e,
+           be, (int)take);
+#endif
     best = take ? i : best;
     be = take ? e : be;
   }
