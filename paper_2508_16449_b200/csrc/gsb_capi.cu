@@ -163,6 +163,7 @@ void gsb_ctx_destroy(gsb_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_tabs);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_ticks);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -1,6 +1,5 @@
 // gsb_decode.cu — decode dual-loop controller path.
-//   K3a k_window_series  : TbtWindow P95 per fine tick + TpsWindow rate per coarse tick,
-//                          one warp per telemetry stream (sorted window kept in registers)
+//   (K3a, the window statistics, lives in gsb_window.cu)
 //   K4  k_band_tables    : build_band_table for many (profile, t_slo, workers, batch) tuples
 //   K3b k_decode_replay  : DecodeController state machine, one lane per trajectory,
 //                          sequential in time, parallel across scenarios
@@ -16,134 +15,6 @@ using gsb::std_max;
 using gsb::std_min;
 
 namespace {
-
-constexpr int kSlots = GSB_MAX_TBT_WINDOW / 32;  // sorted-window slots per lane
-
-// ---------------------------------------------------------------- K3a: window series
-// Lane l holds sorted positions [l*kSlots, (l+1)*kSlots) of the current TBT window padded with
-// +inf; insert/remove are warp-wide shifts, the P95 read is one shuffle. The ring itself (for
-// FIFO eviction, decode_ctl.cpp:120-123) lives in shared memory.
-struct SeriesParams {
-  int64_t n_streams;
-  const int64_t* ev_off;
-  const double* t_ms;
-  const int32_t* tokens;
-  const int64_t* gap_off;
-  const double* gaps;
-  int cap;
-  double fine, coarse, t_end;
-  int64_t n_fine, n_coarse;
-  uint8_t* fine_has;
-  double* fine_p95;
-  double* coarse_tps;
-};
-
-__device__ __forceinline__ int warp_count_less(const double (&srt)[kSlots], double v) {
-  int c = 0;
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) c += srt[j] < v ? 1 : 0;
-  return __reduce_add_sync(0xffffffffu, c);
-}
-
-// remove the element at sorted position q (shift left, +inf enters at the end)
-__device__ __forceinline__ void warp_remove_at(double (&srt)[kSlots], int q, int lane) {
-  const double next_first = __shfl_down_sync(0xffffffffu, srt[0], 1);
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) {
-    const int idx = lane * kSlots + j;
-    const double nxt = (j + 1 < kSlots) ? srt[(j + 1) % kSlots] : (lane == 31 ? INFINITY : next_first);
-    if (idx >= q) srt[j] = nxt;
-  }
-}
-
-// insert v at sorted position q (shift right; the last slot falls off)
-__device__ __forceinline__ void warp_insert_at(double (&srt)[kSlots], int q, double v, int lane) {
-  const double prev_last = __shfl_up_sync(0xffffffffu, srt[kSlots - 1], 1);
-  double out[kSlots];
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) {
-    const int idx = lane * kSlots + j;
-    const double prv = j > 0 ? srt[j - 1] : prev_last;
-    out[j] = idx > q ? prv : (idx == q ? v : srt[j]);
-  }
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) srt[j] = out[j];
-}
-
-__device__ __forceinline__ double warp_get(const double (&srt)[kSlots], int pos) {
-  const int owner = pos / kSlots, slot = pos - owner * kSlots;
-  double v = srt[0];
-#pragma unroll
-  for (int j = 1; j < kSlots; ++j) v = slot == j ? srt[j] : v;
-  return __shfl_sync(0xffffffffu, v, owner);
-}
-
-__global__ void __launch_bounds__(128) k_window_series(const __grid_constant__ SeriesParams a) {
-  __shared__ double s_ring[4][GSB_MAX_TBT_WINDOW];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * 4 + wib;
-  if (s >= a.n_streams) return;
-  double* ring = s_ring[wib];
-  double srt[kSlots];
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) srt[j] = INFINITY;
-  int n = 0, head = 0;
-  const int cap = a.cap;
-  const int64_t e0 = a.ev_off[s], e1 = a.ev_off[s + 1];
-  int64_t j = e0, live = e0;
-  int tokens = 0;  // TpsWindow's int sum over live events (decode_ctl.cpp:115-116)
-  double tf = a.fine, tc = a.coarse;
-  int64_t kf = 0, kc = 0;
-  for (;;) {
-    const double t = std_min(tf, tc);
-    if (t > a.t_end) break;
-    // step-end telemetry at <= t is recorded before the tick (simkernel.cpp:21-31,44-50)
-    while (j < e1 && a.t_ms[j] <= t) {
-      for (int64_t g = a.gap_off[j]; g < a.gap_off[j + 1]; ++g) {
-        const double x = a.gaps[g];
-        // TbtWindow::record: push_back, then pop_front while over capacity
-        if (n == cap) {
-          const double old = ring[head];
-          warp_remove_at(srt, warp_count_less(srt, old), lane);
-          __syncwarp();
-          if (lane == 0) ring[head] = x;
-          head = head + 1 == cap ? 0 : head + 1;
-        } else {
-          if (lane == 0) ring[(head + n) % cap] = x;
-          ++n;
-        }
-        __syncwarp();
-        warp_insert_at(srt, warp_count_less(srt, x), x, lane);
-      }
-      tokens += a.tokens[j];
-      ++j;
-    }
-    if (tc == t) {
-      // TpsWindow::tps: drop events with t < now - window (front pops), tokens*1000/window
-      while (live < j && a.t_ms[live] < t - a.coarse) {
-        tokens -= a.tokens[live];
-        ++live;
-      }
-      if (lane == 0) a.coarse_tps[s * a.n_coarse + kc] = tokens * 1000.0 / a.coarse;
-      ++kc;
-      tc = t + a.coarse;
-    }
-    if (tf == t) {
-      // TbtWindow::p95 -> quantile(q = 0.95): sorted[ceil(0.95 n) - 1] (metrics.cpp:16-18)
-      double p95 = 0.0;
-      if (n > 0) {
-        const int rank = static_cast<int>(ceil(0.95 * static_cast<double>(n)));
-        p95 = warp_get(srt, rank == 0 ? 0 : rank - 1);
-      }
-      if (lane == 0) {
-        a.fine_has[s * a.n_fine + kf] = n > 0 ? 1 : 0;
-        a.fine_p95[s * a.n_fine + kf] = p95;
-      }
-      ++kf;
-      tf = t + a.fine;
-    }
-  }
-}
 
 // ---------------------------------------------------------------- K4: band tables
 struct BandParams {
@@ -404,35 +275,6 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
 }  // namespace
 
 extern "C" {
-
-int gsb_window_series(gsb_ctx* ctx, const gsb_telemetry* tel, int tbt_capacity,
-                      double fine_period_ms, double coarse_period_ms, double t_end_ms,
-                      uint8_t* d_fine_has, double* d_fine_p95, double* d_coarse_tps, void* stream) {
-  if (!ctx || !tel) return GSB_INVALID_ARGUMENT;
-  if (tbt_capacity < 1 || tbt_capacity > GSB_MAX_TBT_WINDOW)
-    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode ctl: tbt window must hold 1..256 samples");
-  if (fine_period_ms <= 0 || coarse_period_ms <= 0)
-    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode ctl: periods must be > 0");
-  if (tel->n_streams <= 0) return GSB_OK;
-  SeriesParams sp{};
-  sp.n_streams = tel->n_streams;
-  sp.ev_off = tel->d_ev_off;
-  sp.t_ms = tel->d_t_ms;
-  sp.tokens = tel->d_tokens;
-  sp.gap_off = tel->d_gap_off;
-  sp.gaps = tel->d_gaps;
-  sp.cap = tbt_capacity;
-  sp.fine = fine_period_ms;
-  sp.coarse = coarse_period_ms;
-  sp.t_end = t_end_ms;
-  sp.n_fine = gsb_n_ticks(fine_period_ms, t_end_ms);
-  sp.n_coarse = gsb_n_ticks(coarse_period_ms, t_end_ms);
-  sp.fine_has = d_fine_has;
-  sp.fine_p95 = d_fine_p95;
-  sp.coarse_tps = d_coarse_tps;
-  k_window_series<<<static_cast<unsigned>((tel->n_streams + 3) / 4), 128, 0, gsb_pick_stream(ctx, stream)>>>(sp);
-  return gsb_check_launch(ctx, "window_series");
-}
 
 int gsb_build_band_tables(gsb_ctx* ctx, int64_t n_tables, const gsb_profile* d_profiles,
                           const int32_t* d_profile_of, const double* d_t_slo_ms,
