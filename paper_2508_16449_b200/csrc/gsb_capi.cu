@@ -1,5 +1,6 @@
 // gsb_capi.cu — context management, host-side validation (the reference's typed-exception
 // rules mapped to status codes) and profile table construction for libgsb.so.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -256,13 +257,20 @@ int gsb_set_profiles(gsb_ctx* ctx, int n, const gsb_profile* profiles) {
     t.k2 = pr.k2;
     t.k1 = pr.k1;
     t.k0 = pr.k0;
+    t.all_fast = 1;
+    t.P_min = INFINITY;
+    t.P_max = -INFINITY;
     for (int i = 0; i < t.G; ++i) {
       const double f = grid_at(pr, static_cast<size_t>(i));
       t.f[i] = f;
       t.P[i] = power_at(pr, f);
       t.rcp_f[i] = gsb::short_divisor(f) ? 1.0 / f : 0.0;
+      t.all_fast &= t.rcp_f[i] != 0.0 ? 1 : 0;
+      t.P_min = std::min(t.P_min, t.P[i]);
+      t.P_max = std::max(t.P_max, t.P[i]);
     }
     ctx->profiles[p] = pr;
+    ctx->h_tabs[p] = t;
   }
   ctx->n_profiles = n;
   cudaSetDevice(ctx->device);

@@ -23,9 +23,6 @@ struct U32ToI64 {
   __host__ __device__ int64_t operator()(uint32_t x) const { return static_cast<int64_t>(x); }
 };
 
-constexpr int kRouteThreads = 256;
-constexpr int kRouteChunk = 1024;  // requests staged in shared memory per round
-
 struct RouteParams {
   int32_t n_thr;
   int32_t thr[GSB_MAX_CLASSES - 1];
@@ -38,103 +35,164 @@ struct RouteParams {
 };
 
 // ---------------------------------------------------------------- K1a: window bounds
+// floor(a / d) for a >= 0, d > 0 without a 64-bit integer divide: a double estimate, then an
+// exact integer correction (the estimate is off by at most one for a < 2^62).
+__device__ __forceinline__ int64_t div_floor(int64_t a, int64_t d, double rd) {
+  int64_t q = static_cast<int64_t>(static_cast<double>(a) * rd);
+  if (q * d > a) --q;
+  if ((q + 1) * d <= a) ++q;
+  return q;
+}
+
+// bounds[k] = #requests whose window index (arrival / W - w0) is < k, k = 0..n_windows, i.e. the
+// first request of window k (arrivals are non-decreasing, trace.cpp:109-111). Request i owns
+// the entries k in (w(i-1), w(i)] (request 0 covers k <= w(0), a virtual request n the tail),
+// so every entry is written exactly once. A thread takes a tile of 8 requests: with sorted
+// arrivals the tile only needs per-request work when its first and last windows differ.
+constexpr int kBoundsTile = 8;
+
 __global__ void k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms,
                                 int64_t w0, int64_t n_windows, int64_t* __restrict__ bounds) {
-  const int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (k > n_windows) return;
-  const int64_t key = (w0 + k) * window_ms;
-  int64_t lo = 0, hi = n;  // first index with arrival >= key
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (__ldg(arrival + mid) < key)
-      lo = mid + 1;
-    else
-      hi = mid;
+  const double rd = 1.0 / static_cast<double>(window_ms);
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t i0 = t * kBoundsTile;
+  if (i0 > n) return;
+  const int64_t i1 = min(i0 + kBoundsTile, n + 1);  // requests [i0, i1) incl. the virtual n
+  auto win = [&](int64_t i) -> int64_t {
+    if (i < 0) return -1;
+    if (i >= n) return n_windows;
+    return div_floor(__ldg(arrival + i), window_ms, rd) - w0;
+  };
+  int64_t wp = win(i0 - 1);
+  const int64_t wlast = win(i1 - 1);
+  if (wlast == wp) return;  // no window edge inside this tile
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t wi = win(i);
+    const int64_t lo = max(wp + 1, int64_t{0});
+    const int64_t hi = min(wi, n_windows);
+    for (int64_t k = lo; k <= hi; ++k) bounds[k] = i;
+    wp = wi;
   }
-  bounds[k] = lo;
 }
 
 // classify(), router.cpp:26-31: number of thresholds strictly below the prompt.
 __device__ __forceinline__ int classify_dev(const RouteParams& rp, int32_t L) {
   int c = 0;
 #pragma unroll
-  for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) c += (k < rp.n_thr && rp.thr[k] < L) ? 1 : 0;
+  for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) c += rp.thr[k] < L ? 1 : 0;  // unused = INT_MAX
   return c;
 }
 
 // ---------------------------------------------------------------- K1b: route + bin
-// One CTA owns WPB = 256 / C consecutive windows; thread t owns cell (window t / C, class t % C).
-// The CTA streams its request range through shared memory in 1 KiB chunks: a coalesced,
-// lane-parallel pass classifies each request once and computes its per-profile reference
-// latency term once; then every cell thread folds its window's slice in arrival order into
-// its own fp64 chain (registers), so each chain sees exactly the reference's summation order.
-template <int P>
-__global__ void __launch_bounds__(kRouteThreads)
+// One warp owns G = min(8, 32 / C) consecutive windows; lane (g, c) owns the fp64 chains of cell
+// (window g, class c) for all P profiles. The warp walks its windows in rounds of 32 requests:
+//   1. lane-parallel (coalesced, each request once): load prompt (+ arrival), classify()
+//      (router.cpp:26-31), per-profile reference latency terms, prefill deadline
+//      (simkernel.cpp:499-501) -> a per-warp shared-memory table; one ballot per class gives
+//      each owner the set of this round's rows in its class;
+//   2. fold: every owner visits its class's rows IN ARRIVAL ORDER (ascending lane bit) and
+//      adds them to its P chains, so each chain is exactly the reference's left-to-right sum
+//      (prefill_opt.cpp:9-14).
+constexpr int kWarpsPerBlock = 4;
+
+template <int C, int P, bool DEADLINE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
 k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
             const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
             uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
             double* __restrict__ t_ref, double* __restrict__ min_deadline) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* s_term = reinterpret_cast<double*>(smem);            // [P][chunk]
-  double* s_dl = s_term + P * kRouteChunk;                      // [chunk] (deadline mode)
-  uint8_t* s_cls = reinterpret_cast<uint8_t*>(s_dl + kRouteChunk);
-
-  const int C = rp.C;
-  const int WPB = kRouteThreads / C;
-  const int t = threadIdx.x;
-  const int64_t wb = static_cast<int64_t>(blockIdx.x) * WPB;
-  const int wl = t / C, c = t - (t / C) * C;
-  const int64_t w = wb + wl;
-  const bool owner = wl < WPB && w < rp.n_windows;
-  const int64_t wend = min(wb + WPB, rp.n_windows);
-  const int64_t rs = bounds[wb], re = bounds[wend];
-  const int64_t my_s = owner ? bounds[w] : 0, my_e = owner ? bounds[w + 1] : 0;
-
+  constexpr int G = (32 / C) < 8 ? (32 / C) : 8;  // windows per warp
+  __shared__ double s_term[kWarpsPerBlock][G][32][P];
+  __shared__ double s_dl[kWarpsPerBlock][DEADLINE ? G : 1][32];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w_first = (static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib) * G;
+  if (w_first >= rp.n_windows) return;
+  // this lane's owner role
+  const int og = lane / C, oc = lane % C;
+  const bool owner = lane < G * C && w_first + og < rp.n_windows;
+  // window extents (lane g < G reads window g's bounds; broadcast below)
+  int64_t ws[G], we[G];
+  int64_t rounds = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int64_t w = w_first + g;
+    ws[g] = w < rp.n_windows ? bounds[w] : 0;
+    we[g] = w < rp.n_windows ? bounds[w + 1] : 0;
+    const int64_t r = (we[g] - ws[g] + 31) >> 5;
+    rounds = r > rounds ? r : rounds;
+  }
   double acc[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) acc[p] = 0.0;
-  uint32_t cnt = 0;
   double mdl = INFINITY;
-
-  for (int64_t cs = rs; cs < re; cs += kRouteChunk) {
-    const int64_t ce = min(cs + kRouteChunk, re);
-    for (int64_t i = cs + t; i < ce; i += kRouteThreads) {
-      const int32_t L = prompt[i];
-      const int cl = C > 1 ? classify_dev(rp, L) : 0;
-      cls_out[i] = static_cast<uint8_t>(cl);
-      const int k = static_cast<int>(i - cs);
-      s_cls[k] = static_cast<uint8_t>(cl);
-      const double Ld = static_cast<double>(L);
+  uint32_t cnt = 0;
+  // software pipeline: the prompts (and arrivals) of round r+1 are in flight while round r is
+  // classified and folded, so HBM latency overlaps the fold instead of stalling classify()
+  int32_t Lnext[G];
+  int64_t Anext[DEADLINE ? G : 1];
 #pragma unroll
-      for (int p = 0; p < P; ++p) s_term[p * kRouteChunk + k] = (rp.lat_a[p] * Ld + rp.lat_b[p]) * Ld + rp.lat_c[p];
-      if (rp.want_deadline) {
-        // (arrival + TTFT(SM/L)) - first_token_allowance, simkernel.cpp:499-501
-        const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
-        s_dl[k] = static_cast<double>(arrival[i]) + ttft - rp.allowance;
-      }
+  for (int g = 0; g < G; ++g) {
+    const int64_t i = ws[g] + lane;
+    Lnext[g] = i < we[g] ? __ldg(prompt + i) : 0;
+    if (DEADLINE) Anext[g] = i < we[g] ? __ldg(arrival + i) : 0;
+  }
+  for (int64_t r = 0; r < rounds; ++r) {
+    int32_t Lcur[G];
+    int64_t Acur[DEADLINE ? G : 1];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      Lcur[g] = Lnext[g];
+      if (DEADLINE) Acur[g] = Anext[g];
+      const int64_t i = ws[g] + ((r + 1) << 5) + lane;
+      const bool in = r + 1 < rounds && i < we[g];
+      Lnext[g] = in ? __ldg(prompt + i) : 0;
+      if (DEADLINE) Anext[g] = in ? __ldg(arrival + i) : 0;
     }
-    __syncthreads();
-    if (owner) {
-      const int64_t a0 = max(my_s, cs), a1 = min(my_e, ce);
-      for (int64_t i = a0; i < a1; ++i) {
-        const int k = static_cast<int>(i - cs);
-        if (s_cls[k] == c) {
+    // phase 1: lane-parallel per request; class membership becomes per-class ballot masks
+    unsigned my_mask = 0;
 #pragma unroll
-          for (int p = 0; p < P; ++p) acc[p] = acc[p] + 1.0 * s_term[p * kRouteChunk + k];
-          ++cnt;
-          if (rp.want_deadline) mdl = std_min(mdl, s_dl[k]);
+    for (int g = 0; g < G; ++g) {
+      const int64_t i = ws[g] + (r << 5) + lane;
+      int cl = -1;
+      if (i < we[g]) {
+        const int32_t L = Lcur[g];
+        cl = C > 1 ? classify_dev(rp, L) : 0;
+        cls_out[i] = static_cast<uint8_t>(cl);
+        const double Ld = static_cast<double>(L);
+#pragma unroll
+        for (int p = 0; p < P; ++p) s_term[wib][g][lane][p] = (rp.lat_a[p] * Ld + rp.lat_b[p]) * Ld + rp.lat_c[p];
+        if (DEADLINE) {
+          const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
+          s_dl[wib][g][lane] = static_cast<double>(Acur[g]) + ttft - rp.allowance;
         }
       }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const unsigned m = __ballot_sync(0xffffffffu, cl == c);
+        my_mask = (og == g && oc == c) ? m : my_mask;
+      }
     }
-    __syncthreads();
+    __syncwarp();
+    // phase 2: ordered fold: the owner visits its class's rows in ascending arrival order
+    if (owner) {
+      cnt += __popc(my_mask);
+      while (my_mask) {
+        const int j = __ffs(static_cast<int>(my_mask)) - 1;
+        my_mask &= my_mask - 1;
+#pragma unroll
+        for (int p = 0; p < P; ++p) acc[p] = acc[p] + 1.0 * s_term[wib][og][j][p];
+        if (DEADLINE) mdl = std_min(mdl, s_dl[wib][og][j]);
+      }
+    }
+    __syncwarp();
   }
   if (owner) {
     const int64_t cells = rp.n_windows * C;
-    const int64_t cell = w * C + c;
-    count[cell] = cnt;
+    const int64_t cell = (w_first + og) * C + oc;
 #pragma unroll
     for (int p = 0; p < P; ++p) t_ref[p * cells + cell] = acc[p];
-    if (rp.want_deadline && min_deadline) min_deadline[cell] = mdl;
+    count[cell] = cnt;
+    if (DEADLINE && min_deadline) min_deadline[cell] = mdl;
   }
 }
 
@@ -189,14 +247,137 @@ __device__ __forceinline__ int argmin_clock(const double* s_f, const double* s_r
   return best;
 }
 
+// W of a cell per the window mode (prefill_opt.cpp:63-67 for DEADLINE_SLACK):
+// min_j(deadline_j - now) == min_deadline - now because subtraction is monotone.
+__device__ __forceinline__ double cell_window(const SelectParams& sp, int64_t cell,
+                                              const double* __restrict__ min_deadline,
+                                              const double* __restrict__ window) {
+  if (sp.mode == GSB_FIXED_WINDOW) return sp.fixed_window;
+  if (sp.mode == GSB_DEADLINE_SLACK) {
+    const double now = static_cast<double>((sp.w0 + cell / sp.C) * sp.window_ms);
+    return std_max(sp.margin * (min_deadline[cell] - now), sp.min_budget);
+  }
+  return window[cell];
+}
+
+// Specialisation for a G-clock grid whose every clock is a short divisor: the clock tables are
+// KERNEL PARAMETERS (constant-bank operands of the DFMA/DMUL themselves, no shared-memory loads)
+// and the clock loop is fully unrolled: 15 DP-pipe instructions per (cell, clock), nothing else
+// but two selects. The three division range guards of div_pre are hoisted to ONE per-cell test:
+// with 1 <= f_i <= 4096 and TF = T*f_ref,
+//   busy_i   = TF / f_i                 dividend TF
+//   active_i = (P_i*busy_i) / 1000      dividend in [TF*P_min/4096*(1-u), TF*P_max]
+//   idle_i   = (p_idle*(W-busy_i))/1000 dividend 0, or |.| in
+//              [p_idle*min(W, TF/4096)*2^-53*(1-u), p_idle*max(W, TF)]
+// (W - busy is a multiple of 2^(e-52), e the smaller exponent, hence >= min * 2^-53 unless 0;
+// a zero dividend is exact on the fast path too). All of these inside [2^-900, 2^1000] keeps
+// every dividend in div_pre's fast range [2^-959, 2^1023]; otherwise the cell takes IEEE '/'.
+template <int G>
+struct ClockConst {
+  double f[G], r[G], P[G];
+};
+
+__device__ __forceinline__ bool cell_fast(double TF, double W, double p_idle, double P_min,
+                                          double P_max) {
+  const double lo = 0x1p-900, hi = 0x1p+1000;
+  const double x_lo = TF * P_min * 0x1p-12, x_hi = TF * P_max;
+  const double y_lo = p_idle * fmin(W, TF * 0x1p-12) * 0x1p-53, y_hi = p_idle * fmax(W, TF);
+  return TF >= lo && TF <= hi && W >= lo && W <= hi && x_lo >= lo && x_hi <= hi && y_lo >= lo &&
+         y_hi <= hi;
+}
+
+template <int G>
+struct ClockSet {  // every profile of the pass, one kernel-parameter block (<= 32 KB)
+  ClockConst<G> c[GSB_MAX_PROFILES];
+  double f_ref[GSB_MAX_PROFILES], p_idle[GSB_MAX_PROFILES];
+  double P_min[GSB_MAX_PROFILES], P_max[GSB_MAX_PROFILES];
+};
+
+template <int G, int PI>
+__device__ __forceinline__ void select_cells_c(const SelectParams& sp, const ClockSet<G>& cs,
+                                               const double* __restrict__ t_ref,
+                                               const uint32_t* __restrict__ count,
+                                               const double* __restrict__ min_deadline,
+                                               double* __restrict__ window,
+                                               int16_t* __restrict__ f_idx,
+                                               double* __restrict__ energy) {
+  const ClockConst<G>& cc = cs.c[PI];
+  const int p = PI;
+  const double f_ref = cs.f_ref[PI], p_idle = cs.p_idle[PI], P_min = cs.P_min[PI],
+               P_max = cs.P_max[PI];
+  const int64_t n = sp.n_cells;
+  for (int64_t cell = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; cell < n;
+       cell += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t o = p * n + cell;
+    if (count && count[cell] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
+      f_idx[o] = -2;
+      energy[o] = 0.0;
+      continue;
+    }
+    const double W = cell_window(sp, cell, min_deadline, window);
+    if (p == 0 && window && sp.mode != GSB_PER_CELL_WINDOW) window[cell] = W;
+    const double TF = t_ref[o] * f_ref;
+    int best = -1;
+    double be = 0.0;
+    if (cell_fast(TF, W, p_idle, P_min, P_max)) {
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        const double f = cc.f[i], r = cc.r[i];
+        double q = __dmul_rn(TF, r);
+        double e = __fma_rn(-f, q, TF);
+        const double busy = __fma_rn(r, e, q);
+        const double x = __dmul_rn(cc.P[i], busy);
+        q = __dmul_rn(x, gsb::kRcp1000);
+        e = __fma_rn(-1000.0, q, x);
+        const double active = __fma_rn(gsb::kRcp1000, e, q);
+        const double y = __dmul_rn(p_idle, __dsub_rn(W, busy));
+        q = __dmul_rn(y, gsb::kRcp1000);
+        e = __fma_rn(-1000.0, q, y);
+        const double idle = __fma_rn(gsb::kRcp1000, e, q);
+        const double E = __dadd_rn(active, idle);
+        const bool take = (busy <= W) && (best < 0 || E < be);
+        best = take ? i : best;
+        be = take ? E : be;
+      }
+    } else {
+      for (int i = 0; i < G; ++i) {
+        const double busy = __ddiv_rn(TF, cc.f[i]);
+        const double active = __ddiv_rn(__dmul_rn(cc.P[i], busy), 1000.0);
+        const double idle = __ddiv_rn(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0);
+        const double E = __dadd_rn(active, idle);
+        const bool take = (busy <= W) && (best < 0 || E < be);
+        best = take ? i : best;
+        be = take ? E : be;
+      }
+    }
+    f_idx[o] = static_cast<int16_t>(best);
+    energy[o] = best >= 0 ? be : 0.0;
+  }
+}
+
+// blockIdx.y = profile; the switch picks an instantiation whose table offsets are constants
+template <int G>
+__global__ void __launch_bounds__(256)
+k_prefill_select_c(const __grid_constant__ SelectParams sp, const __grid_constant__ ClockSet<G> cs,
+                   const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
+                   const double* __restrict__ min_deadline, double* __restrict__ window,
+                   int16_t* __restrict__ f_idx, double* __restrict__ energy) {
+  switch (blockIdx.y) {
+    case 0: select_cells_c<G, 0>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
+    case 1: select_cells_c<G, 1>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
+    case 2: select_cells_c<G, 2>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
+    default: select_cells_c<G, 3>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
+  }
+}
+
 __global__ void __launch_bounds__(256)
 k_prefill_select(const __grid_constant__ SelectParams sp, const ProfTab* __restrict__ tabs,
-                 const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
+                 int p_base, const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
                  const double* __restrict__ min_deadline, double* __restrict__ window,
                  int16_t* __restrict__ f_idx, double* __restrict__ energy) {
   __shared__ double s_f[GSB_MAX_GRID], s_r[GSB_MAX_GRID], s_P[GSB_MAX_GRID];
   __shared__ int s_fast;
-  const int p = blockIdx.y;
+  const int p = p_base + static_cast<int>(blockIdx.y);
   const ProfTab* tab = tabs + p;
   const int G = tab->G;
   for (int i = threadIdx.x; i < G; i += blockDim.x) {
@@ -337,70 +518,88 @@ __global__ void k_energy_batches(const ProfTab* __restrict__ tab, int64_t n_batc
 }
 
 // ---------------------------------------------------------------- per-class summary
-// One CTA per (profile, class): each thread folds cells w = t, t+256, ... sequentially, then a
-// fixed-shape shared-memory tree combines them -> bitwise identical on every run/rank.
+// Two fixed-shape levels => bitwise identical on every run and every rank:
+//   partial: block (pc, chunk) folds windows [chunk*kSumChunk, ...) of (profile, class) pc:
+//            thread t takes windows t, t+256, ... sequentially, then a shared-memory tree;
+//   final:   one block per pc combines the chunk partials with the same tree.
+constexpr int kSumChunk = 512;
+
+struct Part {
+  double sum, mn;
+  long long cmd, inf, emp, arg;
+};
+
+__device__ __forceinline__ void part_combine(Part& x, const Part& y) {
+  x.sum = x.sum + y.sum;
+  x.cmd += y.cmd;
+  x.inf += y.inf;
+  x.emp += y.emp;
+  if (y.arg >= 0 && (x.arg < 0 || y.mn < x.mn || (y.mn == x.mn && y.arg < x.arg))) {
+    x.mn = y.mn;
+    x.arg = y.arg;
+  }
+}
+
+__device__ __forceinline__ Part block_tree(Part v) {
+  __shared__ Part s[256];
+  const int t = threadIdx.x;
+  s[t] = v;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (t < k) part_combine(s[t], s[t + k]);
+    __syncthreads();
+  }
+  return s[0];
+}
+
 __global__ void __launch_bounds__(256)
-k_summary(int C, int64_t n_cells, const int16_t* __restrict__ f_idx, const double* __restrict__ energy,
-          gsb_class_summary* __restrict__ out) {
-  __shared__ double s_sum[256], s_min[256];
-  __shared__ long long s_cmd[256], s_inf[256], s_emp[256], s_arg[256];
-  const int pc = blockIdx.x;
+k_summary_partial(int C, int64_t n_cells, const int16_t* __restrict__ f_idx,
+                  const double* __restrict__ energy, Part* __restrict__ parts, int n_chunks) {
+  const int pc = blockIdx.y, chunk = blockIdx.x;
   const int p = pc / C, c = pc - (pc / C) * C;
   const int64_t n_w = n_cells / C;
-  double sum = 0.0, mn = INFINITY;
-  long long cmd = 0, inf = 0, emp = 0, arg = -1;
-  for (int64_t w = threadIdx.x; w < n_w; w += blockDim.x) {
+  const int64_t w_lo = static_cast<int64_t>(chunk) * kSumChunk;
+  const int64_t w_hi = min(w_lo + kSumChunk, n_w);
+  Part v{0.0, INFINITY, 0, 0, 0, -1};
+  for (int64_t w = w_lo + threadIdx.x; w < w_hi; w += blockDim.x) {
     const int64_t cell = w * C + c;
     const int64_t o = p * n_cells + cell;
     const int fi = f_idx[o];
     if (fi == -2) {
-      ++emp;
+      ++v.emp;
       continue;
     }
-    ++cmd;
+    ++v.cmd;
     if (fi < 0) {
-      ++inf;
+      ++v.inf;
       continue;
     }
     const double e = energy[o];
-    sum = sum + e;
-    if (e < mn) {
-      mn = e;
-      arg = cell;
+    v.sum = v.sum + e;
+    if (e < v.mn) {
+      v.mn = e;
+      v.arg = cell;
     }
   }
-  const int t = threadIdx.x;
-  s_sum[t] = sum;
-  s_min[t] = mn;
-  s_cmd[t] = cmd;
-  s_inf[t] = inf;
-  s_emp[t] = emp;
-  s_arg[t] = arg;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (t < s) {
-      s_sum[t] = s_sum[t] + s_sum[t + s];
-      s_cmd[t] += s_cmd[t + s];
-      s_inf[t] += s_inf[t + s];
-      s_emp[t] += s_emp[t + s];
-      const double m2 = s_min[t + s];
-      const long long a2 = s_arg[t + s];
-      if (a2 >= 0 && (s_arg[t] < 0 || m2 < s_min[t] || (m2 == s_min[t] && a2 < s_arg[t]))) {
-        s_min[t] = m2;
-        s_arg[t] = a2;
-      }
-    }
-    __syncthreads();
-  }
-  if (t == 0) {
-    gsb_class_summary r;
-    r.n_cmd = s_cmd[0];
-    r.n_infeasible = s_inf[0];
-    r.n_empty = s_emp[0];
-    r.sum_energy_j = s_sum[0];
-    r.min_energy_j = s_min[0];
-    r.argmin_cell = s_arg[0];
-    out[pc] = r;
+  const Part r = block_tree(v);
+  if (threadIdx.x == 0) parts[static_cast<int64_t>(pc) * n_chunks + chunk] = r;
+}
+
+__global__ void __launch_bounds__(256)
+k_summary_final(const Part* __restrict__ parts, int n_chunks, gsb_class_summary* __restrict__ out) {
+  const int pc = blockIdx.x;
+  Part v{0.0, INFINITY, 0, 0, 0, -1};
+  for (int k = threadIdx.x; k < n_chunks; k += blockDim.x) part_combine(v, parts[static_cast<int64_t>(pc) * n_chunks + k]);
+  const Part r = block_tree(v);
+  if (threadIdx.x == 0) {
+    gsb_class_summary o;
+    o.n_cmd = r.cmd;
+    o.n_infeasible = r.inf;
+    o.n_empty = r.emp;
+    o.sum_energy_j = r.sum;
+    o.min_energy_j = r.mn;
+    o.argmin_cell = r.arg;
+    out[pc] = o;
   }
 }
 
@@ -466,7 +665,8 @@ __global__ void k_selftest_div(const ProfTab* __restrict__ tab, int64_t per_div,
 RouteParams make_route_params(gsb_ctx* ctx, const gsb_route_cfg* cfg) {
   RouteParams rp{};
   rp.n_thr = cfg->enabled ? cfg->n_thresholds : 0;
-  for (int i = 0; i < GSB_MAX_CLASSES - 1; ++i) rp.thr[i] = i < cfg->n_thresholds ? cfg->thresholds[i] : 0;
+  for (int i = 0; i < GSB_MAX_CLASSES - 1; ++i)
+    rp.thr[i] = i < rp.n_thr ? cfg->thresholds[i] : 2147483647;  // never below a prompt
   rp.C = cfg->enabled ? cfg->n_thresholds + 1 : 1;
   rp.slo_boundary = cfg->slo_boundary_tokens;
   rp.window_ms = cfg->window_ms;
@@ -503,9 +703,11 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   if (!ctx) return GSB_INVALID_ARGUMENT;
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
-  const int64_t n = cfg->n_windows + 1;
-  k_window_bounds<<<static_cast<unsigned>((n + 255) / 256), 256, 0, gsb_pick_stream(ctx, stream)>>>(
-      d_arrival, n_req, cfg->window_ms, cfg->w0, cfg->n_windows, d_bounds);
+  const int64_t tiles = n_req / kBoundsTile + 1;
+  const int64_t blocks = (tiles + 255) / 256;
+  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
+                    gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms, cfg->w0,
+                                                    cfg->n_windows, d_bounds);
   return gsb_check_launch(ctx, "window_bounds");
 }
 
@@ -519,23 +721,30 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const i
   (void)n_req;
   RouteParams rp = make_route_params(ctx, cfg);
   rp.want_deadline = d_min_deadline != nullptr;
-  const int WPB = kRouteThreads / rp.C;
-  const int64_t blocks = (cfg->n_windows + WPB - 1) / WPB;
-  const size_t smem = static_cast<size_t>(ctx->n_profiles + 1) * kRouteChunk * sizeof(double) + kRouteChunk;
+  const int P = ctx->n_profiles;
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  switch (ctx->n_profiles) {
-#define GSB_ROUTE_CASE(P)                                                                          \
-  case P:                                                                                          \
-    cudaFuncSetAttribute(k_route_bin<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
-                         static_cast<int>(smem));                                                   \
-    k_route_bin<P><<<static_cast<unsigned>(blocks), kRouteThreads, smem, s>>>(                     \
-        rp, d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline);             \
+  const bool dl = rp.want_deadline != 0;
+  const int G = std::min(8, 32 / rp.C);
+  const int64_t warps = (cfg->n_windows + G - 1) / G;
+  const unsigned blocks = static_cast<unsigned>((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  const int key = (rp.C - 1) * 8 + (P - 1) * 2 + (dl ? 1 : 0);
+  switch (key) {
+#define GSB_RB(CC, PP)                                                                           \
+  case ((CC)-1) * 8 + ((PP)-1) * 2:                                                             \
+    k_route_bin<CC, PP, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(                          \
+        rp, d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline);          \
+    break;                                                                                       \
+  case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                         \
+    k_route_bin<CC, PP, true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(                           \
+        rp, d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline);          \
     break;
-    GSB_ROUTE_CASE(1)
-    GSB_ROUTE_CASE(2)
-    GSB_ROUTE_CASE(3)
-    GSB_ROUTE_CASE(4)
-#undef GSB_ROUTE_CASE
+#define GSB_RB_P(CC) GSB_RB(CC, 1) GSB_RB(CC, 2) GSB_RB(CC, 3) GSB_RB(CC, 4)
+    GSB_RB_P(1) GSB_RB_P(2) GSB_RB_P(3) GSB_RB_P(4) GSB_RB_P(5) GSB_RB_P(6) GSB_RB_P(7)
+    GSB_RB(8, 1) GSB_RB(8, 2) GSB_RB(8, 3) GSB_RB(8, 4)
+#undef GSB_RB_P
+#undef GSB_RB
+    default:
+      return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "route: need 1..8 classes, 1..4 profiles");
   }
   return gsb_check_launch(ctx, "route_bin");
 }
@@ -584,11 +793,40 @@ int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
   sp.n_cells = n_cells;
   const int64_t want = (n_cells + 255) / 256;
   const unsigned gx = static_cast<unsigned>(std::min<int64_t>(want, 65535LL * 16));
-  dim3 grid(gx, static_cast<unsigned>(ctx->n_profiles));
-  k_prefill_select<<<grid, 256, 0, gsb_pick_stream(ctx, stream)>>>(
-      sp, static_cast<const ProfTab*>(ctx->d_tabs), d_t_ref, d_count, d_min_deadline, d_window,
-      d_f_idx, d_energy);
-  return gsb_check_launch(ctx, "prefill_select");
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  bool all_c = true;
+  for (int p = 0; p < ctx->n_profiles; ++p) {
+    const ProfTab& t = ctx->h_tabs[p];
+    all_c = all_c && t.G == 81 && t.all_fast && t.f_min >= 1.0 && t.f_max <= 4096.0;
+  }
+  if (all_c) {
+    ClockSet<81> cs{};  // filled per call (host), passed by value as the kernel parameter
+    for (int p = 0; p < ctx->n_profiles; ++p) {
+      const ProfTab& t = ctx->h_tabs[p];
+      for (int i = 0; i < 81; ++i) {
+        cs.c[p].f[i] = t.f[i];
+        cs.c[p].r[i] = t.rcp_f[i];
+        cs.c[p].P[i] = t.P[i];
+      }
+      cs.f_ref[p] = t.f_ref;
+      cs.p_idle[p] = t.p_idle;
+      cs.P_min[p] = t.P_min;
+      cs.P_max[p] = t.P_max;
+    }
+    k_prefill_select_c<81><<<dim3(gx, static_cast<unsigned>(ctx->n_profiles)), 256, 0, s>>>(
+        sp, cs, d_t_ref, d_count, d_min_deadline, d_window, d_f_idx, d_energy);
+    return gsb_check_launch(ctx, "prefill_select");
+  }
+  for (int p = 0; p < ctx->n_profiles; ++p) {
+    {
+      k_prefill_select<<<dim3(gx, 1), 256, 0, s>>>(sp, static_cast<const ProfTab*>(ctx->d_tabs), p,
+                                                   d_t_ref, d_count, d_min_deadline, d_window,
+                                                   d_f_idx, d_energy);
+    }
+    const int rc = gsb_check_launch(ctx, "prefill_select");
+    if (rc) return rc;
+  }
+  return GSB_OK;
 }
 
 int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int64_t n_batches,
@@ -634,8 +872,15 @@ int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_c
                         void* stream) {
   if (!ctx || n_profiles < 1 || n_classes < 1 || n_cells % n_classes)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: bad shape");
-  k_summary<<<static_cast<unsigned>(n_profiles * n_classes), 256, 0, gsb_pick_stream(ctx, stream)>>>(
-      n_classes, n_cells, d_f_idx, d_energy, d_out);
+  const int64_t n_w = n_cells / n_classes;
+  const int n_chunks = static_cast<int>(std::max<int64_t>(1, (n_w + kSumChunk - 1) / kSumChunk));
+  Part* parts = static_cast<Part*>(
+      gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(n_chunks) * n_profiles * n_classes));
+  if (!parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "summary: scratch allocation failed");
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  k_summary_partial<<<dim3(static_cast<unsigned>(n_chunks), static_cast<unsigned>(n_profiles * n_classes)),
+                      256, 0, s>>>(n_classes, n_cells, d_f_idx, d_energy, parts, n_chunks);
+  k_summary_final<<<static_cast<unsigned>(n_profiles * n_classes), 256, 0, s>>>(parts, n_chunks, d_out);
   return gsb_check_launch(ctx, "prefill_summary");
 }
 
