@@ -324,6 +324,15 @@ def run_gsb(args, rank, world, dist):
     ms_dec = max_over_ranks(statistics.mean(dec_ms))
     ms_e2e = max_over_ranks(statistics.mean(e2e_ms))
 
+    # global per-(profile, class) result: every rank's summary, combined in rank order
+    from paper_2508_16449_b200 import distributed as Dd
+    if world > 1:
+        per_rank = gathered.cpu().numpy().reshape(world, -1).view(Dd.SUMMARY_DTYPE)
+    else:
+        per_rank = summ.cpu().numpy().reshape(1, -1).view(Dd.SUMMARY_DTYPE)
+    per_rank = per_rank.reshape(world, P, W["C"])
+    glob = Dd.combine_summaries(per_rank, [r * nW * W["C"] for r in range(world)])
+
     # ---------------- parity spot check + CPU baseline (rank 0, checker only)
     cpu = None
     parity = None
@@ -375,6 +384,10 @@ def run_gsb(args, rank, world, dist):
                         "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm, "kernel_ms": k1_ms,
                         "bytes_per_request": K1_BYTES_PER_REQ},
         "fp64_peak_measured_dfma_per_s": dfma_per_s,
+        "result": {"commands": int(glob["n_cmd"].sum()),
+                   "infeasible": int(glob["n_infeasible"].sum()),
+                   "empty_cells": int(glob["n_empty"].sum()),
+                   "sum_energy_j_per_profile": [float(x) for x in glob["sum_energy_j"].sum(axis=1)]},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }

@@ -1,0 +1,116 @@
+"""N > 1 host logic on CPU: window sharding, the gloo all-gather of per-class summaries and
+the rank-order combine, checked against a single-process pass over all windows (the
+per-cell decisions come from the CPU oracle here; on the GPU they come from K1/K2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2508_16449_b200 import distributed as D
+
+THR = [512, 1024]
+WMS = 5_000
+TOTAL_W = 157
+
+
+def _summary(fi, en, C):
+    """numpy restatement of gsb_prefill_summary for one profile: [C] SUMMARY_DTYPE."""
+    out = np.zeros(C, D.SUMMARY_DTYPE)
+    fi = fi.reshape(-1, C)
+    en = en.reshape(-1, C)
+    for c in range(C):
+        f, e = fi[:, c], en[:, c]
+        out[c]["n_empty"] = (f == -2).sum()
+        out[c]["n_cmd"] = (f != -2).sum()
+        out[c]["n_infeasible"] = (f == -1).sum()
+        ok = f >= 0
+        out[c]["sum_energy_j"] = float(np.sum(e[ok]))
+        if ok.any():
+            k = int(np.argmin(np.where(ok, e, np.inf)))
+            out[c]["min_energy_j"] = e[k]
+            out[c]["argmin_cell"] = k * C + c
+        else:
+            out[c]["min_energy_j"] = np.inf
+            out[c]["argmin_cell"] = -1
+    return out
+
+
+def _decide(restate, prof, a, p, w0, n):
+    cls, cnt, tref, mdl, _ = restate.route_bin(a, p, THR, WMS, w0, n, [prof], fifo=False)
+    C = len(THR) + 1
+    fi = np.full(n * C, -2, np.int64)
+    en = np.zeros(n * C)
+    for cell in range(n * C):
+        if cnt[cell]:
+            r = restate.select_t(prof, tref[0, cell], 0.95 * WMS)
+            fi[cell], en[cell] = (-1, 0.0) if r is None else (r[0], r[2])
+    return fi, en
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    from oracle.oracle import Restatement, default_profile
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    R = Restatement()
+    prof = default_profile()
+    a, p, _ = R.gen_poisson_trace(6.0, TOTAL_W * WMS, seed=5)
+    w0, n = D.window_shard(TOTAL_W, world, rank)
+    lo, hi = D.trace_slice(a, WMS, w0, n)
+    fi, en = _decide(R, prof, a[lo:hi], p[lo:hi], w0, n)
+    s = _summary(fi, en, len(THR) + 1)
+    t = torch.from_numpy(s.view(np.uint8).reshape(len(THR) + 1, -1).copy())
+    g = D.gather_summaries(t)
+    per_rank = g.numpy().reshape(world, -1).view(D.SUMMARY_DTYPE).reshape(world, 1, -1)
+    offsets = [D.window_shard(TOTAL_W, world, r)[0] * (len(THR) + 1) for r in range(world)]
+    comb = D.combine_summaries(per_rank, offsets)
+    np.save(os.path.join(out_dir, f"comb{rank}.npy"), comb)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_window_shard_covers_everything():
+    for total in (1, 7, 100, 10_001):
+        for world in (1, 2, 3, 8):
+            got = [D.window_shard(total, world, r) for r in range(world)]
+            assert got[0][0] == 0
+            for (w0, n), (w1, _) in zip(got, got[1:]):
+                assert w0 + n == w1
+            assert sum(n for _, n in got) == total
+
+
+def test_trace_slice_matches_window_rule(restate):
+    a, _, _ = restate.gen_poisson_trace(3.0, 10 * WMS, seed=1)
+    for w0, n in ((0, 3), (2, 5), (9, 1), (0, 10)):
+        lo, hi = D.trace_slice(a, WMS, w0, n)
+        w = a // WMS
+        assert np.all((w[lo:hi] >= w0) & (w[lo:hi] < w0 + n))
+        assert lo == 0 or w[lo - 1] < w0
+        assert hi == len(a) or w[hi] >= w0 + n
+
+
+def test_two_rank_gloo_combine_matches_single_pass(restate, prof, tmp_path):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    c0 = np.load(tmp_path / "comb0.npy")
+    c1 = np.load(tmp_path / "comb1.npy")
+    assert c0.tobytes() == c1.tobytes()  # bitwise identical on every rank
+    a, p, _ = restate.gen_poisson_trace(6.0, TOTAL_W * WMS, seed=5)
+    fi, en = _decide(restate, prof, a, p, 0, TOTAL_W)
+    single = _summary(fi, en, len(THR) + 1)
+    comb = c0[0]
+    for k in ("n_cmd", "n_infeasible", "n_empty", "argmin_cell", "min_energy_j"):
+        np.testing.assert_array_equal(comb[k], single[k])
+    np.testing.assert_allclose(comb["sum_energy_j"], single["sum_energy_j"], rtol=1e-9)
+    assert comb["n_infeasible"].sum() > 0 and comb["n_empty"].sum() >= 0
