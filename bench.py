@@ -344,6 +344,17 @@ def run_gsb(args, rank, world, dist):
         return
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
+    traffic_k2 = traffic_k1 = None  # dram bytes per launch from the committed ncu capture
+    try:
+        import glob as _glob
+        tj = sorted(_glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))[-1]
+        tr = json.load(open(tj))
+        traffic_k2 = next((v["dram_bytes_per_launch"] for k, v in tr.items()
+                           if k.startswith("k_prefill_select")), None)
+        traffic_k1 = sum(v["dram_bytes_per_launch"] for k, v in tr.items()
+                         if k.startswith("k_route_bin") or k.startswith("k_window_bounds")) or None
+    except (IndexError, OSError, ValueError, KeyError):
+        pass
     k2_tflops = evals * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
     peak_tflops = dfma_per_s * 2 / 1e12
     k1_gbs = n_req * K1_BYTES_PER_REQ / (k1_ms / 1e3) / 1e9
@@ -379,10 +390,12 @@ def run_gsb(args, rank, world, dist):
                      "frac": k2_tflops / peak_tflops,
                      "basis": f"{K2_DP_OPS_PER_EVAL} DP-pipe instr/eval x 2 (DFMA-equivalent) vs "
                               "DFMA throughput measured in this run (gsb_fp64_probe)",
-                     "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre, "traffic": None},
+                     "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre, "traffic": traffic_k2,
+                     "traffic_note": "dram__bytes_read+write per launch, profiles/ ncu capture"},
         "roofline_k1": {"bound": "hbm", "kernel": "k_route_bin (K1)", "achieved": k1_gbs,
                         "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm, "kernel_ms": k1_ms,
-                        "bytes_per_request": K1_BYTES_PER_REQ},
+                        "bytes_per_request": K1_BYTES_PER_REQ,
+                        "traffic": traffic_k1},
         "fp64_peak_measured_dfma_per_s": dfma_per_s,
         "result": {"commands": int(glob["n_cmd"].sum()),
                    "infeasible": int(glob["n_infeasible"].sum()),

@@ -650,18 +650,19 @@ int64_t gso_replay_series(const gso_ctl_cfg* cfg, const gso_band_table* table, d
 }
 
 /* Word-wise FNV-1a trajectory digest (K3 outputs). */
+/* per record: w1 = command bits, w2 = band_lo bits ^ (band_hi bits << 13) ^ (bucket << 48)
+ * ^ (action << 56); h = (h ^ w) * FNV64 prime, in log order (same as the GPU K3b). */
 uint64_t gso_digest_records(const gso_decision* r, int64_t n) {
   uint64_t h = 0xcbf29ce484222325ull;
   for (int64_t i = 0; i < n; ++i) {
-    uint64_t bits;
-    memcpy(&bits, &r[i].command_mhz, 8);
-    h = (h ^ bits) * 0x100000001b3ull;
-    memcpy(&bits, &r[i].band_lo, 8);
-    h = (h ^ bits) * 0x100000001b3ull;
-    memcpy(&bits, &r[i].band_hi, 8);
-    h = (h ^ bits) * 0x100000001b3ull;
-    h = (h ^ ((uint64_t)(uint32_t)r[i].action | ((uint64_t)(uint32_t)r[i].bucket << 32))) *
-        0x100000001b3ull;
+    uint64_t cmd, lo, hi;
+    memcpy(&cmd, &r[i].command_mhz, 8);
+    memcpy(&lo, &r[i].band_lo, 8);
+    memcpy(&hi, &r[i].band_hi, 8);
+    const uint64_t w2 = lo ^ (hi << 13) ^ ((uint64_t)(uint32_t)r[i].bucket << 48) ^
+                        ((uint64_t)(uint32_t)r[i].action << 56);
+    h = (h ^ cmd) * 0x100000001b3ull;
+    h = (h ^ w2) * 0x100000001b3ull;
   }
   return h;
 }

@@ -639,23 +639,23 @@ void ref_run_requests(void* h, int32_t* decode_worker, double* prefill_start, do
 
 }  // extern "C"
 
-// Trajectory digest, same definition as gso_digest_records (gs_oracle.c): word-wise
-// FNV-1a style h = (h ^ w) * 0x100000001b3 over (command bits, band_lo bits, band_hi bits,
-// action | bucket << 32) of every record, in log order.
+// Trajectory digest, same definition as gso_digest_records (gs_oracle.c): per record
+// w1 = command bits, w2 = band_lo bits ^ (band_hi bits << 13) ^ (bucket << 48) ^ (action << 56),
+// h = (h ^ w) * 0x100000001b3, in log order.
 static inline uint64_t dig_mix(uint64_t h, uint64_t v) { return (h ^ v) * 0x100000001b3ull; }
 
 extern "C" uint64_t ref_digest_records(const gso_decision* r, int64_t n) {
   uint64_t h = 0xcbf29ce484222325ull;
   for (int64_t i = 0; i < n; ++i) {
-    uint64_t bits;
-    std::memcpy(&bits, &r[i].command_mhz, 8);
-    h = dig_mix(h, bits);
-    std::memcpy(&bits, &r[i].band_lo, 8);
-    h = dig_mix(h, bits);
-    std::memcpy(&bits, &r[i].band_hi, 8);
-    h = dig_mix(h, bits);
-    h = dig_mix(h, static_cast<uint64_t>(static_cast<uint32_t>(r[i].action)) |
-                       (static_cast<uint64_t>(static_cast<uint32_t>(r[i].bucket)) << 32));
+    uint64_t cmd, lo, hi;
+    std::memcpy(&cmd, &r[i].command_mhz, 8);
+    std::memcpy(&lo, &r[i].band_lo, 8);
+    std::memcpy(&hi, &r[i].band_hi, 8);
+    const uint64_t w2 = lo ^ (hi << 13) ^
+                        (static_cast<uint64_t>(static_cast<uint32_t>(r[i].bucket)) << 48) ^
+                        (static_cast<uint64_t>(static_cast<uint32_t>(r[i].action)) << 56);
+    h = dig_mix(h, cmd);
+    h = dig_mix(h, w2);
   }
   return h;
 }

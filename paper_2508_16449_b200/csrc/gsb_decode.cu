@@ -84,43 +84,50 @@ __global__ void k_band_tables(const __grid_constant__ BandParams a) {
 // ---------------------------------------------------------------- K3b: controller replay
 enum : int { A_HOLD = 0, A_UP, A_DOWN, A_CHOLD, A_CPEND, A_CCOMMIT, A_AUP, A_ADOWN };
 
+template <bool COUNTS>
 struct Ctl {
   double lo, hi, sp, last_tps, last_p95;
   int current, pending, consecutive;
   int adj_total, adj_up, adj_dn;
   uint64_t digest;
   int64_t n_rec;
-  int cnt[8];
+  int cnt[COUNTS ? 8 : 1];
   double sum_cmd;
   int64_t n_fine;
 };
 
 __device__ __forceinline__ uint64_t mix(uint64_t h, uint64_t v) { return (h ^ v) * 0x100000001b3ull; }
 
-struct ReplayCtx {
-  const gsb_replay_args* a;
-  int64_t n;
-  int worker;
-  gsb_decision* rec;  // this trajectory's record slab or nullptr
+struct ReplayParams {
+  gsb_replay_args a;
+  int64_t n_fine, n_coarse;
 };
 
-__device__ __forceinline__ void emit(Ctl& c, const ReplayCtx& rc, double now, int bucket, int action) {
-  c.digest = mix(c.digest, static_cast<uint64_t>(__double_as_longlong(c.sp)));
-  c.digest = mix(c.digest, static_cast<uint64_t>(__double_as_longlong(c.lo)));
-  c.digest = mix(c.digest, static_cast<uint64_t>(__double_as_longlong(c.hi)));
-  c.digest = mix(c.digest, static_cast<uint64_t>(static_cast<uint32_t>(action)) |
-                               (static_cast<uint64_t>(static_cast<uint32_t>(bucket)) << 32));
+// One DecisionRecord: digest (w1 = command bits, w2 = band_lo ^ band_hi << 13 ^ bucket << 48 ^
+// action << 56; same definition as gso_digest_records), optional per-action counts and the
+// optional full record.
+template <bool COUNTS, bool RECORDS>
+__device__ __forceinline__ void emit(Ctl<COUNTS>& c, const gsb_replay_args& a, gsb_decision* rec,
+                                     int worker, double now, int bucket, int action) {
+  const uint64_t w1 = static_cast<uint64_t>(__double_as_longlong(c.sp));
+  const uint64_t w2 = static_cast<uint64_t>(__double_as_longlong(c.lo)) ^
+                      (static_cast<uint64_t>(__double_as_longlong(c.hi)) << 13) ^
+                      (static_cast<uint64_t>(static_cast<uint32_t>(bucket)) << 48) ^
+                      (static_cast<uint64_t>(static_cast<uint32_t>(action)) << 56);
+  c.digest = mix(mix(c.digest, w1), w2);
+  if (COUNTS) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) c.cnt[k] += action == k ? 1 : 0;
-  if (rc.rec && c.n_rec < rc.a->rec_cap) {
-    gsb_decision& r = rc.rec[c.n_rec];
+    for (int k = 0; k < 8; ++k) c.cnt[k] += action == k ? 1 : 0;
+  }
+  if (RECORDS && c.n_rec < a.rec_cap) {
+    gsb_decision& r = rec[c.n_rec];
     r.tick_ms = now;
     r.tps = c.last_tps;
     r.p95_tbt_ms = c.last_p95;
     r.band_lo = c.lo;
     r.band_hi = c.hi;
     r.command_mhz = c.sp;
-    r.worker = rc.worker;
+    r.worker = worker;
     r.bucket = bucket;
     r.action = action;
     r.pad_ = 0;
@@ -128,19 +135,43 @@ __device__ __forceinline__ void emit(Ctl& c, const ReplayCtx& rc, double now, in
   ++c.n_rec;
 }
 
-struct ReplayParams {
-  gsb_replay_args a;
-  int64_t n_fine, n_coarse;
-};
-
 // FreqBandTable::band via DecodeController::load_band (decode_ctl.cpp:52-57, 137-142)
-__device__ __forceinline__ void load_band(Ctl& c, const double* f_opt, int bucket, double step,
-                                          double f_min, double f_max) {
+template <bool COUNTS>
+__device__ __forceinline__ void load_band(Ctl<COUNTS>& c, const double* f_opt, int bucket,
+                                          double step, double f_min, double f_max) {
   const double f = f_opt[bucket];
   c.lo = std_max(f_min, f - step);
   c.hi = std_min(f_max, f + step);
 }
 
+// smallest double > x (x finite)
+__device__ __forceinline__ double next_up(double x) {
+  if (x == 0.0) return 4.9406564584124654e-324;
+  const long long b = __double_as_longlong(x);
+  return __longlong_as_double(x > 0.0 ? b + 1 : b - 1);
+}
+
+// Fine-loop direction (decode_ctl.cpp:150-157): margin = RN(p95 / den), dir = +1 if margin > U,
+// -1 if margin < L. No full division: q1 = fma(r, fma(-den, q, p95), q) with q = RN(p95 * r),
+// r = RN(1/den), is always within one ulp of RN(p95/den), so the decision
+// is exact unless q1 falls in [U, succ(U)] or [pred(L), L]; only then the IEEE quotient is formed.
+__device__ __forceinline__ int fine_dir(double p95, double den, double r, double U, double succU,
+                                        double L, double predL) {
+  if (gsb::dividend_in_fast_range(p95)) {
+    const double q = __dmul_rn(p95, r);
+    const double e = __fma_rn(-den, q, p95);
+    const double q1 = __fma_rn(r, e, q);
+    if (q1 > succU) return +1;
+    if (!(q1 >= U)) {
+      if (q1 < predL) return -1;
+      if (q1 > L) return 0;
+    }
+  }
+  const double m = __ddiv_rn(p95, den);
+  return m > U ? +1 : (m < L ? -1 : 0);
+}
+
+template <bool COUNTS, bool RECORDS>
 __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ ReplayParams rp) {
   const gsb_replay_args& a = rp.a;
   const int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -149,14 +180,15 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   const int NB = a.n_buckets;
   const int64_t tb = a.d_table_of[n];
   const int64_t s = a.d_stream_of[n];
+  const int worker = a.d_worker[n];
   const double* tps_hi = a.d_tps_hi + tb * NB;
   double f_opt[GSB_MAX_BUCKETS];  // per-controller copy; adaptation mutates it (decode_ctl.hpp:132)
   for (int b = 0; b < NB; ++b) f_opt[b] = a.d_f_opt[tb * NB + b];
-  const ReplayCtx rc{&a, n, a.d_worker[n], a.d_records ? a.d_records + n * a.rec_cap : nullptr};
+  gsb_decision* rec = RECORDS ? a.d_records + n * a.rec_cap : nullptr;
   const double f_min = a.f_min_mhz, f_max = a.f_max_mhz, step = cfg.step_mhz;
 
   // DecodeController ctor (decode_ctl.cpp:130-140): start in the top bucket at its f_opt
-  Ctl c;
+  Ctl<COUNTS> c;
   c.current = NB - 1;
   c.pending = -1;
   c.consecutive = 0;
@@ -167,90 +199,206 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   c.adj_total = c.adj_up = c.adj_dn = 0;
   c.digest = 0xcbf29ce484222325ull;
   c.n_rec = 0;
+  if (COUNTS) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) c.cnt[k] = 0;
+    for (int k = 0; k < 8; ++k) c.cnt[k] = 0;
+  }
   c.sum_cmd = 0.0;
   c.n_fine = 0;
 
   const double den = cfg.margin_decode * cfg.tslo_ms;
-  const double rden = gsb::short_divisor_dev(den) ? 1.0 / den : 0.0;
+  const double rden = 1.0 / den;
+  const double U = cfg.upper_margin, L = cfg.lower_margin;
+  const double succU = next_up(U), predL = -next_up(-L);
+  // dir * delta of decode_ctl.cpp:159-160 as a select: (+1)*d = d, (-1)*d = -d, 0*d = +0
   const double delta = std_min(cfg.step_mhz, cfg.max_step_mhz);
   const double adapt_period = cfg.adapt_period_s * 1000.0;
   const uint8_t* __restrict__ fine_has = a.d_fine_has + s * rp.n_fine;
   const double* __restrict__ fine_p95 = a.d_fine_p95 + s * rp.n_fine;
   const double* __restrict__ coarse_tps = a.d_coarse_tps + s * rp.n_coarse;
 
-  double tf = cfg.fine_period_ms, tc = cfg.coarse_period_ms, ta = adapt_period;
-  int64_t kf = 0, kc = 0;
-  for (;;) {
-    const double t = std_min(tf, std_min(tc, ta));
-    if (t > a.t_end_ms) break;
-    if (tc == t) {
-      // on_coarse_tick, decode_ctl.cpp:169-198
-      c.last_tps = coarse_tps[kc++] * cfg.tps_scale;
-      int observed = NB - 1;
-      for (int b = NB - 1; b >= 0; --b)
-        if (c.last_tps <= tps_hi[b]) observed = b;  // first bucket with tps <= tps_hi
-      int action;
-      if (observed == c.current) {
-        c.pending = -1;
-        c.consecutive = 0;
-        action = A_CHOLD;
-      } else {
-        if (observed == c.pending) {
-          ++c.consecutive;
-        } else {
-          c.pending = observed;
-          c.consecutive = 1;
-        }
-        if (c.consecutive >= cfg.hysteresis_count) {
-          c.current = observed;
-          load_band(c, f_opt, c.current, step, f_min, f_max);
-          c.sp = std_clamp(c.sp, c.lo, c.hi);
+  // prefetch ring: the series value of fine tick kf+j sits in pr[j] / hr[j], so the shared
+  // series' L1/L2 latency is hidden behind four ticks of controller work
+  const int64_t nf = rp.n_fine;
+  double pr[4];
+  uint8_t hr[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    pr[j] = j < nf ? fine_p95[j] : 0.0;
+    hr[j] = j < nf ? fine_has[j] : 0;
+  }
+
+  // Tick driver (simkernel.cpp:243-248,441-464): next instant = min of the three schedules,
+  // at equal times coarse (kind 5) < adapt (6) < fine (7). Generic in the tick type: when all
+  // periods are whole milliseconds every accumulated instant is an exact integer, so int64
+  // ticks reproduce the reference's repeated double additions exactly with ALU compares.
+  auto run = [&](auto fine_p, auto coarse_p, auto adapt_p, auto t_end) {
+    using TT = decltype(fine_p);
+    TT tf = fine_p, tc = coarse_p, ta = adapt_p;
+    int64_t kf = 0, kc = 0;
+    for (;;) {
+      const TT m1 = (tc < tf) ? tc : tf;
+      const TT t = (ta < m1) ? ta : m1;
+      if (t > t_end) break;
+      const double td = static_cast<double>(t);
+      if (tc == t) {
+        // on_coarse_tick, decode_ctl.cpp:169-198
+        c.last_tps = coarse_tps[kc++] * cfg.tps_scale;
+        int observed = NB - 1;
+        for (int b = NB - 1; b >= 0; --b)
+          if (c.last_tps <= tps_hi[b]) observed = b;  // first bucket with tps <= tps_hi
+        int action;
+        if (observed == c.current) {
           c.pending = -1;
           c.consecutive = 0;
-          c.adj_total = c.adj_up = c.adj_dn = 0;  // adjustments_.clear()
-          action = A_CCOMMIT;
+          action = A_CHOLD;
         } else {
-          action = A_CPEND;
+          if (observed == c.pending) {
+            ++c.consecutive;
+          } else {
+            c.pending = observed;
+            c.consecutive = 1;
+          }
+          if (c.consecutive >= cfg.hysteresis_count) {
+            c.current = observed;
+            load_band(c, f_opt, c.current, step, f_min, f_max);
+            c.sp = std_clamp(c.sp, c.lo, c.hi);
+            c.pending = -1;
+            c.consecutive = 0;
+            c.adj_total = c.adj_up = c.adj_dn = 0;  // adjustments_.clear()
+            action = A_CCOMMIT;
+          } else {
+            action = A_CPEND;
+          }
+        }
+        emit<COUNTS, RECORDS>(c, a, rec, worker, td, observed, action);
+        tc = t + coarse_p;
+      }
+      if (ta == t) {
+        // on_adapt_tick, decode_ctl.cpp:200-228
+        const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
+        c.adj_total = c.adj_up = c.adj_dn = 0;
+        if (total != 0) {
+          int shift = 0;
+          if (up > cfg.bias_threshold * total)
+            shift = +1;
+          else if (dn > cfg.bias_threshold * total)
+            shift = -1;
+          if (shift != 0) {
+            f_opt[c.current] = std_clamp(f_opt[c.current] + shift * step, f_min, f_max);
+            load_band(c, f_opt, c.current, step, f_min, f_max);
+            c.sp = std_clamp(c.sp, c.lo, c.hi);
+            emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current, shift > 0 ? A_AUP : A_ADOWN);
+          }
+        }
+        ta = t + adapt_p;
+      }
+      if (tf == t) {
+        // on_fine_tick, decode_ctl.cpp:148-167
+        int dir = 0;
+        const double p95 = pr[0];
+        if (hr[0]) {
+          c.last_p95 = p95;
+          dir = fine_dir(p95, den, rden, U, succU, L, predL);
+        }
+        pr[0] = pr[1];
+        pr[1] = pr[2];
+        pr[2] = pr[3];
+        hr[0] = hr[1];
+        hr[1] = hr[2];
+        hr[2] = hr[3];
+        const int64_t nxt = kf + 4;
+        pr[3] = nxt < nf ? fine_p95[nxt] : 0.0;
+        hr[3] = nxt < nf ? fine_has[nxt] : 0;
+        ++kf;
+        const double raw = c.sp + (dir > 0 ? delta : (dir < 0 ? -delta : 0.0));
+        const double clamped = std_clamp(raw, c.lo, c.hi);
+        const bool hit = dir != 0 && clamped != raw;
+        c.sp = clamped;
+        c.adj_total += 1;
+        c.adj_up += (hit && dir > 0) ? 1 : 0;
+        c.adj_dn += (hit && dir < 0) ? 1 : 0;
+        c.sum_cmd = c.sum_cmd + c.sp;
+        c.n_fine += 1;
+        emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current,
+                              dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
+        tf = t + fine_p;
+      }
+    }
+  };
+  // Aligned schedule: coarse and adapt periods are whole multiples of a whole-ms fine period,
+  // so every coarse/adapt instant IS a fine instant (k * fine) and the merge reduces to the
+  // fine ticks k = 1..nf with two down-counters; same event order (coarse, adapt, fine).
+  auto run_aligned = [&](int64_t fine_p, int64_t rc, int64_t ra, int64_t nticks) {
+    int64_t cc = rc, ca = ra, kc = 0;
+    for (int64_t k = 1; k <= nticks; ++k) {
+      const double td = RECORDS ? static_cast<double>(k * fine_p) : 0.0;
+      if (--cc == 0) {
+        cc = rc;
+        c.last_tps = coarse_tps[kc++] * cfg.tps_scale;
+        int observed = NB - 1;
+        for (int b = NB - 1; b >= 0; --b)
+          if (c.last_tps <= tps_hi[b]) observed = b;
+        int action;
+        if (observed == c.current) {
+          c.pending = -1;
+          c.consecutive = 0;
+          action = A_CHOLD;
+        } else {
+          if (observed == c.pending) {
+            ++c.consecutive;
+          } else {
+            c.pending = observed;
+            c.consecutive = 1;
+          }
+          if (c.consecutive >= cfg.hysteresis_count) {
+            c.current = observed;
+            load_band(c, f_opt, c.current, step, f_min, f_max);
+            c.sp = std_clamp(c.sp, c.lo, c.hi);
+            c.pending = -1;
+            c.consecutive = 0;
+            c.adj_total = c.adj_up = c.adj_dn = 0;
+            action = A_CCOMMIT;
+          } else {
+            action = A_CPEND;
+          }
+        }
+        emit<COUNTS, RECORDS>(c, a, rec, worker, td, observed, action);
+      }
+      if (--ca == 0) {
+        ca = ra;
+        const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
+        c.adj_total = c.adj_up = c.adj_dn = 0;
+        if (total != 0) {
+          int shift = 0;
+          if (up > cfg.bias_threshold * total)
+            shift = +1;
+          else if (dn > cfg.bias_threshold * total)
+            shift = -1;
+          if (shift != 0) {
+            f_opt[c.current] = std_clamp(f_opt[c.current] + shift * step, f_min, f_max);
+            load_band(c, f_opt, c.current, step, f_min, f_max);
+            c.sp = std_clamp(c.sp, c.lo, c.hi);
+            emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current, shift > 0 ? A_AUP : A_ADOWN);
+          }
         }
       }
-      emit(c, rc, t, observed, action);
-      tc = t + cfg.coarse_period_ms;
-    }
-    if (ta == t) {
-      // on_adapt_tick, decode_ctl.cpp:200-228
-      const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
-      c.adj_total = c.adj_up = c.adj_dn = 0;
-      if (total != 0) {
-        int shift = 0;
-        if (up > cfg.bias_threshold * total)
-          shift = +1;
-        else if (dn > cfg.bias_threshold * total)
-          shift = -1;
-        if (shift != 0) {
-          f_opt[c.current] = std_clamp(f_opt[c.current] + shift * step, f_min, f_max);
-          load_band(c, f_opt, c.current, step, f_min, f_max);
-          c.sp = std_clamp(c.sp, c.lo, c.hi);
-          emit(c, rc, t, c.current, shift > 0 ? A_AUP : A_ADOWN);
-        }
-      }
-      ta = t + adapt_period;
-    }
-    if (tf == t) {
-      // on_fine_tick, decode_ctl.cpp:148-167
       int dir = 0;
-      if (fine_has[kf]) {
-        const double p95 = fine_p95[kf];
+      const double p95 = pr[0];
+      if (hr[0]) {
         c.last_p95 = p95;
-        const double margin = rden != 0.0 ? gsb::div_pre_fast(p95, den, rden) : __ddiv_rn(p95, den);
-        if (margin > cfg.upper_margin)
-          dir = +1;
-        else if (margin < cfg.lower_margin)
-          dir = -1;
+        dir = fine_dir(p95, den, rden, U, succU, L, predL);
       }
-      ++kf;
-      const double raw = c.sp + dir * delta;
+      pr[0] = pr[1];
+      pr[1] = pr[2];
+      pr[2] = pr[3];
+      hr[0] = hr[1];
+      hr[1] = hr[2];
+      hr[2] = hr[3];
+      const int64_t nxt = k + 3;  // fine tick index k-1 is consumed now
+      pr[3] = nxt < nf ? fine_p95[nxt] : 0.0;
+      hr[3] = nxt < nf ? fine_has[nxt] : 0;
+      const double raw = c.sp + (dir > 0 ? delta : (dir < 0 ? -delta : 0.0));
       const double clamped = std_clamp(raw, c.lo, c.hi);
       const bool hit = dir != 0 && clamped != raw;
       c.sp = clamped;
@@ -258,14 +406,29 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
       c.adj_up += (hit && dir > 0) ? 1 : 0;
       c.adj_dn += (hit && dir < 0) ? 1 : 0;
       c.sum_cmd = c.sum_cmd + c.sp;
-      c.n_fine += 1;
-      emit(c, rc, t, c.current, dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
-      tf = t + cfg.fine_period_ms;
+      emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current,
+                            dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
     }
+    c.n_fine = nticks;
+  };
+  auto whole_ms = [](double x) { return x >= 1.0 && x < 2147483648.0 && x == rint(x); };
+  const bool int_sched = whole_ms(cfg.fine_period_ms) && whole_ms(cfg.coarse_period_ms) &&
+                         whole_ms(adapt_period) && a.t_end_ms >= 0.0 &&
+                         a.t_end_ms < 4503599627370496.0;
+  const int64_t fi = static_cast<int64_t>(cfg.fine_period_ms);
+  const int64_t ci = static_cast<int64_t>(cfg.coarse_period_ms);
+  const int64_t ai = static_cast<int64_t>(adapt_period);
+  if (int_sched && ci % fi == 0 && ai % fi == 0) {
+    run_aligned(fi, ci / fi, ai / fi, static_cast<int64_t>(floor(a.t_end_ms)) / fi);
+  } else if (int_sched) {
+    run(static_cast<int64_t>(cfg.fine_period_ms), static_cast<int64_t>(cfg.coarse_period_ms),
+        static_cast<int64_t>(adapt_period), static_cast<int64_t>(floor(a.t_end_ms)));
+  } else {
+    run(cfg.fine_period_ms, cfg.coarse_period_ms, adapt_period, a.t_end_ms);
   }
   a.d_digest[n] = c.digest;
   a.d_n_rec[n] = c.n_rec;
-  if (a.d_counts) {
+  if (COUNTS) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) a.d_counts[n * 8 + k] = c.cnt[k];
   }
@@ -299,7 +462,17 @@ int gsb_decode_replay(gsb_ctx* ctx, const gsb_replay_args* a, void* stream) {
   if (a->n_traj <= 0) return GSB_OK;
   ReplayParams rp{*a, gsb_n_ticks(a->fine_period_ms, a->t_end_ms),
                   gsb_n_ticks(a->coarse_period_ms, a->t_end_ms)};
-  k_decode_replay<<<static_cast<unsigned>((a->n_traj + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(rp);
+  const unsigned blocks = static_cast<unsigned>((a->n_traj + 127) / 128);
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  const bool counts = a->d_counts != nullptr, records = a->d_records != nullptr && a->rec_cap > 0;
+  if (counts && records)
+    k_decode_replay<true, true><<<blocks, 128, 0, s>>>(rp);
+  else if (counts)
+    k_decode_replay<true, false><<<blocks, 128, 0, s>>>(rp);
+  else if (records)
+    k_decode_replay<false, true><<<blocks, 128, 0, s>>>(rp);
+  else
+    k_decode_replay<false, false><<<blocks, 128, 0, s>>>(rp);
   return gsb_check_launch(ctx, "decode_replay");
 }
 

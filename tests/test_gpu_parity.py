@@ -373,6 +373,54 @@ def test_decode_replay_matches_oracle_full_records(eng, restate):
         assert (got == want[:cap]).all(), n
 
 
+def test_fine_loop_threshold_edges(eng, restate):
+    """p95 values within a few ulps of upper*den and lower*den: the division-free margin test
+    of K3b must take exactly the reference's decisions (decode_ctl.cpp:150-157)."""
+    api = _api()
+    gp = api.GpuProfile.default_profile()
+    rng = np.random.default_rng(13)
+    cfgs, series = [], []
+    for it in range(48):
+        tslo = float(rng.uniform(40.0, 160.0))
+        margin = float(rng.choice([0.6, 0.95, 1.0, 1.3, float(rng.uniform(0.2, 2.0))]))
+        c = api.DecodeCtlConfig(tslo_ms=tslo, margin_decode=margin, coarse_period_ms=1e9,
+                                adapt_period_s=1e9, tps_scale=1.0)
+        den = margin * tslo
+        vals = []
+        for thr in (c.upper_margin, c.lower_margin):
+            base = thr * den
+            for k in range(-4, 5):
+                vals.append(np.nextafter(base, np.inf * k) if k else base)
+                v = base
+                for _ in range(abs(k)):
+                    v = np.nextafter(v, np.inf if k > 0 else -np.inf)
+                vals.append(v)
+        vals = np.array(vals)
+        rng.shuffle(vals)
+        cfgs.append(c)
+        series.append(vals)
+    nf = max(len(v) for v in series)
+    t_end = 20.0 * nf
+    has = np.ones((len(cfgs), nf), np.uint8)
+    p95 = np.stack([np.resize(v, nf) for v in series])
+    tps = np.zeros((len(cfgs), 1))
+    one = band_table([0.0], [math.inf], [705.0])
+    lo, hi, fo = np.array([[0.0]]), np.array([[math.inf]]), np.array([[705.0]])
+    dev = lambda x, dt: torch.as_tensor(x, device="cuda").to(dt)
+    out = eng.decode_replay(cfgs, [0] * len(cfgs), np.arange(len(cfgs)), [0] * len(cfgs), lo, hi,
+                            fo, gp.grid, dev(has, torch.uint8), dev(p95, torch.float64),
+                            dev(tps, torch.float64), t_end, rec_cap=nf + 4)
+    torch.cuda.synchronize()
+    recs = out["records"].cpu().numpy()
+    for n, c in enumerate(cfgs):
+        oc = default_ctl_cfg(tslo_ms=c.tslo_ms, margin_decode=c.margin_decode,
+                             coarse_period_ms=1e9, adapt_period_s=1e9, tps_scale=1.0)
+        want = restate.replay_series(oc, one, 210.0, 1410.0, 0, has[n], p95[n], tps[n], t_end)
+        got = recs[n, :len(want)].reshape(-1).view(want.dtype)
+        assert int(out["n_rec"][n].item()) == len(want)
+        assert (got == want).all(), n
+
+
 def test_decode_replay_reproduces_reference_closed_loop_run(eng, ref, prof):
     """The reference simulator's own controllers (greenllm, sinusoid decode load): their
     captured per-tick inputs replayed on the GPU give the reference's decision log."""

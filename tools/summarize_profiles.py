@@ -1,0 +1,108 @@
+"""Turn gpurun_out/<round>_* ncu outputs into the committed evidence under profiles/:
+  profiles/<round>_launches.csv     raw launch list (gpu__time_duration per launch)
+  profiles/<round>_launch_summary.md per-kernel mean device time and share of the bench run
+  profiles/<round>_kernels.md        key `--set full` metrics per captured kernel
+  profiles/<round>_traffic.json      dram bytes / launch and duration of each captured kernel
+usage: python tools/summarize_profiles.py r1
+"""
+import collections
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = {
+    "gpu__time_duration.sum": "duration",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_pct",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct_active",
+    "sm__inst_issued.avg.pct_of_peak_sustained_active": "issue_pct_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
+    "launch__registers_per_thread": "regs",
+    "smsp__inst_executed.sum": "warp_insts",
+}
+UNIT_SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+              "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6,
+              "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def launch_summary(rnd):
+    src = os.path.join(OUT, f"{rnd}_launches.csv")
+    shutil.copy(src, os.path.join(PROF, f"{rnd}_launches.csv"))
+    rows = list(csv.reader(open(src)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.defaultdict(list)
+    for r in rows[start + 1:]:
+        if len(r) > vi:
+            agg[r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "")].append(
+                float(r[vi].replace(",", "")) * UNIT_SCALE.get(r[ui], 1e-3))
+    tot = sum(sum(v) for v in agg.values())
+    lines = [f"# {rnd} launch list summary (ncu gpu__time_duration.sum, --clock-control none;",
+             "# cold-cache and serialised: compare shares, not absolute times)", "",
+             "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v):.2f} | {sum(v):.1f} | {sum(v)/tot:.1%} |")
+    open(os.path.join(PROF, f"{rnd}_launch_summary.md"), "w").write("\n".join(lines) + "\n")
+
+
+def rep_metrics(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        rec = {"kernel": d.get("Kernel Name", "").split("(")[0].replace("void ", "")
+               .replace("<unnamed>::", "")}
+        for m, k in METRICS.items():
+            if m in d and d[m] not in ("", "n/a"):
+                u = units[hdr.index(m)]
+                try:
+                    rec[k] = float(d[m].replace(",", "")) * UNIT_SCALE.get(u, 1.0)
+                except ValueError:
+                    pass
+        out.append(rec)
+    return out
+
+
+def main(rnd):
+    os.makedirs(PROF, exist_ok=True)
+    launch_summary(rnd)
+    recs = []
+    for part in ("prefill", "decode"):
+        rep = os.path.join(OUT, f"{rnd}_{part}.ncu-rep")
+        if os.path.exists(rep):
+            recs += rep_metrics(rep)
+    lines = [f"# {rnd} ncu --set full captures (key metrics per launch)", "",
+             "| kernel | us | DRAM R+W MB | DRAM % | SM % | FP64 pipe % (active) | issue % (active) | occupancy % | regs | warp insts |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
+    traffic = {}
+    for r in recs:
+        mb = (r.get("dram_read", 0) + r.get("dram_write", 0)) / 1e6
+        lines.append(f"| `{r['kernel']}` | {r.get('duration', 0):.1f} | {mb:.2f} | "
+                     f"{r.get('dram_pct', 0):.1f} | {r.get('sm_pct', 0):.1f} | "
+                     f"{r.get('fp64_pipe_pct_active', 0):.1f} | {r.get('issue_pct_active', 0):.1f} | "
+                     f"{r.get('occupancy_pct', 0):.1f} | {r.get('regs', 0):.0f} | "
+                     f"{r.get('warp_insts', 0):.3g} |")
+        traffic.setdefault(r["kernel"], {"dram_bytes_per_launch": mb * 1e6,
+                                         "duration_us": r.get("duration", 0)})
+    open(os.path.join(PROF, f"{rnd}_kernels.md"), "w").write("\n".join(lines) + "\n")
+    json.dump(traffic, open(os.path.join(PROF, f"{rnd}_traffic.json"), "w"), indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1")
