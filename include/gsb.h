@@ -102,6 +102,23 @@ int gsb_ctl_cfg_validate(const gsb_ctl_cfg* c, char* msg, size_t msg_cap);
  * f_i, 1/f_i and P(f_i) are built once here, gpu_model.cpp:24-28, gpu_model.hpp:64). */
 int gsb_set_profiles(gsb_ctx* ctx, int n_profiles, const gsb_profile* profiles);
 
+/* As gsb_set_profiles; flags & GSB_PROFILES_UNCHECKED skips GpuProfile::validate and keeps only
+ * the structural checks the kernels need (finite grid, step > 0, 1..GSB_MAX_GRID clocks). The
+ * reference's evaluators never validate their profile argument (prefill_opt.cpp:16-56), and its
+ * tests call them with profiles validate() rejects (flat power, test_prefill_opt.cpp:98,135). */
+#define GSB_PROFILES_UNCHECKED 1
+int gsb_set_profiles_ex(gsb_ctx* ctx, int n_profiles, const gsb_profile* profiles, int flags);
+
+/* ---------------------------------------------------------------- device memory */
+/* Plumbing for hosts without their own CUDA runtime (cgo, JNI, the C++ drop-in in
+ * paper_2508_16449_b200/cpp): device allocation on the context's device and copies on `stream`
+ * (NULL = the context's stream). kind: 0 host->device, 1 device->host, 2 device->device.
+ * gsb_memcpy returns once the copy is enqueued; call gsb_synchronize before reading a
+ * device->host result. */
+int gsb_malloc(gsb_ctx* ctx, size_t bytes, void** d_out);
+int gsb_free(gsb_ctx* ctx, void* d_ptr);
+int gsb_memcpy(gsb_ctx* ctx, void* dst, const void* src, size_t bytes, int kind, void* stream);
+
 /* ---------------------------------------------------------------- K1: route + bin */
 /* Routing / binning configuration. Offline window convention: window k of
  * the pass covers [(w0+k)*window_ms, (w0+k+1)*window_ms); jobs of a cell are the requests
@@ -119,6 +136,11 @@ typedef struct gsb_route_cfg {
 /* RoutingConfig::validate (router.cpp:7-24) for n_prefill_workers / worker_map. */
 int gsb_routing_validate(const gsb_route_cfg* cfg, int n_prefill_workers,
                          const int32_t* worker_map, char* msg, size_t msg_cap);
+
+/* classify(cfg, prompt) (router.cpp:26-31) for n prompts: the number of the n_thresholds
+ * (host array, 0..GSB_MAX_CLASSES-1 entries, any order) strictly below the prompt. */
+int gsb_classify(gsb_ctx* ctx, int n_thresholds, const int32_t* thresholds, int64_t n,
+                 const int32_t* d_prompt, int32_t* d_class, void* stream);
 
 /* Window start indices: bounds[k] = first request with arrival >= (w0+k)*window_ms,
  * k = 0..n_windows (arrival must be non-decreasing, trace.cpp:109-111). */
@@ -191,6 +213,21 @@ int gsb_energy_batches(gsb_ctx* ctx, int profile, int64_t n_batches, const int64
                        const int32_t* d_prompt, const double* d_wf, const double* d_f_mhz,
                        const double* d_window, double* d_busy, double* d_active, double* d_idle,
                        double* d_total, uint8_t* d_feasible, void* stream);
+
+/* PrefillBatch::t_ref_total_ms(m) (prefill_opt.cpp:9-14) of n ragged batches under the latency
+ * model lat_abc = {a, b, c} alone (the reference takes a LatencyModel, not a profile):
+ * d_out[b] = left-to-right sum of wf*((a*L+b)*L+c); 0 for an empty batch. */
+int gsb_t_ref_batches(gsb_ctx* ctx, const double lat_abc[3], int64_t n_batches,
+                      const int64_t* d_off, const int32_t* d_prompt, const double* d_wf,
+                      double* d_out, void* stream);
+
+/* energy_total_closed_form_j (prefill_opt.cpp:33-43, Eq. 13; a cross-check of energy_total)
+ * per batch at clock d_f_mhz[b] and window d_window[b]; NaN for an off-grid clock (the
+ * reference's ModelError). */
+int gsb_energy_closed_form_batches(gsb_ctx* ctx, int profile, int64_t n_batches,
+                                   const int64_t* d_off, const int32_t* d_prompt,
+                                   const double* d_wf, const double* d_f_mhz,
+                                   const double* d_window, double* d_out, void* stream);
 
 /* Per (profile, class) summary of a K2 pass for the end-of-run reductions:
  * n_cmd, n_infeasible, n_empty, sum_energy (fixed-shape tree order, deterministic),
@@ -272,6 +309,47 @@ typedef struct gsb_replay_args {
   int64_t rec_cap;
 } gsb_replay_args;
 int gsb_decode_replay(gsb_ctx* ctx, const gsb_replay_args* a, void* stream);
+
+/* Resumable DecodeController state (the private members of decode_ctl.hpp:129-151): band,
+ * set point, last observations, coarse-loop streak, the adjustment counts adaptation reads,
+ * and the controller's own (adapted) copy of the table's f_opt. initialized == 0 means "not
+ * yet constructed": the kernel applies the constructor (decode_ctl.cpp:130-140) first. */
+typedef struct gsb_ctl_state {
+  double band_lo, band_hi, set_point, last_tps, last_p95;
+  int32_t current_bucket, pending_bucket, consecutive;
+  int32_t adj_total, adj_up, adj_down;
+  int32_t initialized, pad_;
+  double f_opt[GSB_MAX_BUCKETS];
+} gsb_ctl_state;
+
+/* Scripted DecodeController (decode_ctl.hpp:116-150 call sequences, e.g. the reference's own
+ * unit tests): trajectory n executes calls [d_ev_off[n], d_ev_off[n+1]) in order, kind 0 =
+ * on_fine_tick(t, has ? value : nullopt), 1 = on_coarse_tick(t, value), 2 = on_adapt_tick(t).
+ * Uses a->n_traj, d_cfg, d_table_of, d_worker, n_buckets, d_tps_hi, d_f_opt, f_min/f_max,
+ * d_digest, d_n_rec, d_records/rec_cap (records of THIS call, from index 0).
+ * d_state [N] (optional, in/out): resumes each controller from its state (constructing it from
+ * table d_table_of[n] when initialized == 0) and writes the state after the script back, so a
+ * long-lived controller costs O(calls) in total. NULL = construct fresh, discard the state. */
+int gsb_decode_script(gsb_ctx* ctx, const gsb_replay_args* a, const int64_t* d_ev_off,
+                      const int8_t* d_kind, const double* d_t, const double* d_value,
+                      const uint8_t* d_has, gsb_ctl_state* d_state, void* stream);
+
+/* Nearest-rank quantile (metrics.cpp:11-19) of each of n_sets sample sets
+ * [d_off[s], d_off[s+1]), set sizes 1..4096 (TbtWindow::p95 is q = 0.95 over the ring). An
+ * empty or oversized set yields NaN (the reference throws std::invalid_argument). */
+int gsb_quantile_batch(gsb_ctx* ctx, double q, int64_t n_sets, const int64_t* d_off,
+                       const double* d_samples, double* d_out, void* stream);
+
+/* TpsWindow::tps(now) (decode_ctl.cpp:113-118) for n windows: events [d_off[w], d_off[w+1])
+ * (time-sorted, as recorded) with window span d_window_ms[w], evaluated at d_now[w]. */
+int gsb_tps_window_batch(gsb_ctx* ctx, int64_t n, const int64_t* d_off, const double* d_t,
+                         const int32_t* d_tokens, const double* d_window_ms, const double* d_now,
+                         double* d_out, void* stream);
+
+/* decode_steady_state (decode_ctl.cpp:28-50) for n (tps, f, max_batch) points of one profile. */
+int gsb_steady_state_batch(gsb_ctx* ctx, int64_t n, const gsb_profile* d_profile,
+                           const double* d_tps, const double* d_f, const int32_t* d_max_batch,
+                           uint8_t* d_sustainable, double* d_batch, double* d_tbt, void* stream);
 
 /* Host-side validation of a replay batch (band tables + configs), host pointers. */
 int gsb_replay_validate(const gsb_ctl_cfg* cfgs, int64_t n, int32_t n_buckets,

@@ -381,6 +381,9 @@ class Reference:
         L.ref_replay_telemetry.argtypes = [C.POINTER(CtlCfg), C.POINTER(BandTable), _d, _d, _d, _d,
                                            C.c_int, C.POINTER(Telemetry), _d, _p, _i64]
         L.ref_replay_telemetry.restype = _i64
+        L.ref_decode_script.argtypes = [C.POINTER(CtlCfg), C.POINTER(BandTable), _d, _d, _d, _d,
+                                        C.c_int, _i64, _p, _p, _p, _p, _p, _i64, _p, _p, _p]
+        L.ref_decode_script.restype = _i64
         L.ref_replay_many.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _d, _d, _d, _d, _d, C.c_int,
                                       _p, _p]
         L.ref_digest_records.argtypes = [_p, _i64]
@@ -529,6 +532,25 @@ class Reference:
             if n <= cap:
                 return out[:n]
             cap = n
+
+    def decode_script(self, cfg, table: _TableHolder, prof: Profile, worker, kind, t, value, has):
+        """DecodeController on an explicit call script -> (records, command, bucket, f_opt)."""
+        kind = np.ascontiguousarray(kind, np.int8)
+        t = np.ascontiguousarray(t, np.float64)
+        value = np.ascontiguousarray(value, np.float64)
+        has = np.ascontiguousarray(has, np.uint8)
+        out = np.zeros(max(1, len(kind)), DECISION_DTYPE)
+        cmd = C.c_double()
+        bucket = C.c_int32()
+        f_opt = np.zeros(table.c.n, np.float64)
+        n = self.lib.ref_decode_script(C.byref(cfg), C.byref(table.c), prof.f_min_mhz,
+                                       prof.f_max_mhz, prof.step_mhz, prof.f_ref_mhz, worker,
+                                       len(kind), ptr(kind), ptr(t), ptr(value), ptr(has),
+                                       ptr(out), len(out), C.byref(cmd), C.byref(bucket),
+                                       ptr(f_opt))
+        if n < 0:
+            raise ValueError("ModelError")
+        return out[:n], cmd.value, bucket.value, f_opt
 
     def replay_many(self, cfgs, tables, table_of, tels, tel_of, worker_of, prof, t_end, threads=1):
         n = len(cfgs)

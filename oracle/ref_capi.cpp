@@ -456,6 +456,39 @@ int64_t ref_replay_telemetry(const gso_ctl_cfg* cc, const gso_band_table* tb, do
   }
 }
 
+// DecodeController driven by an explicit call script (kind 0 fine, 1 coarse, 2 adapt), the
+// shape of the reference's own unit tests; also returns command(), current_bucket() and the
+// (adapted) table f_opt after the script.
+int64_t ref_decode_script(const gso_ctl_cfg* cc, const gso_band_table* tb, double f_min,
+                          double f_max, double step, double f_ref, int worker, int64_t n_ev,
+                          const int8_t* kind, const double* t, const double* value,
+                          const uint8_t* has, gso_decision* out, int64_t cap, double* final_cmd,
+                          int32_t* final_bucket, double* final_f_opt) {
+  try {
+    DecodeController ctl(to_cfg(cc), to_table(tb), FrequencyGrid{f_min, f_max, step, f_ref}, worker);
+    for (int64_t e = 0; e < n_ev; ++e) {
+      if (kind[e] == 1) {
+        ctl.on_coarse_tick(t[e], value[e]);
+      } else if (kind[e] == 2) {
+        ctl.on_adapt_tick(t[e]);
+      } else {
+        std::optional<double> p;
+        if (has[e]) p = value[e];
+        ctl.on_fine_tick(t[e], p);
+      }
+    }
+    const auto& log = ctl.log();
+    const int64_t n = static_cast<int64_t>(log.size());
+    for (int64_t i = 0; i < n && i < cap; ++i) to_c_record(log[static_cast<size_t>(i)], out + i);
+    *final_cmd = ctl.command();
+    *final_bucket = ctl.current_bucket();
+    for (std::size_t b = 0; b < ctl.table().buckets.size(); ++b) final_f_opt[b] = ctl.table().buckets[b].f_opt_mhz;
+    return n;
+  } catch (const ModelError&) {
+    return -1;
+  }
+}
+
 // Open-loop replay of many scenarios on shared telemetry (timed CPU baseline).
 // Scenario s uses cfgs[s], tables[table_of[s]], telemetry tels[tel_of[s]], worker id
 // worker_of[s]; emits per-scenario record counts and FNV digests.

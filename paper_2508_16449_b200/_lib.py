@@ -72,6 +72,13 @@ class CReplayArgs(C.Structure):
                 ("d_counts", _p), ("d_mean_cmd", _p), ("d_records", _p), ("rec_cap", _i64)]
 
 
+class CCtlState(C.Structure):
+    _fields_ = [("band_lo", _d), ("band_hi", _d), ("set_point", _d), ("last_tps", _d),
+                ("last_p95", _d), ("current_bucket", _i32), ("pending_bucket", _i32),
+                ("consecutive", _i32), ("adj_total", _i32), ("adj_up", _i32), ("adj_down", _i32),
+                ("initialized", _i32), ("pad_", _i32), ("f_opt", _d * 32)]
+
+
 # every symbol include/gsb.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "gsb_version", "gsb_status_string", "gsb_ctx_create", "gsb_ctx_destroy", "gsb_last_error",
@@ -80,6 +87,9 @@ EXPORTS = (
     "gsb_fifo_order", "gsb_prefill_select", "gsb_select_batches", "gsb_energy_batches",
     "gsb_prefill_summary", "gsb_n_ticks", "gsb_window_series", "gsb_build_band_tables",
     "gsb_decode_replay", "gsb_replay_validate", "gsb_fp64_probe", "gsb_selftest_division",
+    "gsb_decode_script", "gsb_quantile_batch", "gsb_tps_window_batch", "gsb_steady_state_batch",
+    "gsb_set_profiles_ex", "gsb_malloc", "gsb_free", "gsb_memcpy", "gsb_classify",
+    "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
 )
 
 _lib = None
@@ -127,5 +137,16 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_replay_validate.argtypes = [_p, _i64, _i32, _p, _p, _i64, C.c_char_p, C.c_size_t]
     L.gsb_fp64_probe.argtypes = [_p, _i64, C.c_int, _p, _p]
     L.gsb_selftest_division.argtypes = [_p, _i64, _u64, _p, _p]
+    L.gsb_decode_script.argtypes = [_p, P(CReplayArgs), _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_quantile_batch.argtypes = [_p, _d, _i64, _p, _p, _p, _p]
+    L.gsb_tps_window_batch.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_steady_state_batch.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_set_profiles_ex.argtypes = [_p, C.c_int, _p, C.c_int]
+    L.gsb_malloc.argtypes = [_p, C.c_size_t, P(_p)]
+    L.gsb_free.argtypes = [_p, _p]
+    L.gsb_memcpy.argtypes = [_p, _p, _p, C.c_size_t, C.c_int, _p]
+    L.gsb_classify.argtypes = [_p, C.c_int, _p, _i64, _p, _p, _p]
+    L.gsb_t_ref_batches.argtypes = [_p, P(_d), _i64, _p, _p, _p, _p, _p]
+    L.gsb_energy_closed_form_batches.argtypes = [_p, C.c_int, _i64, _p, _p, _p, _p, _p, _p, _p]
     _lib = L
     return L

@@ -656,10 +656,103 @@ class Engine:
         return out
 
     def classify_many(self, routing: RoutingConfig, prompts) -> np.ndarray:
-        """classify (router.cpp:26-31) for a vector of prompts, on the GPU (K1 with one window)."""
-        prompts = np.ascontiguousarray(prompts, np.int32)
-        rr = self.route_bin(np.zeros(len(prompts), np.int64), prompts, routing, 1, 0, 1)
-        return rr.cls.cpu().numpy().astype(np.int64)
+        """classify (router.cpp:26-31) for a vector of prompts, on the GPU (gsb_classify)."""
+        thr = np.ascontiguousarray(routing.thresholds, np.int32)
+        if len(thr) > L.GSB_MAX_CLASSES - 1:
+            raise RouterError("routing: more than 7 thresholds (GSB_MAX_CLASSES)")
+        p = self._dev(np.ascontiguousarray(prompts, np.int32), torch.int32)
+        out = self._empty(p.numel(), torch.int32)
+        self._check(self.lib.gsb_classify(self.ctx, len(thr), thr.ctypes.data_as(C.c_void_p),
+                                          p.numel(), _ptr(p), _ptr(out), self.stream()))
+        return out.cpu().numpy().astype(np.int64)
+
+    def t_ref_batches(self, lat: LatencyModel, off, prompt, wf=None) -> torch.Tensor:
+        """PrefillBatch::t_ref_total_ms(m) (prefill_opt.cpp:9-14) per CSR batch, under a bare
+        LatencyModel (gsb_t_ref_batches)."""
+        off = self._dev(off, torch.int64)
+        prompt = self._dev(prompt, torch.int32)
+        wf_t = None if wf is None else self._dev(wf, torch.float64)
+        out = self._empty(off.numel() - 1, torch.float64)
+        abc = (C.c_double * 3)(lat.a, lat.b, lat.c)
+        self._check(self.lib.gsb_t_ref_batches(self.ctx, abc, off.numel() - 1, _ptr(off),
+                                               _ptr(prompt), _ptr(wf_t), _ptr(out), self.stream()))
+        return out
+
+    def energy_closed_form_batches(self, off, prompt, f_mhz, windows,
+                                   profile: Optional[GpuProfile] = None, wf=None) -> torch.Tensor:
+        """energy_total_closed_form_j (prefill_opt.cpp:33-43) per CSR batch; NaN off-grid."""
+        pi = 0 if profile is None else self._profile_index(profile)
+        ins = [self._dev(off, torch.int64), self._dev(prompt, torch.int32),
+               None if wf is None else self._dev(wf, torch.float64),
+               self._dev(f_mhz, torch.float64), self._dev(windows, torch.float64)]
+        nb = ins[0].numel() - 1
+        out = self._empty(nb, torch.float64)
+        self._check(self.lib.gsb_energy_closed_form_batches(self.ctx, pi, nb, *[_ptr(x) for x in ins],
+                                                            _ptr(out), self.stream()))
+        return out
+
+    # ---------------------------------------------------------------- window statistics
+    def quantile_batch(self, off, samples, q: float) -> torch.Tensor:
+        """Nearest-rank quantile (metrics.cpp:11-19) of every CSR sample set (<= 4096 each)."""
+        off = self._dev(off, torch.int64)
+        s = self._dev(samples, torch.float64)
+        out = self._empty(off.numel() - 1, torch.float64)
+        self._check(self.lib.gsb_quantile_batch(self.ctx, q, off.numel() - 1, _ptr(off), _ptr(s),
+                                                _ptr(out), self.stream()))
+        return out
+
+    def tps_window_batch(self, off, t_ms, tokens, window_ms, now_ms) -> torch.Tensor:
+        """TpsWindow::tps(now) (decode_ctl.cpp:113-118) for every CSR event window."""
+        ins = [self._dev(off, torch.int64), self._dev(t_ms, torch.float64),
+               self._dev(tokens, torch.int32), self._dev(window_ms, torch.float64),
+               self._dev(now_ms, torch.float64)]
+        n = ins[0].numel() - 1
+        out = self._empty(n, torch.float64)
+        self._check(self.lib.gsb_tps_window_batch(self.ctx, n, *[_ptr(x) for x in ins], _ptr(out),
+                                                  self.stream()))
+        return out
+
+    def steady_state_batch(self, profile: GpuProfile, tps, f, max_batch):
+        """decode_steady_state (decode_ctl.cpp:28-50) at many points: (sustainable u8, batch,
+        tbt_ms) device tensors."""
+        dp = self._dev(np.frombuffer(bytes(profile.to_c()), np.uint8), torch.uint8)
+        ins = [self._dev(tps, torch.float64), self._dev(f, torch.float64),
+               self._dev(max_batch, torch.int32)]
+        n = ins[0].numel()
+        sus, b, t = self._empty(n, torch.uint8), self._empty(n, torch.float64), self._empty(n, torch.float64)
+        self._check(self.lib.gsb_steady_state_batch(self.ctx, n, _ptr(dp), *[_ptr(x) for x in ins],
+                                                    _ptr(sus), _ptr(b), _ptr(t), self.stream()))
+        return sus, b, t
+
+    def decode_script(self, cfgs, table_of, worker, tps_hi, f_opt, grid: FrequencyGrid, ev_off,
+                      kind, t_ms, value, has, state: Optional[torch.Tensor] = None,
+                      rec_cap: int = 0):
+        """K3s: DecodeController driven by explicit call scripts (decode_ctl.hpp:116-150), one
+        lane per controller; `state` (uint8 [N, sizeof gsb_ctl_state], zero = fresh) resumes
+        and receives each controller's state. Returns dict of device tensors."""
+        cfg_arr = cfgs if isinstance(cfgs, np.ndarray) else ctl_cfg_array(cfgs)
+        N = len(cfg_arr)
+        tps_hi_h = np.ascontiguousarray(tps_hi.cpu().numpy() if isinstance(tps_hi, torch.Tensor)
+                                        else tps_hi, np.float64)
+        NB = tps_hi_h.reshape(-1, tps_hi_h.shape[-1]).shape[1]
+        keep = [self._dev(cfg_arr.view(np.uint8), torch.uint8), self._dev(table_of, torch.int32),
+                self._dev(worker, torch.int32), self._dev(tps_hi_h, torch.float64),
+                self._dev(f_opt, torch.float64), self._dev(ev_off, torch.int64),
+                self._dev(kind, torch.int8), self._dev(t_ms, torch.float64),
+                self._dev(value, torch.float64), self._dev(has, torch.uint8)]
+        out = {"digest": self._empty(N, torch.int64), "n_rec": self._empty(N, torch.int64),
+               "records": (self._empty((N, rec_cap, DECISION_DTYPE.itemsize), torch.uint8)
+                           if rec_cap else None),
+               "state": state if state is not None else torch.zeros(
+                   (N, C.sizeof(L.CCtlState)), dtype=torch.uint8, device=self.device)}
+        a = L.CReplayArgs(N, _ptr(keep[0]), _ptr(keep[1]), None, _ptr(keep[2]), NB, _ptr(keep[3]),
+                          _ptr(keep[4]), grid.f_min_mhz, grid.f_max_mhz, 0.0, 0.0, 0.0, None, None,
+                          None, _ptr(out["digest"]), _ptr(out["n_rec"]), None, None,
+                          _ptr(out["records"]), rec_cap)
+        self._check(self.lib.gsb_decode_script(self.ctx, C.byref(a), *[_ptr(x) for x in keep[5:]],
+                                               _ptr(out["state"]), self.stream()))
+        torch.cuda.current_stream(self.device).synchronize()
+        return out
 
     def classify(self, routing: RoutingConfig, prompt_tokens: int) -> int:
         return int(self.classify_many(routing, [prompt_tokens])[0])

@@ -82,6 +82,19 @@ std::string validate_profile(const gsb_profile& p) {
   return "";
 }
 
+// What the clock tables need to be well formed when GpuProfile::validate is skipped.
+std::string structural_check(const gsb_profile& p) {
+  const double v[] = {p.f_min_mhz, p.f_max_mhz, p.step_mhz, p.f_ref_mhz, p.lat_a, p.lat_b, p.lat_c,
+                      p.k3, p.k2, p.k1, p.k0, p.p_idle_w};
+  for (double x : v)
+    if (!std::isfinite(x)) return "profile: non-finite coefficient";
+  if (p.f_min_mhz <= 0.0 || p.f_max_mhz < p.f_min_mhz || p.step_mhz <= 0.0)
+    return "grid: need 0 < f_min <= f_max and step > 0";
+  if ((p.f_max_mhz - p.f_min_mhz) / p.step_mhz > GSB_MAX_GRID - 1)
+    return "profile: grid larger than GSB_MAX_GRID";
+  return "";
+}
+
 }  // namespace
 
 int gsb_set_error(gsb_ctx* ctx, int status, const std::string& msg) {
@@ -179,6 +192,35 @@ int gsb_synchronize(gsb_ctx* c) {
   return GSB_OK;
 }
 
+int gsb_malloc(gsb_ctx* c, size_t bytes, void** d_out) {
+  if (!c || !d_out) return GSB_INVALID_ARGUMENT;
+  *d_out = nullptr;
+  if (bytes == 0) return GSB_OK;
+  cudaSetDevice(c->device);
+  const cudaError_t e = cudaMalloc(d_out, bytes);
+  if (e != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, std::string("malloc: ") + cudaGetErrorString(e));
+  return GSB_OK;
+}
+
+int gsb_free(gsb_ctx* c, void* d_ptr) {
+  if (!c) return GSB_INVALID_ARGUMENT;
+  if (!d_ptr) return GSB_OK;
+  cudaSetDevice(c->device);
+  const cudaError_t e = cudaFree(d_ptr);
+  if (e != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, std::string("free: ") + cudaGetErrorString(e));
+  return GSB_OK;
+}
+
+int gsb_memcpy(gsb_ctx* c, void* dst, const void* src, size_t bytes, int kind, void* stream) {
+  if (!c || kind < 0 || kind > 2) return GSB_INVALID_ARGUMENT;
+  if (bytes == 0) return GSB_OK;
+  static const cudaMemcpyKind kinds[3] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost,
+                                          cudaMemcpyDeviceToDevice};
+  const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kinds[kind], gsb_pick_stream(c, stream));
+  if (e != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, std::string("memcpy: ") + cudaGetErrorString(e));
+  return GSB_OK;
+}
+
 int gsb_profile_validate(const gsb_profile* p, char* msg, size_t cap) {
   if (!p) return GSB_INVALID_ARGUMENT;
   const std::string m = validate_profile(*p);
@@ -235,12 +277,16 @@ int gsb_routing_validate(const gsb_route_cfg* cfg, int n_prefill_workers,
 }
 
 int gsb_set_profiles(gsb_ctx* ctx, int n, const gsb_profile* profiles) {
+  return gsb_set_profiles_ex(ctx, n, profiles, 0);
+}
+
+int gsb_set_profiles_ex(gsb_ctx* ctx, int n, const gsb_profile* profiles, int flags) {
   if (!ctx || n < 1 || n > GSB_MAX_PROFILES || !profiles)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "set_profiles: need 1..4 profiles");
   std::vector<gsb::ProfTab> tabs(GSB_MAX_PROFILES);
   for (int p = 0; p < n; ++p) {
     const gsb_profile& pr = profiles[p];
-    const std::string m = validate_profile(pr);
+    const std::string m = (flags & GSB_PROFILES_UNCHECKED) ? structural_check(pr) : validate_profile(pr);
     if (!m.empty()) return gsb_set_error(ctx, GSB_MODEL_ERROR, m);
     gsb::ProfTab& t = tabs[static_cast<size_t>(p)];
     std::memset(&t, 0, sizeof t);

@@ -47,6 +47,32 @@ __device__ bool steady_tbt(const gsb_profile& p, double tps, double f, int max_b
   return true;
 }
 
+// decode_steady_state (decode_ctl.cpp:28-50) for a batch of (tps, f, max_batch) points
+__global__ void k_steady(int64_t n, const gsb_profile* __restrict__ prof, const double* __restrict__ tps,
+                         const double* __restrict__ f, const int32_t* __restrict__ max_batch,
+                         uint8_t* __restrict__ sust, double* __restrict__ batch, double* __restrict__ tbt) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const gsb_profile p = *prof;
+  const double fr = p.dec_f_ref_mhz / f[i];
+  const double s0 = p.dec_alpha0_ms + p.dec_beta0_ms * fr;
+  const double s1 = p.dec_alpha1_ms + p.dec_beta1_ms * fr;
+  const int mb = max_batch[i];
+  const double cap_tps = 1000.0 * mb / (s0 + s1 * mb);
+  if (tps[i] > cap_tps) {
+    sust[i] = 0;
+    batch[i] = mb;
+    tbt[i] = s0 + s1 * mb;
+    return;
+  }
+  const double denom = 1000.0 - tps[i] * s1;
+  double b = denom > 0 ? tps[i] * s0 / denom : static_cast<double>(mb);
+  b = std_clamp(b, 1.0, static_cast<double>(mb));
+  sust[i] = 1;
+  batch[i] = b;
+  tbt[i] = s0 + s1 * b;
+}
+
 // build_band_table, decode_ctl.cpp:76-111: one lane per (table, level), clocks ascending,
 // strict '<' on energy per token P(f)/level.
 __global__ void k_band_tables(const __grid_constant__ BandParams a) {
@@ -119,7 +145,7 @@ __device__ __forceinline__ void emit(Ctl<COUNTS>& c, const gsb_replay_args& a, g
 #pragma unroll
     for (int k = 0; k < 8; ++k) c.cnt[k] += action == k ? 1 : 0;
   }
-  if (RECORDS && c.n_rec < a.rec_cap) {
+  if (RECORDS && rec && c.n_rec < a.rec_cap) {
     gsb_decision& r = rec[c.n_rec];
     r.tick_ms = now;
     r.tps = c.last_tps;
@@ -171,6 +197,133 @@ __device__ __forceinline__ int fine_dir(double p95, double den, double r, double
   return m > U ? +1 : (m < L ? -1 : 0);
 }
 
+// Per-trajectory constants of the controller (decode_ctl.hpp:13-29 plus derived values).
+struct CtlK {
+  double den, rden, U, succU, L, predL, delta, step, f_min, f_max, tps_scale, bias;
+  int hysteresis, NB;
+  const double* tps_hi;
+};
+
+__device__ __forceinline__ CtlK make_k(const gsb_ctl_cfg& cfg, int NB, const double* tps_hi,
+                                       double f_min, double f_max) {
+  CtlK k;
+  k.den = cfg.margin_decode * cfg.tslo_ms;
+  k.rden = 1.0 / k.den;
+  k.U = cfg.upper_margin;
+  k.L = cfg.lower_margin;
+  k.succU = next_up(k.U);
+  k.predL = -next_up(-k.L);
+  // dir * delta of decode_ctl.cpp:159-160 as a select: (+1)*d = d, (-1)*d = -d, 0*d = +0
+  k.delta = std_min(cfg.step_mhz, cfg.max_step_mhz);
+  k.step = cfg.step_mhz;
+  k.f_min = f_min;
+  k.f_max = f_max;
+  k.tps_scale = cfg.tps_scale;
+  k.bias = cfg.bias_threshold;
+  k.hysteresis = cfg.hysteresis_count;
+  k.NB = NB;
+  k.tps_hi = tps_hi;
+  return k;
+}
+
+// DecodeController ctor (decode_ctl.cpp:130-140): start in the top bucket at its f_opt
+template <bool COUNTS>
+__device__ __forceinline__ void ctl_init(Ctl<COUNTS>& c, const double* f_opt, const CtlK& k) {
+  c.current = k.NB - 1;
+  c.pending = -1;
+  c.consecutive = 0;
+  load_band(c, f_opt, c.current, k.step, k.f_min, k.f_max);
+  c.sp = f_opt[c.current];
+  c.last_tps = 0.0;
+  c.last_p95 = 0.0;
+  c.adj_total = c.adj_up = c.adj_dn = 0;
+  c.digest = 0xcbf29ce484222325ull;
+  c.n_rec = 0;
+  if (COUNTS) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c.cnt[q] = 0;
+  }
+  c.sum_cmd = 0.0;
+  c.n_fine = 0;
+}
+
+// on_coarse_tick, decode_ctl.cpp:169-198
+template <bool COUNTS, bool RECORDS>
+__device__ __forceinline__ void on_coarse(Ctl<COUNTS>& c, double* f_opt, const CtlK& k,
+                                          double worker_tps, double now,
+                                          const gsb_replay_args& a, gsb_decision* rec, int worker) {
+  c.last_tps = worker_tps * k.tps_scale;
+  int observed = k.NB - 1;
+  for (int b = k.NB - 1; b >= 0; --b)
+    if (c.last_tps <= k.tps_hi[b]) observed = b;  // first bucket with tps <= tps_hi
+  int action;
+  if (observed == c.current) {
+    c.pending = -1;
+    c.consecutive = 0;
+    action = A_CHOLD;
+  } else {
+    if (observed == c.pending) {
+      ++c.consecutive;
+    } else {
+      c.pending = observed;
+      c.consecutive = 1;
+    }
+    if (c.consecutive >= k.hysteresis) {
+      c.current = observed;
+      load_band(c, f_opt, c.current, k.step, k.f_min, k.f_max);
+      c.sp = std_clamp(c.sp, c.lo, c.hi);
+      c.pending = -1;
+      c.consecutive = 0;
+      c.adj_total = c.adj_up = c.adj_dn = 0;  // adjustments_.clear()
+      action = A_CCOMMIT;
+    } else {
+      action = A_CPEND;
+    }
+  }
+  emit<COUNTS, RECORDS>(c, a, rec, worker, now, observed, action);
+}
+
+// on_adapt_tick, decode_ctl.cpp:200-228 (adjustments_ is only read as three counts)
+template <bool COUNTS, bool RECORDS>
+__device__ __forceinline__ void on_adapt(Ctl<COUNTS>& c, double* f_opt, const CtlK& k, double now,
+                                         const gsb_replay_args& a, gsb_decision* rec, int worker) {
+  const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
+  c.adj_total = c.adj_up = c.adj_dn = 0;
+  if (total == 0) return;
+  int shift = 0;
+  if (up > k.bias * total)
+    shift = +1;
+  else if (dn > k.bias * total)
+    shift = -1;
+  if (shift == 0) return;
+  f_opt[c.current] = std_clamp(f_opt[c.current] + shift * k.step, k.f_min, k.f_max);
+  load_band(c, f_opt, c.current, k.step, k.f_min, k.f_max);
+  c.sp = std_clamp(c.sp, c.lo, c.hi);
+  emit<COUNTS, RECORDS>(c, a, rec, worker, now, c.current, shift > 0 ? A_AUP : A_ADOWN);
+}
+
+// on_fine_tick, decode_ctl.cpp:148-167
+template <bool COUNTS, bool RECORDS>
+__device__ __forceinline__ void on_fine(Ctl<COUNTS>& c, const CtlK& k, bool has, double p95,
+                                        double now, const gsb_replay_args& a, gsb_decision* rec,
+                                        int worker) {
+  int dir = 0;
+  if (has) {
+    c.last_p95 = p95;
+    dir = fine_dir(p95, k.den, k.rden, k.U, k.succU, k.L, k.predL);
+  }
+  const double raw = c.sp + (dir > 0 ? k.delta : (dir < 0 ? -k.delta : 0.0));
+  const double clamped = std_clamp(raw, c.lo, c.hi);
+  const bool hit = dir != 0 && clamped != raw;
+  c.sp = clamped;
+  c.adj_total += 1;
+  c.adj_up += (hit && dir > 0) ? 1 : 0;
+  c.adj_dn += (hit && dir < 0) ? 1 : 0;
+  c.sum_cmd = c.sum_cmd + c.sp;
+  c.n_fine += 1;
+  emit<COUNTS, RECORDS>(c, a, rec, worker, now, c.current, dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
+}
+
 template <bool COUNTS, bool RECORDS>
 __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ ReplayParams rp) {
   const gsb_replay_args& a = rp.a;
@@ -181,37 +334,12 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   const int64_t tb = a.d_table_of[n];
   const int64_t s = a.d_stream_of[n];
   const int worker = a.d_worker[n];
-  const double* tps_hi = a.d_tps_hi + tb * NB;
   double f_opt[GSB_MAX_BUCKETS];  // per-controller copy; adaptation mutates it (decode_ctl.hpp:132)
   for (int b = 0; b < NB; ++b) f_opt[b] = a.d_f_opt[tb * NB + b];
   gsb_decision* rec = RECORDS ? a.d_records + n * a.rec_cap : nullptr;
-  const double f_min = a.f_min_mhz, f_max = a.f_max_mhz, step = cfg.step_mhz;
-
-  // DecodeController ctor (decode_ctl.cpp:130-140): start in the top bucket at its f_opt
+  const CtlK k = make_k(cfg, NB, a.d_tps_hi + tb * NB, a.f_min_mhz, a.f_max_mhz);
   Ctl<COUNTS> c;
-  c.current = NB - 1;
-  c.pending = -1;
-  c.consecutive = 0;
-  load_band(c, f_opt, c.current, step, f_min, f_max);
-  c.sp = f_opt[c.current];
-  c.last_tps = 0.0;
-  c.last_p95 = 0.0;
-  c.adj_total = c.adj_up = c.adj_dn = 0;
-  c.digest = 0xcbf29ce484222325ull;
-  c.n_rec = 0;
-  if (COUNTS) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c.cnt[k] = 0;
-  }
-  c.sum_cmd = 0.0;
-  c.n_fine = 0;
-
-  const double den = cfg.margin_decode * cfg.tslo_ms;
-  const double rden = 1.0 / den;
-  const double U = cfg.upper_margin, L = cfg.lower_margin;
-  const double succU = next_up(U), predL = -next_up(-L);
-  // dir * delta of decode_ctl.cpp:159-160 as a select: (+1)*d = d, (-1)*d = -d, 0*d = +0
-  const double delta = std_min(cfg.step_mhz, cfg.max_step_mhz);
+  ctl_init(c, f_opt, k);
   const double adapt_period = cfg.adapt_period_s * 1000.0;
   const uint8_t* __restrict__ fine_has = a.d_fine_has + s * rp.n_fine;
   const double* __restrict__ fine_p95 = a.d_fine_p95 + s * rp.n_fine;
@@ -227,6 +355,20 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
     pr[j] = j < nf ? fine_p95[j] : 0.0;
     hr[j] = j < nf ? fine_has[j] : 0;
   }
+  auto fine_tick = [&](int64_t kf, double now) {
+    const bool has = hr[0] != 0;
+    const double p95 = pr[0];
+    pr[0] = pr[1];
+    pr[1] = pr[2];
+    pr[2] = pr[3];
+    hr[0] = hr[1];
+    hr[1] = hr[2];
+    hr[2] = hr[3];
+    const int64_t nxt = kf + 4;
+    pr[3] = nxt < nf ? fine_p95[nxt] : 0.0;
+    hr[3] = nxt < nf ? fine_has[nxt] : 0;
+    on_fine<COUNTS, RECORDS>(c, k, has, p95, now, a, rec, worker);
+  };
 
   // Tick driver (simkernel.cpp:243-248,441-464): next instant = min of the three schedules,
   // at equal times coarse (kind 5) < adapt (6) < fine (7). Generic in the tick type: when all
@@ -242,86 +384,15 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
       if (t > t_end) break;
       const double td = static_cast<double>(t);
       if (tc == t) {
-        // on_coarse_tick, decode_ctl.cpp:169-198
-        c.last_tps = coarse_tps[kc++] * cfg.tps_scale;
-        int observed = NB - 1;
-        for (int b = NB - 1; b >= 0; --b)
-          if (c.last_tps <= tps_hi[b]) observed = b;  // first bucket with tps <= tps_hi
-        int action;
-        if (observed == c.current) {
-          c.pending = -1;
-          c.consecutive = 0;
-          action = A_CHOLD;
-        } else {
-          if (observed == c.pending) {
-            ++c.consecutive;
-          } else {
-            c.pending = observed;
-            c.consecutive = 1;
-          }
-          if (c.consecutive >= cfg.hysteresis_count) {
-            c.current = observed;
-            load_band(c, f_opt, c.current, step, f_min, f_max);
-            c.sp = std_clamp(c.sp, c.lo, c.hi);
-            c.pending = -1;
-            c.consecutive = 0;
-            c.adj_total = c.adj_up = c.adj_dn = 0;  // adjustments_.clear()
-            action = A_CCOMMIT;
-          } else {
-            action = A_CPEND;
-          }
-        }
-        emit<COUNTS, RECORDS>(c, a, rec, worker, td, observed, action);
+        on_coarse<COUNTS, RECORDS>(c, f_opt, k, coarse_tps[kc++], td, a, rec, worker);
         tc = t + coarse_p;
       }
       if (ta == t) {
-        // on_adapt_tick, decode_ctl.cpp:200-228
-        const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
-        c.adj_total = c.adj_up = c.adj_dn = 0;
-        if (total != 0) {
-          int shift = 0;
-          if (up > cfg.bias_threshold * total)
-            shift = +1;
-          else if (dn > cfg.bias_threshold * total)
-            shift = -1;
-          if (shift != 0) {
-            f_opt[c.current] = std_clamp(f_opt[c.current] + shift * step, f_min, f_max);
-            load_band(c, f_opt, c.current, step, f_min, f_max);
-            c.sp = std_clamp(c.sp, c.lo, c.hi);
-            emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current, shift > 0 ? A_AUP : A_ADOWN);
-          }
-        }
+        on_adapt<COUNTS, RECORDS>(c, f_opt, k, td, a, rec, worker);
         ta = t + adapt_p;
       }
       if (tf == t) {
-        // on_fine_tick, decode_ctl.cpp:148-167
-        int dir = 0;
-        const double p95 = pr[0];
-        if (hr[0]) {
-          c.last_p95 = p95;
-          dir = fine_dir(p95, den, rden, U, succU, L, predL);
-        }
-        pr[0] = pr[1];
-        pr[1] = pr[2];
-        pr[2] = pr[3];
-        hr[0] = hr[1];
-        hr[1] = hr[2];
-        hr[2] = hr[3];
-        const int64_t nxt = kf + 4;
-        pr[3] = nxt < nf ? fine_p95[nxt] : 0.0;
-        hr[3] = nxt < nf ? fine_has[nxt] : 0;
-        ++kf;
-        const double raw = c.sp + (dir > 0 ? delta : (dir < 0 ? -delta : 0.0));
-        const double clamped = std_clamp(raw, c.lo, c.hi);
-        const bool hit = dir != 0 && clamped != raw;
-        c.sp = clamped;
-        c.adj_total += 1;
-        c.adj_up += (hit && dir > 0) ? 1 : 0;
-        c.adj_dn += (hit && dir < 0) ? 1 : 0;
-        c.sum_cmd = c.sum_cmd + c.sp;
-        c.n_fine += 1;
-        emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current,
-                              dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
+        fine_tick(kf++, td);
         tf = t + fine_p;
       }
     }
@@ -331,85 +402,18 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   // fine ticks k = 1..nf with two down-counters; same event order (coarse, adapt, fine).
   auto run_aligned = [&](int64_t fine_p, int64_t rc, int64_t ra, int64_t nticks) {
     int64_t cc = rc, ca = ra, kc = 0;
-    for (int64_t k = 1; k <= nticks; ++k) {
-      const double td = RECORDS ? static_cast<double>(k * fine_p) : 0.0;
+    for (int64_t q = 1; q <= nticks; ++q) {
+      const double td = RECORDS ? static_cast<double>(q * fine_p) : 0.0;
       if (--cc == 0) {
         cc = rc;
-        c.last_tps = coarse_tps[kc++] * cfg.tps_scale;
-        int observed = NB - 1;
-        for (int b = NB - 1; b >= 0; --b)
-          if (c.last_tps <= tps_hi[b]) observed = b;
-        int action;
-        if (observed == c.current) {
-          c.pending = -1;
-          c.consecutive = 0;
-          action = A_CHOLD;
-        } else {
-          if (observed == c.pending) {
-            ++c.consecutive;
-          } else {
-            c.pending = observed;
-            c.consecutive = 1;
-          }
-          if (c.consecutive >= cfg.hysteresis_count) {
-            c.current = observed;
-            load_band(c, f_opt, c.current, step, f_min, f_max);
-            c.sp = std_clamp(c.sp, c.lo, c.hi);
-            c.pending = -1;
-            c.consecutive = 0;
-            c.adj_total = c.adj_up = c.adj_dn = 0;
-            action = A_CCOMMIT;
-          } else {
-            action = A_CPEND;
-          }
-        }
-        emit<COUNTS, RECORDS>(c, a, rec, worker, td, observed, action);
+        on_coarse<COUNTS, RECORDS>(c, f_opt, k, coarse_tps[kc++], td, a, rec, worker);
       }
       if (--ca == 0) {
         ca = ra;
-        const int total = c.adj_total, up = c.adj_up, dn = c.adj_dn;
-        c.adj_total = c.adj_up = c.adj_dn = 0;
-        if (total != 0) {
-          int shift = 0;
-          if (up > cfg.bias_threshold * total)
-            shift = +1;
-          else if (dn > cfg.bias_threshold * total)
-            shift = -1;
-          if (shift != 0) {
-            f_opt[c.current] = std_clamp(f_opt[c.current] + shift * step, f_min, f_max);
-            load_band(c, f_opt, c.current, step, f_min, f_max);
-            c.sp = std_clamp(c.sp, c.lo, c.hi);
-            emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current, shift > 0 ? A_AUP : A_ADOWN);
-          }
-        }
+        on_adapt<COUNTS, RECORDS>(c, f_opt, k, td, a, rec, worker);
       }
-      int dir = 0;
-      const double p95 = pr[0];
-      if (hr[0]) {
-        c.last_p95 = p95;
-        dir = fine_dir(p95, den, rden, U, succU, L, predL);
-      }
-      pr[0] = pr[1];
-      pr[1] = pr[2];
-      pr[2] = pr[3];
-      hr[0] = hr[1];
-      hr[1] = hr[2];
-      hr[2] = hr[3];
-      const int64_t nxt = k + 3;  // fine tick index k-1 is consumed now
-      pr[3] = nxt < nf ? fine_p95[nxt] : 0.0;
-      hr[3] = nxt < nf ? fine_has[nxt] : 0;
-      const double raw = c.sp + (dir > 0 ? delta : (dir < 0 ? -delta : 0.0));
-      const double clamped = std_clamp(raw, c.lo, c.hi);
-      const bool hit = dir != 0 && clamped != raw;
-      c.sp = clamped;
-      c.adj_total += 1;
-      c.adj_up += (hit && dir > 0) ? 1 : 0;
-      c.adj_dn += (hit && dir < 0) ? 1 : 0;
-      c.sum_cmd = c.sum_cmd + c.sp;
-      emit<COUNTS, RECORDS>(c, a, rec, worker, td, c.current,
-                            dir > 0 ? A_UP : (dir < 0 ? A_DOWN : A_HOLD));
+      fine_tick(q - 1, td);
     }
-    c.n_fine = nticks;
   };
   auto whole_ms = [](double x) { return x >= 1.0 && x < 2147483648.0 && x == rint(x); };
   const bool int_sched = whole_ms(cfg.fine_period_ms) && whole_ms(cfg.coarse_period_ms) &&
@@ -421,8 +425,7 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   if (int_sched && ci % fi == 0 && ai % fi == 0) {
     run_aligned(fi, ci / fi, ai / fi, static_cast<int64_t>(floor(a.t_end_ms)) / fi);
   } else if (int_sched) {
-    run(static_cast<int64_t>(cfg.fine_period_ms), static_cast<int64_t>(cfg.coarse_period_ms),
-        static_cast<int64_t>(adapt_period), static_cast<int64_t>(floor(a.t_end_ms)));
+    run(fi, ci, ai, static_cast<int64_t>(floor(a.t_end_ms)));
   } else {
     run(cfg.fine_period_ms, cfg.coarse_period_ms, adapt_period, a.t_end_ms);
   }
@@ -430,9 +433,82 @@ __global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ R
   a.d_n_rec[n] = c.n_rec;
   if (COUNTS) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a.d_counts[n * 8 + k] = c.cnt[k];
+    for (int q = 0; q < 8; ++q) a.d_counts[n * 8 + q] = c.cnt[q];
   }
   if (a.d_mean_cmd) a.d_mean_cmd[n] = c.n_fine ? c.sum_cmd / static_cast<double>(c.n_fine) : 0.0;
+}
+
+// ---------------------------------------------------------------- K3s: scripted controller
+// The reference's DecodeController API takes arbitrary call sequences (tests drive it with
+// explicit times and values, proj/tests/test_decode_ctl.cpp). One lane per controller walks
+// its script of (kind, t, value, has) calls through the same handlers as K3b.
+struct ScriptParams {
+  gsb_replay_args a;  // n_traj, d_cfg, d_table_of, d_worker, n_buckets, d_tps_hi, d_f_opt,
+                      // f_min/f_max, d_digest, d_n_rec, d_records, rec_cap
+  const int64_t* ev_off;
+  const int8_t* kind;  // 0 fine, 1 coarse, 2 adapt
+  const double* t;
+  const double* value;
+  const uint8_t* has;
+  gsb_ctl_state* state;  // optional, in/out
+};
+
+__global__ void __launch_bounds__(128) k_decode_script(const __grid_constant__ ScriptParams sp) {
+  const gsb_replay_args& a = sp.a;
+  const int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (n >= a.n_traj) return;
+  const gsb_ctl_cfg cfg = a.d_cfg[n];
+  const int NB = a.n_buckets;
+  const int64_t tb = a.d_table_of[n];
+  const int worker = a.d_worker[n];
+  gsb_ctl_state* st = sp.state ? sp.state + n : nullptr;
+  const bool resume = st && st->initialized;
+  double f_opt[GSB_MAX_BUCKETS];
+  for (int b = 0; b < NB; ++b) f_opt[b] = resume ? st->f_opt[b] : a.d_f_opt[tb * NB + b];
+  gsb_decision* rec = a.d_records ? a.d_records + n * a.rec_cap : nullptr;
+  const CtlK k = make_k(cfg, NB, a.d_tps_hi + tb * NB, a.f_min_mhz, a.f_max_mhz);
+  Ctl<false> c;
+  ctl_init(c, f_opt, k);
+  if (resume) {
+    c.lo = st->band_lo;
+    c.hi = st->band_hi;
+    c.sp = st->set_point;
+    c.last_tps = st->last_tps;
+    c.last_p95 = st->last_p95;
+    c.current = st->current_bucket;
+    c.pending = st->pending_bucket;
+    c.consecutive = st->consecutive;
+    c.adj_total = st->adj_total;
+    c.adj_up = st->adj_up;
+    c.adj_dn = st->adj_down;
+  }
+  for (int64_t e = sp.ev_off[n]; e < sp.ev_off[n + 1]; ++e) {
+    const double now = sp.t[e];
+    if (sp.kind[e] == 1)
+      on_coarse<false, true>(c, f_opt, k, sp.value[e], now, a, rec, worker);
+    else if (sp.kind[e] == 2)
+      on_adapt<false, true>(c, f_opt, k, now, a, rec, worker);
+    else
+      on_fine<false, true>(c, k, sp.has[e] != 0, sp.value[e], now, a, rec, worker);
+  }
+  a.d_digest[n] = c.digest;
+  a.d_n_rec[n] = c.n_rec;
+  if (st) {
+    st->band_lo = c.lo;
+    st->band_hi = c.hi;
+    st->set_point = c.sp;
+    st->last_tps = c.last_tps;
+    st->last_p95 = c.last_p95;
+    st->current_bucket = c.current;
+    st->pending_bucket = c.pending;
+    st->consecutive = c.consecutive;
+    st->adj_total = c.adj_total;
+    st->adj_up = c.adj_up;
+    st->adj_down = c.adj_dn;
+    st->initialized = 1;
+    st->pad_ = 0;
+    for (int b = 0; b < NB; ++b) st->f_opt[b] = f_opt[b];
+  }
 }
 
 }  // namespace
@@ -453,6 +529,29 @@ int gsb_build_band_tables(gsb_ctx* ctx, int64_t n_tables, const gsb_profile* d_p
   const int64_t n = n_tables * n_levels;
   k_band_tables<<<static_cast<unsigned>((n + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(bp);
   return gsb_check_launch(ctx, "band_tables");
+}
+
+int gsb_steady_state_batch(gsb_ctx* ctx, int64_t n, const gsb_profile* d_profile,
+                           const double* d_tps, const double* d_f, const int32_t* d_max_batch,
+                           uint8_t* d_sustainable, double* d_batch, double* d_tbt, void* stream) {
+  if (!ctx) return GSB_INVALID_ARGUMENT;
+  if (n <= 0) return GSB_OK;
+  k_steady<<<static_cast<unsigned>((n + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(
+      n, d_profile, d_tps, d_f, d_max_batch, d_sustainable, d_batch, d_tbt);
+  return gsb_check_launch(ctx, "steady_state");
+}
+
+int gsb_decode_script(gsb_ctx* ctx, const gsb_replay_args* a, const int64_t* d_ev_off,
+                      const int8_t* d_kind, const double* d_t, const double* d_value,
+                      const uint8_t* d_has, gsb_ctl_state* d_state, void* stream) {
+  if (!ctx || !a) return GSB_INVALID_ARGUMENT;
+  if (a->n_buckets < 1 || a->n_buckets > GSB_MAX_BUCKETS)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "band table: need 1..32 buckets");
+  if (a->n_traj <= 0) return GSB_OK;
+  ScriptParams sp{*a, d_ev_off, d_kind, d_t, d_value, d_has, d_state};
+  k_decode_script<<<static_cast<unsigned>((a->n_traj + 127) / 128), 128, 0,
+                    gsb_pick_stream(ctx, stream)>>>(sp);
+  return gsb_check_launch(ctx, "decode_script");
 }
 
 int gsb_decode_replay(gsb_ctx* ctx, const gsb_replay_args* a, void* stream) {

@@ -694,9 +694,106 @@ int check_route_cfg(gsb_ctx* ctx, const gsb_route_cfg* cfg) {
   return GSB_OK;
 }
 
+// ---------------------------------------------------------------- single-call entry kernels
+// classify() for a flat prompt array (router.cpp:26-31); thresholds by value, unused = INT_MAX.
+struct Thr {
+  int32_t t[GSB_MAX_CLASSES - 1];
+};
+
+__global__ void k_classify(Thr th, int64_t n, const int32_t* __restrict__ prompt,
+                           int32_t* __restrict__ cls) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t L = prompt[i];
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) c += th.t[k] < L ? 1 : 0;
+    cls[i] = c;
+  }
+}
+
+// PrefillBatch::t_ref_total_ms under a bare LatencyModel (prefill_opt.cpp:9-14)
+__global__ void k_t_ref_batches(double la, double lb, double lc, int64_t n_batches,
+                                const int64_t* __restrict__ off, const int32_t* __restrict__ prompt,
+                                const double* __restrict__ wf, double* __restrict__ out) {
+  const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (b >= n_batches) return;
+  double T = 0.0;
+  for (int64_t j = off[b]; j < off[b + 1]; ++j) {
+    const double L = static_cast<double>(prompt[j]);
+    T = T + (wf ? wf[j] : 1.0) * ((la * L + lb) * L + lc);
+  }
+  out[b] = T;
+}
+
+// energy_total_closed_form_j (prefill_opt.cpp:33-43), same operation order
+__global__ void k_energy_closed_form(const ProfTab* __restrict__ tab, int64_t n_batches,
+                                     const int64_t* __restrict__ off,
+                                     const int32_t* __restrict__ prompt,
+                                     const double* __restrict__ wf, const double* __restrict__ f_mhz,
+                                     const double* __restrict__ window, double* __restrict__ out) {
+  const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (b >= n_batches) return;
+  const double f = f_mhz[b];
+  const double k = (f - tab->f_min) / tab->step;
+  if (f < tab->f_min - 1e-9 || f > tab->f_max + 1e-9 || !(fabs(k - rint(k)) < 1e-9)) {
+    out[b] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double T = 0.0;
+  for (int64_t j = off[b]; j < off[b + 1]; ++j) {
+    const double L = static_cast<double>(prompt[j]);
+    T = T + (wf ? wf[j] : 1.0) * ((tab->lat_a * L + tab->lat_b) * L + tab->lat_c);
+  }
+  const double fT = tab->f_ref * T;
+  const double poly = tab->k3 * f * f + tab->k2 * f + tab->k1 + tab->k0 / f;
+  const double active = fT * poly / 1000.0;
+  const double idle = tab->p_idle * (window[b] - fT / f) / 1000.0;
+  out[b] = active + idle;
+}
+
 }  // namespace
 
 extern "C" {
+
+int gsb_classify(gsb_ctx* ctx, int n_thresholds, const int32_t* thresholds, int64_t n,
+                 const int32_t* d_prompt, int32_t* d_class, void* stream) {
+  if (!ctx) return GSB_INVALID_ARGUMENT;
+  if (n_thresholds < 0 || n_thresholds > GSB_MAX_CLASSES - 1 || (n_thresholds && !thresholds))
+    return gsb_set_error(ctx, GSB_ROUTER_ERROR, "routing: more than 7 thresholds");
+  if (n <= 0) return GSB_OK;
+  Thr th;
+  for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) th.t[k] = k < n_thresholds ? thresholds[k] : INT_MAX;
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_classify<<<blocks, 256, 0, gsb_pick_stream(ctx, stream)>>>(th, n, d_prompt, d_class);
+  return gsb_check_launch(ctx, "classify");
+}
+
+int gsb_t_ref_batches(gsb_ctx* ctx, const double lat_abc[3], int64_t n_batches,
+                      const int64_t* d_off, const int32_t* d_prompt, const double* d_wf,
+                      double* d_out, void* stream) {
+  if (!ctx || !lat_abc) return GSB_INVALID_ARGUMENT;
+  if (n_batches <= 0) return GSB_OK;
+  k_t_ref_batches<<<static_cast<unsigned>((n_batches + 255) / 256), 256, 0,
+                    gsb_pick_stream(ctx, stream)>>>(lat_abc[0], lat_abc[1], lat_abc[2], n_batches,
+                                                   d_off, d_prompt, d_wf, d_out);
+  return gsb_check_launch(ctx, "t_ref_batches");
+}
+
+int gsb_energy_closed_form_batches(gsb_ctx* ctx, int profile, int64_t n_batches,
+                                   const int64_t* d_off, const int32_t* d_prompt,
+                                   const double* d_wf, const double* d_f_mhz,
+                                   const double* d_window, double* d_out, void* stream) {
+  if (!ctx) return GSB_INVALID_ARGUMENT;
+  if (profile < 0 || profile >= ctx->n_profiles)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "energy_closed_form: bad profile index");
+  if (n_batches <= 0) return GSB_OK;
+  k_energy_closed_form<<<static_cast<unsigned>((n_batches + 255) / 256), 256, 0,
+                         gsb_pick_stream(ctx, stream)>>>(
+      static_cast<const ProfTab*>(ctx->d_tabs) + profile, n_batches, d_off, d_prompt, d_wf,
+      d_f_mhz, d_window, d_out);
+  return gsb_check_launch(ctx, "energy_closed_form");
+}
 
 int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
                       const int64_t* d_arrival, int64_t* d_bounds, void* stream) {

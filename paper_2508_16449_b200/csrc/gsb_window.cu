@@ -219,3 +219,85 @@ extern "C" int gsb_window_series(gsb_ctx* ctx, const gsb_telemetry* tel, int tbt
   }
   return GSB_OK;
 }
+
+// ---------------------------------------------------------------- batched quantile / TPS
+namespace {
+
+constexpr int kQMax = 4096;
+
+// One CTA per set: stage <= 4096 samples in shared memory (padded with +inf to a power of two),
+// bitonic sort, read sorted[ceil(q n) - 1] (rank 0 -> minimum), metrics.cpp:14-18.
+__global__ void __launch_bounds__(256) k_quantile(double q, int64_t n_sets,
+                                                  const int64_t* __restrict__ off,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ out) {
+  __shared__ double s[kQMax];
+  const int64_t set = blockIdx.x;
+  if (set >= n_sets) return;
+  const int64_t b0 = off[set], n64 = off[set + 1] - b0;
+  if (n64 <= 0 || n64 > kQMax) {
+    if (threadIdx.x == 0) out[set] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const int n = static_cast<int>(n64);
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s[i] = i < n ? x[b0 + i] : INFINITY;
+  __syncthreads();
+  for (int kk = 2; kk <= m; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & kk) == 0;
+          const double a = s[i], b = s[p];
+          if ((a > b) == up) {
+            s[i] = b;
+            s[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    const int64_t rank = static_cast<int64_t>(ceil(q * static_cast<double>(n)));
+    out[set] = s[rank == 0 ? 0 : rank - 1];
+  }
+}
+
+__global__ void k_tps_window(int64_t n, const int64_t* __restrict__ off, const double* __restrict__ t,
+                             const int32_t* __restrict__ tokens, const double* __restrict__ window,
+                             const double* __restrict__ now, double* __restrict__ out) {
+  const int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (w >= n) return;
+  const double thr = now[w] - window[w];
+  int64_t j = off[w];
+  const int64_t e = off[w + 1];
+  while (j < e && t[j] < thr) ++j;  // front pops (events are time-sorted)
+  int sum = 0;
+  for (; j < e; ++j) sum += tokens[j];
+  out[w] = sum * 1000.0 / window[w];
+}
+
+}  // namespace
+
+extern "C" int gsb_quantile_batch(gsb_ctx* ctx, double q, int64_t n_sets, const int64_t* d_off,
+                                  const double* d_samples, double* d_out, void* stream) {
+  if (!ctx) return GSB_INVALID_ARGUMENT;
+  if (!(q >= 0.0 && q <= 1.0)) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "quantile: q outside [0, 1]");
+  if (n_sets <= 0) return GSB_OK;
+  k_quantile<<<static_cast<unsigned>(n_sets), 256, 0, gsb_pick_stream(ctx, stream)>>>(q, n_sets, d_off,
+                                                                                     d_samples, d_out);
+  return gsb_check_launch(ctx, "quantile");
+}
+
+extern "C" int gsb_tps_window_batch(gsb_ctx* ctx, int64_t n, const int64_t* d_off, const double* d_t,
+                                    const int32_t* d_tokens, const double* d_window_ms,
+                                    const double* d_now, double* d_out, void* stream) {
+  if (!ctx) return GSB_INVALID_ARGUMENT;
+  if (n <= 0) return GSB_OK;
+  k_tps_window<<<static_cast<unsigned>((n + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(
+      n, d_off, d_t, d_tokens, d_window_ms, d_now, d_out);
+  return gsb_check_launch(ctx, "tps_window");
+}
