@@ -107,6 +107,9 @@ int gsb_set_profiles(gsb_ctx* ctx, int n_profiles, const gsb_profile* profiles);
  * reference's evaluators never validate their profile argument (prefill_opt.cpp:16-56), and its
  * tests call them with profiles validate() rejects (flat power, test_prefill_opt.cpp:98,135). */
 #define GSB_PROFILES_UNCHECKED 1
+/* flags & GSB_PROFILES_ASYNC: return without waiting for the (pinned, stream-ordered) table
+ * upload; valid when every later launch uses the context's own stream (stream == NULL). */
+#define GSB_PROFILES_ASYNC 2
 int gsb_set_profiles_ex(gsb_ctx* ctx, int n_profiles, const gsb_profile* profiles, int flags);
 
 /* ---------------------------------------------------------------- device memory */
@@ -117,6 +120,9 @@ int gsb_set_profiles_ex(gsb_ctx* ctx, int n_profiles, const gsb_profile* profile
  * device->host result. */
 int gsb_malloc(gsb_ctx* ctx, size_t bytes, void** d_out);
 int gsb_free(gsb_ctx* ctx, void* d_ptr);
+/* Page-locked host memory (asynchronous DMA for gsb_memcpy). */
+int gsb_host_alloc(gsb_ctx* ctx, size_t bytes, void** h_out);
+int gsb_host_free(gsb_ctx* ctx, void* h_ptr);
 int gsb_memcpy(gsb_ctx* ctx, void* dst, const void* src, size_t bytes, int kind, void* stream);
 
 /* ---------------------------------------------------------------- K1: route + bin */

@@ -88,7 +88,8 @@ EXPORTS = (
     "gsb_prefill_summary", "gsb_n_ticks", "gsb_window_series", "gsb_build_band_tables",
     "gsb_decode_replay", "gsb_replay_validate", "gsb_fp64_probe", "gsb_selftest_division",
     "gsb_decode_script", "gsb_quantile_batch", "gsb_tps_window_batch", "gsb_steady_state_batch",
-    "gsb_set_profiles_ex", "gsb_malloc", "gsb_free", "gsb_memcpy", "gsb_classify",
+    "gsb_set_profiles_ex", "gsb_malloc", "gsb_free", "gsb_host_alloc", "gsb_host_free",
+    "gsb_memcpy", "gsb_classify",
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
 )
 
@@ -144,6 +145,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_set_profiles_ex.argtypes = [_p, C.c_int, _p, C.c_int]
     L.gsb_malloc.argtypes = [_p, C.c_size_t, P(_p)]
     L.gsb_free.argtypes = [_p, _p]
+    L.gsb_host_alloc.argtypes = [_p, C.c_size_t, P(_p)]
+    L.gsb_host_free.argtypes = [_p, _p]
     L.gsb_memcpy.argtypes = [_p, _p, _p, C.c_size_t, C.c_int, _p]
     L.gsb_classify.argtypes = [_p, C.c_int, _p, _i64, _p, _p, _p]
     L.gsb_t_ref_batches.argtypes = [_p, P(_d), _i64, _p, _p, _p, _p, _p]

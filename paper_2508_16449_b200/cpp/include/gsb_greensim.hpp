@@ -27,6 +27,13 @@
 #include <utility>
 #include <vector>
 
+// Request / PromptClass / TraceError and quantile() come from greensim/trace.hpp and
+// greensim/metrics.hpp: the minimal ones in ../include_min for the standalone drop-in, or the
+// reference's own when its simulator is compiled over this library (paper_2508_16449_b200/cpp/
+// Makefile, target sim).
+#include "greensim/metrics.hpp"
+#include "greensim/trace.hpp"
+
 namespace greensim {
 
 // ------------------------------------------------------------------ errors
@@ -35,11 +42,6 @@ struct ModelError : std::runtime_error {
 };
 struct RouterError : std::runtime_error {
   using std::runtime_error::runtime_error;
-};
-struct TraceError : std::runtime_error {
-  enum class Kind { EmptyTrace, NonMonotoneArrivals, MalformedRow, BadHeader, ClassMismatch, BadShape };
-  TraceError(Kind k, const std::string& msg) : std::runtime_error(msg), kind(k) {}
-  Kind kind;
 };
 // No B200 / libgsb failure (not in the reference: it has no device).
 struct GpuError : std::runtime_error {
@@ -98,17 +100,7 @@ struct GpuProfile {
 double prefill_latency_raw_ms(const LatencyModel& m, double prompt_tokens, double f);
 double decode_step_raw_ms(const DecodeStepModel& m, double batch, double f);
 
-// ------------------------------------------------------------------ requests and routing
-enum class PromptClass { ShortMedium = 0, Long = 1 };
-
-struct Request {
-  std::int64_t id = 0;
-  std::int64_t arrival_ms = 0;
-  int prompt_tokens = 0;
-  int output_tokens = 0;
-  std::optional<PromptClass> cls;
-};
-
+// ------------------------------------------------------------------ routing
 struct RoutingConfig {
   bool enabled = true;
   std::vector<int> thresholds{1024};
@@ -197,8 +189,6 @@ std::vector<PrefillFreqCommand> queue_optimizer_tick(const std::vector<ClassQueu
                                                      const GpuProfile& profile);
 
 // ------------------------------------------------------------------ decode control
-double quantile(std::span<const double> samples, double q);
-
 struct DecodeCtlConfig {
   double tslo_ms = 100.0;
   double margin_decode = 0.95;

@@ -31,6 +31,8 @@ struct Runtime {
   gsb_ctx* ctx = nullptr;
   void* d_buf = nullptr;
   size_t d_cap = 0;
+  unsigned char* h_pin = nullptr;  // page-locked mirror of d_buf (async DMA both ways)
+  size_t h_cap = 0;
   gsb_profile installed{};
   bool has_installed = false;
 };
@@ -94,27 +96,32 @@ class Call {
 
   void commit() {
     const size_t total = std::max<size_t>(image_.size(), kAlign);
-    if (total > rt_.d_cap) {
-      if (rt_.d_buf) {
-        gsb_synchronize(rt_.ctx);
-        gsb_free(rt_.ctx, rt_.d_buf);
-        rt_.d_buf = nullptr;
-        rt_.d_cap = 0;
-      }
+    if (total > rt_.d_cap) {  // every earlier call has synchronized: the buffers are idle
+      gsb_free(rt_.ctx, rt_.d_buf);
+      gsb_host_free(rt_.ctx, rt_.h_pin);
+      rt_.d_buf = nullptr;
+      rt_.h_pin = nullptr;
+      rt_.d_cap = rt_.h_cap = 0;
       const size_t cap = std::max<size_t>(total * 2, size_t{1} << 20);
       check(rt_.ctx, gsb_malloc(rt_.ctx, cap, &rt_.d_buf));
-      rt_.d_cap = cap;
+      void* h = nullptr;
+      check(rt_.ctx, gsb_host_alloc(rt_.ctx, cap, &h));
+      rt_.h_pin = static_cast<unsigned char*>(h);
+      rt_.d_cap = rt_.h_cap = cap;
     }
-    check(rt_.ctx, gsb_memcpy(rt_.ctx, rt_.d_buf, image_.data(), image_.size(), 0, nullptr));
+    std::memcpy(rt_.h_pin, image_.data(), image_.size());
+    check(rt_.ctx, gsb_memcpy(rt_.ctx, rt_.d_buf, rt_.h_pin, image_.size(), 0, nullptr));
   }
   template <class T>
   T* dev(size_t off) const { return reinterpret_cast<T*>(static_cast<unsigned char*>(rt_.d_buf) + off); }
 
   void fetch() {
-    if (first_out_ != npos && first_out_ < image_.size())
-      check(rt_.ctx, gsb_memcpy(rt_.ctx, image_.data() + first_out_, dev<unsigned char>(first_out_),
+    const bool tail = first_out_ != npos && first_out_ < image_.size();
+    if (tail)
+      check(rt_.ctx, gsb_memcpy(rt_.ctx, rt_.h_pin + first_out_, dev<unsigned char>(first_out_),
                                 image_.size() - first_out_, 1, nullptr));
     check(rt_.ctx, gsb_synchronize(rt_.ctx));
+    if (tail) std::memcpy(image_.data() + first_out_, rt_.h_pin + first_out_, image_.size() - first_out_);
   }
   template <class T>
   const T* host(size_t off) const { return reinterpret_cast<const T*>(image_.data() + off); }
@@ -123,7 +130,8 @@ class Call {
   // Unchecked: the reference's evaluators never call GpuProfile::validate.
   void install(const gsb_profile& p) {
     if (rt_.has_installed && std::memcmp(&rt_.installed, &p, sizeof p) == 0) return;
-    check(rt_.ctx, gsb_set_profiles_ex(rt_.ctx, 1, &p, GSB_PROFILES_UNCHECKED));
+    // ASYNC: every launch of this library goes to the context's stream, behind the upload
+    check(rt_.ctx, gsb_set_profiles_ex(rt_.ctx, 1, &p, GSB_PROFILES_UNCHECKED | GSB_PROFILES_ASYNC));
     rt_.installed = p;
     rt_.has_installed = true;
   }

@@ -163,7 +163,9 @@ int gsb_ctx_create(int device, gsb_ctx** out) {
   c->n_sms = prop.multiProcessorCount;
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&c->d_tabs, sizeof(gsb::ProfTab) * GSB_MAX_PROFILES) != cudaSuccess) {
+      cudaMalloc(&c->d_tabs, sizeof(gsb::ProfTab) * GSB_MAX_PROFILES) != cudaSuccess ||
+      cudaMallocHost(reinterpret_cast<void**>(&c->h_stage), sizeof(gsb::ProfTab) * GSB_MAX_PROFILES) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->stage_free, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return GSB_CUDA_ERROR;
   }
@@ -176,6 +178,8 @@ void gsb_ctx_destroy(gsb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaFree(c->d_tabs);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  if (c->stage_free) cudaEventDestroy(c->stage_free);
   cudaFree(c->d_scratch);
   cudaFree(c->d_ticks);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -208,6 +212,22 @@ int gsb_free(gsb_ctx* c, void* d_ptr) {
   cudaSetDevice(c->device);
   const cudaError_t e = cudaFree(d_ptr);
   if (e != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, std::string("free: ") + cudaGetErrorString(e));
+  return GSB_OK;
+}
+
+int gsb_host_alloc(gsb_ctx* c, size_t bytes, void** h_out) {
+  if (!c || !h_out) return GSB_INVALID_ARGUMENT;
+  *h_out = nullptr;
+  if (bytes == 0) return GSB_OK;
+  cudaSetDevice(c->device);
+  const cudaError_t e = cudaMallocHost(h_out, bytes);
+  if (e != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, std::string("host_alloc: ") + cudaGetErrorString(e));
+  return GSB_OK;
+}
+
+int gsb_host_free(gsb_ctx* c, void* h_ptr) {
+  if (!c) return GSB_INVALID_ARGUMENT;
+  if (h_ptr && cudaFreeHost(h_ptr) != cudaSuccess) return gsb_set_error(c, GSB_CUDA_ERROR, "host_free failed");
   return GSB_OK;
 }
 
@@ -283,12 +303,18 @@ int gsb_set_profiles(gsb_ctx* ctx, int n, const gsb_profile* profiles) {
 int gsb_set_profiles_ex(gsb_ctx* ctx, int n, const gsb_profile* profiles, int flags) {
   if (!ctx || n < 1 || n > GSB_MAX_PROFILES || !profiles)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "set_profiles: need 1..4 profiles");
-  std::vector<gsb::ProfTab> tabs(GSB_MAX_PROFILES);
+  for (int p = 0; p < n; ++p) {  // all-or-nothing: check every profile before touching state
+    const std::string m = (flags & GSB_PROFILES_UNCHECKED) ? structural_check(profiles[p])
+                                                           : validate_profile(profiles[p]);
+    if (!m.empty()) return gsb_set_error(ctx, GSB_MODEL_ERROR, m);
+  }
+  cudaSetDevice(ctx->device);
+  // the pinned staging area is reused: wait until the previous upload has read it
+  if (cudaEventSynchronize(ctx->stage_free) != cudaSuccess)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "set_profiles: staging wait failed");
   for (int p = 0; p < n; ++p) {
     const gsb_profile& pr = profiles[p];
-    const std::string m = (flags & GSB_PROFILES_UNCHECKED) ? structural_check(pr) : validate_profile(pr);
-    if (!m.empty()) return gsb_set_error(ctx, GSB_MODEL_ERROR, m);
-    gsb::ProfTab& t = tabs[static_cast<size_t>(p)];
+    gsb::ProfTab& t = ctx->h_stage[p];
     std::memset(&t, 0, sizeof t);
     t.G = static_cast<int32_t>(grid_size(pr));
     t.f_min = pr.f_min_mhz;
@@ -319,11 +345,13 @@ int gsb_set_profiles_ex(gsb_ctx* ctx, int n, const gsb_profile* profiles, int fl
     ctx->h_tabs[p] = t;
   }
   ctx->n_profiles = n;
-  cudaSetDevice(ctx->device);
-  const cudaError_t e = cudaMemcpyAsync(ctx->d_tabs, tabs.data(), sizeof(gsb::ProfTab) * GSB_MAX_PROFILES,
+  const cudaError_t e = cudaMemcpyAsync(ctx->d_tabs, ctx->h_stage, sizeof(gsb::ProfTab) * n,
                                         cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return gsb_set_error(ctx, GSB_CUDA_ERROR, cudaGetErrorString(e));
-  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+  cudaEventRecord(ctx->stage_free, ctx->stream);
+  // GSB_PROFILES_ASYNC: the upload is ordered on the context's own stream only (callers that
+  // launch with stream == NULL); otherwise wait so launches on any stream see the tables
+  if (!(flags & GSB_PROFILES_ASYNC) && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "set_profiles: sync failed");
   return GSB_OK;
 }

@@ -247,6 +247,61 @@ __device__ __forceinline__ int argmin_clock(const double* s_f, const double* s_r
   return best;
 }
 
+// The same ascending strict-'<' scan spread over a warp (latency path for single batches): lane
+// l evaluates clocks l, l+32, ... The sequential scan's result is (a) the first feasible clock if
+// its energy is NaN (nothing compares below NaN, so it sticks), else (b) the lowest-index minimum
+// over the feasible non-NaN energies (later NaNs never win). Each lane tracks its first feasible
+// clock and its own (b); the warp reduces both with index tie-breaks, so the outcome is the
+// sequential one bit for bit. Returns the clock index (-1: none feasible) in every lane.
+template <bool FAST>
+__device__ __forceinline__ int argmin_clock_warp(const double* s_f, const double* s_r,
+                                                 const double* s_P, int G, double TF, double W,
+                                                 double p_idle, double* best_e) {
+  const int lane = threadIdx.x & 31;
+  int first = INT_MAX;
+  double first_e = 0.0;
+  int best = -1;
+  double be = 0.0;
+  for (int i = lane; i < G; i += 32) {
+    const double f = s_f[i];
+    const double busy = FAST ? gsb::div_pre_fast(TF, f, s_r[i]) : __ddiv_rn(TF, f);
+    const double active = gsb::div_pre_fast(__dmul_rn(s_P[i], busy), 1000.0, gsb::kRcp1000);
+    const double idle = gsb::div_pre_fast(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0, gsb::kRcp1000);
+    const double e = __dadd_rn(active, idle);
+    if (busy <= W) {
+      if (first == INT_MAX) {
+        first = i;
+        first_e = e;
+      }
+      if (e == e && (best < 0 || e < be)) {
+        best = i;
+        be = e;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int of = __shfl_xor_sync(0xffffffffu, first, o);
+    const double ofe = __shfl_xor_sync(0xffffffffu, first_e, o);
+    if (of < first) {
+      first = of;
+      first_e = ofe;
+    }
+    const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const double obe = __shfl_xor_sync(0xffffffffu, be, o);
+    if (ob >= 0 && (best < 0 || obe < be || (obe == be && ob < best))) {
+      best = ob;
+      be = obe;
+    }
+  }
+  if (first != INT_MAX && first_e != first_e) {
+    *best_e = first_e;
+    return first;
+  }
+  *best_e = be;
+  return best;
+}
+
 // W of a cell per the window mode (prefill_opt.cpp:63-67 for DEADLINE_SLACK):
 // min_j(deadline_j - now) == min_deadline - now because subtraction is monotone.
 __device__ __forceinline__ double cell_window(const SelectParams& sp, int64_t cell,
@@ -385,11 +440,7 @@ k_prefill_select(const __grid_constant__ SelectParams sp, const ProfTab* __restr
     s_r[i] = tab->rcp_f[i];
     s_P[i] = tab->P[i];
   }
-  if (threadIdx.x == 0) {
-    int fast = 1;
-    for (int i = 0; i < G; ++i) fast &= tab->rcp_f[i] != 0.0;
-    s_fast = fast;
-  }
+  if (threadIdx.x == 0) s_fast = tab->all_fast;  // every rcp_f[i] != 0, set by gsb_set_profiles
   __syncthreads();
   const bool fast = s_fast != 0;
   const double f_ref = tab->f_ref, p_idle = tab->p_idle;
@@ -439,22 +490,24 @@ k_select_batches(const __grid_constant__ SelectParams sp, const ProfTab* __restr
     s_r[i] = tab->rcp_f[i];
     s_P[i] = tab->P[i];
   }
-  if (threadIdx.x == 0) {
-    int fast = 1;
-    for (int i = 0; i < G; ++i) fast &= tab->rcp_f[i] != 0.0;
-    s_fast = fast;
-  }
+  if (threadIdx.x == 0) s_fast = tab->all_fast;  // every rcp_f[i] != 0, set by gsb_set_profiles
   __syncthreads();
-  const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (b >= n_batches) return;
+  // one warp per batch: the queue tick and select_frequency calls are a handful of batches, so
+  // latency (the 81-clock chain) matters more than lanes per batch
+  const int64_t b = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const bool lead = (threadIdx.x & 31) == 0;
+  if (b >= n_batches) return;  // warp-uniform
   const int64_t j0 = off[b], j1 = off[b + 1];
   if (j1 <= j0) {
-    f_idx[b] = -2;
-    energy[b] = 0.0;
-    if (t_out) t_out[b] = 0.0;
+    if (lead) {
+      f_idx[b] = -2;
+      energy[b] = 0.0;
+      if (t_out) t_out[b] = 0.0;
+    }
     return;
   }
-  // PrefillBatch::t_ref_total_ms, prefill_opt.cpp:9-14
+  // PrefillBatch::t_ref_total_ms, prefill_opt.cpp:9-14 (every lane folds the same jobs in the
+  // same order: broadcast loads, identical bits)
   double T = 0.0;
   double min_slack = INFINITY;
   const double now = (sp.mode == GSB_DEADLINE_SLACK) ? now_ms[b] : 0.0;
@@ -471,14 +524,16 @@ k_select_batches(const __grid_constant__ SelectParams sp, const ProfTab* __restr
     W = std_max(sp.margin * min_slack, sp.min_budget);
   else
     W = window[b];
-  if (window && sp.mode != GSB_PER_CELL_WINDOW) window[b] = W;
-  if (t_out) t_out[b] = T;
   const double TF = T * tab->f_ref;
   double be;
-  const int best = s_fast ? argmin_clock<true>(s_f, s_r, s_P, G, TF, W, tab->p_idle, &be)
-                          : argmin_clock<false>(s_f, s_r, s_P, G, TF, W, tab->p_idle, &be);
-  f_idx[b] = static_cast<int16_t>(best);
-  energy[b] = best >= 0 ? be : 0.0;
+  const int best = s_fast ? argmin_clock_warp<true>(s_f, s_r, s_P, G, TF, W, tab->p_idle, &be)
+                          : argmin_clock_warp<false>(s_f, s_r, s_P, G, TF, W, tab->p_idle, &be);
+  if (lead) {
+    if (window && sp.mode != GSB_PER_CELL_WINDOW) window[b] = W;
+    if (t_out) t_out[b] = T;
+    f_idx[b] = static_cast<int16_t>(best);
+    energy[b] = best >= 0 ? be : 0.0;
+  }
 }
 
 // energy_total(batch, f, window) breakdown, prefill_opt.cpp:16-31; feasible = 2 flags the
@@ -944,7 +999,7 @@ int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int
   sp.margin = cfg->qopt.margin_prefill;
   sp.min_budget = cfg->qopt.min_budget_ms;
   sp.n_cells = n_batches;
-  k_select_batches<<<static_cast<unsigned>((n_batches + 255) / 256), 256, 0, gsb_pick_stream(ctx, stream)>>>(
+  k_select_batches<<<static_cast<unsigned>((n_batches + 7) / 8), 256, 0, gsb_pick_stream(ctx, stream)>>>(
       sp, static_cast<const ProfTab*>(ctx->d_tabs) + profile, n_batches, d_off, d_prompt, d_wf,
       d_deadline, d_now, d_window, d_f_idx, d_energy, d_t_ref_out);
   return gsb_check_launch(ctx, "select_batches");

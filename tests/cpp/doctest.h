@@ -93,7 +93,13 @@ inline void report(bool ok, const char* kind, const char* expr, const char* file
     doctest::detail::report(doctest_ok_, "REQUIRE", #__VA_ARGS__, __FILE__, __LINE__);         \
     if (!doctest_ok_) throw doctest::detail::RequireFailed{};                                  \
   } while (0)
-#define CHECK_THROWS_AS(expr, ...)                                                             \
+#define REQUIRE_FALSE(...)                                                                     \
+  do {                                                                                         \
+    const bool doctest_ok_ = !static_cast<bool>(__VA_ARGS__);                                  \
+    doctest::detail::report(doctest_ok_, "REQUIRE_FALSE", #__VA_ARGS__, __FILE__, __LINE__);   \
+    if (!doctest_ok_) throw doctest::detail::RequireFailed{};                                  \
+  } while (0)
+#define CHECK_THROWS_AS(expr, ...)                                                            \
   do {                                                                                         \
     bool doctest_ok_ = false;                                                                  \
     try {                                                                                      \

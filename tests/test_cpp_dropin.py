@@ -1,10 +1,12 @@
 """The C++ drop-in boundary ("Existing C++ API must stay unchanged").
 
-The reference's own unit tests for the path — proj/tests/test_prefill_opt.cpp and
-proj/tests/test_decode_ctl.cpp — are compiled UNMODIFIED against paper_2508_16449_b200/cpp/include
-(greensim/*.hpp) and linked to libgreensim_b200.so -> libgsb.so (build: paper_2508_16449_b200/cpp/
-Makefile, into oracle/_ref/dropin/). On a B200 every case must pass with every evaluation running
-in the sm_100a kernels; without a GPU the binaries must refuse (no CPU path).
+The reference's own unit tests for the path — proj/tests/test_prefill_opt.cpp,
+test_decode_ctl.cpp, test_router.cpp — plus test_simkernel.cpp (the reference simulator's tests,
+whose governed runs take every routing / clock / controller decision through the drop-in) are
+compiled UNMODIFIED against paper_2508_16449_b200/cpp/include (greensim/*.hpp) and linked to
+libgreensim_b200.so -> libgsb.so (build: paper_2508_16449_b200/cpp/Makefile, into
+oracle/_ref/dropin/). On a B200 every case must pass with every evaluation running in the sm_100a
+kernels; without a GPU the binaries must refuse (no CPU path).
 """
 from __future__ import annotations
 
@@ -15,8 +17,12 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2508_16449_b200", "lib")
-REF_BINS = [os.path.join(ROOT, "oracle", "_ref", "dropin", n) for n in ("test_prefill_opt", "test_decode_ctl")]
-OWN_BINS = [os.path.join(ROOT, "tests", "cpp", "bin", "test_router_dropin")]
+# the reference's own unit tests, unmodified; test_router / test_simkernel run the reference's
+# simulator compiled over the drop-in (every decision it takes is a libgsb launch)
+REF_BINS = [os.path.join(ROOT, "oracle", "_ref", "dropin", n)
+            for n in ("test_prefill_opt", "test_decode_ctl", "test_router", "test_simkernel")]
+OWN_BINS = [os.path.join(ROOT, "tests", "cpp", "bin", n)
+            for n in ("test_router_dropin", "test_acceptance_dropin")]
 ALL_BINS = REF_BINS + OWN_BINS
 
 
