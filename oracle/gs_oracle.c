@@ -10,19 +10,20 @@
  * exact comparison directions.
  */
 #include "gs_oracle.h"
+#include "gs_oracle_int.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
-static double std_min(double a, double b) { return (b < a) ? b : a; }
-static double std_max(double a, double b) { return (a < b) ? b : a; }
-static double std_clamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+GSO_INTERNAL double std_min(double a, double b) { return (b < a) ? b : a; }
+GSO_INTERNAL double std_max(double a, double b) { return (a < b) ? b : a; }
+GSO_INTERNAL double std_clamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
 
 /* ---------------- grid and models (gpu_model.cpp, gpu_model.hpp) ---------------- */
 
 /* FrequencyGrid::on_grid, gpu_model.cpp:18-22 */
-static int on_grid(const gso_profile* p, double f) {
+GSO_INTERNAL int on_grid(const gso_profile* p, double f) {
   if (f < p->f_min_mhz - 1e-9 || f > p->f_max_mhz + 1e-9) return 0;
   const double k = (f - p->f_min_mhz) / p->step_mhz;
   return fabs(k - round(k)) < 1e-9;
@@ -251,7 +252,7 @@ int gso_route_bin(int64_t n_req, const int64_t* arrival_ms, const int32_t* promp
 
 /* ---------------- decode control (decode_ctl.cpp, metrics.cpp) ---------------- */
 
-static int cmp_double(const void* a, const void* b) {
+GSO_INTERNAL int cmp_double(const void* a, const void* b) {
   const double x = *(const double*)a, y = *(const double*)b;
   return (x > y) - (x < y);
 }
@@ -341,7 +342,7 @@ int gso_ctl_cfg_validate(const gso_ctl_cfg* c) {
   return 0;
 }
 
-static int table_validate(const gso_band_table* t) {
+GSO_INTERNAL int table_validate(const gso_band_table* t) {
   if (t->n <= 0) return -1;
   if (t->tps_lo[0] != 0.0) return -1;
   for (int i = 0; i + 1 < t->n; ++i) {
@@ -353,13 +354,7 @@ static int table_validate(const gso_band_table* t) {
 }
 
 /* TBT ring (TbtWindow, decode_ctl.cpp:120-128) */
-typedef struct {
-  int cap, n, head;
-  double* buf;
-  double* scratch;
-} ring_t;
-
-static void ring_record(ring_t* r, double x) {
+GSO_INTERNAL void ring_record(ring_t* r, double x) {
   if (r->n < r->cap) {
     r->buf[(r->head + r->n) % r->cap] = x;
     r->n++;
@@ -369,7 +364,7 @@ static void ring_record(ring_t* r, double x) {
   }
 }
 
-static double ring_p95(ring_t* r) {
+GSO_INTERNAL double ring_p95(ring_t* r) {
   for (int i = 0; i < r->n; ++i) r->scratch[i] = r->buf[(r->head + i) % r->cap];
   qsort(r->scratch, (size_t)r->n, sizeof(double), cmp_double);
   const size_t rank = (size_t)ceil(0.95 * (double)r->n);
@@ -432,21 +427,7 @@ void gso_window_series(const gso_telemetry* tel, int tbt_capacity, double fine_p
 /* DecodeController, decode_ctl.cpp:130-228. The adjustments_ vector is only ever read as
  * three counts (size, clamped-up, clamped-down) and cleared as a whole, so counters
  * restate it exactly. */
-typedef struct {
-  gso_ctl_cfg cfg;
-  int n;
-  const double* tps_hi;
-  double* f_opt; /* per-controller copy (adaptation mutates it) */
-  double f_min, f_max;
-  int worker;
-  int current, pending, consecutive;
-  double lo, hi, sp, last_tps, last_p95;
-  int64_t adj_total, adj_up, adj_dn;
-  gso_decision* out;
-  int64_t cap, n_rec;
-} ctl_t;
-
-static void ctl_log(ctl_t* c, double now, int bucket, int action) {
+GSO_INTERNAL void ctl_log(ctl_t* c, double now, int bucket, int action) {
   if (c->n_rec < c->cap) {
     gso_decision* r = &c->out[c->n_rec];
     r->tick_ms = now;
@@ -464,20 +445,20 @@ static void ctl_log(ctl_t* c, double now, int bucket, int action) {
 }
 
 /* FreqBandTable::band :52-57 via DecodeController::load_band :137-142 */
-static void ctl_load_band(ctl_t* c, int bucket) {
+GSO_INTERNAL void ctl_load_band(ctl_t* c, int bucket) {
   const double f = c->f_opt[bucket];
   c->lo = std_max(c->f_min, f - c->cfg.step_mhz);
   c->hi = std_min(c->f_max, f + c->cfg.step_mhz);
 }
 
 /* FreqBandTable::bucket_index :47-51 */
-static int ctl_bucket_index(const ctl_t* c, double tps) {
+GSO_INTERNAL int ctl_bucket_index(const ctl_t* c, double tps) {
   for (int i = 0; i < c->n; ++i)
     if (tps <= c->tps_hi[i]) return i;
   return c->n - 1;
 }
 
-static void ctl_init(ctl_t* c) {
+GSO_INTERNAL void ctl_init(ctl_t* c) {
   c->current = c->n - 1;
   c->pending = -1;
   c->consecutive = 0;
@@ -490,7 +471,7 @@ static void ctl_init(ctl_t* c) {
 }
 
 /* on_fine_tick :148-167 */
-static void ctl_fine(ctl_t* c, double now, int has, double p95) {
+GSO_INTERNAL void ctl_fine(ctl_t* c, double now, int has, double p95) {
   int dir = 0;
   if (has) {
     c->last_p95 = p95;
@@ -512,7 +493,7 @@ static void ctl_fine(ctl_t* c, double now, int has, double p95) {
 }
 
 /* on_coarse_tick :169-198 */
-static void ctl_coarse(ctl_t* c, double now, double worker_tps) {
+GSO_INTERNAL void ctl_coarse(ctl_t* c, double now, double worker_tps) {
   c->last_tps = worker_tps * c->cfg.tps_scale;
   const int observed = ctl_bucket_index(c, c->last_tps);
   int action;
@@ -543,7 +524,7 @@ static void ctl_coarse(ctl_t* c, double now, double worker_tps) {
 }
 
 /* on_adapt_tick :200-228 */
-static void ctl_adapt(ctl_t* c, double now) {
+GSO_INTERNAL void ctl_adapt(ctl_t* c, double now) {
   const int total = (int)c->adj_total;
   const int up = (int)c->adj_up, dn = (int)c->adj_dn;
   c->adj_total = c->adj_up = c->adj_dn = 0;
@@ -560,7 +541,7 @@ static void ctl_adapt(ctl_t* c, double now) {
   ctl_log(c, now, c->current, shift > 0 ? GSO_ACT_ADAPT_UP : GSO_ACT_ADAPT_DOWN);
 }
 
-static int ctl_setup(ctl_t* c, const gso_ctl_cfg* cfg, const gso_band_table* t, double f_min,
+GSO_INTERNAL int ctl_setup(ctl_t* c, const gso_ctl_cfg* cfg, const gso_band_table* t, double f_min,
                      double f_max, int worker, gso_decision* out, int64_t cap) {
   if (gso_ctl_cfg_validate(cfg) != 0 || table_validate(t) != 0) return -1;
   memset(c, 0, sizeof(*c));

@@ -164,6 +164,99 @@ int64_t gso_gen_sinusoid_decode_trace(double tps_mean, double tps_amp, double pe
                                       int64_t duration_ms, uint64_t seed, int64_t cap,
                                       int64_t* arrival, int32_t* prompt, int32_t* output);
 
+/* ---------------- the reference simulator (simkernel.cpp) ----------------
+ * gso_sim_run restates greensim::run (simkernel.cpp:119-560): the two-pool discrete-event
+ * simulator that calls the decision engine. It is pinned field-by-field against the
+ * reference's own run() (tests/test_oracle_sim.py) and serves two roles: it records the
+ * decode-enqueue stream in the reference's processing order (same-time ties follow the
+ * event sequence numbers, simkernel.cpp:44-50), and it is the checker for the GPU
+ * closed-loop decode pool (K5). gso_pool_run drives the SAME decode-pool code from such a
+ * stream alone (prefill never waits on decode, so the stream is a function of the prefill
+ * side only). Results are read through an opaque handle (gso_sim_free). */
+typedef struct gso_sim_cfg { /* SimConfig, simkernel.hpp:88-104 */
+  int32_t n_prefill_workers, n_decode_workers, gpus_per_prefill_worker, max_batch, max_queue;
+  int32_t pad_;
+  double actuation_delay_ms, handoff_delay_ms, band_tps_lo, band_tps_hi, band_tps_step;
+} gso_sim_cfg;
+
+typedef struct gso_slo { double ttft_sm_ms, ttft_l_ms, tbt_p95_ms; } gso_slo; /* SloConfig :53-62 */
+
+typedef struct gso_policy {  /* GovernorPolicy, simkernel.hpp:26-45 */
+  int32_t kind;              /* 0 defaultnv, 1 fixed, 2 greenllm, 3 prefillsplit */
+  int32_t routing_enabled;   /* RoutingConfig::enabled (router.hpp:19-29) */
+  int32_t n_thresholds;
+  int32_t thresholds[7];
+  const int32_t* worker_map; /* [n_prefill_workers] */
+  double fixed_freq_mhz;
+  gso_qopt_cfg prefill_opt;
+  gso_ctl_cfg decode_ctl;
+} gso_policy;
+
+typedef struct gso_scripted { /* ScriptedFreqEvent, simkernel.hpp:76-81 */
+  double time_ms;
+  int32_t prefill_pool, worker;
+  double f_mhz;
+} gso_scripted;
+
+/* Decode-side summary of one run (the K5 output). Digests:
+ *   decision_digest  per decode worker, the K3 record digest (gso_digest_records) of that
+ *                    worker's DecisionRecords in log order; combined h = (h ^ d_w) * P over w
+ *   freq_digest      per decode worker, FNV-1a over (applied_ms bits, f bits) of its applied
+ *                    changes (t = 0 initial rows excluded); combined the same way
+ *   request_digest   sum mod 2^64 over requests that reached the decode pool of
+ *                    FNV-1a(id, first_token bits, gap bits..., finish bits, decode_worker),
+ *                    or FNV-1a(id, 0xdead) for a decode-side rejection */
+typedef struct gso_pool_summary {
+  double decode_pool_j, active_decode_j, idle_j, sim_end_ms;
+  int64_t n_completed, n_rejected, n_ttft_ok, n_tbt_ok, tbt_samples, tbt_samples_ok;
+  int64_t n_decisions, n_freq_changes, n_steps;
+  uint64_t decision_digest, freq_digest, request_digest;
+} gso_pool_summary;
+
+void* gso_sim_run(const gso_profile* prof, const gso_policy* pol, const gso_slo* slo,
+                  const gso_sim_cfg* cfg, int64_t n, const int64_t* arrival_ms,
+                  const int32_t* prompt, const int32_t* output, const int8_t* cls /* NULL/-1 */,
+                  int64_t n_scripted, const gso_scripted* scripted, char* err, size_t err_cap);
+/* Decode pool alone, driven by an enqueue stream (t, request) in processing order.
+ * end_floor_ms = the prefill side's contribution to sim_end_ms (simkernel.cpp:506-512). */
+void* gso_pool_run(const gso_profile* prof, const gso_policy* pol, const gso_slo* slo,
+                   const gso_sim_cfg* cfg, int64_t n, const int64_t* arrival_ms,
+                   const int32_t* prompt, const int32_t* output, const int8_t* cls,
+                   int64_t n_stream,
+                   const double* enq_t, const int64_t* enq_req, double end_floor_ms,
+                   char* err, size_t err_cap);
+void gso_sim_free(void* h);
+/* [0] requests, [1] tbt samples, [2] decisions, [3] timeline rows, [4] prefill commands,
+ * [5] enqueues, [6] prefill workers, [7] decode workers, [8] rejected, [9] decode steps */
+void gso_sim_sizes(void* h, int64_t* s);
+void gso_sim_requests(void* h, int32_t* class_queue, int32_t* prefill_worker,
+                      int32_t* decode_worker, double* prefill_start, double* prefill_end,
+                      double* first_token, double* finish, uint8_t* completed, uint8_t* rejected,
+                      int8_t* cls);
+void gso_sim_tbt(void* h, int64_t* off /* [n+1] */, double* samples);
+/* per worker: active_prefill_j, active_decode_j, idle_j; n_intervals per worker */
+void gso_sim_ledgers(void* h, double* prefill3, double* decode3, int64_t* n_intervals);
+void gso_sim_decisions(void* h, gso_decision* out);
+void gso_sim_timeline(void* h, double* t, uint8_t* pool, int32_t* worker, double* f);
+void gso_sim_commands(void* h, double* tick, int32_t* cls, int32_t* worker, double* f,
+                      double* window, uint8_t* infeasible);
+void gso_sim_enqueue(void* h, double* t, int64_t* req);
+/* [0] sim_end_ms, [1] last_arrival_ms, [2] end floor (prefill-side part of sim_end) */
+void gso_sim_scalars(void* h, double* d);
+void gso_sim_summary(void* h, const gso_slo* slo, gso_pool_summary* out);
+
+/* The K5 summary from plain arrays (shared by the restatement and the reference shim). */
+void gso_pool_summary_from(const gso_slo* slo, int64_t n, const double* arrival,
+                           const int8_t* cls, const int32_t* decode_worker,
+                           const double* prefill_end, const double* first_token,
+                           const double* finish, const uint8_t* completed,
+                           const uint8_t* rejected, const int64_t* tbt_off,
+                           const double* tbt, int n_decode, const double* decode3,
+                           int64_t n_dec, const gso_decision* dec, int64_t n_tl,
+                           const double* tl_t, const uint8_t* tl_pool, const int32_t* tl_worker,
+                           const double* tl_f, double sim_end_ms, int64_t n_steps,
+                           gso_pool_summary* out);
+
 #ifdef __cplusplus
 }
 #endif

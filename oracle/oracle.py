@@ -67,6 +67,126 @@ class Telemetry(C.Structure):
     _fields_ = [("n_events", _i64), ("t_ms", _p), ("tokens", _p), ("gap_off", _p), ("gaps", _p)]
 
 
+class SimCfg(C.Structure):
+    """gso_sim_cfg == greensim::SimConfig (simkernel.hpp:88-104) minus scripted_freq."""
+
+    _fields_ = [("n_prefill_workers", _i32), ("n_decode_workers", _i32),
+                ("gpus_per_prefill_worker", _i32), ("max_batch", _i32), ("max_queue", _i32),
+                ("pad_", _i32), ("actuation_delay_ms", _d), ("handoff_delay_ms", _d),
+                ("band_tps_lo", _d), ("band_tps_hi", _d), ("band_tps_step", _d)]
+
+
+class Slo(C.Structure):
+    """gso_slo == greensim::SloConfig (simkernel.hpp:53-62)."""
+
+    _fields_ = [("ttft_sm_ms", _d), ("ttft_l_ms", _d), ("tbt_p95_ms", _d)]
+
+
+class Policy(C.Structure):
+    """gso_policy == greensim::GovernorPolicy (simkernel.hpp:26-45)."""
+
+    _fields_ = [("kind", _i32), ("routing_enabled", _i32), ("n_thresholds", _i32),
+                ("thresholds", _i32 * 7), ("worker_map", _p), ("fixed_freq_mhz", _d),
+                ("prefill_opt", QoptCfg), ("decode_ctl", CtlCfg)]
+
+
+class Scripted(C.Structure):
+    _fields_ = [("time_ms", _d), ("prefill_pool", _i32), ("worker", _i32), ("f_mhz", _d)]
+
+
+class PoolSummary(C.Structure):
+    """gso_pool_summary: the decode-side (K5) summary of one run (gs_oracle.h)."""
+
+    _fields_ = [("decode_pool_j", _d), ("active_decode_j", _d), ("idle_j", _d),
+                ("sim_end_ms", _d), ("n_completed", _i64), ("n_rejected", _i64),
+                ("n_ttft_ok", _i64), ("n_tbt_ok", _i64), ("tbt_samples", _i64),
+                ("tbt_samples_ok", _i64), ("n_decisions", _i64), ("n_freq_changes", _i64),
+                ("n_steps", _i64), ("decision_digest", _u64), ("freq_digest", _u64),
+                ("request_digest", _u64)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+POLICY_KINDS = {"defaultnv": 0, "fixed": 1, "greenllm": 2, "prefillsplit": 3}
+
+
+def default_sim_cfg(**kw) -> SimCfg:
+    """SimConfig defaults (simkernel.hpp:88-104)."""
+    c = SimCfg(2, 4, 2, 64, 10000, 0, 5.0, 0.0, 200.0, 3000.0, 200.0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def default_slo(**kw) -> Slo:
+    c = Slo(400.0, 2000.0, 100.0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class PolicyHolder:
+    """A Policy plus the worker_map array it points to."""
+
+    def __init__(self, kind="greenllm", thresholds=(1024,), worker_map=(0, 1), routing=True,
+                 fixed_f=0.0, qcfg=None, ccfg=None):
+        self.wm = np.ascontiguousarray(worker_map, np.int32)
+        thr = (_i32 * 7)(*thresholds)
+        self.c = Policy(POLICY_KINDS[kind], 1 if routing else 0, len(thresholds), thr,
+                        ptr(self.wm), fixed_f, qcfg or default_qopt_cfg(),
+                        ccfg or default_ctl_cfg())
+
+
+def _read_sim(lib, pre: str, h) -> dict:
+    """Pulls every output of a gso_sim_* / ref_sim_* handle into numpy arrays."""
+    z = np.zeros(10, np.int64)
+    getattr(lib, pre + "sizes")(h, ptr(z))
+    n, nt, nd, ntl, nc, ne, npw, ndw = (int(x) for x in z[:8])
+    o = {"n_rejected_total": int(z[8]), "n_steps": int(z[9])}
+    for k, dt in (("class_queue", np.int32), ("prefill_worker", np.int32),
+                  ("decode_worker", np.int32), ("prefill_start", np.float64),
+                  ("prefill_end", np.float64), ("first_token", np.float64),
+                  ("finish", np.float64), ("completed", np.uint8), ("rejected", np.uint8),
+                  ("cls", np.int8)):
+        o[k] = np.zeros(n, dt)
+    getattr(lib, pre + "requests")(h, *(ptr(o[k]) for k in (
+        "class_queue", "prefill_worker", "decode_worker", "prefill_start", "prefill_end",
+        "first_token", "finish", "completed", "rejected", "cls")))
+    o["tbt_off"] = np.zeros(n + 1, np.int64)
+    o["tbt"] = np.zeros(max(nt, 1))
+    getattr(lib, pre + "tbt")(h, ptr(o["tbt_off"]), ptr(o["tbt"]))
+    o["tbt"] = o["tbt"][:nt]
+    o["prefill3"] = np.zeros((npw, 3))
+    o["decode3"] = np.zeros((ndw, 3))
+    o["n_intervals"] = np.zeros(npw + ndw, np.int64)
+    getattr(lib, pre + "ledgers")(h, ptr(o["prefill3"]), ptr(o["decode3"]), ptr(o["n_intervals"]))
+    o["decisions"] = np.zeros(nd, DECISION_DTYPE)
+    getattr(lib, pre + "decisions")(h, ptr(o["decisions"]))
+    o["tl_t"] = np.zeros(ntl)
+    o["tl_pool"] = np.zeros(ntl, np.uint8)
+    o["tl_worker"] = np.zeros(ntl, np.int32)
+    o["tl_f"] = np.zeros(ntl)
+    getattr(lib, pre + "timeline")(h, *(ptr(o[k]) for k in ("tl_t", "tl_pool", "tl_worker", "tl_f")))
+    o["cmd_tick"] = np.zeros(nc)
+    o["cmd_class"] = np.zeros(nc, np.int32)
+    o["cmd_worker"] = np.zeros(nc, np.int32)
+    o["cmd_f"] = np.zeros(nc)
+    o["cmd_window"] = np.zeros(nc)
+    o["cmd_infeasible"] = np.zeros(nc, np.uint8)
+    getattr(lib, pre + "commands")(h, *(ptr(o[k]) for k in (
+        "cmd_tick", "cmd_class", "cmd_worker", "cmd_f", "cmd_window", "cmd_infeasible")))
+    sc = np.zeros(8)
+    getattr(lib, pre + "scalars")(h, ptr(sc))
+    o["scalars"] = sc
+    o["sim_end_ms"] = float(sc[0])
+    if ne >= 0:
+        o["enq_t"] = np.zeros(ne)
+        o["enq_req"] = np.zeros(ne, np.int64)
+        getattr(lib, pre + "enqueue")(h, ptr(o["enq_t"]), ptr(o["enq_req"]))
+    return o
+
+
 DECISION_DTYPE = np.dtype([("tick_ms", "<f8"), ("tps", "<f8"), ("p95_tbt_ms", "<f8"),
                            ("band_lo", "<f8"), ("band_hi", "<f8"), ("command_mhz", "<f8"),
                            ("worker", "<i4"), ("bucket", "<i4"), ("action", "<i4"),
@@ -172,6 +292,20 @@ class Restatement:
         L.gso_gen_poisson_trace.restype = _i64
         L.gso_gen_sinusoid_decode_trace.argtypes = [_d, _d, _d, _i64, _u64, _i64, _p, _p, _p]
         L.gso_gen_sinusoid_decode_trace.restype = _i64
+        SP = [C.POINTER(Profile), C.POINTER(Policy), C.POINTER(Slo), C.POINTER(SimCfg)]
+        L.gso_sim_run.argtypes = SP + [_i64, _p, _p, _p, _p, _i64, _p, C.c_char_p, C.c_size_t]
+        L.gso_sim_run.restype = _p
+        L.gso_pool_run.argtypes = SP + [_i64, _p, _p, _p, _p, _i64, _p, _p, _d, C.c_char_p,
+                                        C.c_size_t]
+        L.gso_pool_run.restype = _p
+        L.gso_sim_free.argtypes = [_p]
+        for f, k in (("sizes", 1), ("requests", 10), ("tbt", 2), ("ledgers", 3), ("decisions", 1),
+                     ("timeline", 4), ("commands", 6), ("enqueue", 2), ("scalars", 1)):
+            getattr(L, "gso_sim_" + f).argtypes = [_p] + [_p] * k
+        L.gso_sim_summary.argtypes = [_p, C.POINTER(Slo), C.POINTER(PoolSummary)]
+        L.gso_pool_summary_from.argtypes = ([C.POINTER(Slo), _i64] + [_p] * 10 + [C.c_int, _p, _i64,
+                                            _p, _i64, _p, _p, _p, _p, _d, _i64,
+                                            C.POINTER(PoolSummary)])
 
     # ---- prefill ----
     def grid(self, prof: Profile) -> np.ndarray:
@@ -346,6 +480,71 @@ class Restatement:
             cap = n
 
 
+    # ---- the reference simulator restated (gs_sim.c) ----
+    def sim_run(self, prof, policy: "PolicyHolder", slo, cfg, arrival, prompt, output, cls=None,
+                scripted=None) -> dict:
+        """gso_sim_run: the whole two-pool simulator (simkernel.cpp); dict of arrays."""
+        arrival = np.ascontiguousarray(arrival, np.int64)
+        prompt = np.ascontiguousarray(prompt, np.int32)
+        output = np.ascontiguousarray(output, np.int32)
+        cls = None if cls is None else np.ascontiguousarray(cls, np.int8)
+        sc = None
+        if scripted:
+            sc = (Scripted * len(scripted))(*[Scripted(*x) for x in scripted])
+        err = C.create_string_buffer(256)
+        h = self.lib.gso_sim_run(C.byref(prof), C.byref(policy.c), C.byref(slo), C.byref(cfg),
+                                 len(arrival), ptr(arrival), ptr(prompt), ptr(output), ptr(cls),
+                                 len(scripted or ()), sc, err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        try:
+            out = _read_sim(self.lib, "gso_sim_", h)
+            sm = PoolSummary()
+            self.lib.gso_sim_summary(h, C.byref(slo), C.byref(sm))
+            out["summary"] = sm.as_dict()
+            return out
+        finally:
+            self.lib.gso_sim_free(h)
+
+    def pool_run(self, prof, policy: "PolicyHolder", slo, cfg, arrival, prompt, output, enq_t,
+                 enq_req, end_floor, cls=None) -> dict:
+        """gso_pool_run: the decode pool alone, driven by a recorded enqueue stream."""
+        arrival = np.ascontiguousarray(arrival, np.int64)
+        prompt = np.ascontiguousarray(prompt, np.int32)
+        output = np.ascontiguousarray(output, np.int32)
+        cls = None if cls is None else np.ascontiguousarray(cls, np.int8)
+        enq_t = np.ascontiguousarray(enq_t, np.float64)
+        enq_req = np.ascontiguousarray(enq_req, np.int64)
+        err = C.create_string_buffer(256)
+        h = self.lib.gso_pool_run(C.byref(prof), C.byref(policy.c), C.byref(slo), C.byref(cfg),
+                                  len(arrival), ptr(arrival), ptr(prompt), ptr(output), ptr(cls),
+                                  len(enq_t), ptr(enq_t), ptr(enq_req), float(end_floor), err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        try:
+            out = _read_sim(self.lib, "gso_sim_", h)
+            sm = PoolSummary()
+            self.lib.gso_sim_summary(h, C.byref(slo), C.byref(sm))
+            out["summary"] = sm.as_dict()
+            return out
+        finally:
+            self.lib.gso_sim_free(h)
+
+    def pool_summary_from(self, slo, arrival, o: dict) -> dict:
+        """The K5 summary of any simulator output dict (e.g. the reference's run())."""
+        arrival = np.ascontiguousarray(arrival, np.float64)
+        sm = PoolSummary()
+        d3 = np.ascontiguousarray(o["decode3"])
+        self.lib.gso_pool_summary_from(
+            C.byref(slo), len(arrival), ptr(arrival), ptr(o["cls"]), ptr(o["decode_worker"]),
+            ptr(o["prefill_end"]), ptr(o["first_token"]), ptr(o["finish"]), ptr(o["completed"]),
+            ptr(o["rejected"]), ptr(o["tbt_off"]), ptr(o["tbt"] if len(o["tbt"]) else np.zeros(1)),
+            d3.shape[0], ptr(d3), len(o["decisions"]), ptr(o["decisions"]), len(o["tl_t"]),
+            ptr(o["tl_t"]), ptr(o["tl_pool"]), ptr(o["tl_worker"]), ptr(o["tl_f"]),
+            float(o["sim_end_ms"]), int(o.get("n_steps", -1)), C.byref(sm))
+        return sm.as_dict()
+
+
 class Reference:
     """The unmodified reference library behind ref_capi.cpp."""
 
@@ -402,6 +601,16 @@ class Reference:
         L.ref_run_controller_inputs.argtypes = [_p] + [_p] * 9
         L.ref_run_decisions.argtypes = [_p, _p]
         L.ref_run_requests.argtypes = [_p] + [_p] * 8
+        SP = [C.POINTER(Profile), C.POINTER(Policy), C.POINTER(Slo), C.POINTER(SimCfg)]
+        L.ref_sim_run.argtypes = SP + [_i64, _p, _p, _p, _p, _i64, _p, C.c_char_p, C.c_size_t]
+        L.ref_sim_run.restype = _p
+        L.ref_sim_free.argtypes = [_p]
+        for f, k in (("sizes", 1), ("requests", 10), ("tbt", 2), ("ledgers", 3), ("decisions", 1),
+                     ("timeline", 4), ("commands", 6), ("scalars", 1)):
+            getattr(L, "ref_sim_" + f).argtypes = [_p] + [_p] * k
+        L.ref_sim_run_many.argtypes = [C.POINTER(Profile), C.POINTER(Policy), _p, _i64,
+                                       C.POINTER(Slo), C.POINTER(SimCfg), _i64, _p, _p, _p,
+                                       C.c_int, _p, _p]
 
     def default_profile(self) -> Profile:
         p = Profile()
@@ -658,6 +867,41 @@ class Reference:
             return out
         finally:
             self.lib.ref_run_free(h)
+
+    def sim_run(self, prof, policy: "PolicyHolder", slo, cfg, arrival, prompt, output, cls=None,
+                scripted=None) -> dict:
+        """The reference's own run() (simkernel.cpp) behind the gso_sim_* getters' layout."""
+        arrival = np.ascontiguousarray(arrival, np.int64)
+        prompt = np.ascontiguousarray(prompt, np.int32)
+        output = np.ascontiguousarray(output, np.int32)
+        cls = None if cls is None else np.ascontiguousarray(cls, np.int8)
+        sc = None
+        if scripted:
+            sc = (Scripted * len(scripted))(*[Scripted(*x) for x in scripted])
+        err = C.create_string_buffer(256)
+        h = self.lib.ref_sim_run(C.byref(prof), C.byref(policy.c), C.byref(slo), C.byref(cfg),
+                                 len(arrival), ptr(arrival), ptr(prompt), ptr(output), ptr(cls),
+                                 len(scripted or ()), sc, err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        try:
+            return _read_sim(self.lib, "ref_sim_", h)
+        finally:
+            self.lib.ref_sim_free(h)
+
+    def sim_run_many(self, prof, policy: "PolicyHolder", cfgs, slo, sim_cfg, arrival, prompt,
+                     output, threads=1):
+        """One reference run() per controller config (CPU baseline of K5)."""
+        arrival = np.ascontiguousarray(arrival, np.int64)
+        prompt = np.ascontiguousarray(prompt, np.int32)
+        output = np.ascontiguousarray(output, np.int32)
+        arr = (CtlCfg * len(cfgs))(*cfgs)
+        ej = np.zeros(len(cfgs))
+        nd = np.zeros(len(cfgs), np.int64)
+        self.lib.ref_sim_run_many(C.byref(prof), C.byref(policy.c), arr, len(cfgs), C.byref(slo),
+                                  C.byref(sim_cfg), len(arrival), ptr(arrival), ptr(prompt),
+                                  ptr(output), threads, ptr(ej), ptr(nd))
+        return ej, nd
 
 
 def reference_available() -> bool:

@@ -723,3 +723,243 @@ extern "C" void ref_replay_many(int64_t n_scen, const gso_ctl_cfg* cfgs,
     pool.emplace_back(work, n_scen * t / threads, n_scen * (t + 1) / threads);
   for (auto& th : pool) th.join();
 }
+
+// ---- the reference simulator behind the same getters as gso_sim_* (gs_sim.c) ------------
+// Inputs mirror gso_sim_run; results come from the reference's own greensim::run().
+namespace {
+struct RefSim {
+  RunResult r;
+  std::vector<gso_decision> dec;
+  int64_t n_steps = 0;
+};
+
+Trace to_trace(int64_t n, const int64_t* arrival, const int32_t* prompt, const int32_t* output,
+               const int8_t* cls) {
+  Trace tr;
+  tr.meta.name = "capi";
+  for (int64_t i = 0; i < n; ++i) {
+    Request q;
+    q.id = i;
+    q.arrival_ms = arrival[i];
+    q.prompt_tokens = prompt[i];
+    q.output_tokens = output[i];
+    if (cls && (cls[i] == 0 || cls[i] == 1)) q.cls = static_cast<PromptClass>(cls[i]);
+    tr.requests.push_back(q);
+    tr.meta.duration_ms = std::max(tr.meta.duration_ms, arrival[i]);
+  }
+  return tr;
+}
+
+GovernorPolicy to_policy(const gso_policy* p, int n_prefill) {
+  GovernorPolicy pol;
+  switch (p->kind) {
+    case 0: pol = GovernorPolicy::default_nv(); break;
+    case 1: pol = GovernorPolicy::fixed(p->fixed_freq_mhz); break;
+    case 2: pol = GovernorPolicy::greenllm(); break;
+    default: pol = GovernorPolicy::prefill_split(); break;
+  }
+  if (p->kind >= 2) {
+    pol.routing.enabled = p->routing_enabled != 0;
+    pol.routing.thresholds.assign(p->thresholds, p->thresholds + p->n_thresholds);
+    pol.routing.worker_map.assign(p->worker_map, p->worker_map + n_prefill);
+  }
+  pol.prefill_opt = to_qcfg(&p->prefill_opt);
+  pol.decode_ctl = to_cfg(&p->decode_ctl);
+  return pol;
+}
+
+SimConfig to_simcfg(const gso_sim_cfg* c) {
+  SimConfig s;
+  s.n_prefill_workers = c->n_prefill_workers;
+  s.n_decode_workers = c->n_decode_workers;
+  s.gpus_per_prefill_worker = c->gpus_per_prefill_worker;
+  s.actuation_delay_ms = c->actuation_delay_ms;
+  s.handoff_delay_ms = c->handoff_delay_ms;
+  s.max_batch = c->max_batch;
+  s.max_queue = c->max_queue;
+  s.band_tps_lo = c->band_tps_lo;
+  s.band_tps_hi = c->band_tps_hi;
+  s.band_tps_step = c->band_tps_step;
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+void* ref_sim_run(const gso_profile* prof, const gso_policy* pol, const gso_slo* slo,
+                  const gso_sim_cfg* cfg, int64_t n, const int64_t* arrival_ms,
+                  const int32_t* prompt, const int32_t* output, const int8_t* cls,
+                  int64_t n_scripted, const gso_scripted* scripted, char* err, size_t err_cap) {
+  SloConfig sc;
+  sc.ttft_sm_ms = slo->ttft_sm_ms;
+  sc.ttft_l_ms = slo->ttft_l_ms;
+  sc.tbt_p95_ms = slo->tbt_p95_ms;
+  SimConfig sim = to_simcfg(cfg);
+  for (int64_t k = 0; k < n_scripted; ++k)
+    sim.scripted_freq.push_back({scripted[k].time_ms, scripted[k].prefill_pool != 0,
+                                 scripted[k].worker, scripted[k].f_mhz});
+  auto* h = new RefSim;
+  try {
+    h->r = run(to_trace(n, arrival_ms, prompt, output, cls), to_profile(prof),
+               to_policy(pol, cfg->n_prefill_workers), 1, sc, sim);
+  } catch (const std::exception& e) {
+    if (err && err_cap) std::snprintf(err, err_cap, "%s", e.what());
+    delete h;
+    return nullptr;
+  }
+  for (const auto& d : h->r.decode_decisions) {
+    gso_decision c;
+    to_c_record(d, &c);
+    h->dec.push_back(c);
+  }
+  // decode steps = decode-ledger intervals that are active-decode phase changes are not
+  // a step count; count TBT-producing steps instead is impossible, so report -1.
+  h->n_steps = -1;
+  return h;
+}
+
+void ref_sim_free(void* h) { delete static_cast<RefSim*>(h); }
+
+void ref_sim_sizes(void* hv, int64_t* z) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  int64_t nt = 0;
+  for (const auto& q : r.requests) nt += static_cast<int64_t>(q.tbt_ms.size());
+  z[0] = static_cast<int64_t>(r.requests.size());
+  z[1] = nt;
+  z[2] = static_cast<int64_t>(r.decode_decisions.size());
+  z[3] = static_cast<int64_t>(r.freq_timeline.size());
+  z[4] = static_cast<int64_t>(r.prefill_commands.size());
+  z[5] = -1;  // the enqueue stream is not observable from a RunResult
+  z[6] = static_cast<int64_t>(r.prefill_ledgers.size());
+  z[7] = static_cast<int64_t>(r.decode_ledgers.size());
+  z[8] = r.overload.rejected_requests;
+  z[9] = static_cast<RefSim*>(hv)->n_steps;
+}
+
+void ref_sim_requests(void* hv, int32_t* class_queue, int32_t* prefill_worker,
+                      int32_t* decode_worker, double* prefill_start, double* prefill_end,
+                      double* first_token, double* finish, uint8_t* completed, uint8_t* rejected,
+                      int8_t* cls) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  for (size_t i = 0; i < r.requests.size(); ++i) {
+    const auto& q = r.requests[i];
+    class_queue[i] = q.class_queue;
+    prefill_worker[i] = q.prefill_worker;
+    decode_worker[i] = q.decode_worker;
+    prefill_start[i] = q.prefill_start_ms;
+    prefill_end[i] = q.prefill_end_ms;
+    first_token[i] = q.first_token_ms;
+    finish[i] = q.finish_ms;
+    completed[i] = q.completed ? 1 : 0;
+    rejected[i] = q.rejected ? 1 : 0;
+    cls[i] = static_cast<int8_t>(q.cls);
+  }
+}
+
+void ref_sim_tbt(void* hv, int64_t* off, double* samples) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  off[0] = 0;
+  for (size_t i = 0; i < r.requests.size(); ++i) {
+    const auto& t = r.requests[i].tbt_ms;
+    std::copy(t.begin(), t.end(), samples + off[i]);
+    off[i + 1] = off[i] + static_cast<int64_t>(t.size());
+  }
+}
+
+void ref_sim_ledgers(void* hv, double* p3, double* d3, int64_t* n_int) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  size_t k = 0;
+  for (size_t w = 0; w < r.prefill_ledgers.size(); ++w, ++k) {
+    const auto& l = r.prefill_ledgers[w];
+    p3[3 * w] = l.active_prefill_j;
+    p3[3 * w + 1] = l.active_decode_j;
+    p3[3 * w + 2] = l.idle_j;
+    n_int[k] = static_cast<int64_t>(l.intervals.size());
+  }
+  for (size_t w = 0; w < r.decode_ledgers.size(); ++w, ++k) {
+    const auto& l = r.decode_ledgers[w];
+    d3[3 * w] = l.active_prefill_j;
+    d3[3 * w + 1] = l.active_decode_j;
+    d3[3 * w + 2] = l.idle_j;
+    n_int[k] = static_cast<int64_t>(l.intervals.size());
+  }
+}
+
+void ref_sim_decisions(void* hv, gso_decision* out) {
+  const auto& d = static_cast<RefSim*>(hv)->dec;
+  std::copy(d.begin(), d.end(), out);
+}
+
+void ref_sim_timeline(void* hv, double* t, uint8_t* pool, int32_t* worker, double* f) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  for (size_t k = 0; k < r.freq_timeline.size(); ++k) {
+    t[k] = r.freq_timeline[k].applied_ms;
+    pool[k] = r.freq_timeline[k].prefill_pool ? 1 : 0;
+    worker[k] = r.freq_timeline[k].worker;
+    f[k] = r.freq_timeline[k].f_mhz;
+  }
+}
+
+void ref_sim_commands(void* hv, double* tick, int32_t* cls, int32_t* worker, double* f,
+                      double* window, uint8_t* infeasible) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  for (size_t k = 0; k < r.prefill_commands.size(); ++k) {
+    const auto& c = r.prefill_commands[k];
+    tick[k] = c.tick_ms;
+    cls[k] = c.class_id;
+    worker[k] = c.worker;
+    f[k] = c.f_mhz;
+    window[k] = c.window_ms;
+    infeasible[k] = c.infeasible ? 1 : 0;
+  }
+}
+
+// [0] sim_end_ms, [1] last_arrival_ms, [2] -1 (no end floor), [3] prefill_pool_j,
+// [4] decode_pool_j, [5] ttft_pct, [6] tbt_pct (per request), [7] tbt_pct (aggregate)
+void ref_sim_scalars(void* hv, double* d) {
+  const auto& r = static_cast<RefSim*>(hv)->r;
+  d[0] = r.sim_end_ms;
+  d[1] = r.last_arrival_ms;
+  d[2] = -1.0;
+  d[3] = r.prefill_pool_j();
+  d[4] = r.decode_pool_j();
+  const PassRates a = slo_pass_rates(r, r.slo, false);
+  const PassRates b = slo_pass_rates(r, r.slo, true);
+  d[5] = a.ttft_pct;
+  d[6] = a.tbt_pct;
+  d[7] = b.tbt_pct;
+}
+
+// CPU baseline for the closed loop: one full reference run() per scenario (its own decode
+// controller config), `threads` std::threads. Outputs decode_pool_j and the decision count.
+void ref_sim_run_many(const gso_profile* prof, const gso_policy* base, const gso_ctl_cfg* cfgs,
+                      int64_t n_scen, const gso_slo* slo, const gso_sim_cfg* cfg, int64_t n,
+                      const int64_t* arrival_ms, const int32_t* prompt, const int32_t* output,
+                      int threads, double* decode_j, int64_t* n_decisions) {
+  auto work = [&](int64_t lo, int64_t hi) {
+    const Trace tr = to_trace(n, arrival_ms, prompt, output, nullptr);
+    const GpuProfile gp = to_profile(prof);
+    SloConfig sc;
+    sc.ttft_sm_ms = slo->ttft_sm_ms;
+    sc.ttft_l_ms = slo->ttft_l_ms;
+    sc.tbt_p95_ms = slo->tbt_p95_ms;
+    const SimConfig sim = to_simcfg(cfg);
+    for (int64_t s = lo; s < hi; ++s) {
+      gso_policy p = *base;
+      p.decode_ctl = cfgs[s];
+      const RunResult r = run(tr, gp, to_policy(&p, cfg->n_prefill_workers), 1, sc, sim);
+      decode_j[s] = r.decode_pool_j();
+      n_decisions[s] = static_cast<int64_t>(r.decode_decisions.size());
+    }
+  };
+  if (threads <= 1) {
+    work(0, n_scen);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back(work, n_scen * t / threads, n_scen * (t + 1) / threads);
+  for (auto& th : pool) th.join();
+}
+
+}  // extern "C"
