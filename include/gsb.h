@@ -362,6 +362,82 @@ int gsb_replay_validate(const gsb_ctl_cfg* cfgs, int64_t n, int32_t n_buckets,
                         const double* tps_lo, const double* tps_hi, int64_t n_tables,
                         char* msg, size_t msg_cap);
 
+
+/* ---------------------------------------------------------------- K5: closed-loop decode pool */
+/* The decode side of the reference simulator (simkernel.cpp:330-464: continuous batching up to
+ * max_batch, step time decode_step_raw_ms (gpu_model.cpp:99-103), least-loaded enqueue,
+ * actuation delay, identical-target drop, per-worker power ledgers, TbtWindow/TpsWindow and the
+ * DecodeController's fine/coarse/adapt ticks, which stop once nothing is outstanding) replayed
+ * for N scenarios at once, one warp each. The input is the decode-enqueue stream: the
+ * (time, request) pairs of simkernel.cpp:347 in the reference's processing order. The prefill
+ * pool never waits on the decode pool, so one stream (recorded by the oracle's restated
+ * simulator, or any caller's own) serves every decode parameter set. */
+typedef struct gsb_pool_cfg {  /* SimConfig (simkernel.hpp:88-104) decode side + SloConfig */
+  int32_t n_decode_workers;    /* 1..30 */
+  int32_t max_batch;           /* 1..256 */
+  int32_t max_queue;           /* per-worker backlog cap: enqueue at load >= cap is rejected */
+  int32_t tbt_cap;             /* >= every scenario's tbt_window_tokens, <= GSB_MAX_TBT_WINDOW */
+  int32_t tps_cap;             /* TpsWindow deque capacity (gsb_decode_pool_tps_cap) */
+  int32_t pending_cap;         /* per-worker FIFO capacity (>= max_queue is always enough) */
+  double actuation_delay_ms;
+  double tbt_p95_ms;           /* SloConfig::tbt_p95_ms (pass-rate counts) */
+} gsb_pool_cfg;
+
+typedef struct gsb_pool_stream {
+  int64_t n_streams;
+  const int64_t* d_off;          /* [S+1] enqueues of stream s are [off[s], off[s+1]) */
+  const double* d_t_ms;          /* [E] enqueue instants, processing order */
+  const int32_t* d_req;          /* [E] request ids */
+  const double* d_end_floor_ms;  /* [S] prefill side's part of sim_end_ms (NULL = 0) */
+  int64_t n_requests;            /* per-request arrays below, indexed by request id */
+  const int32_t* d_output_tokens;
+  const double* d_arrival_ms;
+  const double* d_ttft_slo_ms;   /* SloConfig::ttft_for(SM/L) of the request */
+} gsb_pool_stream;
+
+/* Decode-side outcome of one scenario. Digests (identical definitions in the oracle,
+ * gs_oracle.h gso_pool_summary): decision_digest = FNV over workers of each worker's K3
+ * record digest; freq_digest = FNV over workers of FNV-1a(applied_ms, f) of its applied
+ * changes; request_digest = sum mod 2^64 of FNV-1a(id, first_token, gaps..., finish, worker)
+ * per completed request (FNV-1a(id, 0xdead) per decode-side rejection). status != 0 means a
+ * capacity was exceeded (1 pending FIFO, 2 TPS deque, 4 pending clock applications, 8 tbt_cap
+ * below a scenario's window): the scenario's outputs are then invalid. */
+typedef struct gsb_pool_summary {
+  double decode_pool_j, active_decode_j, idle_j, sim_end_ms;
+  int64_t n_completed, n_rejected, n_ttft_ok, n_tbt_ok, tbt_samples, tbt_samples_ok;
+  int64_t n_decisions, n_freq_changes, n_steps;
+  uint64_t decision_digest, freq_digest, request_digest;
+  int32_t status, pad_;
+} gsb_pool_summary;
+
+typedef struct gsb_pool_args {
+  int64_t n_scen;
+  const gsb_ctl_cfg* d_cfg;      /* [N] DecodeCtlConfig per scenario */
+  const double* d_fixed_mhz;     /* [N] optional: > 0 pins every decode clock, no controller
+                                    (FixedFreq; DefaultNV / PrefillSplit pass f_max) */
+  const int32_t* d_table_of;     /* [N] band table (NULL = 0) */
+  const int32_t* d_stream_of;    /* [N] enqueue stream (NULL = 0) */
+  int32_t n_buckets;
+  const double* d_tps_hi;        /* [T][n_buckets] */
+  const double* d_f_opt;         /* [T][n_buckets] */
+  gsb_pool_summary* d_out;       /* [N] */
+  double* d_ledger;              /* optional [N][W][2]: active_decode_j, idle_j per worker */
+  gsb_decision* d_records;       /* optional [N][W][rec_cap]: each worker's log in order */
+  int64_t rec_cap;
+  double* d_freq;                /* optional [N][W][freq_cap][2]: (applied_ms, f) per worker */
+  int64_t freq_cap;
+  int32_t* d_req_worker;         /* optional [N][n_requests]: RequestRecord::decode_worker */
+  double* d_req_first;           /* optional [N][n_requests]: first_token_ms */
+  double* d_req_finish;          /* optional [N][n_requests]: finish_ms */
+} gsb_pool_args;
+
+/* Upper bound on the TpsWindow deque length for a profile (2 coarse periods of the shortest
+ * possible step + 3); -1 when unbounded or > 4096. */
+int gsb_decode_pool_tps_cap(const gsb_profile* prof, int32_t max_batch, double coarse_period_ms);
+/* prof is a HOST pointer (passed as a kernel parameter); everything in st / a is device memory. */
+int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* cfg,
+                    const gsb_pool_stream* st, const gsb_pool_args* a, void* stream);
+
 /* ---------------------------------------------------------------- microbenchmarks */
 /* FP64 pipe peak probe: n_threads lanes each run `iters` independent DFMA chains;
  * returns the DFMA count in *d_out-sized work (used by bench.py for the roofline). */

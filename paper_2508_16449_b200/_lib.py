@@ -79,6 +79,35 @@ class CCtlState(C.Structure):
                 ("initialized", _i32), ("pad_", _i32), ("f_opt", _d * 32)]
 
 
+class CPoolCfg(C.Structure):
+    _fields_ = [("n_decode_workers", _i32), ("max_batch", _i32), ("max_queue", _i32),
+                ("tbt_cap", _i32), ("tps_cap", _i32), ("pending_cap", _i32),
+                ("actuation_delay_ms", _d), ("tbt_p95_ms", _d)]
+
+
+class CPoolStream(C.Structure):
+    _fields_ = [("n_streams", _i64), ("d_off", _p), ("d_t_ms", _p), ("d_req", _p),
+                ("d_end_floor_ms", _p), ("n_requests", _i64), ("d_output_tokens", _p),
+                ("d_arrival_ms", _p), ("d_ttft_slo_ms", _p)]
+
+
+class CPoolSummary(C.Structure):
+    _fields_ = [("decode_pool_j", _d), ("active_decode_j", _d), ("idle_j", _d),
+                ("sim_end_ms", _d), ("n_completed", _i64), ("n_rejected", _i64),
+                ("n_ttft_ok", _i64), ("n_tbt_ok", _i64), ("tbt_samples", _i64),
+                ("tbt_samples_ok", _i64), ("n_decisions", _i64), ("n_freq_changes", _i64),
+                ("n_steps", _i64), ("decision_digest", _u64), ("freq_digest", _u64),
+                ("request_digest", _u64), ("status", _i32), ("pad_", _i32)]
+
+
+class CPoolArgs(C.Structure):
+    _fields_ = [("n_scen", _i64), ("d_cfg", _p), ("d_fixed_mhz", _p), ("d_table_of", _p),
+                ("d_stream_of", _p), ("n_buckets", _i32), ("d_tps_hi", _p), ("d_f_opt", _p),
+                ("d_out", _p), ("d_ledger", _p), ("d_records", _p), ("rec_cap", _i64),
+                ("d_freq", _p), ("freq_cap", _i64), ("d_req_worker", _p), ("d_req_first", _p),
+                ("d_req_finish", _p)]
+
+
 # every symbol include/gsb.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "gsb_version", "gsb_status_string", "gsb_ctx_create", "gsb_ctx_destroy", "gsb_last_error",
@@ -91,6 +120,7 @@ EXPORTS = (
     "gsb_set_profiles_ex", "gsb_malloc", "gsb_free", "gsb_host_alloc", "gsb_host_free",
     "gsb_memcpy", "gsb_classify",
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
+    "gsb_decode_pool", "gsb_decode_pool_tps_cap",
 )
 
 _lib = None
@@ -151,5 +181,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_classify.argtypes = [_p, C.c_int, _p, _i64, _p, _p, _p]
     L.gsb_t_ref_batches.argtypes = [_p, P(_d), _i64, _p, _p, _p, _p, _p]
     L.gsb_energy_closed_form_batches.argtypes = [_p, C.c_int, _i64, _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_decode_pool_tps_cap.argtypes = [P(CProfile), _i32, _d]
+    L.gsb_decode_pool.argtypes = [_p, P(CProfile), P(CPoolCfg), P(CPoolStream), P(CPoolArgs), _p]
     _lib = L
     return L

@@ -344,6 +344,53 @@ def ctl_cfg_array(cfgs: Sequence[DecodeCtlConfig]) -> np.ndarray:
     return a
 
 
+# ------------------------------------------------------------------ simkernel.hpp (decode pool)
+@dataclass
+class SimConfig:
+    """greensim::SimConfig (simkernel.hpp:88-104), the fields the decode pool reads."""
+    n_prefill_workers: int = 2
+    n_decode_workers: int = 4
+    gpus_per_prefill_worker: int = 2
+    actuation_delay_ms: float = 5.0
+    handoff_delay_ms: float = 0.0
+    max_batch: int = 64
+    max_queue: int = 10000
+    band_tps_lo: float = 200.0
+    band_tps_hi: float = 3000.0
+    band_tps_step: float = 200.0
+
+    def band_levels(self) -> np.ndarray:
+        """The coarse band-table TPS levels, lo..hi inclusive (simkernel.cpp:200-203)."""
+        lv, l = [], self.band_tps_lo
+        while l <= self.band_tps_hi + 1e-9:
+            lv.append(l)
+            l += self.band_tps_step
+        return np.array(lv, np.float64)
+
+
+@dataclass
+class DecodeStream:
+    """A decode-enqueue stream (simkernel.cpp:347): (instant, request id) in the reference's
+    processing order, plus the per-request fields the decode pool reads. One stream drives
+    every decode parameter set (the prefill pool never waits on decode)."""
+    t_ms: np.ndarray           # f64 [E]
+    req: np.ndarray            # i32 [E]
+    output_tokens: np.ndarray  # i32 [R] by request id
+    arrival_ms: np.ndarray     # f64 [R]
+    ttft_slo_ms: np.ndarray    # f64 [R] SloConfig::ttft_for(SM/L)
+    end_floor_ms: float = 0.0  # prefill side's part of sim_end_ms
+
+
+POOL_SUMMARY_DTYPE = np.dtype([
+    ("decode_pool_j", "<f8"), ("active_decode_j", "<f8"), ("idle_j", "<f8"),
+    ("sim_end_ms", "<f8"), ("n_completed", "<i8"), ("n_rejected", "<i8"), ("n_ttft_ok", "<i8"),
+    ("n_tbt_ok", "<i8"), ("tbt_samples", "<i8"), ("tbt_samples_ok", "<i8"),
+    ("n_decisions", "<i8"), ("n_freq_changes", "<i8"), ("n_steps", "<i8"),
+    ("decision_digest", "<u8"), ("freq_digest", "<u8"), ("request_digest", "<u8"),
+    ("status", "<i4"), ("pad_", "<i4")])
+assert POOL_SUMMARY_DTYPE.itemsize == C.sizeof(L.CPoolSummary)
+
+
 # ------------------------------------------------------------------ results
 @dataclass
 class RouteResult:
@@ -868,6 +915,108 @@ class Engine:
         """Re-launch a prepared replay (all inputs/outputs already on the device): the
         timed / graph-captured decode step is this single K3b launch."""
         self._check(self.lib.gsb_decode_replay(self.ctx, C.byref(plan["_args"]), self.stream()))
+
+    # ---------------------------------------------------------------- K5: decode pool
+    def decode_pool(self, cfgs, stream: DecodeStream, profile: GpuProfile,
+                    sim: SimConfig = SimConfig(), slo: SloConfig = SloConfig(),
+                    fixed_mhz=None, details: bool = False, rec_cap: int = 0,
+                    freq_cap: int = 0, launch: bool = True) -> dict:
+        """K5: the closed-loop decode pool (simkernel.cpp:330-464) for N scenarios, one warp
+        each, all on one enqueue stream. cfgs: N DecodeCtlConfigs (or a CTL_DTYPE array);
+        fixed_mhz: optional [N] pinned clocks (> 0: FixedFreq-like, no controller). Band
+        tables are built on the GPU (K4) per distinct t_slo*margin (simkernel.cpp:200-205).
+        Returns a plan dict with device tensors; summary() reads it back."""
+        cfg_arr = cfgs if isinstance(cfgs, np.ndarray) else ctl_cfg_array(cfgs)
+        N = len(cfg_arr)
+        fx = (np.zeros(N) if fixed_mhz is None
+              else np.ascontiguousarray(np.broadcast_to(fixed_mhz, (N,)), np.float64))
+        levels = sim.band_levels()
+        t_eff = cfg_arr["tslo_ms"] * cfg_arr["margin_decode"]
+        uniq, table_of = np.unique(t_eff, return_inverse=True)
+        T, NB = len(uniq), len(levels)
+        lo, hi, fo, _ = self.build_band_tables([profile], [0] * T, uniq,
+                                               [sim.n_decode_workers] * T,
+                                               [sim.max_batch] * T, levels)
+        ctl = fx <= 0.0
+        if ctl.any():
+            msg = C.create_string_buffer(256)
+            sub = np.ascontiguousarray(cfg_arr[ctl])
+            rc = self.lib.gsb_replay_validate(sub.ctypes.data_as(C.c_void_p), len(sub), NB,
+                                              np.ascontiguousarray(lo.cpu().numpy()).ctypes.data_as(C.c_void_p),
+                                              np.ascontiguousarray(hi.cpu().numpy()).ctypes.data_as(C.c_void_p),
+                                              T, msg, 256)
+            if rc != L.OK:
+                raise ModelError(msg.value.decode())
+        if np.any(~ctl & ~np.array([profile.grid.on_grid(float(f)) for f in fx])):
+            raise ModelError("decode pool: fixed frequency is off-grid")
+        tps_cap = max(self.lib.gsb_decode_pool_tps_cap(C.byref(profile.to_c()), sim.max_batch,
+                                                       float(c)) for c in np.unique(cfg_arr["coarse_period_ms"]))
+        if tps_cap < 1:
+            raise ModelError("decode pool: TPS window unbounded for this profile")
+        min_fine = float(np.min(cfg_arr["fine_period_ms"][ctl])) if ctl.any() else 1.0
+        if ctl.any() and sim.actuation_delay_ms / min_fine + 1 > 4:
+            raise ModelError("decode pool: actuation delay above 3 fine periods is not supported")
+        n_req = len(stream.output_tokens)
+        pc = L.CPoolCfg(sim.n_decode_workers, sim.max_batch, sim.max_queue,
+                              int(max(1, cfg_arr["tbt_window_tokens"].max())), int(tps_cap),
+                              int(min(sim.max_queue, max(1, len(stream.t_ms)))),
+                              sim.actuation_delay_ms, slo.tbt_p95_ms)
+        keep = {
+            "off": self._dev(np.array([0, len(stream.t_ms)], np.int64), torch.int64),
+            "t": self._dev(np.ascontiguousarray(stream.t_ms, np.float64), torch.float64),
+            "req": self._dev(np.ascontiguousarray(stream.req, np.int32), torch.int32),
+            "floor": self._dev(np.array([stream.end_floor_ms], np.float64), torch.float64),
+            "out": self._dev(np.ascontiguousarray(stream.output_tokens, np.int32), torch.int32),
+            "arr": self._dev(np.ascontiguousarray(stream.arrival_ms, np.float64), torch.float64),
+            "ttft": self._dev(np.ascontiguousarray(stream.ttft_slo_ms, np.float64), torch.float64),
+            "cfg": self._dev(cfg_arr.view(np.uint8), torch.uint8),
+            "fixed": self._dev(fx, torch.float64),
+            "table_of": self._dev(table_of.astype(np.int32), torch.int32),
+            "tps_hi": hi.contiguous(), "f_opt": fo.contiguous(),
+        }
+        st = L.CPoolStream(1, _ptr(keep["off"]), _ptr(keep["t"]), _ptr(keep["req"]),
+                           _ptr(keep["floor"]), n_req, _ptr(keep["out"]), _ptr(keep["arr"]),
+                           _ptr(keep["ttft"]))
+        W = sim.n_decode_workers
+        out = {"summary": self._empty(N * POOL_SUMMARY_DTYPE.itemsize, torch.uint8),
+               "ledger": self._empty((N, W, 2), torch.float64) if details else None,
+               "records": (self._empty((N, W, rec_cap, DECISION_DTYPE.itemsize), torch.uint8)
+                           if rec_cap else None),
+               "freq": self._empty((N, W, freq_cap, 2), torch.float64) if freq_cap else None,
+               "req_worker": self._empty((N, n_req), torch.int32) if details else None,
+               "req_first": self._empty((N, n_req), torch.float64) if details else None,
+               "req_finish": self._empty((N, n_req), torch.float64) if details else None}
+        if details:
+            out["req_worker"].fill_(-1)
+            out["req_first"].fill_(-1.0)
+            out["req_finish"].fill_(-1.0)
+        a = L.CPoolArgs(N, _ptr(keep["cfg"]), _ptr(keep["fixed"]), _ptr(keep["table_of"]), None,
+                        NB, _ptr(keep["tps_hi"]), _ptr(keep["f_opt"]), _ptr(out["summary"]),
+                        _ptr(out["ledger"]), _ptr(out["records"]), rec_cap, _ptr(out["freq"]),
+                        freq_cap, _ptr(out["req_worker"]), _ptr(out["req_first"]),
+                        _ptr(out["req_finish"]))
+        plan = {"out": out, "_keep": keep, "_args": a, "_cfg": pc, "_stream": st,
+                "_prof": profile.to_c(), "n": N, "W": W}
+        if launch:
+            self.run_pool(plan)
+        return plan
+
+    def run_pool(self, plan: dict) -> None:
+        """(Re-)launch a prepared decode-pool plan: one K5 launch."""
+        self._check(self.lib.gsb_decode_pool(self.ctx, C.byref(plan["_prof"]), C.byref(plan["_cfg"]),
+                                             C.byref(plan["_stream"]), C.byref(plan["_args"]),
+                                             self.stream()))
+
+    @staticmethod
+    def pool_summary(plan: dict) -> np.ndarray:
+        """The [N] gsb_pool_summary records (POOL_SUMMARY_DTYPE); raises ModelError when a
+        scenario exceeded a capacity (its outputs are invalid)."""
+        sm = plan["out"]["summary"].cpu().numpy().view(POOL_SUMMARY_DTYPE)
+        bad = np.nonzero(sm["status"])[0]
+        if len(bad):
+            raise ModelError(f"decode pool: capacity exceeded in {len(bad)} scenarios "
+                             f"(status {int(sm['status'][bad[0]])})")
+        return sm
 
     def selftest_division(self, per_divisor: int, seed: int = 12345) -> int:
         bad = self._empty(1, torch.int64)

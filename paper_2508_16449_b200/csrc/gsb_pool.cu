@@ -1,0 +1,720 @@
+// gsb_pool.cu — K5: the closed-loop decode pool.
+//
+// Replays the decode side of the reference simulator (simkernel.cpp:330-464: batching,
+// step times, least-loaded enqueue, actuation delay, ledgers, TBT/TPS windows and the
+// DecodeController ticks) for thousands of controller parameter sets at once, all driven by
+// one decode-enqueue stream (the prefill pool never waits on the decode pool, so the stream
+// is independent of decode parameters; the oracle records it, oracle/gs_sim.c).
+//
+// One WARP per scenario, sequential in simulated time. Every iteration selects the next event
+// exactly as the reference's priority queue would (time, then kind: step end 2 < enqueue 3 <
+// freq applied 4 < coarse 5 < adapt 6 < fine 7, simkernel.cpp:21-31,44-50) with three warp
+// min-reductions, then runs it:
+//   * a step end spreads its batch's streams over the lanes (first token / gap / completion,
+//     stream compaction by ballot), then refills the batch from the worker's FIFO;
+//   * ticks run one controller per lane (lane w = decode worker w);
+//   * the nearest-rank P95 of the TBT window is a warp-parallel rank count over RUNS: every
+//     gap recorded by one step end equals that step's duration (each active stream last
+//     emitted at the step's start, simkernel.cpp:365-379), so the 256-sample ring is a short
+//     deque of (value, count) runs and the P95 is exact without sorting.
+// Events that the reference orders only by insertion sequence (two workers' step ends, or
+// freq applications, at the same instant) touch disjoint worker state and commute.
+// Per-worker state lives in shared memory; the FIFO of waiting requests in a global
+// workspace slot owned by the warp (persistent grid, scenarios claimed by atomic counter).
+#include <cmath>
+
+#include "gsb_common.cuh"
+#include "gsb_ctl.cuh"
+
+using gsb::std_clamp;
+using gsb::std_max;
+using gsb::std_min;
+using namespace gsbctl;
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kFQ = 4;  // pending clock applications per worker (delay / fine period + 1)
+constexpr uint64_t kFnv0 = 0xcbf29ce484222325ull;
+constexpr unsigned kFull = 0xffffffffu;
+
+enum : int { K_STEP = 2, K_ENQ = 3, K_FREQ = 4, K_COARSE = 5, K_ADAPT = 6, K_FINE = 7, K_NONE = 15 };
+enum : int { PH_DECODE = 1, PH_IDLE = 2 };
+enum : int { ST_PENDING = 1, ST_TPS = 2, ST_FREQ = 4, ST_TBT = 8 };
+
+struct PoolParams {
+  gsb_profile prof;
+  gsb_pool_cfg cfg;
+  gsb_pool_stream st;
+  gsb_pool_args a;
+  int W, MB, RC, TC;
+  int64_t warp_bytes;
+  int32_t* ws_pending;  // [n_warps][W][pending_cap]
+  unsigned* counter;
+};
+
+// shared-memory carve-up of one warp's region
+struct Smem {
+  uint64_t* h;     // [W][MB] request digest chain
+  double* rv;      // [W][RC] TBT run values
+  double* tt;      // [W][TC] TPS event times
+  double* fq_t;    // [W][kFQ]
+  double* fq_f;    // [W][kFQ]
+  int32_t* req;    // [W][MB]
+  int32_t* emit;   // [W][MB]
+  int32_t* out;    // [W][MB]
+  int32_t* nle;    // [W][MB] gaps <= SLO (bit 31: TTFT met)
+  int32_t* ttok;   // [W][TC]
+  uint16_t* rc;    // [W][RC] TBT run counts
+};
+
+__host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC) {
+  int64_t b = 8ll * W * MB + 8ll * W * RC + 8ll * W * TC + 16ll * W * kFQ + 16ll * W * MB +
+              4ll * W * TC + 2ll * W * RC;
+  return (b + 15) & ~15ll;
+}
+
+__device__ __forceinline__ Smem carve(char* base, int W, int MB, int RC, int TC) {
+  Smem s;
+  char* p = base;
+  s.h = reinterpret_cast<uint64_t*>(p); p += 8ll * W * MB;
+  s.rv = reinterpret_cast<double*>(p); p += 8ll * W * RC;
+  s.tt = reinterpret_cast<double*>(p); p += 8ll * W * TC;
+  s.fq_t = reinterpret_cast<double*>(p); p += 8ll * W * kFQ;
+  s.fq_f = reinterpret_cast<double*>(p); p += 8ll * W * kFQ;
+  s.req = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
+  s.emit = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
+  s.out = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
+  s.nle = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
+  s.ttok = reinterpret_cast<int32_t*>(p); p += 4ll * W * TC;
+  s.rc = reinterpret_cast<uint16_t*>(p);
+  return s;
+}
+
+__device__ __forceinline__ uint64_t dbits(double x) {
+  return static_cast<uint64_t>(__double_as_longlong(x));
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFull, v, src); }
+
+// Per-lane state of decode worker w = lane (lanes >= W carry inert copies).
+struct Worker {
+  double freq, target, P;        // applied clock, last command, P(freq)
+  double t_end, t_start;         // step end (+inf when idle), step start
+  int n_active;
+  int64_t p_head, p_tail;        // FIFO [head, tail) in the workspace ring
+  int fq_head, fq_n;             // pending clock applications
+  double ps_last, ps_power;      // PowerState (simkernel.cpp:53-57)
+  int ps_phase;
+  double act_j, idle_j;          // WorkerLedger sums
+  int r_head, r_n, r_total;      // TBT runs ring
+  bool p95_valid;
+  double p95;
+  int t_head, t_n;               // TPS ring
+  uint64_t fdig;                 // applied-clock digest
+  int64_t n_freq;
+  double last_applied;
+};
+
+// ledger_close / ledger_set (simkernel.cpp:60-79)
+__device__ __forceinline__ void ledger_close(Worker& wk, double now) {
+  if (now > wk.ps_last) {
+    const double joules = wk.ps_power * (now - wk.ps_last) / 1000.0;
+    if (wk.ps_phase == PH_DECODE)
+      wk.act_j += joules;
+    else
+      wk.idle_j += joules;
+  }
+  wk.ps_last = now;
+}
+__device__ __forceinline__ void ledger_set(Worker& wk, double now, int phase, double power) {
+  if (phase == wk.ps_phase && power == wk.ps_power) return;
+  ledger_close(wk, now);
+  wk.ps_phase = phase;
+  wk.ps_power = power;
+}
+
+__device__ __forceinline__ double power_at(const gsb_profile& p, double f) {
+  return ((p.k3 * f + p.k2) * f + p.k1) * f + p.k0;  // gpu_model.hpp:64
+}
+
+// Nearest-rank P95 of worker w's TBT window (metrics.cpp:11-19): the value v of a run with
+// #(< v) <= rank-1 < #(<= v). Warp-parallel rank count over the runs; all lanes get it.
+__device__ double window_p95(const Smem& s, int RC, int w, int r_head, int r_n, int total, int lane) {
+  const double* rv = s.rv + w * RC;
+  const uint16_t* rc = s.rc + w * RC;
+  const int idx = static_cast<int>(ceil(0.95 * static_cast<double>(total))) - 1;
+  double found = 0.0;
+  bool have = false;
+  for (int base = 0; base < r_n; base += 32) {
+    const int i = base + lane;
+    bool cand = false;
+    double v = 0.0;
+    if (i < r_n) {
+      int pos = r_head + i;
+      if (pos >= RC) pos -= RC;
+      v = rv[pos];
+      int less = 0, eq = 0;
+      int q = r_head;
+      for (int j = 0; j < r_n; ++j) {
+        const double x = rv[q];
+        const int c = rc[q];
+        less += x < v ? c : 0;
+        eq += x == v ? c : 0;
+        if (++q == RC) q = 0;
+      }
+      cand = less <= idx && idx < less + eq;
+    }
+    const unsigned m = __ballot_sync(kFull, cand);
+    if (m && !have) {
+      found = shfl_d(v, __ffs(m) - 1);
+      have = true;
+    }
+  }
+  return found;
+}
+
+template <bool REQ_OUT>
+__device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, int64_t n, int lane) {
+  const gsb_profile& prof = P.prof;
+  const gsb_pool_cfg& cfg = P.cfg;
+  const gsb_pool_args& a = P.a;
+  const gsb_pool_stream& st = P.st;
+  const int W = P.W, MB = P.MB, RC = P.RC, TC = P.TC;
+  const int64_t PC = cfg.pending_cap;
+  const bool is_w = lane < W;
+  const int w = lane;
+
+  const gsb_ctl_cfg ccfg = a.d_cfg[n];
+  const double fixed = a.d_fixed_mhz ? a.d_fixed_mhz[n] : 0.0;
+  const bool ctl_on = !(fixed > 0.0);
+  const int NB = a.n_buckets;
+  const int64_t tb = a.d_table_of ? a.d_table_of[n] : 0;
+  const int64_t sid = a.d_stream_of ? a.d_stream_of[n] : 0;
+  const int64_t e_begin = st.d_off[sid], e_end = st.d_off[sid + 1];
+  const int64_t n_stream = e_end - e_begin;
+  const double end_floor = st.d_end_floor_ms ? st.d_end_floor_ms[sid] : 0.0;
+  const double tbt_thr = cfg.tbt_p95_ms;
+  int status = 0;
+  if (ccfg.tbt_window_tokens > RC) status |= ST_TBT;
+
+  // controller (lane w), DecodeController ctor (decode_ctl.cpp:130-140)
+  double f_opt[GSB_MAX_BUCKETS];
+  const CtlK k = make_k(ccfg, NB, a.d_tps_hi + tb * NB, prof.f_min_mhz, prof.f_max_mhz);
+  Ctl<false> c;
+  if (ctl_on) {
+    for (int b = 0; b < NB; ++b) f_opt[b] = a.d_f_opt[tb * NB + b];
+    ctl_init(c, f_opt, k);
+  } else {
+    c.n_rec = 0;
+    c.digest = kFnv0;
+  }
+  gsb_decision* rec = (a.d_records && a.rec_cap > 0 && is_w)
+                          ? a.d_records + (n * W + w) * a.rec_cap : nullptr;
+  double* fout = (a.d_freq && a.freq_cap > 0 && is_w) ? a.d_freq + (n * W + w) * a.freq_cap * 2
+                                                      : nullptr;
+  const int tbt_cap = ccfg.tbt_window_tokens;
+  const double tps_window = ccfg.coarse_period_ms;
+
+  // Sim::init (simkernel.cpp:195-233): decode clocks start at controllers_[0].command()
+  const double f0 = ctl_on ? shfl_d(c.sp, 0) : fixed;
+  Worker wk;
+  wk.freq = wk.target = f0;
+  wk.P = power_at(prof, f0);
+  wk.t_end = INFINITY;
+  wk.t_start = 0.0;
+  wk.n_active = 0;
+  wk.p_head = wk.p_tail = 0;
+  wk.fq_head = wk.fq_n = 0;
+  wk.ps_last = 0.0;
+  wk.ps_power = prof.p_idle_w;
+  wk.ps_phase = PH_IDLE;
+  wk.act_j = wk.idle_j = 0.0;
+  wk.r_head = wk.r_n = wk.r_total = 0;
+  wk.p95_valid = false;
+  wk.p95 = 0.0;
+  wk.t_head = wk.t_n = 0;
+  wk.fdig = kFnv0;
+  wk.n_freq = 0;
+  wk.last_applied = 0.0;
+
+  // uniform state
+  double tf = ccfg.fine_period_ms, tc = ccfg.coarse_period_ms, ta = ccfg.adapt_period_s * 1000.0;
+  bool fine_on = ctl_on, coarse_on = ctl_on, adapt_on = ctl_on;
+  int64_t e = e_begin;
+  double t_enq = e < e_end ? st.d_t_ms[e] : INFINITY;
+  int64_t n_done = 0;
+  // lane-local accumulators (warp-reduced at the end)
+  int64_t n_completed = 0, n_rejected = 0, n_ttft_ok = 0, n_tbt_ok = 0, samples = 0, samples_ok = 0;
+  int64_t n_steps = 0;
+  uint64_t rdig = 0;
+  double max_finish = 0.0;
+  double* req_first = REQ_OUT ? a.d_req_first + n * st.n_requests : nullptr;
+  double* req_finish = REQ_OUT ? a.d_req_finish + n * st.n_requests : nullptr;
+  int32_t* req_worker = REQ_OUT ? a.d_req_worker + n * st.n_requests : nullptr;
+
+  int32_t* S_req = s.req;
+  int32_t* S_emit = s.emit;
+  int32_t* S_out = s.out;
+  int32_t* S_nle = s.nle;
+  uint64_t* S_h = s.h;
+
+  // start_decode_step (simkernel.cpp:330-345) of worker ww, whole warp
+  auto start_step = [&](int ww, double now) {
+    const int na = __shfl_sync(kFull, wk.n_active, ww);
+    const int64_t ph = __shfl_sync(kFull, wk.p_head, ww);
+    const int64_t pt = __shfl_sync(kFull, wk.p_tail, ww);
+    const int take = static_cast<int>(min(static_cast<int64_t>(MB - na), pt - ph));
+    const int32_t* ring = pend + static_cast<int64_t>(ww) * PC;
+    for (int j = lane; j < take; j += 32) {
+      const int32_t r = ring[(ph + j) % PC];
+      const int slot = ww * MB + na + j;
+      S_req[slot] = r;
+      S_emit[slot] = 0;
+      S_out[slot] = st.d_output_tokens[r];
+      S_nle[slot] = 0;
+      S_h[slot] = mix(kFnv0, static_cast<uint64_t>(r));
+    }
+    __syncwarp();
+    if (lane == ww) {
+      wk.p_head = ph + take;
+      wk.n_active = na + take;
+      if (wk.n_active == 0) {
+        ledger_set(wk, now, PH_IDLE, prof.p_idle_w);
+      } else {
+        const double B = static_cast<double>(wk.n_active);
+        // decode_step_raw_ms, gpu_model.cpp:99-103
+        const double step = (prof.dec_alpha0_ms + prof.dec_alpha1_ms * B) +
+                            (prof.dec_beta0_ms + prof.dec_beta1_ms * B) * prof.dec_f_ref_mhz / wk.freq;
+        wk.t_start = now;
+        wk.t_end = now + step;
+        ledger_set(wk, now, PH_DECODE, wk.P);
+      }
+    }
+  };
+
+  for (;;) {
+    // ---- next event: lexicographic min of (t, kind, lane) over the candidates
+    double ct = INFINITY;
+    int ck = K_NONE;
+    if (is_w) {
+      const double tq = wk.fq_n ? s.fq_t[w * kFQ + wk.fq_head] : INFINITY;
+      if (wk.t_end <= tq) {
+        ct = wk.t_end;
+        ck = K_STEP;
+      } else {
+        ct = tq;
+        ck = K_FREQ;
+      }
+      if (ct == INFINITY) ck = K_NONE;
+    } else if (lane == W) {
+      ct = t_enq;
+      ck = ct == INFINITY ? K_NONE : K_ENQ;
+    } else if (lane == W + 1) {
+      // ticks: coarse (5) < adapt (6) < fine (7) at equal times
+      double t = INFINITY;
+      int kk = K_NONE;
+      if (coarse_on) { t = tc; kk = K_COARSE; }
+      if (adapt_on && ta < t) { t = ta; kk = K_ADAPT; }
+      if (fine_on && tf < t) { t = tf; kk = K_FINE; }
+      ct = t;
+      ck = kk;
+    }
+    const uint64_t tb_ = dbits(ct);  // non-negative doubles order as their bit patterns
+    const unsigned hi = __reduce_min_sync(kFull, static_cast<unsigned>(tb_ >> 32));
+    const unsigned lo = __reduce_min_sync(kFull, static_cast<unsigned>(tb_ >> 32) == hi
+                                                     ? static_cast<unsigned>(tb_) : 0xffffffffu);
+    const bool at_min = (static_cast<unsigned>(tb_ >> 32) == hi) && (static_cast<unsigned>(tb_) == lo);
+    const unsigned code = __reduce_min_sync(kFull, at_min ? static_cast<unsigned>(ck * 32 + lane) : 0xffffffffu);
+    const int kind = static_cast<int>(code >> 5);
+    if (kind >= K_NONE) break;
+    const int src = static_cast<int>(code & 31);
+    const double now = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(hi) << 32) | lo));
+
+    if (kind == K_STEP) {
+      // ---- on_decode_step_end (simkernel.cpp:365-393), worker src
+      const int ww = src;
+      const int na = __shfl_sync(kFull, wk.n_active, ww);
+      const double gap = now - shfl_d(wk.t_start, ww);
+      int kept = 0, gaps_rec = 0;
+      for (int base = 0; base < na; base += 32) {
+        const int j = base + lane;
+        bool keep = false;
+        int32_t r = 0, em = 0, ou = 0, nl = 0;
+        uint64_t h = 0;
+        if (j < na) {
+          const int slot = ww * MB + j;
+          r = S_req[slot];
+          em = S_emit[slot];
+          ou = S_out[slot];
+          nl = S_nle[slot];
+          h = S_h[slot];
+          if (em == 0) {
+            // first token: TTFT = first_token - arrival (simkernel.hpp:125)
+            if (now - st.d_arrival_ms[r] <= st.d_ttft_slo_ms[r]) nl |= static_cast<int32_t>(0x80000000u);
+            h = mix(h, dbits(now));
+            if (REQ_OUT) req_first[r] = now;
+          } else {
+            h = mix(h, dbits(gap));
+            nl += gap <= tbt_thr ? 1 : 0;
+            ++gaps_rec;
+          }
+          ++em;
+          if (em >= ou) {
+            // completion: slo_pass_rates terms (metrics.cpp:42-72)
+            h = mix(mix(h, dbits(now)), static_cast<uint64_t>(static_cast<uint32_t>(ww)));
+            rdig += h;
+            ++n_completed;
+            const int ng = em - 1;
+            const int le = nl & 0x7fffffff;
+            if (nl < 0) ++n_ttft_ok;
+            const int rank = static_cast<int>(ceil(0.95 * static_cast<double>(ng)));
+            if (ng == 0 || le >= rank) ++n_tbt_ok;
+            samples += ng;
+            samples_ok += le;
+            max_finish = std_max(max_finish, now);
+            if (REQ_OUT) req_finish[r] = now;
+          } else {
+            keep = true;
+          }
+        }
+        const unsigned km = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) {
+          const int dst = ww * MB + kept + __popc(km & ((1u << lane) - 1u));
+          S_req[dst] = r;
+          S_emit[dst] = em;
+          S_out[dst] = ou;
+          S_nle[dst] = nl;
+          S_h[dst] = h;
+        }
+        kept += __popc(km);
+        __syncwarp();
+      }
+      const int g_total = __reduce_add_sync(kFull, static_cast<unsigned>(gaps_rec));
+      const int n_fin = na - kept;
+      if (lane == ww) {
+        wk.n_active = kept;
+        wk.t_end = INFINITY;
+        ++n_steps;
+        // TbtWindow::record x g_total equal gaps (decode_ctl.cpp:120-123) as one run
+        if (g_total > 0) {
+          int drop = wk.r_total + g_total - tbt_cap;
+          if (g_total >= tbt_cap) {
+            wk.r_n = 0;
+            wk.r_total = 0;
+            drop = 0;
+          }
+          while (drop > 0) {
+            const int pos = w * RC + wk.r_head;
+            const int cnt = s.rc[pos];
+            if (cnt <= drop) {
+              drop -= cnt;
+              wk.r_total -= cnt;
+              if (++wk.r_head == RC) wk.r_head = 0;
+              --wk.r_n;
+            } else {
+              s.rc[pos] = static_cast<uint16_t>(cnt - drop);
+              wk.r_total -= drop;
+              drop = 0;
+            }
+          }
+          const int g = min(g_total, tbt_cap);
+          int pos = wk.r_head + wk.r_n;
+          if (pos >= RC) pos -= RC;
+          s.rv[w * RC + pos] = gap;
+          s.rc[w * RC + pos] = static_cast<uint16_t>(g);
+          ++wk.r_n;
+          wk.r_total += g;
+          wk.p95_valid = false;
+        }
+        // TpsWindow::record (decode_ctl.hpp:73)
+        if (wk.t_n >= TC) {
+          status |= ST_TPS;
+        } else {
+          int pos = wk.t_head + wk.t_n;
+          if (pos >= TC) pos -= TC;
+          s.tt[w * TC + pos] = now;
+          s.ttok[w * TC + pos] = na;
+          ++wk.t_n;
+        }
+      }
+      n_done += n_fin;
+      __syncwarp();
+      start_step(ww, now);
+    } else if (kind == K_ENQ) {
+      // ---- on_decode_enqueue (simkernel.cpp:347-363): least-loaded, lowest index on ties
+      const int32_t r = st.d_req[e];
+      const unsigned load = is_w ? static_cast<unsigned>(wk.n_active + (wk.p_tail - wk.p_head)) : 0x7ffffffu;
+      const unsigned best_code = __reduce_min_sync(kFull, is_w ? (load << 5) | lane : 0xffffffffu);
+      const int best = static_cast<int>(best_code & 31);
+      const int64_t best_load = best_code >> 5;
+      if (best_load >= cfg.max_queue) {
+        if (lane == 0) rdig += mix(mix(kFnv0, static_cast<uint64_t>(r)), 0xdeadull);
+        n_rejected += lane == 0 ? 1 : 0;
+        ++n_done;
+      } else {
+        bool stepping = false;
+        if (lane == best) {
+          if (wk.p_tail - wk.p_head >= PC) {
+            status |= ST_PENDING;
+          } else {
+            pend[static_cast<int64_t>(best) * PC + (wk.p_tail % PC)] = r;
+            ++wk.p_tail;
+          }
+          stepping = wk.t_end != INFINITY;
+        }
+        if (REQ_OUT && lane == 0) req_worker[r] = best;
+        stepping = __shfl_sync(kFull, stepping, best);
+        __syncwarp();
+        if (!stepping) start_step(best, now);
+      }
+      ++e;
+      t_enq = e < e_end ? st.d_t_ms[e] : INFINITY;
+    } else if (kind == K_FREQ) {
+      // ---- on_freq_applied, decode branch (simkernel.cpp:428-436)
+      if (lane == src) {
+        const double f = s.fq_f[w * kFQ + wk.fq_head];
+        if (++wk.fq_head == kFQ) wk.fq_head = 0;
+        --wk.fq_n;
+        if (f != wk.freq) {
+          wk.freq = f;
+          wk.P = power_at(prof, f);
+          if (wk.t_end != INFINITY) ledger_set(wk, now, PH_DECODE, wk.P);
+          wk.fdig = mix(mix(wk.fdig, dbits(now)), dbits(f));
+          if (fout && wk.n_freq < a.freq_cap) {
+            fout[2 * wk.n_freq] = now;
+            fout[2 * wk.n_freq + 1] = f;
+          }
+          ++wk.n_freq;
+          wk.last_applied = now;
+        }
+      }
+    } else {
+      // ---- control ticks (simkernel.cpp:441-464); stop once nothing is outstanding
+      const bool live = n_done < n_stream;
+      if (kind == K_COARSE) {
+        if (!live) {
+          coarse_on = false;
+        } else {
+          if (is_w) {
+            // TpsWindow::tps (decode_ctl.cpp:113-118)
+            const double lim = now - tps_window;
+            while (wk.t_n > 0 && s.tt[w * TC + wk.t_head] < lim) {
+              if (++wk.t_head == TC) wk.t_head = 0;
+              --wk.t_n;
+            }
+            int tokens = 0;
+            int q = wk.t_head;
+            for (int j = 0; j < wk.t_n; ++j) {
+              tokens += s.ttok[w * TC + q];
+              if (++q == TC) q = 0;
+            }
+            on_coarse<false, true>(c, f_opt, k, tokens * 1000.0 / tps_window, now, a.rec_cap, rec, w);
+          }
+          tc = now + ccfg.coarse_period_ms;
+        }
+      } else if (kind == K_ADAPT) {
+        if (!live) {
+          adapt_on = false;
+        } else {
+          if (is_w) on_adapt<false, true>(c, f_opt, k, now, a.rec_cap, rec, w);
+          ta = now + ccfg.adapt_period_s * 1000.0;
+        }
+      } else {
+        if (!live) {
+          fine_on = false;
+        } else {
+          // refresh stale P95s, one worker at a time, whole warp
+          unsigned stale = __ballot_sync(kFull, is_w && !wk.p95_valid && wk.r_n > 0);
+          while (stale) {
+            const int ww = __ffs(stale) - 1;
+            stale &= stale - 1;
+            const int rh = __shfl_sync(kFull, wk.r_head, ww);
+            const int rn = __shfl_sync(kFull, wk.r_n, ww);
+            const int rt = __shfl_sync(kFull, wk.r_total, ww);
+            const double v = window_p95(s, RC, ww, rh, rn, rt, lane);
+            if (lane == ww) {
+              wk.p95 = v;
+              wk.p95_valid = true;
+            }
+          }
+          if (is_w) {
+            on_fine<false, true>(c, k, wk.r_n > 0, wk.p95, now, a.rec_cap, rec, w);
+            // command_freq (simkernel.cpp:397-404): identical targets are dropped
+            const double cmd = c.sp;
+            if (cmd != wk.target) {
+              wk.target = cmd;
+              if (wk.fq_n >= kFQ) {
+                status |= ST_FREQ;
+              } else {
+                int pos = wk.fq_head + wk.fq_n;
+                if (pos >= kFQ) pos -= kFQ;
+                s.fq_t[w * kFQ + pos] = now + cfg.actuation_delay_ms;
+                s.fq_f[w * kFQ + pos] = cmd;
+                ++wk.fq_n;
+              }
+            }
+          }
+          tf = now + ccfg.fine_period_ms;
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- finalize (simkernel.cpp:503-520) and the summary
+  double end = std_max(end_floor, max_finish);
+  end = std_max(end, is_w ? wk.last_applied : 0.0);
+  for (int off = 16; off > 0; off >>= 1) end = std_max(end, __shfl_xor_sync(kFull, end, off));
+  if (is_w) ledger_close(wk, end);
+  if (a.d_ledger && is_w) {
+    a.d_ledger[(n * W + w) * 2] = wk.act_j;
+    a.d_ledger[(n * W + w) * 2 + 1] = wk.idle_j;
+  }
+  auto sum64 = [&](int64_t v) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+  };
+  auto sumu64 = [&](uint64_t v) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+  };
+  n_completed = sum64(n_completed);
+  n_rejected = sum64(n_rejected);
+  n_ttft_ok = sum64(n_ttft_ok);
+  n_tbt_ok = sum64(n_tbt_ok);
+  samples = sum64(samples);
+  samples_ok = sum64(samples_ok);
+  rdig = sumu64(rdig);
+  const int64_t n_dec = sum64(is_w ? c.n_rec : 0);
+  const int64_t n_fc = sum64(is_w ? wk.n_freq : 0);
+  n_steps = sum64(is_w ? n_steps : 0);
+  status = static_cast<int>(__reduce_or_sync(kFull, static_cast<unsigned>(status)));
+  // RunResult::decode_pool_j (simkernel.cpp:617-621), worker order
+  double e_sum = 0.0, act = 0.0, idle = 0.0;
+  uint64_t dd = kFnv0, fd = kFnv0;
+  for (int ww = 0; ww < W; ++ww) {
+    const double aj = shfl_d(wk.act_j, ww);
+    const double ij = shfl_d(wk.idle_j, ww);
+    e_sum += 0.0 + aj + ij;
+    act += aj;
+    idle += ij;
+    dd = mix(dd, __shfl_sync(kFull, c.digest, ww));
+    fd = mix(fd, __shfl_sync(kFull, wk.fdig, ww));
+  }
+  if (lane == 0) {
+    gsb_pool_summary o;
+    o.decode_pool_j = e_sum;
+    o.active_decode_j = act;
+    o.idle_j = idle;
+    o.sim_end_ms = end;
+    o.n_completed = n_completed;
+    o.n_rejected = n_rejected;
+    o.n_ttft_ok = n_ttft_ok;
+    o.n_tbt_ok = n_tbt_ok;
+    o.tbt_samples = samples;
+    o.tbt_samples_ok = samples_ok;
+    o.n_decisions = n_dec;
+    o.n_freq_changes = n_fc;
+    o.n_steps = n_steps;
+    o.decision_digest = dd;
+    o.freq_digest = fd;
+    o.request_digest = rdig;
+    o.status = status;
+    o.pad_ = 0;
+    a.d_out[n] = o;
+  }
+}
+
+template <bool REQ_OUT>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_decode_pool(const __grid_constant__ PoolParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const Smem s = carve(smem + wib * P.warp_bytes, P.W, P.MB, P.RC, P.TC);
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  int32_t* pend = P.ws_pending + slot * P.W * P.cfg.pending_cap;
+  for (;;) {
+    unsigned n = 0;
+    if (lane == 0) n = atomicAdd(P.counter, 1u);
+    n = __shfl_sync(kFull, n, 0);
+    if (n >= P.a.n_scen) break;
+    run_scenario<REQ_OUT>(P, s, pend, static_cast<int64_t>(n), lane);
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsb_decode_pool_tps_cap(const gsb_profile* prof, int32_t max_batch, double coarse_period_ms) {
+  // the TPS deque holds the step ends of at most two coarse periods (trimmed at each coarse
+  // tick, simkernel.cpp:453-458): 2 * period / shortest step + 3
+  if (!prof || !(coarse_period_ms > 0.0)) return -1;
+  double best = INFINITY;
+  for (int b = 1; b <= max_batch; ++b) {
+    const double B = b;
+    const double s = (prof->dec_alpha0_ms + prof->dec_alpha1_ms * B) +
+                     (prof->dec_beta0_ms + prof->dec_beta1_ms * B) * prof->dec_f_ref_mhz / prof->f_max_mhz;
+    best = s < best ? s : best;
+  }
+  if (!(best > 0.0)) return -1;
+  const double n = 2.0 * coarse_period_ms / best + 3.0;
+  return n > 4096.0 ? -1 : static_cast<int>(n);
+}
+
+int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* cfg,
+                    const gsb_pool_stream* st, const gsb_pool_args* a, void* stream) {
+  if (!ctx || !prof || !cfg || !st || !a) return GSB_INVALID_ARGUMENT;
+  const int W = cfg->n_decode_workers, MB = cfg->max_batch;
+  if (W < 1 || W > 30) return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: 1..30 decode workers");
+  if (MB < 1 || MB > 256) return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: max_batch 1..256");
+  if (cfg->max_queue < 1) return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: max_queue >= 1");
+  if (cfg->tbt_cap < 1 || cfg->tbt_cap > GSB_MAX_TBT_WINDOW)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: tbt_cap 1..256");
+  if (cfg->tps_cap < 1 || cfg->pending_cap < 1)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: capacities must be positive");
+  if (a->n_buckets < 1 || a->n_buckets > GSB_MAX_BUCKETS)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "band table: need 1..32 buckets");
+  if (a->n_scen <= 0) return GSB_OK;
+  if (a->n_scen > 0xffffffffll) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "decode pool: too many scenarios");
+  const bool req_out = a->d_req_first && a->d_req_finish && a->d_req_worker;
+  PoolParams P;
+  P.prof = *prof;
+  P.cfg = *cfg;
+  P.st = *st;
+  P.a = *a;
+  P.W = W;
+  P.MB = MB;
+  P.RC = cfg->tbt_cap;
+  P.TC = cfg->tps_cap;
+  P.warp_bytes = smem_bytes(W, MB, P.RC, P.TC);
+  const int64_t block_smem = P.warp_bytes * kWarpsPerBlock;
+  if (block_smem > 227 * 1024)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
+  auto kern = req_out ? k_decode_pool<true> : k_decode_pool<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(block_smem)) != cudaSuccess)
+    return gsb_check_launch(ctx, "decode_pool attr");
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32,
+                                                static_cast<size_t>(block_smem));
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = static_cast<int64_t>(ctx->n_sms) * per_sm;
+  const int64_t need = (a->n_scen + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks > need) blocks = need;
+  const int64_t ws_ints = blocks * kWarpsPerBlock * W * static_cast<int64_t>(cfg->pending_cap);
+  const size_t bytes = 256 + static_cast<size_t>(ws_ints) * 4;
+  char* scratch = static_cast<char*>(gsb_scratch(ctx, bytes));
+  if (!scratch) return gsb_set_error(ctx, GSB_CUDA_ERROR, "decode pool: workspace allocation failed");
+  P.counter = reinterpret_cast<unsigned*>(scratch);
+  P.ws_pending = reinterpret_cast<int32_t*>(scratch + 256);
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  cudaMemsetAsync(P.counter, 0, sizeof(unsigned), s);
+  kern<<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, static_cast<size_t>(block_smem), s>>>(P);
+  return gsb_check_launch(ctx, "decode_pool");
+}
+
+}  // extern "C"

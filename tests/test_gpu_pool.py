@@ -1,0 +1,151 @@
+"""K5 parity: the GPU closed-loop decode pool (gsb_decode_pool) against the restated
+simulator's decode pool (oracle/gs_sim.c, itself pinned to the reference's run() in
+tests/test_oracle_sim.py) and, where oracle/_ref is present, against the reference's own
+run() at each parameter set. Everything is bit-exact: per-request first-token / finish
+instants and decode workers, per-worker decision logs and applied clocks, ledger energies,
+the SLO counts and the digests."""
+import numpy as np
+import pytest
+
+from oracle.oracle import (CtlCfg, PolicyHolder, default_ctl_cfg, default_profile,
+                           default_sim_cfg, default_slo)
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    from paper_2508_16449_b200 import api
+    return api
+
+
+def _stream(api, g, arrival, output, slo):
+    """The decode-enqueue stream recorded by the restated simulator, as a DecodeStream."""
+    ttft = np.where(g["cls"] == 0, slo.ttft_sm_ms, slo.ttft_l_ms).astype(np.float64)
+    return api.DecodeStream(g["enq_t"], g["enq_req"].astype(np.int32),
+                            np.ascontiguousarray(output, np.int32),
+                            np.asarray(arrival, np.float64), ttft, float(g["scalars"][2]))
+
+
+def _ctl(api, c: CtlCfg):
+    return api.DecodeCtlConfig(c.tslo_ms, c.margin_decode, c.fine_period_ms, c.coarse_period_ms,
+                               c.adapt_period_s, c.step_mhz, c.max_step_mhz, c.hysteresis_count,
+                               c.bias_threshold, c.tbt_window_tokens, c.tps_scale,
+                               c.upper_margin, c.lower_margin)
+
+
+def _sim_cfg(api, c):
+    return api.SimConfig(c.n_prefill_workers, c.n_decode_workers, c.gpus_per_prefill_worker,
+                         c.actuation_delay_ms, c.handoff_delay_ms, c.max_batch, c.max_queue,
+                         c.band_tps_lo, c.band_tps_hi, c.band_tps_step)
+
+
+def _variants(rng, n_random):
+    v = [dict(), dict(hysteresis_count=1), dict(hysteresis_count=5),
+         dict(step_mhz=30.0, max_step_mhz=30.0), dict(step_mhz=15.0, max_step_mhz=45.0),
+         dict(margin_decode=0.6), dict(margin_decode=1.5, upper_margin=0.9, lower_margin=0.5),
+         dict(tslo_ms=60.0), dict(adapt_period_s=2.0, bias_threshold=0.5),
+         dict(tbt_window_tokens=32), dict(tbt_window_tokens=1),
+         dict(fine_period_ms=25.0, coarse_period_ms=150.0), dict(tps_scale=2.0)]
+    for _ in range(n_random):
+        step = float(rng.choice([15.0, 30.0, 45.0]))
+        v.append(dict(hysteresis_count=int(rng.integers(1, 7)), step_mhz=step,
+                      max_step_mhz=step * float(rng.choice([1, 2, 3])),
+                      tslo_ms=float(rng.choice([60.0, 80.0, 100.0, 150.0])),
+                      margin_decode=float(rng.choice([0.6, 0.8, 0.95, 1.2])),
+                      bias_threshold=float(rng.choice([0.5, 0.8, 0.95])),
+                      tbt_window_tokens=int(rng.choice([16, 64, 256]))))
+    return v
+
+
+SCENES = {
+    "sinusoid": dict(trace=("sin", 1500.0, 1000.0, 120000.0, 150000, 11), cfg={}, slo={}),
+    "sinusoid_tight": dict(trace=("sin", 1500.0, 1000.0, 120000.0, 150000, 11), cfg={},
+                           slo=dict(tbt_p95_ms=60.0, ttft_sm_ms=150.0)),
+    "overload": dict(trace=("sin", 1500.0, 1000.0, 120000.0, 60000, 5),
+                     cfg=dict(max_batch=4, max_queue=6, n_decode_workers=2), slo={}),
+    "poisson_8w": dict(trace=("poi", 5.0, 600_000, 7), cfg=dict(n_decode_workers=8,
+                                                               max_batch=32), slo={}),
+}
+
+
+@pytest.mark.parametrize("scene", list(SCENES))
+def test_decode_pool_matches_oracle(gsb, restate, scene):
+    api = _api()
+    sc = SCENES[scene]
+    prof = default_profile()
+    t = sc["trace"]
+    if t[0] == "sin":
+        a, p, o = restate.gen_sinusoid_decode_trace(*t[1:])
+    else:
+        a, p, o = restate.gen_poisson_trace(t[1], t[2], 512.0, 4096.0, 0.10, 128.0, t[3])
+    slo = default_slo(**sc["slo"])
+    cfg = default_sim_cfg(**sc["cfg"])
+    g0 = restate.sim_run(prof, PolicyHolder(), slo, cfg, a, p, o)
+    stream = _stream(api, g0, a, o, slo)
+    rng = np.random.default_rng(sum(map(ord, scene)))
+    variants = _variants(rng, 24)
+    ccfgs = [default_ctl_cfg(**kw) for kw in variants]
+    fixed = [0.0] * len(ccfgs) + [210.0, 900.0, 1410.0]
+    ccfgs += [default_ctl_cfg()] * 3
+    sim = _sim_cfg(api, cfg)
+    plan = gsb.decode_pool([_ctl(api, c) for c in ccfgs], stream,
+                           api.GpuProfile.default_profile(), sim,
+                           api.SloConfig(slo.ttft_sm_ms, slo.ttft_l_ms, slo.tbt_p95_ms),
+                           fixed_mhz=np.array(fixed), details=True, rec_cap=40000,
+                           freq_cap=4000)
+    sm = gsb.pool_summary(plan)
+    W = cfg.n_decode_workers
+    led = plan["out"]["ledger"].cpu().numpy()
+    rw = plan["out"]["req_worker"].cpu().numpy()
+    rf = plan["out"]["req_first"].cpu().numpy()
+    rfin = plan["out"]["req_finish"].cpu().numpy()
+    recs = plan["out"]["records"].cpu().numpy()
+    frq = plan["out"]["freq"].cpu().numpy()
+    for i, (c, f) in enumerate(zip(ccfgs, fixed)):
+        pol = (PolicyHolder(ccfg=c) if f == 0.0
+               else PolicyHolder(kind="fixed", fixed_f=f, routing=False, ccfg=c))
+        q = restate.pool_run(prof, pol, slo, cfg, a, p, o, g0["enq_t"], g0["enq_req"],
+                             g0["scalars"][2])
+        want = q["summary"]
+        got = {k: sm[k][i].item() for k in want}
+        assert got == want, (i, variants[i] if i < len(variants) else f,
+                             {k: (got[k], want[k]) for k in want if got[k] != want[k]})
+        np.testing.assert_array_equal(rfin[i], np.where(q["completed"] == 1, q["finish"], -1.0))
+        np.testing.assert_array_equal(rf[i], q["first_token"])
+        np.testing.assert_array_equal(rw[i], q["decode_worker"])
+        assert led[i].tobytes() == np.ascontiguousarray(q["decode3"][:, 1:]).tobytes()
+        dec = q["decisions"]
+        for w in range(W):
+            mine = dec[dec["worker"] == w]
+            got_w = recs[i, w, :len(mine)].reshape(-1).view(dec.dtype)
+            assert got_w.tobytes() == mine.tobytes(), (i, w)
+            rows = (q["tl_pool"] == 0) & (q["tl_worker"] == w)
+            tl = np.stack([q["tl_t"][rows][1:], q["tl_f"][rows][1:]], 1)
+            assert frq[i, w, :len(tl)].tobytes() == tl.tobytes(), (i, w)
+    if scene == "overload":
+        assert sm["n_rejected"].max() > 0
+    if scene == "sinusoid_tight":
+        assert (sm["n_tbt_ok"] < sm["n_completed"]).any()
+
+
+def test_decode_pool_matches_reference_run(gsb, ref, restate):
+    """The GPU pool at non-default controller parameters against the reference's own run()."""
+    api = _api()
+    prof = default_profile()
+    a, p, o = restate.gen_sinusoid_decode_trace(1500.0, 1000.0, 120000.0, 150000, 11)
+    slo, cfg = default_slo(), default_sim_cfg()
+    g0 = restate.sim_run(prof, PolicyHolder(), slo, cfg, a, p, o)
+    stream = _stream(api, g0, a, o, slo)
+    kws = [dict(hysteresis_count=1), dict(margin_decode=0.6), dict(step_mhz=30.0, max_step_mhz=30.0),
+           dict(tslo_ms=60.0, hysteresis_count=5)]
+    ccfgs = [default_ctl_cfg(**k) for k in kws]
+    plan = gsb.decode_pool([_ctl(api, c) for c in ccfgs], stream, api.GpuProfile.default_profile(),
+                           _sim_cfg(api, cfg), api.SloConfig())
+    sm = gsb.pool_summary(plan)
+    for i, c in enumerate(ccfgs):
+        r = ref.sim_run(prof, PolicyHolder(ccfg=c), slo, cfg, a, p, o)
+        want = restate.pool_summary_from(slo, a.astype(np.float64), r)
+        for k in want:
+            if k != "n_steps":
+                assert sm[k][i].item() == want[k], (kws[i], k)
+        assert sm["decode_pool_j"][i] == r["scalars"][4]
