@@ -428,8 +428,9 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
           wk.r_total += g;
           wk.p95_valid = false;
         }
-        // TpsWindow::record (decode_ctl.hpp:73)
-        if (wk.t_n >= TC) {
+        // TpsWindow::record (decode_ctl.hpp:73); unobservable once no coarse tick is left
+        if (!coarse_on) {
+        } else if (wk.t_n >= TC) {
           status |= ST_TPS;
         } else {
           int pos = wk.t_head + wk.t_n;
