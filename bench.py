@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c2", "c4", "c5"])
     ap.add_argument("--windows", type=int, default=0, help="override windows per rank")
     ap.add_argument("--scenarios", type=int, default=100_000)
+    ap.add_argument("--pool-scenarios", type=int, default=20_000,
+                    help="closed-loop decode-pool (K5) scenarios per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-graph", action="store_true")
@@ -248,6 +250,27 @@ def run_gsb(args, rank, world, dist):
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in ts]
 
+    # ---------------- closed-loop decode pool leg (K5): C3 sinusoid, controller sweep
+    pa, pp, po = wl.sinusoid_decode_trace(1500.0, 1000.0, 120_000.0, 150_000, seed=11 + rank)
+    pstream = wl.decode_stream(pa, pp, po)
+    pcfg = wl.pool_sweep(args.pool_scenarios)
+    pprof = api.GpuProfile.default_profile()
+    psim, pslo = api.SimConfig(), api.SloConfig()
+    pplan = eng.decode_pool(pcfg, pstream, pprof, psim, pslo)
+
+    def run_pool(timed_steps, warm):
+        ts = []
+        for i in range(warm + timed_steps):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            eng.run_pool(pplan)
+            s1.record(stream)
+            if i >= warm:
+                ts.append((s0, s1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in ts]
+
     # ---------------- e2e prefill leg: pinned host in, pinned host out
     h_arr = torch.as_tensor(arrival).pin_memory()
     h_prm = torch.as_tensor(prompt).pin_memory()
@@ -309,6 +332,8 @@ def run_gsb(args, rank, world, dist):
         barrier()
         dec_ms = run_decode(args.steps, max(3, args.warmup // 2))
         barrier()
+        pool_ms = run_pool(max(3, args.steps // 4), 3)
+        barrier()
         e2e_ms = run_e2e(args.steps, args.warmup)
         barrier()
     k1_ms, k2_ms = kernel_split()
@@ -323,6 +348,8 @@ def run_gsb(args, rank, world, dist):
     ms_pre = max_over_ranks(statistics.mean(pre_ms))
     ms_dec = max_over_ranks(statistics.mean(dec_ms))
     ms_e2e = max_over_ranks(statistics.mean(e2e_ms))
+    ms_pool = max_over_ranks(statistics.mean(pool_ms))
+    psum = api.Engine.pool_summary(pplan)
 
     # global per-(profile, class) result: every rank's summary, combined in rank order
     from paper_2508_16449_b200 import distributed as Dd
@@ -339,6 +366,9 @@ def run_gsb(args, rank, world, dist):
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cpu, parity = cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep,
                                    tel, plan, lo, hi, fo, T_END)
+        if cpu is not None:
+            cpu["pool"], parity["pool"] = pool_cpu_baseline(args, pa, pp, po, pstream, pcfg,
+                                                            psum)
 
     if rank != 0:
         return
@@ -360,7 +390,7 @@ def run_gsb(args, rank, world, dist):
     k1_gbs = n_req * K1_BYTES_PER_REQ / (k1_ms / 1e3) / 1e9
     # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
     # + summary partial/final (5); decode step = tbt_p95 + tps + decode_replay (3); e2e = 5
-    launches = args.steps * (5 + 3 + 5)
+    launches = args.steps * (5 + 3 + 5) + max(3, args.steps // 4)
     line = {
         "metric": METRIC,
         "value": world * evals / (ms_pre / 1e3),
@@ -385,6 +415,16 @@ def run_gsb(args, rank, world, dist):
                    "unit": "decode-controller scenario replays/s",
                    "fine_ticks_per_s": world * sweep.n_scenarios * 4 * 7500 / (ms_dec / 1e3),
                    "ms_per_step": ms_dec, "trajectories_per_step": len(sweep.cfgs)},
+        "pool": {"value": world * len(pcfg) / (ms_pool / 1e3),
+                 "unit": "closed-loop decode-pool scenario replays/s",
+                 "decode_steps_per_s": world * float(psum["n_steps"].sum()) / (ms_pool / 1e3),
+                 "events_per_scenario": float((psum["n_steps"] + psum["n_decisions"]
+                                               + psum["n_freq_changes"]).mean() + len(pstream.t_ms)),
+                 "ms_per_step": ms_pool, "scenarios_per_step": len(pcfg),
+                 "workload": "C3 sinusoid 1500+-1000 tps, 150 s, 4 decode workers x max_batch 64; "
+                             "sweep hysteresis x step x TBT target x margin x bias; K5 "
+                             "k_decode_pool, one warp per scenario",
+                 "mean_decode_pool_j": float(psum["decode_pool_j"].mean())},
         "roofline": {"bound": "fp64", "kernel": "k_prefill_select (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,
@@ -501,6 +541,42 @@ def cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep, t
     parity = {"prefill_cells_checked": int(len(nonempty)), "prefill_mismatches": mism,
               "decode_trajectories_checked": int(len(idx)), "decode_digest_mismatches": dmism}
     return pre, parity
+
+
+def pool_cpu_baseline(args, pa, pp, po, pstream, pcfg, psum):
+    """K5's CPU reference: greensim::run() (oracle/_ref) per scenario on the same trace, all
+    host threads, bounded sample; plus the restated decode pool (oracle, checker only) on the
+    GPU's exact input stream for a few scenarios, compared field by field."""
+    from oracle import oracle as O
+
+    ref = O.Reference()
+    restate = O.Restatement()
+    threads = os.cpu_count() or 1
+    prof, slo, scfg = O.default_profile(), O.default_slo(), O.default_sim_cfg()
+    pol = O.PolicyHolder()
+    names = pcfg.dtype.names
+    n = max(threads, 8)
+    budget = args.cpu_seconds
+    while True:
+        cfgs = [O.CtlCfg(*[pcfg[i][k] for k in names]) for i in range(min(n, len(pcfg)))]
+        t0 = time.perf_counter()
+        ref.sim_run_many(prof, pol, cfgs, slo, scfg, pa, pp, po, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt > budget / 4 or n >= len(pcfg):
+            break
+        n = int(n * max(2.0, min(8.0, budget / 2 / max(dt, 1e-3))))
+    cpu = {"value": len(cfgs) / dt, "unit": "closed-loop decode-pool scenario replays/s",
+           "cores": threads, "kind": "reference", "seconds": dt,
+           "sample": f"{len(cfgs)} scenarios of the C3 sweep: one greensim::run() each (150 s "
+                     f"sinusoid, 4 decode workers), {threads} std::threads"}
+    idx = np.linspace(0, len(pcfg) - 1, 6).astype(int)
+    mism = 0
+    for i in idx:
+        c = O.CtlCfg(*[pcfg[i][k] for k in names])
+        q = restate.pool_run(prof, O.PolicyHolder(ccfg=c), slo, scfg, pa, pp, po, pstream.t_ms,
+                             pstream.req.astype(np.int64), pstream.end_floor_ms)
+        mism += int(any(psum[k][i].item() != v for k, v in q["summary"].items()))
+    return cpu, {"scenarios_checked": len(idx), "mismatches": mism}
 
 
 # ---------------------------------------------------------------------------- reference arm

@@ -398,8 +398,9 @@ typedef struct gsb_pool_stream {
 /* Decode-side outcome of one scenario. Digests (identical definitions in the oracle,
  * gs_oracle.h gso_pool_summary): decision_digest = FNV over workers of each worker's K3
  * record digest; freq_digest = FNV over workers of FNV-1a(applied_ms, f) of its applied
- * changes; request_digest = sum mod 2^64 of FNV-1a(id, first_token, gaps..., finish, worker)
- * per completed request (FNV-1a(id, 0xdead) per decode-side rejection). status != 0 means a
+ * changes; request_digest = sum mod 2^64 of FNV-1a(id, first_token, finish, worker, n_gaps,
+ * sum of gap bit patterns) per completed request (FNV-1a(id, 0xdead) per decode-side
+ * rejection). status != 0 means a
  * capacity was exceeded (1 pending FIFO, 2 TPS deque, 4 pending clock applications, 8 tbt_cap
  * below a scenario's window): the scenario's outputs are then invalid. */
 typedef struct gsb_pool_summary {

@@ -204,8 +204,10 @@ typedef struct gso_scripted { /* ScriptedFreqEvent, simkernel.hpp:76-81 */
  *   freq_digest      per decode worker, FNV-1a over (applied_ms bits, f bits) of its applied
  *                    changes (t = 0 initial rows excluded); combined the same way
  *   request_digest   sum mod 2^64 over requests that reached the decode pool of
- *                    FNV-1a(id, first_token bits, gap bits..., finish bits, decode_worker),
- *                    or FNV-1a(id, 0xdead) for a decode-side rejection */
+ *                    FNV-1a(id, first_token bits, finish bits, decode_worker, n_gaps,
+ *                    sum of the gaps' bit patterns mod 2^64), or FNV-1a(id, 0xdead) for a
+ *                    decode-side rejection (a request's gaps are consecutive step lengths
+ *                    of its worker, so first/finish/worker plus the sum pin them) */
 typedef struct gso_pool_summary {
   double decode_pool_j, active_decode_j, idle_j, sim_end_ms;
   int64_t n_completed, n_rejected, n_ttft_ok, n_tbt_ok, tbt_samples, tbt_samples_ok;

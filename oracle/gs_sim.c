@@ -832,11 +832,14 @@ void gso_pool_summary_from(const gso_slo* slo, int64_t n, const double* arrival,
         o->tbt_samples++;
         if (tbt[k] <= slo->tbt_p95_ms) o->tbt_samples_ok++;
       }
+      uint64_t gs = 0; /* sum of the gaps' bit patterns mod 2^64 */
+      for (int64_t k = tbt_off[i]; k < tbt_off[i + 1]; ++k) gs += bits(tbt[k]);
       uint64_t h = fnv(FNV0, (uint64_t)i);
       h = fnv(h, bits(first_token[i]));
-      for (int64_t k = tbt_off[i]; k < tbt_off[i + 1]; ++k) h = fnv(h, bits(tbt[k]));
       h = fnv(h, bits(finish[i]));
       h = fnv(h, (uint64_t)(uint32_t)decode_worker[i]);
+      h = fnv(h, (uint64_t)ng);
+      h = fnv(h, gs);
       rd += h;
     } else if (rejected[i] && prefill_end[i] >= 0.0) { /* decode-side rejection */
       o->n_rejected++;

@@ -10,13 +10,17 @@
 // exactly as the reference's priority queue would (time, then kind: step end 2 < enqueue 3 <
 // freq applied 4 < coarse 5 < adapt 6 < fine 7, simkernel.cpp:21-31,44-50) with three warp
 // min-reductions, then runs it:
-//   * a step end spreads its batch's streams over the lanes (first token / gap / completion,
-//     stream compaction by ballot), then refills the batch from the worker's FIFO;
+//   * a step end costs O(1 + admissions + completions), not O(batch): every stream active in
+//     a step emits exactly once and every gap it records is that step's length, so a
+//     stream's whole future is fixed when it joins (it completes at worker step
+//     join + output_tokens - 1), and its TBT statistics are differences of per-worker prefix
+//     sums over steps (count of gaps <= SLO, sum of gap bit patterns). The warp scans the
+//     batch's completion indices with one compare per slot and compacts only on completion;
 //   * ticks run one controller per lane (lane w = decode worker w);
-//   * the nearest-rank P95 of the TBT window is a warp-parallel rank count over RUNS: every
-//     gap recorded by one step end equals that step's duration (each active stream last
-//     emitted at the step's start, simkernel.cpp:365-379), so the 256-sample ring is a short
-//     deque of (value, count) runs and the P95 is exact without sorting.
+//   * for the same reason the 256-sample TBT ring is a short deque of (value, count) runs, and
+//     its nearest-rank P95 is found by warp-wide descending max extraction over the runs
+//     (usually one round: the longest gap's run already covers the top 5%), exact without
+//     sorting.
 // Events that the reference orders only by insertion sequence (two workers' step ends, or
 // freq applications, at the same instant) touch disjoint worker state and commute.
 // Per-worker state lives in shared memory; the FIFO of waiting requests in a global
@@ -55,21 +59,21 @@ struct PoolParams {
 
 // shared-memory carve-up of one warp's region
 struct Smem {
-  uint64_t* h;     // [W][MB] request digest chain
+  uint64_t* bp;    // [W][MB] worker's gap-bits prefix sum at the stream's first token
+  double* first;   // [W][MB] first-token instant
   double* rv;      // [W][RC] TBT run values
   double* tt;      // [W][TC] TPS event times
   double* fq_t;    // [W][kFQ]
   double* fq_f;    // [W][kFQ]
+  int32_t* fin;    // [W][MB] worker step index at which the stream completes
   int32_t* req;    // [W][MB]
-  int32_t* emit;   // [W][MB]
-  int32_t* out;    // [W][MB]
-  int32_t* nle;    // [W][MB] gaps <= SLO (bit 31: TTFT met)
+  int32_t* bc;     // [W][MB] worker's (gap <= SLO) prefix count at the first token; bit 31: TTFT met
   int32_t* ttok;   // [W][TC]
   uint16_t* rc;    // [W][RC] TBT run counts
 };
 
 __host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC) {
-  int64_t b = 8ll * W * MB + 8ll * W * RC + 8ll * W * TC + 16ll * W * kFQ + 16ll * W * MB +
+  int64_t b = 16ll * W * MB + 8ll * W * RC + 8ll * W * TC + 16ll * W * kFQ + 12ll * W * MB +
               4ll * W * TC + 2ll * W * RC;
   return (b + 15) & ~15ll;
 }
@@ -77,15 +81,15 @@ __host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC) {
 __device__ __forceinline__ Smem carve(char* base, int W, int MB, int RC, int TC) {
   Smem s;
   char* p = base;
-  s.h = reinterpret_cast<uint64_t*>(p); p += 8ll * W * MB;
+  s.bp = reinterpret_cast<uint64_t*>(p); p += 8ll * W * MB;
+  s.first = reinterpret_cast<double*>(p); p += 8ll * W * MB;
   s.rv = reinterpret_cast<double*>(p); p += 8ll * W * RC;
   s.tt = reinterpret_cast<double*>(p); p += 8ll * W * TC;
   s.fq_t = reinterpret_cast<double*>(p); p += 8ll * W * kFQ;
   s.fq_f = reinterpret_cast<double*>(p); p += 8ll * W * kFQ;
+  s.fin = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
   s.req = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
-  s.emit = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
-  s.out = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
-  s.nle = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
+  s.bc = reinterpret_cast<int32_t*>(p); p += 4ll * W * MB;
   s.ttok = reinterpret_cast<int32_t*>(p); p += 4ll * W * TC;
   s.rc = reinterpret_cast<uint16_t*>(p);
   return s;
@@ -101,7 +105,10 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 struct Worker {
   double freq, target, P;        // applied clock, last command, P(freq)
   double t_end, t_start;         // step end (+inf when idle), step start
-  int n_active;
+  int n_active, n_new;           // batch size; streams admitted at this step's start
+  int step_idx;                  // step ends so far
+  int c_le;                      // prefix count of steps with gap <= SLO
+  uint64_t p_bits;               // prefix sum of gap bit patterns
   int64_t p_head, p_tail;        // FIFO [head, tail) in the workspace ring
   int fq_head, fq_n;             // pending clock applications
   double ps_last, ps_power;      // PowerState (simkernel.cpp:53-57)
@@ -138,40 +145,38 @@ __device__ __forceinline__ double power_at(const gsb_profile& p, double f) {
   return ((p.k3 * f + p.k2) * f + p.k1) * f + p.k0;  // gpu_model.hpp:64
 }
 
-// Nearest-rank P95 of worker w's TBT window (metrics.cpp:11-19): the value v of a run with
-// #(< v) <= rank-1 < #(<= v). Warp-parallel rank count over the runs; all lanes get it.
+// Nearest-rank P95 of worker w's TBT window (metrics.cpp:11-19): sorted[ceil(0.95 n) - 1], i.e.
+// the k-th largest with k = n - ceil(0.95 n) + 1. Descending max extraction over the runs
+// (gaps are positive doubles, so their bit patterns order like their values): each round takes
+// the largest value below the previous one and all runs equal to it; all lanes get the result.
 __device__ double window_p95(const Smem& s, int RC, int w, int r_head, int r_n, int total, int lane) {
   const double* rv = s.rv + w * RC;
   const uint16_t* rc = s.rc + w * RC;
-  const int idx = static_cast<int>(ceil(0.95 * static_cast<double>(total))) - 1;
-  double found = 0.0;
-  bool have = false;
-  for (int base = 0; base < r_n; base += 32) {
-    const int i = base + lane;
-    bool cand = false;
-    double v = 0.0;
-    if (i < r_n) {
+  const int k = total - (static_cast<int>(ceil(0.95 * static_cast<double>(total))) - 1);
+  uint64_t prev = ~0ull;
+  int acc = 0;
+  for (;;) {
+    uint64_t m = 0;
+    for (int i = lane; i < r_n; i += 32) {
       int pos = r_head + i;
       if (pos >= RC) pos -= RC;
-      v = rv[pos];
-      int less = 0, eq = 0;
-      int q = r_head;
-      for (int j = 0; j < r_n; ++j) {
-        const double x = rv[q];
-        const int c = rc[q];
-        less += x < v ? c : 0;
-        eq += x == v ? c : 0;
-        if (++q == RC) q = 0;
-      }
-      cand = less <= idx && idx < less + eq;
+      const uint64_t b = dbits(rv[pos]);
+      m = (b < prev && b > m) ? b : m;
     }
-    const unsigned m = __ballot_sync(kFull, cand);
-    if (m && !have) {
-      found = shfl_d(v, __ffs(m) - 1);
-      have = true;
+    const unsigned mh = __reduce_max_sync(kFull, static_cast<unsigned>(m >> 32));
+    const unsigned ml = __reduce_max_sync(kFull, static_cast<unsigned>(m >> 32) == mh
+                                                     ? static_cast<unsigned>(m) : 0u);
+    const uint64_t mx = (static_cast<uint64_t>(mh) << 32) | ml;
+    int c = 0;
+    for (int i = lane; i < r_n; i += 32) {
+      int pos = r_head + i;
+      if (pos >= RC) pos -= RC;
+      c += dbits(rv[pos]) == mx ? rc[pos] : 0;
     }
+    acc += static_cast<int>(__reduce_add_sync(kFull, static_cast<unsigned>(c)));
+    if (acc >= k || mx == 0) return __longlong_as_double(static_cast<long long>(mx));
+    prev = mx;
   }
-  return found;
 }
 
 template <bool REQ_OUT>
@@ -223,7 +228,10 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   wk.P = power_at(prof, f0);
   wk.t_end = INFINITY;
   wk.t_start = 0.0;
-  wk.n_active = 0;
+  wk.n_active = wk.n_new = 0;
+  wk.step_idx = 0;
+  wk.c_le = 0;
+  wk.p_bits = 0;
   wk.p_head = wk.p_tail = 0;
   wk.fq_head = wk.fq_n = 0;
   wk.ps_last = 0.0;
@@ -254,10 +262,10 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   int32_t* req_worker = REQ_OUT ? a.d_req_worker + n * st.n_requests : nullptr;
 
   int32_t* S_req = s.req;
-  int32_t* S_emit = s.emit;
-  int32_t* S_out = s.out;
-  int32_t* S_nle = s.nle;
-  uint64_t* S_h = s.h;
+  int32_t* S_fin = s.fin;
+  int32_t* S_bc = s.bc;
+  uint64_t* S_bp = s.bp;
+  double* S_first = s.first;
 
   // start_decode_step (simkernel.cpp:330-345) of worker ww, whole warp
   auto start_step = [&](int ww, double now) {
@@ -267,18 +275,15 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
     const int take = static_cast<int>(min(static_cast<int64_t>(MB - na), pt - ph));
     const int32_t* ring = pend + static_cast<int64_t>(ww) * PC;
     for (int j = lane; j < take; j += 32) {
-      const int32_t r = ring[(ph + j) % PC];
       const int slot = ww * MB + na + j;
-      S_req[slot] = r;
-      S_emit[slot] = 0;
-      S_out[slot] = st.d_output_tokens[r];
-      S_nle[slot] = 0;
-      S_h[slot] = mix(kFnv0, static_cast<uint64_t>(r));
+      S_req[slot] = ring[(ph + j) % PC];
+      S_fin[slot] = 0x7fffffff;  // known at its first token (the end of this step)
     }
     __syncwarp();
     if (lane == ww) {
       wk.p_head = ph + take;
       wk.n_active = na + take;
+      wk.n_new = take;
       if (wk.n_active == 0) {
         ledger_set(wk, now, PH_IDLE, prof.p_idle_w);
       } else {
@@ -335,67 +340,101 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
       // ---- on_decode_step_end (simkernel.cpp:365-393), worker src
       const int ww = src;
       const int na = __shfl_sync(kFull, wk.n_active, ww);
+      const int nn = __shfl_sync(kFull, wk.n_new, ww);
       const double gap = now - shfl_d(wk.t_start, ww);
-      int kept = 0, gaps_rec = 0;
+      const bool le = gap <= tbt_thr;
+      // per-worker prefix sums over steps, identical on every lane
+      const int sidx = __shfl_sync(kFull, wk.step_idx, ww) + 1;
+      const int cle = __shfl_sync(kFull, wk.c_le, ww) + (le ? 1 : 0);
+      const int g_total = na - nn;  // continuing streams record this step's gap
+      const uint64_t pb = (static_cast<uint64_t>(__shfl_sync(kFull, static_cast<long long>(wk.p_bits), ww))) +
+                          (g_total > 0 ? dbits(gap) : 0ull);
+      // first tokens of the streams admitted at this step's start (the last nn slots)
+      for (int j = na - nn + lane; j < na; j += 32) {
+        const int slot = ww * MB + j;
+        const int32_t r = S_req[slot];
+        const int32_t ou = st.d_output_tokens[r];
+        // TTFT = first_token - arrival (simkernel.hpp:125) against SloConfig::ttft_for
+        const bool ttft_ok = now - st.d_arrival_ms[r] <= st.d_ttft_slo_ms[r];
+        S_fin[slot] = sidx + (ou > 1 ? ou - 1 : 0);
+        S_bc[slot] = cle | (ttft_ok ? static_cast<int32_t>(0x80000000u) : 0);
+        S_bp[slot] = pb;
+        S_first[slot] = now;
+        if (REQ_OUT) req_first[r] = now;
+      }
+      __syncwarp();
+      // completions: streams whose last token is this step's (emitted >= output_tokens)
+      int kept = 0;
       for (int base = 0; base < na; base += 32) {
         const int j = base + lane;
-        bool keep = false;
-        int32_t r = 0, em = 0, ou = 0, nl = 0;
-        uint64_t h = 0;
+        const bool done = j < na && S_fin[ww * MB + j] == sidx;
+        const unsigned dm = __ballot_sync(kFull, done);
+        const unsigned live = base + 32 <= na ? kFull : ((1u << (na - base)) - 1u);
+        if (dm == 0) {
+          if (kept != base) {  // shift this chunk down over earlier completions
+            int32_t r = 0, f = 0, c = 0;
+            uint64_t p = 0;
+            double fs = 0.0;
+            if (j < na) {
+              const int slot = ww * MB + j;
+              r = S_req[slot]; f = S_fin[slot]; c = S_bc[slot]; p = S_bp[slot]; fs = S_first[slot];
+            }
+            __syncwarp();
+            if (j < na) {
+              const int dst = ww * MB + kept + lane;
+              S_req[dst] = r; S_fin[dst] = f; S_bc[dst] = c; S_bp[dst] = p; S_first[dst] = fs;
+            }
+            __syncwarp();
+          }
+          kept += __popc(live);
+          continue;
+        }
+        int32_t r = 0, f = 0, c = 0;
+        uint64_t p = 0;
+        double fs = 0.0;
         if (j < na) {
           const int slot = ww * MB + j;
-          r = S_req[slot];
-          em = S_emit[slot];
-          ou = S_out[slot];
-          nl = S_nle[slot];
-          h = S_h[slot];
-          if (em == 0) {
-            // first token: TTFT = first_token - arrival (simkernel.hpp:125)
-            if (now - st.d_arrival_ms[r] <= st.d_ttft_slo_ms[r]) nl |= static_cast<int32_t>(0x80000000u);
-            h = mix(h, dbits(now));
-            if (REQ_OUT) req_first[r] = now;
-          } else {
-            h = mix(h, dbits(gap));
-            nl += gap <= tbt_thr ? 1 : 0;
-            ++gaps_rec;
-          }
-          ++em;
-          if (em >= ou) {
-            // completion: slo_pass_rates terms (metrics.cpp:42-72)
-            h = mix(mix(h, dbits(now)), static_cast<uint64_t>(static_cast<uint32_t>(ww)));
-            rdig += h;
-            ++n_completed;
-            const int ng = em - 1;
-            const int le = nl & 0x7fffffff;
-            if (nl < 0) ++n_ttft_ok;
-            const int rank = static_cast<int>(ceil(0.95 * static_cast<double>(ng)));
-            if (ng == 0 || le >= rank) ++n_tbt_ok;
-            samples += ng;
-            samples_ok += le;
-            max_finish = std_max(max_finish, now);
-            if (REQ_OUT) req_finish[r] = now;
-          } else {
-            keep = true;
-          }
+          r = S_req[slot]; f = S_fin[slot]; c = S_bc[slot]; p = S_bp[slot]; fs = S_first[slot];
         }
+        if (done) {
+          // completion: slo_pass_rates terms (metrics.cpp:42-72) and the request digest
+          const int32_t ou = st.d_output_tokens[r];
+          const int ng = ou > 1 ? ou - 1 : 0;
+          const int nle = cle - (c & 0x7fffffff);
+          if (c < 0) ++n_ttft_ok;
+          const int rank = static_cast<int>(ceil(0.95 * static_cast<double>(ng)));
+          if (ng == 0 || nle >= rank) ++n_tbt_ok;
+          samples += ng;
+          samples_ok += nle;
+          uint64_t h = mix(kFnv0, static_cast<uint64_t>(r));
+          h = mix(h, dbits(fs));
+          h = mix(h, dbits(now));
+          h = mix(h, static_cast<uint64_t>(static_cast<uint32_t>(ww)));
+          h = mix(h, static_cast<uint64_t>(ng));
+          h = mix(h, pb - p);
+          rdig += h;
+          ++n_completed;
+          max_finish = std_max(max_finish, now);
+          if (REQ_OUT) req_finish[r] = now;
+        }
+        const bool keep = j < na && !done;
         const unsigned km = __ballot_sync(kFull, keep);
         __syncwarp();
         if (keep) {
           const int dst = ww * MB + kept + __popc(km & ((1u << lane) - 1u));
-          S_req[dst] = r;
-          S_emit[dst] = em;
-          S_out[dst] = ou;
-          S_nle[dst] = nl;
-          S_h[dst] = h;
+          S_req[dst] = r; S_fin[dst] = f; S_bc[dst] = c; S_bp[dst] = p; S_first[dst] = fs;
         }
         kept += __popc(km);
         __syncwarp();
       }
-      const int g_total = __reduce_add_sync(kFull, static_cast<unsigned>(gaps_rec));
       const int n_fin = na - kept;
       if (lane == ww) {
         wk.n_active = kept;
+        wk.n_new = 0;
         wk.t_end = INFINITY;
+        wk.step_idx = sidx;
+        wk.c_le = cle;
+        wk.p_bits = pb;
         ++n_steps;
         // TbtWindow::record x g_total equal gaps (decode_ctl.cpp:120-123) as one run
         if (g_total > 0) {

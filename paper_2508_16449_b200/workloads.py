@@ -190,3 +190,101 @@ def decode_sweep(n_scenarios: int, n_profiles: int = 4, n_workers: int = 4,
     stream_of = (rep(grid[:, 0] * streams_per_profile, n_workers)
                  + worker % streams_per_profile).astype(np.int32)
     return DecodeSweep(cfgs, table_of, stream_of, worker, tp, table_tslo, N, n_workers)
+
+
+# ------------------------------------------------------------------ closed-loop decode pool (K5)
+def sinusoid_decode_trace(tps_mean: float, tps_amp: float, period_ms: float, duration_ms: int,
+                          seed: int):
+    """Sinusoidal decode workload with the distributions of gen_sinusoid_decode_trace
+    (proj/src/trace.cpp:239-285): request k arrives when the cumulative offered tokens
+    L(t) = mean*t/1000 + amp/1000 * P/2pi * (1 - cos(2pi t/P)) reach the tokens of the
+    requests before it; prompt 32, output uniform on [64, 192]. PCG64 instead of mt19937_64,
+    and a vectorised bisection. Returns (arrival_ms i64, prompt i32, output i32)."""
+    rng = np.random.default_rng(seed)
+    n_max = int(duration_ms / 1000.0 * (tps_mean + tps_amp) / 64.0) + 16
+    out = rng.integers(64, 193, n_max).astype(np.int32)
+    target = np.concatenate([[0.0], np.cumsum(out[:-1], dtype=np.float64)])
+    two_pi = 2.0 * np.pi
+
+    def cum(t):
+        return tps_mean * t / 1000.0 + tps_amp / 1000.0 * (period_ms / two_pi) * (
+            1.0 - np.cos(two_pi * t / period_ms))
+
+    lo = np.zeros(n_max)
+    hi = np.full(n_max, 1000.0)
+    while np.any(cum(hi) < target):
+        hi = np.where(cum(hi) < target, hi + 1000.0, hi)
+    for _ in range(60):
+        mid = 0.5 * (lo + hi)
+        below = cum(mid) < target
+        lo = np.where(below, mid, lo)
+        hi = np.where(below, hi, mid)
+    arrival = np.rint(0.5 * (lo + hi)).astype(np.int64)
+    keep = arrival < duration_ms
+    n = int(np.argmin(keep)) if not keep.all() else n_max
+    return arrival[:n], np.full(n, 32, np.int32), out[:n]
+
+
+def decode_stream(arrival, prompt, output, profile: api.GpuProfile | None = None,
+                  routing: api.RoutingConfig | None = None, slo: api.SloConfig = api.SloConfig(),
+                  handoff_ms: float = 0.0, prefill_f_mhz: float | None = None) -> api.DecodeStream:
+    """Decode-enqueue stream of a prefill pool at a pinned clock (synthetic input for K5):
+    per routing class a FIFO served by that class's workers in arrival order, service time
+    prefill_latency_ms(prompt, f) (gpu_model.cpp:94-97); the request reaches the decode pool
+    handoff_ms after its prefill ends (simkernel.cpp:317-326). The reference's own stream
+    (GreenLLM prefill clocks) is recorded by the oracle for the parity tests instead."""
+    prof = profile or api.GpuProfile.default_profile()
+    rc = routing or api.RoutingConfig()
+    f = prefill_f_mhz or prof.grid.f_max_mhz
+    lat = prof.prefill
+    n = len(arrival)
+    thr = np.asarray(rc.thresholds if rc.enabled else [], np.int64)
+    cls = (np.asarray(prompt, np.int64)[:, None] > thr[None, :]).sum(1) if len(thr) else np.zeros(n, np.int64)
+    workers = {}
+    for w, c in enumerate(rc.worker_map if rc.enabled else [0] * 2):
+        workers.setdefault(int(c), []).append(0.0)
+    L = np.asarray(prompt, np.float64)
+    svc = ((lat.a * L + lat.b) * L + lat.c) * lat.f_ref_mhz / f
+    end = np.zeros(n)
+    arr = np.asarray(arrival, np.float64)
+    for i in range(n):
+        free = workers[int(cls[i])]
+        k = int(np.argmin(free))
+        start = max(arr[i], free[k])
+        free[k] = end[i] = start + svc[i]
+    t = end + handoff_ms
+    order = np.argsort(t, kind="stable")
+    big = np.asarray(prompt) > 1024  # SLO class SM/L (simkernel.cpp:258-260)
+    ttft = np.where(big, slo.ttft_l_ms, slo.ttft_sm_ms).astype(np.float64)
+    return api.DecodeStream(t[order], order.astype(np.int32), np.ascontiguousarray(output, np.int32),
+                            arr, ttft, float(max(end.max(), arr.max())))
+
+
+def pool_sweep(n_scenarios: int, seed: int = 0) -> np.ndarray:
+    """C3: dual-loop controller sweep hysteresis x step size x TBT target (x margin x bias),
+    one DecodeCtlConfig per scenario (CTL_DTYPE [N])."""
+    hyst = np.array([1, 2, 3, 4, 5])
+    steps = np.array([15.0, 30.0, 45.0, 60.0])
+    margins = np.array([0.6, 0.8, 0.95, 1.2, 1.5])
+    bias = np.array([0.7, 0.8])
+    per = len(hyst) * len(steps) * len(margins) * len(bias)
+    n_tslo = max(1, -(-n_scenarios // per))
+    tslos = np.linspace(50.0, 150.0, n_tslo)
+    g = np.stack(np.meshgrid(np.arange(n_tslo), np.arange(len(margins)), np.arange(len(hyst)),
+                             np.arange(len(steps)), np.arange(len(bias)), indexing="ij"),
+                 -1).reshape(-1, 5)[:n_scenarios]
+    cfg = np.zeros(len(g), api.CTL_DTYPE)
+    cfg["tslo_ms"] = tslos[g[:, 0]]
+    cfg["margin_decode"] = margins[g[:, 1]]
+    cfg["fine_period_ms"] = 20.0
+    cfg["coarse_period_ms"] = 200.0
+    cfg["adapt_period_s"] = 6.0
+    cfg["step_mhz"] = steps[g[:, 3]]
+    cfg["max_step_mhz"] = np.maximum(30.0, steps[g[:, 3]])
+    cfg["hysteresis_count"] = hyst[g[:, 2]]
+    cfg["tbt_window_tokens"] = 256
+    cfg["bias_threshold"] = bias[g[:, 4]]
+    cfg["tps_scale"] = 4.0
+    cfg["upper_margin"] = 1.0
+    cfg["lower_margin"] = 0.65
+    return cfg
