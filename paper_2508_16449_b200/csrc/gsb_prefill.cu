@@ -47,153 +47,315 @@ __device__ __forceinline__ int64_t div_floor(int64_t a, int64_t d, double rd) {
 // bounds[k] = #requests whose window index (arrival / W - w0) is < k, k = 0..n_windows, i.e. the
 // first request of window k (arrivals are non-decreasing, trace.cpp:109-111). Request i owns
 // the entries k in (w(i-1), w(i)] (request 0 covers k <= w(0), a virtual request n the tail),
-// so every entry is written exactly once. A thread takes a tile of 8 requests: with sorted
-// arrivals the tile only needs per-request work when its first and last windows differ.
-constexpr int kBoundsTile = 8;
+// so every entry is written exactly once.
+// A warp covers 32 tiles of 32 requests. Each lane reads only the LAST arrival of its tile (one
+// 32-byte sector per 32 requests) and takes the previous tile's from its neighbour: with sorted
+// arrivals a tile holds a window edge iff its two ends differ. The warp then resolves each edge
+// tile cooperatively with one coalesced load of its 32 arrivals, so DRAM traffic is ~1/8 of the
+// arrival array plus the edge tiles.
+constexpr int kBoundsTile = 32;
+constexpr unsigned kFull = 0xffffffffu;
 
-__global__ void k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms,
-                                int64_t w0, int64_t n_windows, int64_t* __restrict__ bounds) {
+__global__ void __launch_bounds__(256)
+k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms, int64_t w0,
+                int64_t n_windows, int64_t* __restrict__ bounds) {
   const double rd = 1.0 / static_cast<double>(window_ms);
-  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t i0 = t * kBoundsTile;
-  if (i0 > n) return;
-  const int64_t i1 = min(i0 + kBoundsTile, n + 1);  // requests [i0, i1) incl. the virtual n
+  const int lane = threadIdx.x & 31;
+  const int64_t span = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) *
+                       (32 * kBoundsTile);
+  if (span > n) return;  // warp-uniform
   auto win = [&](int64_t i) -> int64_t {
     if (i < 0) return -1;
     if (i >= n) return n_windows;
     return div_floor(__ldg(arrival + i), window_ms, rd) - w0;
   };
-  int64_t wp = win(i0 - 1);
-  const int64_t wlast = win(i1 - 1);
-  if (wlast == wp) return;  // no window edge inside this tile
-  for (int64_t i = i0; i < i1; ++i) {
-    const int64_t wi = win(i);
-    const int64_t lo = max(wp + 1, int64_t{0});
-    const int64_t hi = min(wi, n_windows);
-    for (int64_t k = lo; k <= hi; ++k) bounds[k] = i;
-    wp = wi;
+  const int64_t t0 = span + static_cast<int64_t>(lane) * kBoundsTile;
+  const bool live = t0 <= n;
+  const int64_t wlast = live ? win(min(t0 + kBoundsTile - 1, n)) : 0;
+  int64_t wprev = __shfl_up_sync(kFull, wlast, 1);
+  if (lane == 0) wprev = win(t0 - 1);
+  unsigned edges = __ballot_sync(kFull, live && wlast != wprev);
+  while (edges) {
+    const int src = __ffs(static_cast<int>(edges)) - 1;
+    edges &= edges - 1;
+    const int64_t wp0 = __shfl_sync(kFull, wprev, src);
+    const int64_t i = span + static_cast<int64_t>(src) * kBoundsTile + lane;
+    const int64_t wi = i <= n ? win(i) : 0;
+    int64_t wp = __shfl_up_sync(kFull, wi, 1);
+    if (lane == 0) wp = wp0;
+    if (i <= n && wi != wp) {
+      const int64_t hi = min(wi, n_windows);
+      for (int64_t k = max(wp + 1, int64_t{0}); k <= hi; ++k) bounds[k] = i;
+    }
   }
 }
 
-// classify(), router.cpp:26-31: number of thresholds strictly below the prompt.
-__device__ __forceinline__ int classify_dev(const RouteParams& rp, int32_t L) {
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) c += rp.thr[k] < L ? 1 : 0;  // unused = INT_MAX
-  return c;
+// classify(), router.cpp:26-31: number of thresholds strictly below the prompt. The thresholds
+// are ascending and distinct (RoutingConfig::validate, router.cpp:7-11, checked host-side) and
+// padded with INT_MAX, so the count is a branch-free binary search: ceil(log2 C) compares.
+template <int C>
+__device__ __forceinline__ int classify_c(const RouteParams& rp, int32_t L) {
+  if (C == 1) return 0;
+  if (C == 2) return rp.thr[0] < L ? 1 : 0;
+  if (C <= 4) {
+    const int c = rp.thr[1] < L ? 2 : 0;
+    return c + ((c ? rp.thr[2] : rp.thr[0]) < L ? 1 : 0);
+  }
+  const bool hi = rp.thr[3] < L;
+  int c = hi ? 4 : 0;
+  const bool mid = (hi ? rp.thr[5] : rp.thr[1]) < L;
+  c += mid ? 2 : 0;
+  const int32_t t = mid ? (hi ? rp.thr[6] : rp.thr[2]) : (hi ? rp.thr[4] : rp.thr[0]);
+  return c + (t < L ? 1 : 0);
 }
 
 // ---------------------------------------------------------------- K1b: route + bin
-// One warp owns G = min(8, 32 / C) consecutive windows; lane (g, c) owns the fp64 chains of cell
-// (window g, class c) for all P profiles. The warp walks its windows in rounds of 32 requests:
-//   1. lane-parallel (coalesced, each request once): load prompt (+ arrival), classify()
-//      (router.cpp:26-31), per-profile reference latency terms, prefill deadline
-//      (simkernel.cpp:499-501) -> a per-warp shared-memory table; one ballot per class gives
-//      each owner the set of this round's rows in its class;
-//   2. fold: every owner visits its class's rows IN ARRIVAL ORDER (ascending lane bit) and
-//      adds them to its P chains, so each chain is exactly the reference's left-to-right sum
-//      (prefill_opt.cpp:9-14).
-constexpr int kWarpsPerBlock = 4;
+// One CTA of kRouteWarps warps owns G = 32 / P consecutive windows. Per chunk of
+// <= kRouteCap requests of its range (normally one chunk: C4 windows hold ~300 requests, G = 8):
+//   0. one TMA bulk copy (cp.async.bulk, mbarrier completion) stages the chunk's prompts in
+//      shared memory: the only HBM read of the prompts, one instruction, no register ring;
+//   A. each warp takes a contiguous quarter of the chunk: classify() (router.cpp:26-31), write
+//      the class, key = (window g, class c), per-warp key histogram (match.any + leader add),
+//      min of prefill deadlines (simkernel.cpp:499-501) per key (order-free: min is exact);
+//   B. stable counting sort of the chunk positions by key: warp w scatters its quarter from
+//      cursor off[key] + (counts of warps < w), rank among the round's lanes by lane order, so
+//      every (g, c) run is in ARRIVAL order;
+//   C. fold: lane (g, p) of warp w walks window g's runs of the classes c = w (mod warps) and
+//      extends T[g][c][p] += (a_p L + b_p) L + c_p left to right, exactly prefill_opt.cpp:9-14.
+//      The P lanes of a window read the same entry (broadcast); run lengths of a class are
+//      similar across windows, so lanes stay busy, and the warps fold different classes.
+constexpr int kRouteWarps = 4;
+constexpr int kRouteCap = 2544;  // requests per chunk (C4: 9 CTAs per SM, one wave)
 
-template <int C, int P, bool DEADLINE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__device__ __forceinline__ unsigned long long ord_f64(double x) {  // order-preserving key
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord_f64(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <int K, bool DL>
+struct RouteSmem {  // one CTA
+  alignas(16) int32_t stage[kRouteCap + 4];  // prompts of [c0 & ~3, c1)
+  int32_t srt[kRouteCap];                    // the chunk's prompts sorted by key (stable)
+  uint64_t bar;
+  int64_t bnd[33];
+  int32_t lb[33];  // chunk-local window starts, lb[G] = "never"
+  int32_t off[K + 1];
+  int32_t hist[kRouteWarps][K];  // per-warp key counts, then per-warp scatter cursors
+  uint32_t cnt[K];
+  unsigned long long mdl[DL ? K : 1];
+  uint8_t key[kRouteCap];
+};
+
+template <int C, int P, bool DL>
+__global__ void __launch_bounds__(kRouteWarps * 32)
 k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
             const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
             uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
             double* __restrict__ t_ref, double* __restrict__ min_deadline) {
-  constexpr int G = (32 / C) < 8 ? (32 / C) : 8;  // windows per warp
-  __shared__ double s_term[kWarpsPerBlock][G][32][P];
-  __shared__ double s_dl[kWarpsPerBlock][DEADLINE ? G : 1][32];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w_first = (static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib) * G;
-  if (w_first >= rp.n_windows) return;
-  // this lane's owner role
-  const int og = lane / C, oc = lane % C;
-  const bool owner = lane < G * C && w_first + og < rp.n_windows;
-  // window extents (lane g < G reads window g's bounds; broadcast below)
-  int64_t ws[G], we[G];
-  int64_t rounds = 0;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int64_t w = w_first + g;
-    ws[g] = w < rp.n_windows ? bounds[w] : 0;
-    we[g] = w < rp.n_windows ? bounds[w + 1] : 0;
-    const int64_t r = (we[g] - ws[g] + 31) >> 5;
-    rounds = r > rounds ? r : rounds;
+  constexpr int G = 32 / P, K = G * C, E = (K + 31) / 32, NW = kRouteWarps;
+  constexpr int kNever = 0x3fffffff;
+  using S = RouteSmem<K, DL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& s = *reinterpret_cast<S*>(smem_raw);
+  const int tid = threadIdx.x, wib = tid >> 5, lane = tid & 31;
+  const unsigned lt = lanemask_lt();
+  const int64_t w_first = static_cast<int64_t>(blockIdx.x) * G;
+  for (int k = tid; k <= G; k += NW * 32) s.bnd[k] = bounds[min(w_first + k, rp.n_windows)];
+  for (int k = tid; k < K; k += NW * 32) {
+    s.cnt[k] = 0;
+    if (DL) s.mdl[k] = ~0ull;
   }
-  double acc[P];
+  if (tid == 0) gsb::mbar_init(&s.bar, 1);
+  __syncthreads();
+  const int64_t b0 = s.bnd[0], bG = s.bnd[G];
+  const bool tma = (reinterpret_cast<uintptr_t>(prompt) & 15) == 0;
+  uint32_t parity = 0;
+  // fold role: lane (fg, fp) = (window, profile)
+  const int fg = lane / P, fp = lane - (lane / P) * P;
+  const bool folder = lane < G * P;
+  const double la = rp.lat_a[fp], lb = rp.lat_b[fp], lc = rp.lat_c[fp];
+  double acc[C];
 #pragma unroll
-  for (int p = 0; p < P; ++p) acc[p] = 0.0;
-  double mdl = INFINITY;
-  uint32_t cnt = 0;
-  // software pipeline: the prompts (and arrivals) of round r+1 are in flight while round r is
-  // classified and folded, so HBM latency overlaps the fold instead of stalling classify()
-  int32_t Lnext[G];
-  int64_t Anext[DEADLINE ? G : 1];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const int64_t i = ws[g] + lane;
-    Lnext[g] = i < we[g] ? __ldg(prompt + i) : 0;
-    if (DEADLINE) Anext[g] = i < we[g] ? __ldg(arrival + i) : 0;
-  }
-  for (int64_t r = 0; r < rounds; ++r) {
-    int32_t Lcur[G];
-    int64_t Acur[DEADLINE ? G : 1];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      Lcur[g] = Lnext[g];
-      if (DEADLINE) Acur[g] = Anext[g];
-      const int64_t i = ws[g] + ((r + 1) << 5) + lane;
-      const bool in = r + 1 < rounds && i < we[g];
-      Lnext[g] = in ? __ldg(prompt + i) : 0;
-      if (DEADLINE) Anext[g] = in ? __ldg(arrival + i) : 0;
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+
+  for (int64_t c0 = b0; c0 < bG; c0 += kRouteCap) {
+    const int64_t c1 = min(c0 + static_cast<int64_t>(kRouteCap), bG);
+    const int nc = static_cast<int>(c1 - c0);
+    const int64_t a0 = c0 & ~int64_t{3};  // stage[i - a0] = prompt[i]
+    // ---- 0: stage the chunk (TMA for the 16-byte-aligned body, threads for the <= 3 tail)
+    const int64_t a1 = tma ? (c1 & ~int64_t{3}) : a0;
+    if (tid == 0 && a1 > a0) {
+      gsb::fence_proxy_async_smem();
+      const uint32_t bytes = static_cast<uint32_t>((a1 - a0) * 4);
+      gsb::mbar_expect_tx(&s.bar, bytes);
+      gsb::bulk_g2s(s.stage, prompt + a0, bytes, &s.bar);
     }
-    // phase 1: lane-parallel per request; class membership becomes per-class ballot masks
-    unsigned my_mask = 0;
+    for (int64_t i = max(a1, c0) + tid; i < c1; i += NW * 32) s.stage[i - a0] = __ldg(prompt + i);
+    for (int k = tid; k < NW * K; k += NW * 32) (&s.hist[0][0])[k] = 0;
+    if (tid <= G)
+      s.lb[tid] = tid == G ? kNever : static_cast<int>(min(max(s.bnd[tid] - c0, int64_t{0}),
+                                                           static_cast<int64_t>(kNever)));
+    if (a1 > a0) {
+      gsb::mbar_wait(&s.bar, parity);
+      parity ^= 1;
+    }
+    __syncthreads();
+    const int32_t* st = s.stage + (c0 - a0);
+    uint8_t* cls_c = cls_out + c0;
+    // this warp's contiguous part [j0, j1) of the chunk
+    const int q = ((nc + NW * 32 - 1) / (NW * 32)) * 32;
+    const int j0 = min(wib * q, nc), j1 = min(j0 + q, nc);
+    // ---- A: classify, key, histogram, deadlines
+    {
+      int g_lo = 0;  // window of the round's first request (warp-uniform)
+      while (s.lb[g_lo + 1] <= j0) ++g_lo;
+      int nb = s.lb[g_lo + 1];
+      for (int r = j0; r < j1; r += 32) {
+        const int j = r + lane;
+        const bool valid = j < j1;
+        const int32_t L = st[valid ? j : j0];
+        const int cl = classify_c<C>(rp, L);
+        int g = g_lo;
+        if (nb <= r + 32) {  // a window starts inside this round (or right after it)
+          int k = g_lo + 1;
+          for (; s.lb[k] <= r + 32; ++k) g += j >= s.lb[k] ? 1 : 0;
+          g_lo = k - 1;
+          nb = s.lb[k];
+        }
+        const int key = g * C + cl;
+        if (valid) {
+          cls_c[j] = static_cast<uint8_t>(cl);
+          s.key[j] = static_cast<uint8_t>(key);
+          if (DL) {
+            const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
+            const double dl = static_cast<double>(__ldg(arrival + c0 + j)) + ttft - rp.allowance;
+            if (dl == dl) atomicMin(&s.mdl[key], ord_f64(dl));
+          }
+        }
+        const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
+        if (valid && (m & lt) == 0) s.hist[wib][key] += __popc(m);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // ---- exclusive scan of the key totals (warp 0, lane l owns keys [l*E, l*E+E)); the
+    //      per-warp counts become the warps' scatter cursors
+    if (wib == 0) {
+      int loc[E];
+      int sum = 0;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t i = ws[g] + (r << 5) + lane;
-      int cl = -1;
-      if (i < we[g]) {
-        const int32_t L = Lcur[g];
-        cl = C > 1 ? classify_dev(rp, L) : 0;
-        cls_out[i] = static_cast<uint8_t>(cl);
-        const double Ld = static_cast<double>(L);
+      for (int e = 0; e < E; ++e) {
+        const int k = lane * E + e;
+        int t = 0;
+        if (k < K) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) s_term[wib][g][lane][p] = (rp.lat_a[p] * Ld + rp.lat_b[p]) * Ld + rp.lat_c[p];
-        if (DEADLINE) {
-          const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
-          s_dl[wib][g][lane] = static_cast<double>(Acur[g]) + ttft - rp.allowance;
+          for (int w = 0; w < NW; ++w) t += s.hist[w][k];
+        }
+        loc[e] = t;
+        sum += t;
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int k = lane * E + e;
+        if (k < K) {
+          s.off[k] = run;
+          int cur = run;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const int h = s.hist[w][k];
+            s.hist[w][k] = cur;
+            cur += h;
+          }
+          s.cnt[k] += static_cast<uint32_t>(loc[e]);
+          run += loc[e];
         }
       }
+      if (lane == 31) s.off[K] = incl;
+    }
+    __syncthreads();
+    // ---- B: stable scatter of the prompts by key (arrival order inside each key)
+    for (int r = j0; r < j1; r += 32) {
+      const int j = r + lane;
+      const bool valid = j < j1;
+      const int key = valid ? static_cast<int>(s.key[j]) : 0x10000;
+      const int32_t L = st[valid ? j : j0];
+      const unsigned m = __match_any_sync(kFull, key);
+      const int base = valid ? s.hist[wib][key] : 0;
+      __syncwarp();
+      if (valid) {
+        s.srt[base + __popc(m & lt)] = L;
+        if ((m & lt) == 0) s.hist[wib][key] = base + __popc(m);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- C: ordered fold, lane (window fg, profile fp) of warp w, classes c = w (mod NW)
+    if (folder) {
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const unsigned m = __ballot_sync(0xffffffffu, cl == c);
-        my_mask = (og == g && oc == c) ? m : my_mask;
+        if (c % NW != wib) continue;
+        const int o = s.off[fg * C + c], n = s.off[fg * C + c + 1] - o;
+        const int32_t* run = s.srt + o;
+        double a = acc[c];
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+          const double Ld = static_cast<double>(run[j]);
+          a = a + 1.0 * ((la * Ld + lb) * Ld + lc);
+        }
+        acc[c] = a;
       }
     }
-    __syncwarp();
-    // phase 2: ordered fold: the owner visits its class's rows in ascending arrival order
-    if (owner) {
-      cnt += __popc(my_mask);
-      while (my_mask) {
-        const int j = __ffs(static_cast<int>(my_mask)) - 1;
-        my_mask &= my_mask - 1;
+    __syncthreads();
+  }
+  const int64_t cells = rp.n_windows * C;
+  if (folder && w_first + fg < rp.n_windows) {
+    const int64_t cell0 = (w_first + fg) * C;
 #pragma unroll
-        for (int p = 0; p < P; ++p) acc[p] = acc[p] + 1.0 * s_term[wib][og][j][p];
-        if (DEADLINE) mdl = std_min(mdl, s_dl[wib][og][j]);
-      }
+    for (int c = 0; c < C; ++c)
+      if (c % NW == wib) t_ref[fp * cells + cell0 + c] = acc[c];
+  }
+  for (int k = tid; k < K; k += NW * 32) {
+    const int64_t w = w_first + k / C;
+    if (w >= rp.n_windows) continue;
+    const int64_t cell = w * C + k % C;
+    count[cell] = s.cnt[k];
+    if (DL && min_deadline) {
+      const unsigned long long v = s.mdl[DL ? k : 0];
+      min_deadline[cell] = v == ~0ull ? INFINITY : unord_f64(v);
     }
-    __syncwarp();
   }
-  if (owner) {
-    const int64_t cells = rp.n_windows * C;
-    const int64_t cell = (w_first + og) * C + oc;
-#pragma unroll
-    for (int p = 0; p < P; ++p) t_ref[p * cells + cell] = acc[p];
-    count[cell] = cnt;
-    if (DEADLINE && min_deadline) min_deadline[cell] = mdl;
-  }
+}
+
+template <int C, int P, bool DL>
+int launch_route_bin(const RouteParams& rp, const int64_t* d_arrival, const int32_t* d_prompt,
+                     const int64_t* d_bounds, uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                     double* d_min_deadline, cudaStream_t s) {
+  constexpr int G = 32 / P;
+  const size_t smem = sizeof(RouteSmem<G * C, DL>);
+  if (cudaFuncSetAttribute(k_route_bin<C, P, DL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return -1;
+  const unsigned blocks = static_cast<unsigned>((rp.n_windows + G - 1) / G);
+  k_route_bin<C, P, DL><<<blocks, kRouteWarps * 32, smem, s>>>(rp, d_arrival, d_prompt, d_bounds,
+                                                               d_class, d_count, d_t_ref,
+                                                               d_min_deadline);
+  return 0;
 }
 
 // ---------------------------------------------------------------- K1c: Dispatcher FIFO
@@ -855,8 +1017,8 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   if (!ctx) return GSB_INVALID_ARGUMENT;
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
-  const int64_t tiles = n_req / kBoundsTile + 1;
-  const int64_t blocks = (tiles + 255) / 256;
+  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
+  const int64_t blocks = (warps + 7) / 8;
   k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
                     gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms, cfg->w0,
                                                     cfg->n_windows, d_bounds);
@@ -876,28 +1038,26 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const i
   const int P = ctx->n_profiles;
   cudaStream_t s = gsb_pick_stream(ctx, stream);
   const bool dl = rp.want_deadline != 0;
-  const int G = std::min(8, 32 / rp.C);
-  const int64_t warps = (cfg->n_windows + G - 1) / G;
-  const unsigned blocks = static_cast<unsigned>((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
   const int key = (rp.C - 1) * 8 + (P - 1) * 2 + (dl ? 1 : 0);
+  int lrc = 0;
   switch (key) {
-#define GSB_RB(CC, PP)                                                                           \
-  case ((CC)-1) * 8 + ((PP)-1) * 2:                                                             \
-    k_route_bin<CC, PP, false><<<blocks, kWarpsPerBlock * 32, 0, s>>>(                          \
-        rp, d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline);          \
-    break;                                                                                       \
-  case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                         \
-    k_route_bin<CC, PP, true><<<blocks, kWarpsPerBlock * 32, 0, s>>>(                           \
-        rp, d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline);          \
+#define GSB_RB(CC, PP)                                                                          \
+  case ((CC)-1) * 8 + ((PP)-1) * 2:                                                            \
+    lrc = launch_route_bin<CC, PP, false>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count, \
+                                          d_t_ref, d_min_deadline, s);                         \
+    break;                                                                                      \
+  case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                        \
+    lrc = launch_route_bin<CC, PP, true>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,  \
+                                         d_t_ref, d_min_deadline, s);                          \
     break;
 #define GSB_RB_P(CC) GSB_RB(CC, 1) GSB_RB(CC, 2) GSB_RB(CC, 3) GSB_RB(CC, 4)
-    GSB_RB_P(1) GSB_RB_P(2) GSB_RB_P(3) GSB_RB_P(4) GSB_RB_P(5) GSB_RB_P(6) GSB_RB_P(7)
-    GSB_RB(8, 1) GSB_RB(8, 2) GSB_RB(8, 3) GSB_RB(8, 4)
+    GSB_RB_P(1) GSB_RB_P(2) GSB_RB_P(3) GSB_RB_P(4) GSB_RB_P(5) GSB_RB_P(6) GSB_RB_P(7) GSB_RB_P(8)
 #undef GSB_RB_P
 #undef GSB_RB
     default:
       return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "route: need 1..8 classes, 1..4 profiles");
   }
+  if (lrc) return gsb_set_error(ctx, GSB_CUDA_ERROR, "route: shared-memory attribute refused");
   return gsb_check_launch(ctx, "route_bin");
 }
 

@@ -69,6 +69,11 @@ def test_fast_division_equals_ieee(eng):
     ([256, 512, 1024, 2048], 2, 3.0, 60_000),
     ([128, 256, 512, 768, 1024, 2048, 4096], 4, 8.0, 30_000),
     ([1024], 3, 20.0, 1_000),
+    # windows far larger than one warp's staging chunk (kRouteCap): chains continue across chunks
+    ([512, 1024], 4, 150.0, 60_000),
+    ([256, 512, 1024, 2048], 1, 40.0, 30_000),
+    # sparse: most windows empty, window edges far apart
+    ([512, 1024, 4096], 2, 0.02, 1_000),
 ])
 def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms):
     api = _api()

@@ -1,5 +1,7 @@
 """Per-source-line hot spots of one kernel from an ncu report + the local cubin's line info.
-python tools/sass_hotspots.py REPORT.ncu-rep LIB.so KERNEL_SUBSTRING [top]
+python tools/sass_hotspots.py REPORT.ncu-rep LIB.so KERNEL_SUBSTRING [top] [MANGLED_SUBSTRING]
+(the first captured launch whose name matches KERNEL_SUBSTRING; MANGLED_SUBSTRING picks the
+template instantiation in the cubin, e.g. k_route_binILi8ELi4ELb0E)
 (ncu's own source view needs the build path; this maps SASS addresses with nvdisasm -g.)"""
 import collections
 import csv
@@ -12,9 +14,13 @@ import tempfile
 
 rep, lib, kern = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+mangled = sys.argv[5] if len(sys.argv) > 5 else kern
+raw = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kern, "--page", "source", "--csv",
+                      "--print-source", "sass"], capture_output=True, text=True).stdout
 lines = raw.splitlines()
+heads = [i for i, ln in enumerate(lines) if ln.startswith('"Kernel Name"')]
+if len(heads) > 1:
+    lines = lines[:heads[1]]
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
 hdr = rows[0]
 ia, ie, ist = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index(
@@ -38,7 +44,7 @@ for cub in os.listdir(d):
     for ln in sass.splitlines():
         m = re.match(r"\s*\.text\.(\S+):", ln) or re.match(r"^(_Z\S+):$", ln)
         if m:
-            inside = kern in m.group(1)
+            inside = mangled in m.group(1)
             continue
         if not inside:
             continue
