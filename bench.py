@@ -166,10 +166,10 @@ def run_gsb(args, rank, world, dist):
         eng.route_bin(d_arr, d_prm, routing, wms, w0, nW, out=rr)
         if mark:
             ev[1].record(stream)
-        eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel)
+        # K2 + the per-class summary: one launch (objective, argmin, reduction)
+        eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel, summary_out=summ)
         if mark:
             ev[2].record(stream)
-        eng.prefill_summary_dev(sel, W["C"], out=summ)
 
     use_graph = not args.no_graph
     graphs = {}
@@ -389,8 +389,9 @@ def run_gsb(args, rank, world, dist):
     peak_tflops = dfma_per_s * 2 / 1e12
     k1_gbs = n_req * K1_BYTES_PER_REQ / (k1_ms / 1e3) / 1e9
     # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
-    # + summary partial/final (5); decode step = tbt_p95 + tps + decode_replay (3); e2e = 5
-    launches = args.steps * (5 + 3 + 5) + max(3, args.steps // 4)
+    # with the fused summary partials + summary final (4); decode step = tbt_p95 + tps +
+    # decode_replay (3); e2e = 4
+    launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4)
     line = {
         "metric": METRIC,
         "value": world * evals / (ms_pre / 1e3),

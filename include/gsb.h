@@ -248,6 +248,17 @@ int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_c
                         const int16_t* d_f_idx, const double* d_energy,
                         gsb_class_summary* d_out /* [n_profiles*n_classes] */, void* stream);
 
+/* K2 with the per-class summary fused: gsb_prefill_select's outputs plus the
+ * gsb_prefill_summary record of every (profile, class). The per-CTA partials are folded in
+ * K2's epilogue and one small kernel combines them. Same fixed-shape tree as
+ * gsb_prefill_summary, so the two paths give identical bytes. Needs cfg->n_classes with n_cells = windows x classes.
+ * Replaces the reference's end-of-run energy / SLO tallies over queue_optimizer_tick's
+ * commands (prefill_opt.cpp:58-82 callers, simkernel.cpp:487). */
+int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                               const double* d_t_ref, const uint32_t* d_count,
+                               const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
+                               double* d_energy, gsb_class_summary* d_summary, void* stream);
+
 /* ---------------------------------------------------------------- K3/K4: decode control */
 /* Raw decode telemetry of S streams (one decode worker each), CSR layout:
  * events of stream s are [d_ev_off[s], d_ev_off[s+1]) sorted by time; event j emitted

@@ -120,7 +120,7 @@ EXPORTS = (
     "gsb_set_profiles_ex", "gsb_malloc", "gsb_free", "gsb_host_alloc", "gsb_host_free",
     "gsb_memcpy", "gsb_classify",
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
-    "gsb_decode_pool", "gsb_decode_pool_tps_cap",
+    "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
 )
 
 _lib = None
@@ -159,6 +159,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                                      _p, _p, _p, _p]
     L.gsb_energy_batches.argtypes = [_p, C.c_int, _i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]
     L.gsb_prefill_summary.argtypes = [_p, C.c_int, C.c_int, _i64, _p, _p, _p, _p]
+    L.gsb_prefill_select_summary.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, _p, _p, _p, _p,
+                                             _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]
     L.gsb_n_ticks.restype = _i64
     L.gsb_window_series.argtypes = [_p, P(CTelemetry), C.c_int, _d, _d, _d, _p, _p, _p, _p]

@@ -554,19 +554,33 @@ class Engine:
                        fixed_window_ms: float = 0.0,
                        qopt: QueueOptimizerConfig = QueueOptimizerConfig(),
                        window: Optional[torch.Tensor] = None,
-                       out: Optional[SelectResult] = None) -> SelectResult:
-        """K2: energy_total at every (cell, profile, clock) + deterministic argmin."""
+                       out: Optional[SelectResult] = None,
+                       summary_out: Optional[torch.Tensor] = None) -> SelectResult:
+        """K2: energy_total at every (cell, profile, clock) + deterministic argmin. With
+        summary_out (a [P*C, 48] byte tensor, see prefill_summary_dev) the per-(profile,
+        class) summary is folded into the same launch (gsb_prefill_select_summary)."""
         cfg = L.CSelectCfg(mode, rr.n_classes, fixed_window_ms, rr.w0, rr.window_ms, qopt.to_c())
         P, cells = len(self.profiles), rr.n_cells
         if out is None:
             out = SelectResult(self._empty((P, cells), torch.int16),
                                self._empty((P, cells), torch.float64),
                                window if window is not None else self._empty(cells, torch.float64))
+        if summary_out is not None:
+            self._check(self.lib.gsb_prefill_select_summary(
+                self.ctx, C.byref(cfg), cells, _ptr(rr.t_ref), _ptr(rr.count),
+                _ptr(rr.min_deadline), _ptr(out.window_ms), _ptr(out.f_idx), _ptr(out.energy_j),
+                _ptr(summary_out), self.stream()))
+            return out
         self._check(self.lib.gsb_prefill_select(self.ctx, C.byref(cfg), cells, _ptr(rr.t_ref),
                                                 _ptr(rr.count), _ptr(rr.min_deadline),
                                                 _ptr(out.window_ms), _ptr(out.f_idx),
                                                 _ptr(out.energy_j), self.stream()))
         return out
+
+    def summary_buffer(self, n_classes: int) -> torch.Tensor:
+        """Device bytes for P*C gsb_class_summary records (prefill_select(summary_out=...))."""
+        return self._empty((len(self.profiles) * n_classes, C.sizeof(L.CClassSummary)),
+                           torch.uint8)
 
     SUMMARY_DTYPE = np.dtype([("n_cmd", "<i8"), ("n_infeasible", "<i8"), ("n_empty", "<i8"),
                               ("sum_energy_j", "<f8"), ("min_energy_j", "<f8"),

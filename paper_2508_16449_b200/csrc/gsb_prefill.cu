@@ -48,12 +48,14 @@ __device__ __forceinline__ int64_t div_floor(int64_t a, int64_t d, double rd) {
 // first request of window k (arrivals are non-decreasing, trace.cpp:109-111). Request i owns
 // the entries k in (w(i-1), w(i)] (request 0 covers k <= w(0), a virtual request n the tail),
 // so every entry is written exactly once.
-// A warp covers 32 tiles of 32 requests. Each lane reads only the LAST arrival of its tile (one
+// Lane l of a warp owns tile l of 32 requests. It reads only the LAST arrival of its tile (one
 // 32-byte sector per 32 requests) and takes the previous tile's from its neighbour: with sorted
-// arrivals a tile holds a window edge iff its two ends differ. The warp then resolves each edge
-// tile cooperatively with one coalesced load of its 32 arrivals, so DRAM traffic is ~1/8 of the
-// arrival array plus the edge tiles.
+// arrivals a tile holds a window edge iff its two ends differ. The warp then resolves its edge
+// tiles cooperatively, up to four at a time: lane l loads element l of each of them (four
+// independent coalesced loads in flight), so a warp pays two dependent DRAM latencies in the
+// common case and the pass reads ~1/8 of the arrivals plus the edge tiles.
 constexpr int kBoundsTile = 32;
+constexpr int kBoundsBatch = 4;
 constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void __launch_bounds__(256)
@@ -76,56 +78,69 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
   if (lane == 0) wprev = win(t0 - 1);
   unsigned edges = __ballot_sync(kFull, live && wlast != wprev);
   while (edges) {
-    const int src = __ffs(static_cast<int>(edges)) - 1;
-    edges &= edges - 1;
-    const int64_t wp0 = __shfl_sync(kFull, wprev, src);
-    const int64_t i = span + static_cast<int64_t>(src) * kBoundsTile + lane;
-    const int64_t wi = i <= n ? win(i) : 0;
-    int64_t wp = __shfl_up_sync(kFull, wi, 1);
-    if (lane == 0) wp = wp0;
-    if (i <= n && wi != wp) {
-      const int64_t hi = min(wi, n_windows);
-      for (int64_t k = max(wp + 1, int64_t{0}); k <= hi; ++k) bounds[k] = i;
+    int src[kBoundsBatch];
+    int64_t a[kBoundsBatch];
+#pragma unroll
+    for (int k = 0; k < kBoundsBatch; ++k) {  // issue the batch's loads together
+      src[k] = edges ? __ffs(static_cast<int>(edges)) - 1 : -1;
+      edges &= edges - 1;
+      const int64_t i = span + static_cast<int64_t>(src[k]) * kBoundsTile + lane;
+      a[k] = (src[k] >= 0 && i < n) ? __ldg(arrival + i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kBoundsBatch; ++k) {
+      if (src[k] < 0) break;  // warp-uniform
+      const int64_t wp0 = __shfl_sync(kFull, wprev, src[k]);
+      const int64_t i = span + static_cast<int64_t>(src[k]) * kBoundsTile + lane;
+      const int64_t wi = i < n ? div_floor(a[k], window_ms, rd) - w0 : n_windows;
+      int64_t wp = __shfl_up_sync(kFull, wi, 1);
+      if (lane == 0) wp = wp0;
+      if (i <= n && wi != wp) {
+        const int64_t hi = min(wi, n_windows);
+        for (int64_t k2 = max(wp + 1, int64_t{0}); k2 <= hi; ++k2) bounds[k2] = i;
+      }
     }
   }
 }
 
 // classify(), router.cpp:26-31: number of thresholds strictly below the prompt. The thresholds
 // are ascending and distinct (RoutingConfig::validate, router.cpp:7-11, checked host-side) and
-// padded with INT_MAX, so the count is a branch-free binary search: ceil(log2 C) compares.
+// padded with INT_MAX, so the count is a branch-free binary search: ceil(log2 C) compares on
+// thresholds held in registers.
 template <int C>
-__device__ __forceinline__ int classify_c(const RouteParams& rp, int32_t L) {
+__device__ __forceinline__ int classify_c(const int32_t (&t)[GSB_MAX_CLASSES - 1], int32_t L) {
   if (C == 1) return 0;
-  if (C == 2) return rp.thr[0] < L ? 1 : 0;
+  if (C == 2) return t[0] < L ? 1 : 0;
   if (C <= 4) {
-    const int c = rp.thr[1] < L ? 2 : 0;
-    return c + ((c ? rp.thr[2] : rp.thr[0]) < L ? 1 : 0);
+    const bool hi = t[1] < L;
+    return (hi ? 2 : 0) + ((hi ? t[2] : t[0]) < L ? 1 : 0);
   }
-  const bool hi = rp.thr[3] < L;
-  int c = hi ? 4 : 0;
-  const bool mid = (hi ? rp.thr[5] : rp.thr[1]) < L;
-  c += mid ? 2 : 0;
-  const int32_t t = mid ? (hi ? rp.thr[6] : rp.thr[2]) : (hi ? rp.thr[4] : rp.thr[0]);
-  return c + (t < L ? 1 : 0);
+  const bool hi = t[3] < L;
+  const bool mid = (hi ? t[5] : t[1]) < L;
+  const int32_t lo = mid ? (hi ? t[6] : t[2]) : (hi ? t[4] : t[0]);
+  return (hi ? 4 : 0) + (mid ? 2 : 0) + (lo < L ? 1 : 0);
 }
 
 // ---------------------------------------------------------------- K1b: route + bin
 // One CTA of kRouteWarps warps owns G = 32 / P consecutive windows. Per chunk of
 // <= kRouteCap requests of its range (normally one chunk: C4 windows hold ~300 requests, G = 8):
 //   0. one TMA bulk copy (cp.async.bulk, mbarrier completion) stages the chunk's prompts in
-//      shared memory: the only HBM read of the prompts, one instruction, no register ring;
+//      shared memory: the only HBM read of the prompts;
 //   A. each warp takes a contiguous quarter of the chunk: classify() (router.cpp:26-31), write
 //      the class, key = (window g, class c), per-warp key histogram (match.any + leader add),
 //      min of prefill deadlines (simkernel.cpp:499-501) per key (order-free: min is exact);
-//   B. stable counting sort of the chunk positions by key: warp w scatters its quarter from
-//      cursor off[key] + (counts of warps < w), rank among the round's lanes by lane order, so
-//      every (g, c) run is in ARRIVAL order;
+//   B. stable counting sort of the chunk by key: warp w scatters the prompts of its quarter
+//      from cursor off[key] + (counts of warps < w), rank among the round's lanes by lane
+//      order, so every (g, c) run is in ARRIVAL order;
 //   C. fold: lane (g, p) of warp w walks window g's runs of the classes c = w (mod warps) and
 //      extends T[g][c][p] += (a_p L + b_p) L + c_p left to right, exactly prefill_opt.cpp:9-14.
 //      The P lanes of a window read the same entry (broadcast); run lengths of a class are
 //      similar across windows, so lanes stay busy, and the warps fold different classes.
+// Shared memory is 9 B per chunk slot (prompt, key, sorted prompt), so nine CTAs share an SM and
+// the C4 grid (1,250 CTAs) is one wave (P = 1 holds 32 windows x C keys per CTA: fewer CTAs).
 constexpr int kRouteWarps = 4;
-constexpr int kRouteCap = 2544;  // requests per chunk (C4: 9 CTAs per SM, one wave)
+constexpr int kRouteCap = 2544;  // requests per chunk
+constexpr int kRouteMinBlocks = 9;
 
 __device__ __forceinline__ unsigned long long ord_f64(double x) {  // order-preserving key
   const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
@@ -145,6 +160,7 @@ template <int K, bool DL>
 struct RouteSmem {  // one CTA
   alignas(16) int32_t stage[kRouteCap + 4];  // prompts of [c0 & ~3, c1)
   int32_t srt[kRouteCap];                    // the chunk's prompts sorted by key (stable)
+  uint8_t key[kRouteCap];
   uint64_t bar;
   int64_t bnd[33];
   int32_t lb[33];  // chunk-local window starts, lb[G] = "never"
@@ -152,11 +168,10 @@ struct RouteSmem {  // one CTA
   int32_t hist[kRouteWarps][K];  // per-warp key counts, then per-warp scatter cursors
   uint32_t cnt[K];
   unsigned long long mdl[DL ? K : 1];
-  uint8_t key[kRouteCap];
 };
 
 template <int C, int P, bool DL>
-__global__ void __launch_bounds__(kRouteWarps * 32)
+__global__ void __launch_bounds__(kRouteWarps * 32, P == 1 ? 6 : kRouteMinBlocks)
 k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
             const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
             uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
@@ -168,6 +183,9 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
   S& s = *reinterpret_cast<S*>(smem_raw);
   const int tid = threadIdx.x, wib = tid >> 5, lane = tid & 31;
   const unsigned lt = lanemask_lt();
+  int32_t th[GSB_MAX_CLASSES - 1];
+#pragma unroll
+  for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) th[k] = rp.thr[k];
   const int64_t w_first = static_cast<int64_t>(blockIdx.x) * G;
   for (int k = tid; k <= G; k += NW * 32) s.bnd[k] = bounds[min(w_first + k, rp.n_windows)];
   for (int k = tid; k < K; k += NW * 32) {
@@ -183,9 +201,10 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
   const int fg = lane / P, fp = lane - (lane / P) * P;
   const bool folder = lane < G * P;
   const double la = rp.lat_a[fp], lb = rp.lat_b[fp], lc = rp.lat_c[fp];
-  double acc[C];
+  constexpr int CPW = (C + NW - 1) / NW;  // classes per warp in the fold: c = wib + k * NW
+  double acc[CPW];
 #pragma unroll
-  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  for (int k = 0; k < CPW; ++k) acc[k] = 0.0;
 
   for (int64_t c0 = b0; c0 < bG; c0 += kRouteCap) {
     const int64_t c1 = min(c0 + static_cast<int64_t>(kRouteCap), bG);
@@ -204,26 +223,28 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
     if (tid <= G)
       s.lb[tid] = tid == G ? kNever : static_cast<int>(min(max(s.bnd[tid] - c0, int64_t{0}),
                                                            static_cast<int64_t>(kNever)));
-    if (a1 > a0) {
-      gsb::mbar_wait(&s.bar, parity);
+    if (a1 > a0) {  // one thread polls the barrier; the others wait in bar.sync
+      if (tid == 0) gsb::mbar_wait(&s.bar, parity);
       parity ^= 1;
     }
     __syncthreads();
-    const int32_t* st = s.stage + (c0 - a0);
-    uint8_t* cls_c = cls_out + c0;
+    const int sb = static_cast<int>(c0 - a0);  // stage index of chunk position 0
+    const int32_t* st = s.stage + sb;
     // this warp's contiguous part [j0, j1) of the chunk
     const int q = ((nc + NW * 32 - 1) / (NW * 32)) * 32;
     const int j0 = min(wib * q, nc), j1 = min(j0 + q, nc);
+    int32_t* hist_w = s.hist[wib];
     // ---- A: classify, key, histogram, deadlines
     {
       int g_lo = 0;  // window of the round's first request (warp-uniform)
       while (s.lb[g_lo + 1] <= j0) ++g_lo;
       int nb = s.lb[g_lo + 1];
-      for (int r = j0; r < j1; r += 32) {
+      uint8_t* cls_p = cls_out + c0 + j0 + lane;
+      for (int r = j0; r < j1; r += 32, cls_p += 32) {
         const int j = r + lane;
         const bool valid = j < j1;
         const int32_t L = st[valid ? j : j0];
-        const int cl = classify_c<C>(rp, L);
+        const int cl = classify_c<C>(th, L);
         int g = g_lo;
         if (nb <= r + 32) {  // a window starts inside this round (or right after it)
           int k = g_lo + 1;
@@ -232,17 +253,17 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
           nb = s.lb[k];
         }
         const int key = g * C + cl;
+        const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
         if (valid) {
-          cls_c[j] = static_cast<uint8_t>(cl);
+          *cls_p = static_cast<uint8_t>(cl);
           s.key[j] = static_cast<uint8_t>(key);
+          if ((m & lt) == 0) hist_w[key] += __popc(m);
           if (DL) {
             const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
             const double dl = static_cast<double>(__ldg(arrival + c0 + j)) + ttft - rp.allowance;
             if (dl == dl) atomicMin(&s.mdl[key], ord_f64(dl));
           }
         }
-        const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
-        if (valid && (m & lt) == 0) s.hist[wib][key] += __popc(m);
         __syncwarp();
       }
     }
@@ -293,14 +314,15 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
     for (int r = j0; r < j1; r += 32) {
       const int j = r + lane;
       const bool valid = j < j1;
-      const int key = valid ? static_cast<int>(s.key[j]) : 0x10000;
+      const int key = valid ? static_cast<int>(s.key[j]) : 0;
       const int32_t L = st[valid ? j : j0];
-      const unsigned m = __match_any_sync(kFull, key);
-      const int base = valid ? s.hist[wib][key] : 0;
+      const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
+      const int base = hist_w[key];
       __syncwarp();
+      const unsigned below = m & lt;
       if (valid) {
-        s.srt[base + __popc(m & lt)] = L;
-        if ((m & lt) == 0) s.hist[wib][key] = base + __popc(m);
+        s.srt[base + __popc(below)] = L;
+        if (below == 0) hist_w[key] = base + __popc(m);
       }
       __syncwarp();
     }
@@ -308,17 +330,18 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
     // ---- C: ordered fold, lane (window fg, profile fp) of warp w, classes c = w (mod NW)
     if (folder) {
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        if (c % NW != wib) continue;
+      for (int k = 0; k < CPW; ++k) {
+        const int c = wib + k * NW;
+        if (c >= C) break;
         const int o = s.off[fg * C + c], n = s.off[fg * C + c + 1] - o;
         const int32_t* run = s.srt + o;
-        double a = acc[c];
+        double a = acc[k];
 #pragma unroll 4
         for (int j = 0; j < n; ++j) {
           const double Ld = static_cast<double>(run[j]);
           a = a + 1.0 * ((la * Ld + lb) * Ld + lc);
         }
-        acc[c] = a;
+        acc[k] = a;
       }
     }
     __syncthreads();
@@ -327,8 +350,10 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
   if (folder && w_first + fg < rp.n_windows) {
     const int64_t cell0 = (w_first + fg) * C;
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      if (c % NW == wib) t_ref[fp * cells + cell0 + c] = acc[c];
+    for (int k = 0; k < CPW; ++k) {
+      const int c = wib + k * NW;
+      if (c < C) t_ref[fp * cells + cell0 + c] = acc[k];
+    }
   }
   for (int k = tid; k < K; k += NW * 32) {
     const int64_t w = w_first + k / C;
@@ -369,6 +394,142 @@ __global__ void k_fifo(int32_t C, int64_t n_windows, const uint8_t* __restrict__
   int64_t pos = cell_off[cell];
   for (int64_t i = bounds[w]; i < bounds[w + 1]; ++i)
     if (cls[i] == c) fifo[pos++] = i;
+}
+
+// ---------------------------------------------------------------- per-class summary
+// Per (profile, class) reduction of a K2 pass (n_cmd, n_infeasible, n_empty, sum E, argmin
+// cell). Fixed-shape tree, so bitwise identical on every run and every rank:
+//   CTA (x, p) owns cells [256x, 256x+256) of profile p: slot t = cell - 256x;
+//   level 1: thread (segment s < 8, class c) folds the class-c slots of [32s, 32s+32) in slot
+//            order; level 2: thread c folds its 8 segments in order -> parts[p][c][x];
+//   final:   k_summary_final, one warp per (p, c): lane l folds x = l, l+32, ... in order,
+//            then a fixed 5-level shuffle tree.
+// K2 runs levels 1-2 in its own epilogue (gsb_prefill_select_summary: the objective, argmin
+// and partial reduction are one launch); gsb_prefill_summary runs the same tree from the
+// stored f_idx / energy, so both give identical bytes.
+constexpr int kSumCta = 256;
+
+struct Part {
+  double sum, mn;
+  long long cmd, inf, emp, arg;
+};
+
+__device__ __forceinline__ Part part_identity() { return Part{0.0, INFINITY, 0, 0, 0, -1}; }
+
+// one cell's contribution: f_idx -2 empty, -1 infeasible (a command pinned at f_max), else a
+// choice with energy e (the argmin skips non-finite energies, as a '<' scan from +inf does)
+__device__ __forceinline__ Part part_of_cell(int fi, double e, long long cell) {
+  Part v = part_identity();
+  if (fi == -2) {
+    v.emp = 1;
+    return v;
+  }
+  v.cmd = 1;
+  if (fi < 0) {
+    v.inf = 1;
+    return v;
+  }
+  v.sum = e;
+  if (e < INFINITY) {
+    v.mn = e;
+    v.arg = cell;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void part_combine(Part& x, const Part& y) {
+  x.sum = x.sum + y.sum;
+  x.cmd += y.cmd;
+  x.inf += y.inf;
+  x.emp += y.emp;
+  if (y.arg >= 0 && (x.arg < 0 || y.mn < x.mn || (y.mn == x.mn && y.arg < x.arg))) {
+    x.mn = y.mn;
+    x.arg = y.arg;
+  }
+}
+
+struct SumArgs {
+  Part* parts;  // [P][C][gridDim.x]
+};
+
+struct SumSmem {
+  Part s1[kSumCta];  // slot t's contribution
+  Part s2[8 * GSB_MAX_CLASSES];
+};
+
+// Levels 1-2 of the tree for tile (x, p) once sm.s1 holds every slot's contribution (the
+// caller synchronises before and after).
+__device__ __forceinline__ void summary_tile(SumSmem& sm, int C, const SumArgs& sa, int x, int p,
+                                             int nx) {
+  const int t = threadIdx.x;
+  const long long cell0 = static_cast<long long>(x) * kSumCta;
+  if (t < 8 * C) {
+    const int c = t % C, seg = t / C;
+    const int r0 = static_cast<int>((cell0 + seg * 32) % C);
+    Part a = part_identity();
+    for (int j = seg * 32 + (c - r0 + C) % C; j < seg * 32 + 32; j += C) part_combine(a, sm.s1[j]);
+    sm.s2[seg * C + c] = a;
+  }
+  __syncthreads();
+  if (t < C) {
+    Part a = sm.s2[t];
+    for (int seg = 1; seg < 8; ++seg) part_combine(a, sm.s2[seg * C + t]);
+    sa.parts[(static_cast<long long>(p) * C + t) * nx + x] = a;
+  }
+}
+
+__device__ __forceinline__ Part part_shfl_down(const Part& v, int o) {
+  Part r;
+  r.sum = __shfl_down_sync(kFull, v.sum, o);
+  r.mn = __shfl_down_sync(kFull, v.mn, o);
+  r.cmd = __shfl_down_sync(kFull, v.cmd, o);
+  r.inf = __shfl_down_sync(kFull, v.inf, o);
+  r.emp = __shfl_down_sync(kFull, v.emp, o);
+  r.arg = __shfl_down_sync(kFull, v.arg, o);
+  return r;
+}
+
+// one warp per (profile, class) pc: lane l folds the partials x = l, l+32, ... in x order,
+// then a fixed 5-level shuffle tree
+__global__ void __launch_bounds__(32)
+k_summary_final(const Part* __restrict__ parts, int nx, gsb_class_summary* __restrict__ out) {
+  const int pc = blockIdx.x, lane = threadIdx.x;
+  Part a = part_identity();
+  const Part* src = parts + static_cast<long long>(pc) * nx;
+#pragma unroll 4
+  for (int x = lane; x < nx; x += 32) part_combine(a, src[x]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Part y = part_shfl_down(a, o);
+    if (lane < o) part_combine(a, y);
+  }
+  if (lane == 0) {
+    gsb_class_summary o;
+    o.n_cmd = a.cmd;
+    o.n_infeasible = a.inf;
+    o.n_empty = a.emp;
+    o.sum_energy_j = a.sum;
+    o.min_energy_j = a.mn;
+    o.argmin_cell = a.arg;
+    out[pc] = o;
+  }
+}
+
+// gsb_prefill_summary: the same tree from stored f_idx / energy
+__global__ void __launch_bounds__(kSumCta)
+k_summary(int C, int64_t n_cells, const int16_t* __restrict__ f_idx,
+          const double* __restrict__ energy, SumArgs sa) {
+  __shared__ SumSmem sm;
+  const int64_t cell = static_cast<int64_t>(blockIdx.x) * kSumCta + threadIdx.x;
+  Part v = part_identity();
+  if (cell < n_cells) {
+    const int64_t o = static_cast<int64_t>(blockIdx.y) * n_cells + cell;
+    v = part_of_cell(f_idx[o], energy[o], cell);
+  }
+  sm.s1[threadIdx.x] = v;
+  __syncthreads();
+  summary_tile(sm, C, sa, static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
+               static_cast<int>(gridDim.x));
 }
 
 // ---------------------------------------------------------------- K2: objective + argmin
@@ -510,25 +671,28 @@ struct ClockSet {  // every profile of the pass, one kernel-parameter block (<= 
   double P_min[GSB_MAX_PROFILES], P_max[GSB_MAX_PROFILES];
 };
 
-template <int G, int PI>
+// cells first, first + stride, ... of profile PI; SUM: one cell (stride = n) and its summary
+// contribution in *part
+template <int G, int PI, bool SUM>
 __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const ClockSet<G>& cs,
                                                const double* __restrict__ t_ref,
                                                const uint32_t* __restrict__ count,
                                                const double* __restrict__ min_deadline,
                                                double* __restrict__ window,
                                                int16_t* __restrict__ f_idx,
-                                               double* __restrict__ energy) {
+                                               double* __restrict__ energy, Part* part,
+                                               int64_t first, int64_t stride) {
   const ClockConst<G>& cc = cs.c[PI];
   const int p = PI;
   const double f_ref = cs.f_ref[PI], p_idle = cs.p_idle[PI], P_min = cs.P_min[PI],
                P_max = cs.P_max[PI];
   const int64_t n = sp.n_cells;
-  for (int64_t cell = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; cell < n;
-       cell += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t cell = first; cell < n; cell += stride) {
     const int64_t o = p * n + cell;
     if (count && count[cell] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
       f_idx[o] = -2;
       energy[o] = 0.0;
+      if (SUM) *part = part_of_cell(-2, 0.0, cell);
       continue;
     }
     const double W = cell_window(sp, cell, min_deadline, window);
@@ -537,7 +701,9 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
     int best = -1;
     double be = 0.0;
     if (cell_fast(TF, W, p_idle, P_min, P_max)) {
-#pragma unroll
+      // unrolled 9x, not 81x: the table operands become indexed constant loads, and the four
+      // profile variants stay small enough for the instruction cache
+#pragma unroll 9
       for (int i = 0; i < G; ++i) {
         const double f = cc.f[i], r = cc.r[i];
         double q = __dmul_rn(TF, r);
@@ -557,6 +723,7 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
         be = take ? E : be;
       }
     } else {
+#pragma unroll 1
       for (int i = 0; i < G; ++i) {
         const double busy = __ddiv_rn(TF, cc.f[i]);
         const double active = __ddiv_rn(__dmul_rn(cc.P[i], busy), 1000.0);
@@ -569,6 +736,7 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
     }
     f_idx[o] = static_cast<int16_t>(best);
     energy[o] = best >= 0 ? be : 0.0;
+    if (SUM) *part = part_of_cell(best, be, cell);
   }
 }
 
@@ -579,12 +747,82 @@ k_prefill_select_c(const __grid_constant__ SelectParams sp, const __grid_constan
                    const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
                    const double* __restrict__ min_deadline, double* __restrict__ window,
                    int16_t* __restrict__ f_idx, double* __restrict__ energy) {
+  const int64_t first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+#define GSB_SEL(PI)                                                                             \
+  select_cells_c<G, PI, false>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy, nullptr, \
+                               first, stride)
   switch (blockIdx.y) {
-    case 0: select_cells_c<G, 0>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
-    case 1: select_cells_c<G, 1>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
-    case 2: select_cells_c<G, 2>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
-    default: select_cells_c<G, 3>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy); break;
+    case 0: GSB_SEL(0); break;
+    case 1: GSB_SEL(1); break;
+    case 2: GSB_SEL(2); break;
+    default: GSB_SEL(3); break;
   }
+#undef GSB_SEL
+}
+
+// K2 with the per-class summary fused: CTA (x, p) owns the 256-cell tile x of profile p. It
+// compacts the tile's NON-EMPTY cells onto its first threads (ballot + warp-offset scan), so
+// the 81-clock loop runs with every lane busy; warps with nothing to evaluate (and not needed
+// by the summary tree) exit at once and free their slots for the next CTAs. Empty queues give
+// no command (prefill_opt.cpp:64) and cost no FP64 issue slots. Each cell's result goes to its
+// own slot, so the summary tree (summary_tile) is the one gsb_prefill_summary runs, bit for bit.
+template <int G>
+__global__ void __launch_bounds__(kSumCta, 5)
+k_prefill_select_sum(const __grid_constant__ SelectParams sp, const __grid_constant__ ClockSet<G> cs,
+                     const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
+                     const double* __restrict__ min_deadline, double* __restrict__ window,
+                     int16_t* __restrict__ f_idx, double* __restrict__ energy, SumArgs sa) {
+  __shared__ SumSmem sm;
+  __shared__ int s_slot[kSumCta];
+  __shared__ int s_wcnt[kSumCta / 32 + 1];
+  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
+  const int64_t n = sp.n_cells;
+  const int p = static_cast<int>(blockIdx.y), x = static_cast<int>(blockIdx.x);
+  const int64_t cell = static_cast<int64_t>(x) * kSumCta + t;
+  const bool live = cell < n;
+  const bool busy = live && (!count || count[cell] != 0);
+  if (live && !busy) {  // empty queue: no command
+    const int64_t o = p * n + cell;
+    f_idx[o] = -2;
+    energy[o] = 0.0;
+  }
+  sm.s1[t] = live ? part_of_cell(-2, 0.0, cell) : part_identity();
+  const unsigned b = __ballot_sync(kFull, busy);
+  if (lane == 0) s_wcnt[wib] = __popc(b);
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int w = 0; w < kSumCta / 32; ++w) {
+      const int c = s_wcnt[w];
+      s_wcnt[w] = run;
+      run += c;
+    }
+    s_wcnt[kSumCta / 32] = run;
+  }
+  __syncthreads();
+  if (busy) s_slot[s_wcnt[wib] + __popc(b & ((1u << lane) - 1u))] = t;
+  __syncthreads();
+  const int n_busy = s_wcnt[kSumCta / 32];
+  // warps past the compacted work and the summary tree's 8 x C threads leave now
+  if ((wib << 5) >= max(n_busy, 8 * sp.C)) return;
+  if (t < n_busy) {
+    const int slot = s_slot[t];
+    Part v;
+#define GSB_SEL(PI)                                                                            \
+  select_cells_c<G, PI, true>(sp, cs, t_ref, nullptr, min_deadline, window, f_idx, energy, &v, \
+                              static_cast<int64_t>(x) * kSumCta + slot, n)
+    switch (p) {
+      case 0: GSB_SEL(0); break;
+      case 1: GSB_SEL(1); break;
+      case 2: GSB_SEL(2); break;
+      default: GSB_SEL(3); break;
+    }
+#undef GSB_SEL
+    sm.s1[slot] = v;
+  }
+  __syncthreads();
+  summary_tile(sm, sp.C, sa, x, p, static_cast<int>(gridDim.x));
 }
 
 __global__ void __launch_bounds__(256)
@@ -732,92 +970,6 @@ __global__ void k_energy_batches(const ProfTab* __restrict__ tab, int64_t n_batc
   active[b] = a;
   idle[b] = d;
   total[b] = a + d;
-}
-
-// ---------------------------------------------------------------- per-class summary
-// Two fixed-shape levels => bitwise identical on every run and every rank:
-//   partial: block (pc, chunk) folds windows [chunk*kSumChunk, ...) of (profile, class) pc:
-//            thread t takes windows t, t+256, ... sequentially, then a shared-memory tree;
-//   final:   one block per pc combines the chunk partials with the same tree.
-constexpr int kSumChunk = 512;
-
-struct Part {
-  double sum, mn;
-  long long cmd, inf, emp, arg;
-};
-
-__device__ __forceinline__ void part_combine(Part& x, const Part& y) {
-  x.sum = x.sum + y.sum;
-  x.cmd += y.cmd;
-  x.inf += y.inf;
-  x.emp += y.emp;
-  if (y.arg >= 0 && (x.arg < 0 || y.mn < x.mn || (y.mn == x.mn && y.arg < x.arg))) {
-    x.mn = y.mn;
-    x.arg = y.arg;
-  }
-}
-
-__device__ __forceinline__ Part block_tree(Part v) {
-  __shared__ Part s[256];
-  const int t = threadIdx.x;
-  s[t] = v;
-  __syncthreads();
-  for (int k = 128; k > 0; k >>= 1) {
-    if (t < k) part_combine(s[t], s[t + k]);
-    __syncthreads();
-  }
-  return s[0];
-}
-
-__global__ void __launch_bounds__(256)
-k_summary_partial(int C, int64_t n_cells, const int16_t* __restrict__ f_idx,
-                  const double* __restrict__ energy, Part* __restrict__ parts, int n_chunks) {
-  const int pc = blockIdx.y, chunk = blockIdx.x;
-  const int p = pc / C, c = pc - (pc / C) * C;
-  const int64_t n_w = n_cells / C;
-  const int64_t w_lo = static_cast<int64_t>(chunk) * kSumChunk;
-  const int64_t w_hi = min(w_lo + kSumChunk, n_w);
-  Part v{0.0, INFINITY, 0, 0, 0, -1};
-  for (int64_t w = w_lo + threadIdx.x; w < w_hi; w += blockDim.x) {
-    const int64_t cell = w * C + c;
-    const int64_t o = p * n_cells + cell;
-    const int fi = f_idx[o];
-    if (fi == -2) {
-      ++v.emp;
-      continue;
-    }
-    ++v.cmd;
-    if (fi < 0) {
-      ++v.inf;
-      continue;
-    }
-    const double e = energy[o];
-    v.sum = v.sum + e;
-    if (e < v.mn) {
-      v.mn = e;
-      v.arg = cell;
-    }
-  }
-  const Part r = block_tree(v);
-  if (threadIdx.x == 0) parts[static_cast<int64_t>(pc) * n_chunks + chunk] = r;
-}
-
-__global__ void __launch_bounds__(256)
-k_summary_final(const Part* __restrict__ parts, int n_chunks, gsb_class_summary* __restrict__ out) {
-  const int pc = blockIdx.x;
-  Part v{0.0, INFINITY, 0, 0, 0, -1};
-  for (int k = threadIdx.x; k < n_chunks; k += blockDim.x) part_combine(v, parts[static_cast<int64_t>(pc) * n_chunks + k]);
-  const Part r = block_tree(v);
-  if (threadIdx.x == 0) {
-    gsb_class_summary o;
-    o.n_cmd = r.cmd;
-    o.n_infeasible = r.inf;
-    o.n_empty = r.emp;
-    o.sum_energy_j = r.sum;
-    o.min_energy_j = r.mn;
-    o.argmin_cell = r.arg;
-    out[pc] = o;
-  }
 }
 
 // ---------------------------------------------------------------- FP64 pipe probe
@@ -1084,16 +1236,24 @@ int gsb_fifo_order(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const 
   return gsb_check_launch(ctx, "fifo_order");
 }
 
-int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
-                       const double* d_t_ref, const uint32_t* d_count, const double* d_min_deadline,
-                       double* d_window, int16_t* d_f_idx, double* d_energy, void* stream) {
+int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                               const double* d_t_ref, const uint32_t* d_count,
+                               const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
+                               double* d_energy, gsb_class_summary* d_summary, void* stream) {
   if (!ctx || !cfg) return GSB_INVALID_ARGUMENT;
   if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: no profiles set");
   if (cfg->mode == GSB_DEADLINE_SLACK && (!d_min_deadline || cfg->n_classes < 1 || cfg->window_ms <= 0))
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: deadline mode needs min_deadline and layout");
   if (cfg->mode == GSB_PER_CELL_WINDOW && !d_window)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: per-cell mode needs d_window");
-  if (n_cells <= 0) return GSB_OK;
+  if (d_summary && (cfg->n_classes < 1 || cfg->n_classes > GSB_MAX_CLASSES || n_cells % cfg->n_classes))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: summary needs n_cells = windows x n_classes");
+  if (n_cells <= 0) {
+    if (d_summary)
+      return gsb_prefill_summary(ctx, ctx->n_profiles, cfg->n_classes, 0, d_f_idx, d_energy,
+                                 d_summary, stream);
+    return GSB_OK;
+  }
   SelectParams sp{};
   sp.mode = cfg->mode;
   sp.C = cfg->n_classes;
@@ -1125,9 +1285,24 @@ int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
       cs.P_min[p] = t.P_min;
       cs.P_max[p] = t.P_max;
     }
-    k_prefill_select_c<81><<<dim3(gx, static_cast<unsigned>(ctx->n_profiles)), 256, 0, s>>>(
-        sp, cs, d_t_ref, d_count, d_min_deadline, d_window, d_f_idx, d_energy);
-    return gsb_check_launch(ctx, "prefill_select");
+    const dim3 grid(gx, static_cast<unsigned>(ctx->n_profiles));
+    const int64_t tiles = want * ctx->n_profiles;
+    if (d_summary && want == static_cast<int64_t>(gx)) {  // one CTA per 256-cell tile
+      SumArgs sa{static_cast<Part*>(gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(tiles) *
+                                                         static_cast<size_t>(cfg->n_classes)))};
+      if (!sa.parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "select: scratch allocation failed");
+      k_prefill_select_sum<81><<<grid, kSumCta, 0, s>>>(sp, cs, d_t_ref, d_count, d_min_deadline,
+                                                         d_window, d_f_idx, d_energy, sa);
+      k_summary_final<<<static_cast<unsigned>(ctx->n_profiles * cfg->n_classes), 32, 0, s>>>(
+          sa.parts, static_cast<int>(want), d_summary);
+      return gsb_check_launch(ctx, "prefill_select");
+    }
+    k_prefill_select_c<81><<<grid, 256, 0, s>>>(sp, cs, d_t_ref, d_count, d_min_deadline,
+                                                d_window, d_f_idx, d_energy);
+    const int rc = gsb_check_launch(ctx, "prefill_select");
+    if (rc || !d_summary) return rc;
+    return gsb_prefill_summary(ctx, ctx->n_profiles, cfg->n_classes, n_cells, d_f_idx, d_energy,
+                               d_summary, stream);
   }
   for (int p = 0; p < ctx->n_profiles; ++p) {
     {
@@ -1138,8 +1313,19 @@ int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
     const int rc = gsb_check_launch(ctx, "prefill_select");
     if (rc) return rc;
   }
-  return GSB_OK;
+  if (!d_summary) return GSB_OK;
+  return gsb_prefill_summary(ctx, ctx->n_profiles, cfg->n_classes, n_cells, d_f_idx, d_energy,
+                             d_summary, stream);
 }
+
+int gsb_prefill_select(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                       const double* d_t_ref, const uint32_t* d_count, const double* d_min_deadline,
+                       double* d_window, int16_t* d_f_idx, double* d_energy, void* stream) {
+  return gsb_prefill_select_summary(ctx, cfg, n_cells, d_t_ref, d_count, d_min_deadline, d_window,
+                                    d_f_idx, d_energy, nullptr, stream);
+}
+
+
 
 int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int64_t n_batches,
                        const int64_t* d_off, const int32_t* d_prompt, const double* d_wf,
@@ -1182,17 +1368,19 @@ int gsb_energy_batches(gsb_ctx* ctx, int profile, int64_t n_batches, const int64
 int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_cells,
                         const int16_t* d_f_idx, const double* d_energy, gsb_class_summary* d_out,
                         void* stream) {
-  if (!ctx || n_profiles < 1 || n_classes < 1 || n_cells % n_classes)
+  if (!ctx || n_profiles < 1 || n_profiles > GSB_MAX_PROFILES || n_classes < 1 ||
+      n_classes > GSB_MAX_CLASSES || n_cells < 0 || n_cells % n_classes)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: bad shape");
-  const int64_t n_w = n_cells / n_classes;
-  const int n_chunks = static_cast<int>(std::max<int64_t>(1, (n_w + kSumChunk - 1) / kSumChunk));
-  Part* parts = static_cast<Part*>(
-      gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(n_chunks) * n_profiles * n_classes));
-  if (!parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "summary: scratch allocation failed");
+  const int64_t gx = std::max<int64_t>(1, (n_cells + kSumCta - 1) / kSumCta);
+  if (gx > 65535LL * 16) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: too many cells");
+  SumArgs sa{static_cast<Part*>(gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(gx) *
+                                                     n_profiles * n_classes))};
+  if (!sa.parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "summary: scratch allocation failed");
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  k_summary_partial<<<dim3(static_cast<unsigned>(n_chunks), static_cast<unsigned>(n_profiles * n_classes)),
-                      256, 0, s>>>(n_classes, n_cells, d_f_idx, d_energy, parts, n_chunks);
-  k_summary_final<<<static_cast<unsigned>(n_profiles * n_classes), 256, 0, s>>>(parts, n_chunks, d_out);
+  k_summary<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(n_profiles)), kSumCta, 0, s>>>(
+      n_classes, n_cells, d_f_idx, d_energy, sa);
+  k_summary_final<<<static_cast<unsigned>(n_profiles * n_classes), 32, 0, s>>>(
+      sa.parts, static_cast<int>(gx), d_out);
   return gsb_check_launch(ctx, "prefill_summary");
 }
 

@@ -460,6 +460,47 @@ def test_decode_replay_reproduces_reference_closed_loop_run(eng, ref, prof):
         assert (got == want).all()
 
 
+@pytest.mark.parametrize("thr", [[512, 1024], [256, 512, 1024, 2048],
+                                 [128, 256, 512, 768, 1024, 2048, 4096]])
+def test_fused_select_summary_equals_standalone(eng, restate, thr):
+    """gsb_prefill_select_summary (K2 + the per-class reduction in one launch) gives the same
+    per-cell decisions as gsb_prefill_select and the same summary BYTES as
+    gsb_prefill_summary; counts / min are exact against a host recount."""
+    api = _api()
+    profs = synth_profiles(api)
+    eng.set_profiles(profs)
+    C = len(thr) + 1
+    a, p, _ = restate.gen_poisson_trace(5.0, 5_400_000, seed=21)
+    rr = eng.route_bin(a, p, api.RoutingConfig(True, thr, list(range(C))), 45_000)
+    ref = eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=0.95 * 45_000)
+    summ = eng.summary_buffer(C)
+    for _ in range(3):  # repeated launches agree
+        sel = eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=0.95 * 45_000,
+                                 summary_out=summ)
+        fused = summ.cpu().numpy().view(eng.SUMMARY_DTYPE).reshape(len(profs), C)
+        assert torch.equal(sel.f_idx, ref.f_idx)
+        assert torch.equal(sel.energy_j.view(torch.int64), ref.energy_j.view(torch.int64))
+        std = eng.prefill_summary(sel, C)
+        assert fused.tobytes() == std.tobytes()
+    fi = sel.f_idx.cpu().numpy()
+    en = sel.energy_j.cpu().numpy()
+    for pi in range(len(profs)):
+        f2, e2 = fi[pi].reshape(-1, C), en[pi].reshape(-1, C)
+        for c in range(C):
+            s = fused[pi, c]
+            assert s["n_empty"] == (f2[:, c] == -2).sum()
+            assert s["n_cmd"] == (f2[:, c] != -2).sum()
+            assert s["n_infeasible"] == (f2[:, c] == -1).sum()
+            ok = f2[:, c] >= 0
+            if ok.any():
+                e = e2[ok, c]
+                assert abs(s["sum_energy_j"] - e.sum()) <= 1e-11 * abs(e.sum())
+                k = int(np.argmin(np.where(ok, e2[:, c], np.inf)))
+                assert s["min_energy_j"] == e2[k, c] and s["argmin_cell"] == k * C + c
+            else:
+                assert s["argmin_cell"] == -1
+
+
 def test_summary_is_deterministic_and_exact_counts(eng, restate):
     api = _api()
     eng.set_profiles([api.GpuProfile.default_profile()])
