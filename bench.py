@@ -385,7 +385,10 @@ def run_gsb(args, rank, world, dist):
                          if k.startswith("k_route_bin") or k.startswith("k_window_bounds")) or None
     except (IndexError, OSError, ValueError, KeyError):
         pass
-    k2_tflops = evals * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
+    # executed K2 work: only non-empty (cell, profile) pairs run the 81-clock loop (empty
+    # queues give no command, prefill_opt.cpp:64, and are compacted away inside K2)
+    evaluated = int(per_rank[rank]["n_cmd"].sum()) * 81
+    k2_tflops = evaluated * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
     peak_tflops = dfma_per_s * 2 / 1e12
     k1_gbs = n_req * K1_BYTES_PER_REQ / (k1_ms / 1e3) / 1e9
     # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
@@ -403,7 +406,13 @@ def run_gsb(args, rank, world, dist):
         "data": "synthetic (reference-shaped Poisson/bimodal traces; sinusoidal decode telemetry)",
         "config": {"workload": W["name"], "windows_per_gpu": nW, "window_ms": wms,
                    "classes": W["C"], "profiles": P, "clocks": 81, "requests_per_gpu": n_req,
-                   "evals_per_step_per_gpu": evals, "window_mode": "FIXED_WINDOW D=0.95*W",
+                   "evals_per_step_per_gpu": evals,
+                   "evaluated_evals_per_step_per_gpu": evaluated,
+                   "value_counts": "every (window, class, profile, clock) triple of the grid is "
+                                   "decided each step; empty cells are decided as 'no command' "
+                                   "without evaluation (prefill_opt.cpp:64); the roofline counts "
+                                   "only the evaluated triples",
+                   "window_mode": "FIXED_WINDOW D=0.95*W",
                    "decode_scenarios_per_gpu": sweep.n_scenarios, "decode_horizon_ms": T_END,
                    "parallelism": f"dp{world} (windows/scenarios sharded, NCCL all-gather of "
                                   f"per-class summaries)",
@@ -429,8 +438,10 @@ def run_gsb(args, rank, world, dist):
         "roofline": {"bound": "fp64", "kernel": "k_prefill_select (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,
-                     "basis": f"{K2_DP_OPS_PER_EVAL} DP-pipe instr/eval x 2 (DFMA-equivalent) vs "
-                              "DFMA throughput measured in this run (gsb_fp64_probe)",
+                     "basis": f"{K2_DP_OPS_PER_EVAL} DP-pipe instr per EVALUATED (non-empty "
+                              "cell, profile, clock) x 2 (DFMA-equivalent) vs DFMA throughput "
+                              "measured in this run (gsb_fp64_probe); kernel time includes the "
+                              "fused per-class summary and its final combine",
                      "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre, "traffic": traffic_k2,
                      "traffic_note": "dram__bytes_read+write per launch, profiles/ ncu capture"},
         "roofline_k1": {"bound": "hbm", "kernel": "k_route_bin (K1)", "achieved": k1_gbs,

@@ -259,6 +259,52 @@ int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t 
                                const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
                                double* d_energy, gsb_class_summary* d_summary, void* stream);
 
+/* ---------------------------------------------------------------- K6: trace CSV ingest */
+/* greensim::TraceError::Kind (trace.hpp:36-40), in the reference's enum order */
+enum {
+  GSB_TRACE_KIND_EMPTY = 0, GSB_TRACE_KIND_NON_MONOTONE = 1, GSB_TRACE_KIND_MALFORMED = 2,
+  GSB_TRACE_KIND_BAD_HEADER = 3, GSB_TRACE_KIND_CLASS_MISMATCH = 4, GSB_TRACE_KIND_BAD_SHAPE = 5
+};
+/* which load_trace check failed, in the reference's order (trace.cpp:80-127) */
+enum {
+  GSB_TRACE_DETAIL_NONE = 0, GSB_TRACE_DETAIL_COLUMNS = 1, GSB_TRACE_DETAIL_ARRIVAL = 2,
+  GSB_TRACE_DETAIL_PROMPT = 3, GSB_TRACE_DETAIL_OUTPUT = 4, GSB_TRACE_DETAIL_RANGE = 5,
+  GSB_TRACE_DETAIL_MONOTONE = 6, GSB_TRACE_DETAIL_CLASS = 7, GSB_TRACE_DETAIL_MISMATCH = 8
+};
+typedef struct gsb_trace_parse_result {
+  int32_t status;         /* GSB_OK or GSB_TRACE_ERROR */
+  int32_t kind;           /* GSB_TRACE_KIND_* when status == GSB_TRACE_ERROR */
+  int32_t detail;         /* GSB_TRACE_DETAIL_* */
+  int32_t has_class;      /* the header carried the class column */
+  int32_t n_cols;         /* columns of the failing row */
+  int32_t line_len;       /* bytes of line[] */
+  int32_t line_truncated; /* the failing line was longer than line[] */
+  int32_t pad_;
+  int64_t row;            /* the reference's 1-based row counter of the failing line (-1: none) */
+  int64_t n_rows;         /* requests parsed */
+  int64_t max_arrival_ms; /* last (= largest) arrival; Trace::meta.duration_ms = max(0, this) */
+  char line[1024];        /* the failing line after the '\r' strip (NUL-terminated) */
+} gsb_trace_parse_result;
+
+/* greensim::load_trace (trace.cpp:56-129) over a CSV image already in device memory:
+ * "arrival_ms,prompt_tokens,output_tokens[,class]" -> SoA (arrival i64, prompt i32, output i32,
+ * SLO class u8: 0 = SM iff prompt <= class_threshold, 1 = L; trace.cpp:32-34). Request ids are
+ * the row indices. Synchronous (the row count is returned in *res). Errors mirror TraceError:
+ * GSB_TRACE_ERROR with res->kind / res->row and gsb_last_error() = the reference's message;
+ * the earliest failing row wins, and within a row the reference's check order. Outputs need
+ * cap_rows entries; more rows -> GSB_INVALID_ARGUMENT with res->n_rows = the count needed.
+ * n_bytes < 4 GiB. */
+int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t class_threshold,
+                    int64_t cap_rows, int64_t* d_arrival, int32_t* d_prompt, int32_t* d_output,
+                    uint8_t* d_slo_class, gsb_trace_parse_result* res, void* stream);
+
+/* greensim::save_trace_csv (trace.cpp:131-145) into device memory: header (with ",class" iff
+ * d_slo_class != NULL, i.e. every request carries a class) + one row per request, '\n'
+ * line ends, integers as ostream prints them. d_out == NULL: size query. *h_bytes = bytes. */
+int gsb_trace_format(gsb_ctx* ctx, int64_t n, const int64_t* d_arrival, const int32_t* d_prompt,
+                     const int32_t* d_output, const uint8_t* d_slo_class, char* d_out,
+                     int64_t cap_bytes, int64_t* h_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K3/K4: decode control */
 /* Raw decode telemetry of S streams (one decode worker each), CSR layout:
  * events of stream s are [d_ev_off[s], d_ev_off[s+1]) sorted by time; event j emitted

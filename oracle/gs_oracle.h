@@ -259,6 +259,24 @@ void gso_pool_summary_from(const gso_slo* slo, int64_t n, const double* arrival,
                            const double* tl_f, double sim_end_ms, int64_t n_steps,
                            gso_pool_summary* out);
 
+/* ---- trace CSV (gs_trace.c): load_trace / save_trace_csv (trace.cpp:56-145) */
+enum { /* greensim::TraceError::Kind order (trace.hpp:36-40) */
+  GSO_TRACE_EMPTY = 0, GSO_TRACE_NON_MONOTONE = 1, GSO_TRACE_MALFORMED = 2,
+  GSO_TRACE_BAD_HEADER = 3, GSO_TRACE_CLASS_MISMATCH = 4
+};
+typedef struct gso_trace_err {
+  int32_t kind, detail; /* detail: 1 columns, 2-4 bad field, 5 range, 6 monotone, 7 class, 8 mismatch */
+  int64_t row;          /* 1-based row counter of the failing line, -1 if none */
+  char msg[8192];       /* the reference's TraceError message */
+} gso_trace_err;
+/* rows parsed (the first min(rows, cap) are stored), or -1 with *err */
+int64_t gso_trace_parse(const char* bytes, int64_t n, int32_t class_threshold, int64_t cap,
+                        int64_t* arrival, int32_t* prompt, int32_t* output, uint8_t* slo_cls,
+                        int32_t* has_class, gso_trace_err* err);
+/* the CSV text (written when out has room); returns its byte count */
+int64_t gso_trace_format(int64_t n, const int64_t* arrival, const int32_t* prompt,
+                         const int32_t* output, const uint8_t* slo_cls, char* out, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

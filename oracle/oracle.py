@@ -82,6 +82,14 @@ class Slo(C.Structure):
     _fields_ = [("ttft_sm_ms", _d), ("ttft_l_ms", _d), ("tbt_p95_ms", _d)]
 
 
+TRACE_KINDS = ("EmptyTrace", "NonMonotoneArrivals", "MalformedRow", "BadHeader",
+               "ClassMismatch", "BadShape")  # greensim::TraceError::Kind order
+
+
+class TraceErr(C.Structure):
+    _fields_ = [("kind", _i32), ("detail", _i32), ("row", _i64), ("msg", C.c_char * 8192)]
+
+
 class Policy(C.Structure):
     """gso_policy == greensim::GovernorPolicy (simkernel.hpp:26-45)."""
 
@@ -303,9 +311,42 @@ class Restatement:
                      ("timeline", 4), ("commands", 6), ("enqueue", 2), ("scalars", 1)):
             getattr(L, "gso_sim_" + f).argtypes = [_p] + [_p] * k
         L.gso_sim_summary.argtypes = [_p, C.POINTER(Slo), C.POINTER(PoolSummary)]
+        L.gso_trace_parse.argtypes = [C.c_char_p, _i64, _i32, _i64, _p, _p, _p, _p, _p,
+                                      C.POINTER(TraceErr)]
+        L.gso_trace_parse.restype = _i64
+        L.gso_trace_format.argtypes = [_i64, _p, _p, _p, _p, _p, _i64]
+        L.gso_trace_format.restype = _i64
         L.gso_pool_summary_from.argtypes = ([C.POINTER(Slo), _i64] + [_p] * 10 + [C.c_int, _p, _i64,
                                             _p, _i64, _p, _p, _p, _p, _d, _i64,
                                             C.POINTER(PoolSummary)])
+
+    # ---- trace CSV (load_trace / save_trace_csv, trace.cpp:56-145) ----
+    def trace_parse(self, data: bytes, class_threshold: int = 1024):
+        """(arrival, prompt, output, slo_class, has_class) or a TRACE_ERROR tuple
+        ("error", kind name, row, message)."""
+        cap = max(1, len(data) // 2 + 2)
+        a = np.zeros(cap, np.int64)
+        p = np.zeros(cap, np.int32)
+        o = np.zeros(cap, np.int32)
+        c = np.zeros(cap, np.uint8)
+        hc = np.zeros(1, np.int32)
+        err = TraceErr()
+        n = self.lib.gso_trace_parse(data, len(data), class_threshold, cap, ptr(a), ptr(p), ptr(o),
+                                     ptr(c), ptr(hc), C.byref(err))
+        if n < 0:
+            return ("error", TRACE_KINDS[err.kind], err.row if err.row > 0 else None,
+                    err.msg.decode(errors="replace"))
+        return a[:n], p[:n], o[:n], c[:n], bool(hc[0])
+
+    def trace_format(self, a, p, o, cls=None) -> bytes:
+        a = np.ascontiguousarray(a, np.int64)
+        p = np.ascontiguousarray(p, np.int32)
+        o = np.ascontiguousarray(o, np.int32)
+        c = None if cls is None else np.ascontiguousarray(cls, np.uint8)
+        nb = self.lib.gso_trace_format(len(a), ptr(a), ptr(p), ptr(o), ptr(c), None, 0)
+        buf = C.create_string_buffer(nb)
+        self.lib.gso_trace_format(len(a), ptr(a), ptr(p), ptr(o), ptr(c), C.cast(buf, _p), nb)
+        return buf.raw[:nb]
 
     # ---- prefill ----
     def grid(self, prof: Profile) -> np.ndarray:
@@ -776,6 +817,49 @@ class Reference:
                                  prof.f_max_mhz, prof.step_mhz, prof.f_ref_mhz, t_end, threads,
                                  ptr(nrec), ptr(dig))
         return nrec, dig
+
+    def load_trace(self, path: str, class_threshold: int = 1024):
+        """greensim::load_trace itself: same return convention as Restatement.trace_parse
+        (without has_class)."""
+        L = self.lib
+        L.ref_load_trace.argtypes = [C.c_char_p, _i32, _i64, _p, _p, _p, _p, _p, C.c_char_p, _i64]
+        L.ref_load_trace.restype = _i64
+        cap = max(1, os.path.getsize(path) // 2 + 2)
+        a = np.zeros(cap, np.int64)
+        p = np.zeros(cap, np.int32)
+        o = np.zeros(cap, np.int32)
+        c = np.zeros(cap, np.uint8)
+        kind = np.zeros(1, np.int32)
+        msg = C.create_string_buffer(16384)
+        n = L.ref_load_trace(path.encode(), class_threshold, cap, ptr(a), ptr(p), ptr(o), ptr(c),
+                             ptr(kind), msg, 16384)
+        if n < 0:
+            m = msg.value.decode(errors="replace")
+            row = None
+            if m.startswith("row "):
+                row = int(m[4:m.index(":")])
+            elif TRACE_KINDS[kind[0]] == "BadHeader":
+                row = 1
+            return ("error", TRACE_KINDS[kind[0]], row, m)
+        return a[:n], p[:n], o[:n], c[:n]
+
+    def save_trace_csv(self, path: str, a, p, o, cls=None) -> bytes:
+        """greensim::save_trace_csv, run by oracle/_ref/ref_save_trace in its own process."""
+        import subprocess
+        a = np.ascontiguousarray(a, np.int64)
+        n = len(a)
+        blob = (np.int64(n).tobytes() + a.tobytes() + np.ascontiguousarray(p, np.int32).tobytes()
+                + np.ascontiguousarray(o, np.int32).tobytes()
+                + bytes([0 if cls is None else 1])
+                + (np.zeros(n, np.uint8) if cls is None
+                   else np.ascontiguousarray(cls, np.uint8)).tobytes())
+        with open(path + ".soa", "wb") as f:
+            f.write(blob)
+        subprocess.run([os.path.join(os.path.dirname(REF_SO), "ref_save_trace"), path + ".soa",
+                        path], check=True)
+        os.remove(path + ".soa")
+        with open(path, "rb") as f:
+            return f.read()
 
     def digest(self, recs):
         recs = np.ascontiguousarray(recs, DECISION_DTYPE)

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "greensim/decode_ctl.hpp"
+#include "greensim/trace.hpp"
 #include "greensim/gpu_model.hpp"
 #include "greensim/metrics.hpp"
 #include "greensim/prefill_opt.hpp"
@@ -960,6 +961,30 @@ void ref_sim_run_many(const gso_profile* prof, const gso_policy* base, const gso
   for (int t = 0; t < threads; ++t)
     pool.emplace_back(work, n_scen * t / threads, n_scen * (t + 1) / threads);
   for (auto& th : pool) th.join();
+}
+
+// greensim::load_trace on a file (trace.cpp:56-129): rows or -1 with the TraceError kind and
+// message. has_class_col: 1 iff the header carried the class column (every row then has cls).
+int64_t ref_load_trace(const char* path, int32_t thr, int64_t cap, int64_t* arrival,
+                       int32_t* prompt, int32_t* output, uint8_t* cls, int32_t* kind, char* msg,
+                       int64_t msg_cap) {
+  try {
+    const Trace t = load_trace(path, thr);
+    const int64_t n = static_cast<int64_t>(t.requests.size());
+    for (int64_t i = 0; i < n && i < cap; ++i) {
+      const Request& r = t.requests[static_cast<size_t>(i)];
+      arrival[i] = r.arrival_ms;
+      prompt[i] = r.prompt_tokens;
+      output[i] = r.output_tokens;
+      cls[i] = r.cls ? static_cast<uint8_t>(*r.cls) : 255;
+    }
+    *kind = -1;
+    return n;
+  } catch (const TraceError& e) {
+    *kind = static_cast<int32_t>(e.kind);
+    snprintf(msg, static_cast<size_t>(msg_cap), "%s", e.what());
+    return -1;
+  }
 }
 
 }  // extern "C"

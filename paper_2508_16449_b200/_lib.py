@@ -20,6 +20,17 @@ OK, MODEL_ERROR, ROUTER_ERROR, TRACE_ERROR, CUDA_ERROR, INVALID_ARGUMENT = range
 FIXED_WINDOW, DEADLINE_SLACK, PER_CELL_WINDOW = range(3)
 
 
+TRACE_KINDS = ("EmptyTrace", "NonMonotoneArrivals", "MalformedRow", "BadHeader",
+               "ClassMismatch", "BadShape")  # greensim::TraceError::Kind order
+
+
+class CTraceResult(C.Structure):
+    _fields_ = [("status", _i32), ("kind", _i32), ("detail", _i32), ("has_class", _i32),
+                ("n_cols", _i32), ("line_len", _i32), ("line_truncated", _i32), ("pad_", _i32),
+                ("row", _i64), ("n_rows", _i64), ("max_arrival_ms", _i64),
+                ("line", C.c_char * 1024)]
+
+
 class CProfile(C.Structure):
     _fields_ = [(n, _d) for n in (
         "f_min_mhz", "f_max_mhz", "step_mhz", "f_ref_mhz",
@@ -121,6 +132,7 @@ EXPORTS = (
     "gsb_memcpy", "gsb_classify",
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
+    "gsb_trace_parse", "gsb_trace_format",
 )
 
 _lib = None
@@ -184,6 +196,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_t_ref_batches.argtypes = [_p, P(_d), _i64, _p, _p, _p, _p, _p]
     L.gsb_energy_closed_form_batches.argtypes = [_p, C.c_int, _i64, _p, _p, _p, _p, _p, _p, _p]
     L.gsb_decode_pool_tps_cap.argtypes = [P(CProfile), _i32, _d]
+    L.gsb_trace_parse.argtypes = [_p, _p, _i64, _i32, _i64, _p, _p, _p, _p, P(CTraceResult), _p]
+    L.gsb_trace_format.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _i64, P(_i64), _p]
     L.gsb_decode_pool.argtypes = [_p, P(CProfile), P(CPoolCfg), P(CPoolStream), P(CPoolArgs), _p]
     _lib = L
     return L

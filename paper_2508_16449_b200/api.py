@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes as C
 import json
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, Optional, Sequence
 
@@ -36,7 +37,13 @@ class RouterError(RuntimeError):
 
 
 class TraceError(RuntimeError):
-    """greensim::TraceError (trace.hpp:36-40)."""
+    """greensim::TraceError (trace.hpp:36-40); `kind` is the TraceError::Kind name and `row`
+    the reference's 1-based row counter of the failing line (None when not row-bound)."""
+
+    def __init__(self, msg: str, kind: Optional[str] = None, row: Optional[int] = None):
+        super().__init__(msg)
+        self.kind = kind
+        self.row = row
 
 
 class CudaError(RuntimeError):
@@ -442,6 +449,20 @@ def _ptr(t) -> Optional[int]:
     raise TypeError(type(t))
 
 
+@dataclass
+class TraceArrays:
+    """A request trace on the device (greensim::Trace, trace.hpp:16-33) as SoA; request ids are
+    the row indices; slo_class 0 = SM, 1 = L (classify_by_threshold, trace.cpp:32-34)."""
+    arrival_ms: torch.Tensor
+    prompt_tokens: torch.Tensor
+    output_tokens: torch.Tensor
+    slo_class: torch.Tensor
+    has_class_column: bool
+    name: str
+    duration_ms: int
+    nominal_qps: float
+
+
 class Engine:
     """One libgsb context on one CUDA device (single owner, like the reference's objects)."""
 
@@ -548,6 +569,74 @@ class Engine:
                                                 _ptr(out.bounds), _ptr(out.count),
                                                 _ptr(out.cell_off), _ptr(out.fifo), s))
         return out
+
+    # ---------------------------------------------------------------- K6: trace CSV
+    def parse_trace(self, data, class_threshold: int = 1024, name: str = "trace") -> "TraceArrays":
+        """greensim::load_trace (trace.cpp:56-129) of a CSV image (bytes, a uint8 numpy array
+        or a uint8 tensor, host or device) on the GPU. Raises TraceError(kind, row) with the
+        reference's message."""
+        if isinstance(data, (bytes, bytearray, memoryview)):
+            host = torch.frombuffer(bytearray(data), dtype=torch.uint8) if len(data) else \
+                torch.empty(0, dtype=torch.uint8)
+            dev = host.pin_memory().to(self.device, non_blocking=True) if host.numel() else \
+                self._empty(0, torch.uint8)
+        else:
+            dev = self._dev(data, torch.uint8)
+        n = int(dev.numel())
+        # a valid row holds >= 6 bytes ("0,1,1\n"); a malformed file may need more rows: the
+        # call then reports the count and is repeated with room for it
+        cap = max(1, n // 6 + 1)
+        for _ in range(2):
+            arr = self._empty(cap, torch.int64)
+            prm = self._empty(cap, torch.int32)
+            out = self._empty(cap, torch.int32)
+            cls = self._empty(cap, torch.uint8)
+            res = L.CTraceResult()
+            rc = self.lib.gsb_trace_parse(self.ctx, _ptr(dev) if n else None, n,
+                                          int(class_threshold), cap, _ptr(arr), _ptr(prm),
+                                          _ptr(out), _ptr(cls), C.byref(res), self.stream())
+            if rc == L.INVALID_ARGUMENT and res.n_rows > cap:
+                cap = int(res.n_rows)
+                continue
+            break
+        if rc == L.TRACE_ERROR:
+            raise TraceError(self.lib.gsb_last_error(self.ctx).decode(errors="replace"),
+                             L.TRACE_KINDS[res.kind], res.row if res.row > 0 else None)
+        self._check(rc)
+        k = int(res.n_rows)
+        dur = max(0, int(res.max_arrival_ms))  # finalize_meta (trace.cpp:36-45)
+        return TraceArrays(arr[:k], prm[:k], out[:k], cls[:k], bool(res.has_class), name, dur,
+                           1000.0 * k / dur if dur > 0 else 0.0)
+
+    def load_trace(self, path, class_threshold: int = 1024) -> "TraceArrays":
+        """load_trace(path, class_threshold): file bytes -> GPU parse (meta.name = the stem)."""
+        try:
+            with open(path, "rb") as f:
+                data = f.read()
+        except OSError:
+            raise TraceError(f"cannot open trace file: {path}", "MalformedRow") from None
+        return self.parse_trace(data, class_threshold, os.path.splitext(os.path.basename(path))[0])
+
+    def format_trace(self, arrival, prompt, output, slo_class=None) -> bytes:
+        """save_trace_csv's text (trace.cpp:131-145) rendered on the GPU; the class column is
+        written iff slo_class is given (every request carries a class)."""
+        a = self._dev(arrival, torch.int64)
+        p = self._dev(prompt, torch.int32)
+        o = self._dev(output, torch.int32)
+        c = None if slo_class is None else self._dev(slo_class, torch.uint8)
+        n = int(a.numel())
+        nb = C.c_int64(0)
+        self._check(self.lib.gsb_trace_format(self.ctx, n, _ptr(a), _ptr(p), _ptr(o), _ptr(c),
+                                              None, 0, C.byref(nb), self.stream()))
+        buf = self._empty(int(nb.value), torch.uint8)
+        self._check(self.lib.gsb_trace_format(self.ctx, n, _ptr(a), _ptr(p), _ptr(o), _ptr(c),
+                                              _ptr(buf), int(nb.value), C.byref(nb), self.stream()))
+        return bytes(buf.cpu().numpy().tobytes())
+
+    def save_trace_csv(self, tr: "TraceArrays", path) -> None:
+        with open(path, "wb") as f:
+            f.write(self.format_trace(tr.arrival_ms, tr.prompt_tokens, tr.output_tokens,
+                                      tr.slo_class))
 
     # ---------------------------------------------------------------- K2
     def prefill_select(self, rr: RouteResult, mode: int = L.FIXED_WINDOW,

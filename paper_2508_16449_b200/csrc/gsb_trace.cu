@@ -1,0 +1,568 @@
+// gsb_trace.cu — K6: trace CSV ingest and output.
+//
+// gsb_trace_parse replaces greensim::load_trace (trace.cpp:56-129): the request CSV
+// "arrival_ms,prompt_tokens,output_tokens[,class]" becomes the SoA the router/binner (K1)
+// reads, with the reference's row semantics and its first-error-wins TraceError behaviour.
+// gsb_trace_format replaces save_trace_csv (trace.cpp:131-145).
+//
+// Line model (std::getline on an ifstream, trace.cpp:60-78): a line ends at each '\n' and,
+// when the file does not end with '\n', at the end of the file; one trailing '\r' is
+// stripped; line 0 is the header; later empty lines are skipped but still counted by the
+// reference's row counter (row = line index + 1).
+//
+// Passes (HBM-resident bytes, 4 KB tiles of 256 threads x 16 bytes):
+//   1. k_csv_count:  per tile, line ends and non-empty lines (a line is attributed to the tile
+//      holding its end), and the first end (the header's);
+//   2. CUB exclusive scan of the packed (ends << 32 | non-empty) tile counts;
+//   3. k_csv_parse:  per tile, the block-wide rank of each line end gives its line index and
+//      output row; one thread parses one line (field split, from_chars restatement, range and
+//      class checks) and writes arrival/prompt/output/SLO class at its row; errors are folded
+//      into one 64-bit atomicMin key (row << 4 | check), so the earliest row wins and, within
+//      a row, the reference's check order;
+//   4. k_csv_monotone: arrival[r] < arrival[r-1] (trace.cpp:108-111) keyed by r's row.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "gsb_common.cuh"
+
+namespace {
+
+constexpr int kTile = 4096;
+constexpr int kTrThreads = 256;  // x 16 bytes = one tile
+constexpr int kPre = 256;        // bytes staged before the tile (line starts)
+constexpr unsigned long long kNoErr = ~0ull;
+
+struct TraceParams {
+  const unsigned char* bytes;
+  int64_t n;
+  int64_t n_tiles;
+  int64_t header_end;  // position of line 0's end
+  int32_t has_class;
+  int32_t threshold;
+};
+
+__device__ __forceinline__ unsigned char byte_at(const unsigned char* __restrict__ b, int64_t n,
+                                                 int64_t i) {
+  return (i >= 0 && i < n) ? __ldg(b + i) : static_cast<unsigned char>(0);
+}
+
+// a line ends at b: a '\n' byte, or the end of a file whose last byte is not '\n'
+__device__ __forceinline__ bool is_end(const unsigned char* s, int64_t s0, int64_t n, int64_t b,
+                                       bool last_is_nl) {
+  if (b < n) return s[b - s0] == '\n';
+  return b == n && n > 0 && !last_is_nl;
+}
+
+// the line ending at b is empty after the '\r' strip
+__device__ __forceinline__ bool empty_line(const unsigned char* s, int64_t s0, int64_t b) {
+  if (b == 0) return true;
+  const unsigned char c1 = s[b - 1 - s0];
+  if (c1 == '\n') return true;
+  if (c1 == '\r') return b - 1 == 0 || s[b - 2 - s0] == '\n';
+  return false;
+}
+
+// stage [t*kTile - kPre, (t+1)*kTile) (bytes outside the file read as 0)
+__device__ __forceinline__ void stage_tile(const TraceParams& tp, int64_t t, unsigned char* sm) {
+  const int64_t s0 = t * kTile - kPre;
+  for (int i = threadIdx.x; i < (kTile + kPre) / 16; i += kTrThreads) {
+    const int64_t g = s0 + 16 * static_cast<int64_t>(i);
+    uint4 v;
+    if (g >= 0 && g + 16 <= tp.n && (reinterpret_cast<uintptr_t>(tp.bytes + g) & 15) == 0) {
+      v = __ldg(reinterpret_cast<const uint4*>(tp.bytes + g));
+    } else {
+      unsigned char q[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) q[k] = byte_at(tp.bytes, tp.n, g + k);
+      memcpy(&v, q, 16);
+    }
+    *reinterpret_cast<uint4*>(sm + 16 * i) = v;
+  }
+}
+
+struct MinU64 {
+  __device__ __forceinline__ unsigned long long operator()(unsigned long long a,
+                                                           unsigned long long b) const {
+    return a < b ? a : b;
+  }
+};
+
+__global__ void __launch_bounds__(kTrThreads)
+k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt,
+            unsigned long long* __restrict__ first_end) {
+  __shared__ __align__(16) unsigned char sm[kTile + kPre];
+  using BR = cub::BlockReduce<unsigned long long, kTrThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const int64_t t = blockIdx.x;
+  stage_tile(tp, t, sm);
+  __syncthreads();
+  const int64_t s0 = t * kTile - kPre;
+  const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
+  unsigned nl = 0, ne = 0;
+  int64_t first = INT64_MAX;
+  const int64_t b0 = t * kTile + 16 * threadIdx.x;
+#pragma unroll 4
+  for (int k = 0; k < 16; ++k) {
+    const int64_t b = b0 + k;
+    if (b > tp.n) break;
+    if (is_end(sm, s0, tp.n, b, last_is_nl)) {
+      ++nl;
+      ne += empty_line(sm, s0, b) ? 0u : 1u;
+      first = min(first, b);
+    }
+  }
+  const unsigned long long packed =
+      (static_cast<unsigned long long>(nl) << 32) | static_cast<unsigned long long>(ne);
+  const unsigned long long tot = BR(tmp).Sum(packed);
+  __syncthreads();
+  const unsigned long long fmin = BR(tmp).Reduce(static_cast<unsigned long long>(first),
+                                                 MinU64{});
+  if (threadIdx.x == 0) {
+    tile_cnt[t] = tot;
+    if (fmin != static_cast<unsigned long long>(INT64_MAX)) atomicMin(first_end, fmin);
+  }
+}
+
+// std::from_chars<int64_t> over [p, p+len): optional '-', >= 1 digits, whole field, no
+// overflow (trace.cpp:84-91)
+__device__ __forceinline__ bool parse_i64(const unsigned char* p, int len, int64_t* out) {
+  int i = 0;
+  bool neg = false;
+  if (len > 0 && p[0] == '-') {
+    neg = true;
+    i = 1;
+  }
+  if (i >= len) return false;
+  unsigned long long v = 0;
+  int sig = 0;
+  for (; i < len; ++i) {
+    const unsigned d = static_cast<unsigned>(p[i]) - '0';
+    if (d > 9) return false;
+    if (v == 0 && d == 0) continue;  // leading zeros
+    if (++sig > 19) return false;    // > 19 significant digits overflows int64
+    v = v * 10 + d;
+  }
+  const unsigned long long lim = neg ? 0x8000000000000000ull : 0x7fffffffffffffffull;
+  if (v > lim) return false;
+  *out = neg ? static_cast<int64_t>(0ull - v) : static_cast<int64_t>(v);
+  return true;
+}
+
+__device__ __forceinline__ unsigned long long err_key(int64_t line, int detail) {
+  return (static_cast<unsigned long long>(line + 1) << 4) | static_cast<unsigned long long>(detail);
+}
+
+__global__ void __launch_bounds__(kTrThreads)
+k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pref,
+            int64_t* __restrict__ arrival, int32_t* __restrict__ prompt,
+            int32_t* __restrict__ output, uint8_t* __restrict__ slo_cls,
+            uint32_t* __restrict__ line_of_row, unsigned long long* __restrict__ err) {
+  __shared__ __align__(16) unsigned char sm[kTile + kPre];
+  using BS = cub::BlockScan<unsigned long long, kTrThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  const int64_t t = blockIdx.x;
+  stage_tile(tp, t, sm);
+  __syncthreads();
+  const int64_t s0 = t * kTile - kPre;
+  const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
+  const int64_t b0 = t * kTile + 16 * threadIdx.x;
+  unsigned nl = 0, ne = 0;
+  uint32_t ends = 0, nonempty = 0;  // bit k: byte b0 + k ends a (non-empty) line
+#pragma unroll 4
+  for (int k = 0; k < 16; ++k) {
+    const int64_t b = b0 + k;
+    if (b > tp.n) break;
+    if (is_end(sm, s0, tp.n, b, last_is_nl)) {
+      ends |= 1u << k;
+      ++nl;
+      if (!empty_line(sm, s0, b)) {
+        nonempty |= 1u << k;
+        ++ne;
+      }
+    }
+  }
+  unsigned long long pre;
+  BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre);
+  const unsigned long long tp0 = tile_pref[t];
+  int64_t line = static_cast<int64_t>(tp0 >> 32) + static_cast<int64_t>(pre >> 32);
+  int64_t nonempty_before = static_cast<int64_t>(tp0 & 0xffffffffull) +
+                            static_cast<int64_t>(pre & 0xffffffffull);
+  const int expect = tp.has_class ? 4 : 3;
+  while (ends) {
+    const int k = __ffs(static_cast<int>(ends)) - 1;
+    ends &= ends - 1;
+    const int64_t b = b0 + k;
+    const bool ne_line = (nonempty >> k) & 1u;
+    const int64_t my_line = line++;
+    if (!ne_line) continue;  // empty line: skipped (the row counter still advanced)
+    const int64_t ne_idx = nonempty_before++;
+    if (b <= tp.header_end) continue;  // the header
+    const int64_t row = ne_idx - 1;    // the header is the first non-empty line
+    // line start: one past the previous '\n'
+    int64_t st = b - 1;
+    while (st >= 0) {
+      const unsigned char c = st >= s0 ? sm[st - s0] : __ldg(tp.bytes + st);
+      if (c == '\n') break;
+      --st;
+    }
+    ++st;
+    int64_t en = b;
+    if (en > st && (en - 1 >= s0 ? sm[en - 1 - s0] : __ldg(tp.bytes + en - 1)) == '\r') --en;
+    const int len = static_cast<int>(min(en - st, static_cast<int64_t>(INT32_MAX)));
+    const bool in_sm = st >= s0;
+    // fields: split on ',', a trailing ',' adds no empty column (std::getline(ss, col, ','))
+    int fs[4], fl[4];
+    int ncols = 0, f0 = 0;
+    unsigned char local[64];
+    const unsigned char* p;
+    if (in_sm) {
+      p = sm + (st - s0);
+    } else if (len <= 64) {
+      for (int i = 0; i < len; ++i) local[i] = __ldg(tp.bytes + st + i);
+      p = local;
+    } else {
+      p = tp.bytes + st;  // long line (rare): read from global
+    }
+    for (int i = 0; i <= len; ++i) {
+      if (i == len || p[i] == ',') {
+        if (i == len && i == f0 && ncols > 0) break;  // trailing ',' (or empty line, not here)
+        if (ncols < 4) {
+          fs[ncols] = f0;
+          fl[ncols] = i - f0;
+        }
+        ++ncols;
+        f0 = i + 1;
+      }
+    }
+    int detail = 0;
+    int64_t a = 0, pr = 0, ou = 0;
+    if (ncols != expect) {
+      detail = GSB_TRACE_DETAIL_COLUMNS;
+    } else if (!parse_i64(p + fs[0], fl[0], &a)) {
+      detail = GSB_TRACE_DETAIL_ARRIVAL;
+    } else if (!parse_i64(p + fs[1], fl[1], &pr)) {
+      detail = GSB_TRACE_DETAIL_PROMPT;
+    } else if (!parse_i64(p + fs[2], fl[2], &ou)) {
+      detail = GSB_TRACE_DETAIL_OUTPUT;
+    }
+    // static_cast<int>(int64) (trace.cpp:98-99): two's-complement truncation
+    const int32_t pi = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(pr)));
+    const int32_t oi = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(ou)));
+    if (!detail && (a < 0 || pi < 1 || oi < 1)) detail = GSB_TRACE_DETAIL_RANGE;
+    const uint8_t cls = pi <= tp.threshold ? 0 : 1;  // classify_by_threshold, trace.cpp:32-34
+    if (!detail && tp.has_class) {
+      const unsigned char* c = p + fs[3];
+      int fc = -1;
+      if (fl[3] == 2 && c[0] == 'S' && c[1] == 'M') fc = 0;
+      if (fl[3] == 1 && c[0] == 'L') fc = 1;
+      if (fc < 0)
+        detail = GSB_TRACE_DETAIL_CLASS;
+      else if (fc != cls)
+        detail = GSB_TRACE_DETAIL_MISMATCH;
+    }
+    arrival[row] = a;
+    prompt[row] = pi;
+    output[row] = oi;
+    slo_cls[row] = cls;
+    line_of_row[row] = static_cast<uint32_t>(my_line);
+    if (detail) atomicMin(err, err_key(my_line, detail));
+  }
+}
+
+// trace.cpp:108-111: arrivals non-decreasing (checked after the range checks of the same row)
+__global__ void k_csv_monotone(int64_t n_rows, const int64_t* __restrict__ arrival,
+                               const uint32_t* __restrict__ line_of_row,
+                               unsigned long long* __restrict__ err) {
+  const int64_t r = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n_rows) return;
+  if (arrival[r] < arrival[r - 1]) atomicMin(err, err_key(line_of_row[r], GSB_TRACE_DETAIL_MONOTONE));
+}
+
+// the byte range of line L (error reporting): one thread, binary search of the tile prefix
+__global__ void k_csv_locate(const TraceParams tp, const unsigned long long* __restrict__ tile_pref,
+                             int64_t L, int64_t* __restrict__ out /* [2]: start, end */) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t lo = 0, hi = tp.n_tiles - 1;  // last tile with pref.nl <= L
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (static_cast<int64_t>(tile_pref[mid] >> 32) <= L) lo = mid; else hi = mid - 1;
+  }
+  int64_t line = static_cast<int64_t>(tile_pref[lo] >> 32);
+  const bool last_is_nl = tp.n > 0 && tp.bytes[tp.n - 1] == '\n';
+  int64_t b = lo * kTile;
+  for (;; ++b) {
+    const bool e = b < tp.n ? tp.bytes[b] == '\n' : (b == tp.n && tp.n > 0 && !last_is_nl);
+    if (e) {
+      if (line == L) break;
+      ++line;
+    }
+    if (b >= tp.n) break;
+  }
+  int64_t st = b - 1;
+  while (st >= 0 && tp.bytes[st] != '\n') --st;
+  out[0] = st + 1;
+  out[1] = b;
+}
+
+// ---------------------------------------------------------------- save_trace_csv
+__device__ __forceinline__ int n_digits(int64_t v) {  // ostream << int64: '-' + digits
+  unsigned long long u = v < 0 ? 0ull - static_cast<unsigned long long>(v) : static_cast<unsigned long long>(v);
+  int d = 1;
+  while (u >= 10) {
+    u /= 10;
+    ++d;
+  }
+  return d + (v < 0 ? 1 : 0);
+}
+
+__device__ __forceinline__ void put_int(char* dst, int64_t v, int len) {
+  unsigned long long u = v < 0 ? 0ull - static_cast<unsigned long long>(v) : static_cast<unsigned long long>(v);
+  for (int i = len - 1; i >= (v < 0 ? 1 : 0); --i) {
+    dst[i] = static_cast<char>('0' + u % 10);
+    u /= 10;
+  }
+  if (v < 0) dst[0] = '-';
+}
+
+__device__ __forceinline__ int row_len(int64_t a, int32_t p, int32_t o, int cls) {
+  return n_digits(a) + n_digits(p) + n_digits(o) + 2 + (cls < 0 ? 0 : (cls == 0 ? 3 : 2)) + 1;
+}
+
+__global__ void k_csv_row_len(int64_t n, const int64_t* __restrict__ a, const int32_t* __restrict__ p,
+                              const int32_t* __restrict__ o, const uint8_t* __restrict__ cls,
+                              unsigned long long* __restrict__ len) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  len[r] = static_cast<unsigned long long>(row_len(a[r], p[r], o[r], cls ? cls[r] : -1));
+}
+
+__global__ void k_csv_write(int64_t n, int64_t base, const int64_t* __restrict__ a,
+                            const int32_t* __restrict__ p, const int32_t* __restrict__ o,
+                            const uint8_t* __restrict__ cls, const unsigned long long* __restrict__ off,
+                            char* __restrict__ out) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  char* d = out + base + off[r];
+  const int la = n_digits(a[r]), lp = n_digits(p[r]), lo = n_digits(o[r]);
+  put_int(d, a[r], la);
+  d += la;
+  *d++ = ',';
+  put_int(d, p[r], lp);
+  d += lp;
+  *d++ = ',';
+  put_int(d, o[r], lo);
+  d += lo;
+  if (cls) {
+    *d++ = ',';
+    if (cls[r] == 0) {
+      *d++ = 'S';
+      *d++ = 'M';
+    } else {
+      *d++ = 'L';
+    }
+  }
+  *d = '\n';
+}
+
+const char kHdr3[] = "arrival_ms,prompt_tokens,output_tokens";
+const char kHdr4[] = "arrival_ms,prompt_tokens,output_tokens,class";
+
+void set_result_line(gsb_trace_parse_result* r, const char* p, int64_t len) {
+  const int64_t k = std::min<int64_t>(len, static_cast<int64_t>(sizeof(r->line) - 1));
+  memcpy(r->line, p, static_cast<size_t>(k));
+  r->line[k] = 0;
+  r->line_len = static_cast<int32_t>(k);
+  r->line_truncated = len > k ? 1 : 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t class_threshold,
+                    int64_t cap_rows, int64_t* d_arrival, int32_t* d_prompt, int32_t* d_output,
+                    uint8_t* d_slo_class, gsb_trace_parse_result* res, void* stream) {
+  if (!ctx || !res || n_bytes < 0 || (n_bytes > 0 && !d_bytes))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_parse: bad arguments");
+  if (n_bytes >= (int64_t{1} << 32))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_parse: input must be < 4 GiB");
+  memset(res, 0, sizeof(*res));
+  res->row = -1;
+  auto fail = [&](int kind, int detail, int64_t row, const std::string& msg) {
+    res->status = GSB_TRACE_ERROR;
+    res->kind = kind;
+    res->detail = detail;
+    res->row = row;
+    return gsb_set_error(ctx, GSB_TRACE_ERROR, msg);
+  };
+  if (n_bytes == 0) return fail(GSB_TRACE_KIND_EMPTY, 0, -1, "empty trace file");
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  TraceParams tp{};
+  tp.bytes = reinterpret_cast<const unsigned char*>(d_bytes);
+  tp.n = n_bytes;
+  tp.n_tiles = n_bytes / kTile + 1;  // the virtual end at n may open a tile
+  tp.threshold = class_threshold;
+  // scratch: [tile counts + 1][prefix + 1][first_end][err][locate 2][line_of_row (cap)][cub tmp]
+  const size_t nt = static_cast<size_t>(tp.n_tiles) + 1;
+  size_t cub_tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_tmp, static_cast<unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), static_cast<int>(nt), s);
+  const size_t head = (2 * nt + 4) * sizeof(unsigned long long);
+  const size_t lor = static_cast<size_t>(std::max<int64_t>(cap_rows, 1)) * sizeof(uint32_t);
+  char* scr = static_cast<char*>(gsb_scratch(ctx, head + lor + cub_tmp + 256));
+  if (!scr) return gsb_set_error(ctx, GSB_CUDA_ERROR, "trace_parse: scratch allocation failed");
+  auto* cnt = reinterpret_cast<unsigned long long*>(scr);
+  auto* pref = cnt + nt;
+  auto* first_end = pref + nt;
+  auto* err = first_end + 1;
+  auto* loc = reinterpret_cast<int64_t*>(err + 1);
+  auto* line_of_row = reinterpret_cast<uint32_t*>(scr + head);
+  void* d_cub = scr + ((head + lor + 255) / 256) * 256;
+  cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s);
+  cudaMemsetAsync(first_end, 0xff, 2 * sizeof(unsigned long long), s);  // first_end, err = max
+  k_csv_count<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(tp, cnt, first_end);
+  cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, cnt, pref, static_cast<int>(nt), s);
+  unsigned long long h[2];
+  cudaMemcpyAsync(&h[0], first_end, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&h[1], pref + nt - 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_parse");
+  const int64_t header_end = static_cast<int64_t>(h[0]);
+  // header (trace.cpp:63-74): line 0 after one '\r' strip
+  char hb[sizeof(res->line)];
+  const int64_t hl = std::min<int64_t>(header_end, static_cast<int64_t>(sizeof(hb) - 1));
+  cudaMemcpy(hb, d_bytes, static_cast<size_t>(hl), cudaMemcpyDeviceToHost);
+  int64_t hlen = header_end;
+  if (hlen > 0 && hlen <= hl && hb[hlen - 1] == '\r') --hlen;
+  const int64_t hshown = std::min<int64_t>(hlen, hl);
+  const std::string hdr(hb, static_cast<size_t>(hshown));
+  if (hlen == static_cast<int64_t>(sizeof(kHdr3) - 1) && hdr == kHdr3) {
+    tp.has_class = 0;
+  } else if (hlen == static_cast<int64_t>(sizeof(kHdr4) - 1) && hdr == kHdr4) {
+    tp.has_class = 1;
+  } else {
+    std::string full(static_cast<size_t>(header_end), '\0');  // the whole header line
+    if (!full.empty()) cudaMemcpy(&full[0], d_bytes, full.size(), cudaMemcpyDeviceToHost);
+    if (!full.empty() && full.back() == '\r') full.pop_back();
+    set_result_line(res, full.data(), static_cast<int64_t>(full.size()));
+    return fail(GSB_TRACE_KIND_BAD_HEADER, 0, 1, "unrecognized trace header: " + full);
+  }
+  res->has_class = tp.has_class;
+  tp.header_end = header_end;
+  const int64_t n_rows = static_cast<int64_t>(h[1] & 0xffffffffull) - 1;  // minus the header
+  if (n_rows <= 0) return fail(GSB_TRACE_KIND_EMPTY, 0, -1, "trace has no rows");
+  if (n_rows > cap_rows) {
+    res->n_rows = n_rows;
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_parse: more rows than cap_rows");
+  }
+  k_csv_parse<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(
+      tp, pref, d_arrival, d_prompt, d_output, d_slo_class, line_of_row, err);
+  if (n_rows > 1)
+    k_csv_monotone<<<static_cast<unsigned>((n_rows - 1 + 255) / 256), 256, 0, s>>>(
+        n_rows, d_arrival, line_of_row, err);
+  unsigned long long ek = kNoErr;
+  cudaMemcpyAsync(&ek, err, sizeof(ek), cudaMemcpyDeviceToHost, s);
+  int64_t last = 0;
+  cudaMemcpyAsync(&last, d_arrival + n_rows - 1, sizeof(last), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_parse");
+  const int rc = gsb_check_launch(ctx, "trace_parse");
+  if (rc) return rc;
+  if (ek == kNoErr) {
+    res->n_rows = n_rows;
+    res->max_arrival_ms = last;  // arrivals are non-decreasing: the last is the max
+    return GSB_OK;
+  }
+  // the earliest failing row: fetch its bytes, the host formats the reference's message
+  const int64_t row = static_cast<int64_t>(ek >> 4);
+  const int detail = static_cast<int>(ek & 15);
+  k_csv_locate<<<1, 32, 0, s>>>(tp, pref, row - 1, loc);
+  int64_t se[2];
+  cudaMemcpyAsync(se, loc, sizeof(se), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  std::string line(static_cast<size_t>(se[1] - se[0]), '\0');
+  if (!line.empty())
+    cudaMemcpy(&line[0], d_bytes + se[0], line.size(), cudaMemcpyDeviceToHost);
+  if (!line.empty() && line.back() == '\r') line.pop_back();
+  set_result_line(res, line.data(), static_cast<int64_t>(line.size()));
+  const std::string r = "row " + std::to_string(row) + ": ";
+  // column split for the message (same rule as the kernel)
+  std::string cols[4];
+  int ncols = 0;
+  size_t f0 = 0;
+  for (size_t i = 0; i <= line.size(); ++i) {
+    if (i == line.size() || line[i] == ',') {
+      if (i == line.size() && i == f0 && ncols > 0) break;
+      if (ncols < 4) cols[ncols] = line.substr(f0, i - f0);
+      ++ncols;
+      f0 = i + 1;
+    }
+  }
+  res->n_cols = ncols;
+  const int expect = tp.has_class ? 4 : 3;
+  switch (detail) {
+    case GSB_TRACE_DETAIL_COLUMNS:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row,
+                  r + "expected " + std::to_string(expect) + " columns, got " + std::to_string(ncols));
+    case GSB_TRACE_DETAIL_ARRIVAL:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row, r + "bad arrival_ms '" + cols[0] + "'");
+    case GSB_TRACE_DETAIL_PROMPT:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row, r + "bad prompt_tokens '" + cols[1] + "'");
+    case GSB_TRACE_DETAIL_OUTPUT:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row, r + "bad output_tokens '" + cols[2] + "'");
+    case GSB_TRACE_DETAIL_RANGE:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row, r + "out-of-range field");
+    case GSB_TRACE_DETAIL_MONOTONE:
+      return fail(GSB_TRACE_KIND_NON_MONOTONE, detail, row, r + "arrivals must be non-decreasing");
+    case GSB_TRACE_DETAIL_CLASS:
+      return fail(GSB_TRACE_KIND_MALFORMED, detail, row, r + "class must be SM or L");
+    default:
+      return fail(GSB_TRACE_KIND_CLASS_MISMATCH, detail, row,
+                  r + "class column disagrees with threshold " + std::to_string(class_threshold));
+  }
+}
+
+int gsb_trace_format(gsb_ctx* ctx, int64_t n, const int64_t* d_arrival, const int32_t* d_prompt,
+                     const int32_t* d_output, const uint8_t* d_slo_class, char* d_out,
+                     int64_t cap_bytes, int64_t* h_bytes, void* stream) {
+  if (!ctx || !h_bytes || n < 0) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_format: bad arguments");
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  const char* hdr = d_slo_class ? kHdr4 : kHdr3;
+  const int64_t hl = static_cast<int64_t>(strlen(hdr)) + 1;
+  if (n == 0) {
+    *h_bytes = hl;
+    if (!d_out) return GSB_OK;
+    if (cap_bytes < hl) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_format: cap_bytes too small");
+    std::string h = std::string(hdr) + "\n";
+    cudaMemcpyAsync(d_out, h.data(), static_cast<size_t>(hl), cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    return gsb_check_launch(ctx, "trace_format");
+  }
+  size_t cub_tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_tmp, static_cast<unsigned long long*>(nullptr),
+                                static_cast<unsigned long long*>(nullptr), static_cast<int>(n + 1), s);
+  const size_t lens = static_cast<size_t>(n + 1) * sizeof(unsigned long long);
+  char* scr = static_cast<char*>(gsb_scratch(ctx, 2 * lens + cub_tmp + 256));
+  if (!scr) return gsb_set_error(ctx, GSB_CUDA_ERROR, "trace_format: scratch allocation failed");
+  auto* len = reinterpret_cast<unsigned long long*>(scr);
+  auto* off = len + (n + 1);
+  void* d_cub = scr + ((2 * lens + 255) / 256) * 256;
+  cudaMemsetAsync(len + n, 0, sizeof(unsigned long long), s);
+  const unsigned g = static_cast<unsigned>((n + 255) / 256);
+  k_csv_row_len<<<g, 256, 0, s>>>(n, d_arrival, d_prompt, d_output, d_slo_class, len);
+  cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, len, off, static_cast<int>(n + 1), s);
+  unsigned long long body = 0;
+  cudaMemcpyAsync(&body, off + n, sizeof(body), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_format");
+  *h_bytes = hl + static_cast<int64_t>(body);
+  if (!d_out) return GSB_OK;  // size query
+  if (cap_bytes < *h_bytes) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_format: cap_bytes too small");
+  std::string h = std::string(hdr) + "\n";
+  cudaMemcpyAsync(d_out, h.data(), static_cast<size_t>(hl), cudaMemcpyHostToDevice, s);
+  k_csv_write<<<g, 256, 0, s>>>(n, hl, d_arrival, d_prompt, d_output, d_slo_class, off, d_out);
+  cudaStreamSynchronize(s);
+  return gsb_check_launch(ctx, "trace_format");
+}
+
+}  // extern "C"
