@@ -271,6 +271,26 @@ def run_gsb(args, rank, world, dist):
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in ts]
 
+    # ---------------- trace ingest leg (K6): this rank's trace as CSV text, parsed on the GPU
+    csv_text = eng.format_trace(d_arr, d_prm, torch.full_like(d_prm, 128),
+                                (d_prm > 1024).to(torch.uint8))
+    d_csv = torch.frombuffer(bytearray(csv_text), dtype=torch.uint8).to("cuda")
+    eng.parse_trace(d_csv)  # warm (scratch sizing)
+
+    def run_ingest(timed_steps, warm):
+        ts = []
+        for i in range(warm + timed_steps):
+            flush.zero_()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            t = eng.parse_trace(d_csv)
+            s1.record(stream)
+            if i >= warm:
+                ts.append((s0, s1))
+        torch.cuda.synchronize()
+        assert t.arrival_ms.numel() == n_req
+        return [a.elapsed_time(b) for a, b in ts]
+
     # ---------------- e2e prefill leg: pinned host in, pinned host out
     h_arr = torch.as_tensor(arrival).pin_memory()
     h_prm = torch.as_tensor(prompt).pin_memory()
@@ -336,6 +356,8 @@ def run_gsb(args, rank, world, dist):
         barrier()
         e2e_ms = run_e2e(args.steps, args.warmup)
         barrier()
+        ing_ms = run_ingest(max(3, args.steps // 4), 3)
+        barrier()
     k1_ms, k2_ms = kernel_split()
 
     def max_over_ranks(x):
@@ -349,6 +371,7 @@ def run_gsb(args, rank, world, dist):
     ms_dec = max_over_ranks(statistics.mean(dec_ms))
     ms_e2e = max_over_ranks(statistics.mean(e2e_ms))
     ms_pool = max_over_ranks(statistics.mean(pool_ms))
+    ms_ing = max_over_ranks(statistics.mean(ing_ms))
     psum = api.Engine.pool_summary(pplan)
 
     # global per-(profile, class) result: every rank's summary, combined in rank order
@@ -369,6 +392,7 @@ def run_gsb(args, rank, world, dist):
         if cpu is not None:
             cpu["pool"], parity["pool"] = pool_cpu_baseline(args, pa, pp, po, pstream, pcfg,
                                                             psum)
+            cpu["ingest"] = ingest_cpu_baseline(args, csv_text)
 
     if rank != 0:
         return
@@ -394,7 +418,8 @@ def run_gsb(args, rank, world, dist):
     # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
     # with the fused summary partials + summary final (4); decode step = tbt_p95 + tps +
     # decode_replay (3); e2e = 4
-    launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4)
+    # + ingest (K6: count, parse, monotone per call; the CUB scan is library code)
+    launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4) + 3 * max(3, args.steps // 4)
     line = {
         "metric": METRIC,
         "value": world * evals / (ms_pre / 1e3),
@@ -444,6 +469,19 @@ def run_gsb(args, rank, world, dist):
                               "fused per-class summary and its final combine",
                      "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre, "traffic": traffic_k2,
                      "traffic_note": "dram__bytes_read+write per launch, profiles/ ncu capture"},
+        "ingest": {"value": world * len(csv_text) / (ms_ing / 1e3) / 1e9,
+                   "unit": "GB/s of trace CSV parsed (load_trace semantics)",
+                   "rows_per_s": world * n_req / (ms_ing / 1e3), "ms_per_step": ms_ing,
+                   "csv_bytes_per_step": len(csv_text), "rows_per_step": n_req,
+                   "workload": "this rank's trace rendered by save_trace_csv (4 columns), "
+                               "device-resident bytes -> SoA via gsb_trace_parse (K6: count, scan, "
+                               "parse, monotone check; two host syncs per call)",
+                   "roofline": {"bound": "hbm", "achieved": (len(csv_text) * 2 + n_req * 21)
+                                / (ms_ing / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                "frac": (len(csv_text) * 2 + n_req * 21) / (ms_ing / 1e3) / 1e9
+                                / hbm,
+                                "basis": "CSV bytes read twice (count + parse passes) + 17 B/row "
+                                         "written + 4 B/row line index"}},
         "roofline_k1": {"bound": "hbm", "kernel": "k_route_bin (K1)", "achieved": k1_gbs,
                         "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm, "kernel_ms": k1_ms,
                         "bytes_per_request": K1_BYTES_PER_REQ,
@@ -553,6 +591,35 @@ def cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep, t
     parity = {"prefill_cells_checked": int(len(nonempty)), "prefill_mismatches": mism,
               "decode_trajectories_checked": int(len(idx)), "decode_digest_mismatches": dmism}
     return pre, parity
+
+
+def ingest_cpu_baseline(args, csv_text: bytes):
+    """greensim::load_trace (oracle/_ref, the unmodified reference) on a bounded prefix of the
+    same CSV: one thread (the reference loader is a single sequential getline loop)."""
+    import tempfile
+    from oracle import oracle as O
+    if not O.reference_available():
+        return None
+    ref = O.Reference()
+    n = min(len(csv_text), 8 << 20)
+    cut = csv_text.rfind(b"\n", 0, n) + 1
+    with tempfile.NamedTemporaryFile(suffix=".csv", delete=False) as f:
+        f.write(csv_text[:cut])
+        path = f.name
+    try:
+        reps, t_tot = 0, 0.0
+        while t_tot < args.cpu_seconds / 4 and reps < 20:
+            t0 = time.perf_counter()
+            r = ref.load_trace(path, 1024)
+            t_tot += time.perf_counter() - t0
+            reps += 1
+    finally:
+        os.remove(path)
+    rows = len(r[0])
+    return {"value": cut / (t_tot / reps) / 1e9, "unit": "GB/s of trace CSV parsed",
+            "rows_per_s": rows / (t_tot / reps), "cores": 1, "kind": "reference",
+            "sample": f"greensim::load_trace on the first {cut} bytes ({rows} rows) of the same "
+                      f"CSV, {reps} reps"}
 
 
 def pool_cpu_baseline(args, pa, pp, po, pstream, pcfg, psum):

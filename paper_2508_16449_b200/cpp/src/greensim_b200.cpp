@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <limits>
 #include <map>
 #include <mutex>
@@ -881,6 +883,96 @@ AuditResult audit_decision_log(std::span<const DecisionRecord> records, const De
     }
   }
   return res;
+}
+
+// ------------------------------------------------------------------ trace CSV (K6)
+const char* prompt_class_name(PromptClass c) {  // trace.cpp:14-16
+  return c == PromptClass::ShortMedium ? "SM" : "L";
+}
+
+// load_trace (trace.cpp:56-129): the file's bytes go to the device in one copy; K6 parses them
+// (rows, checks, SLO classes) and the SoA comes back in one copy.
+Trace load_trace(const std::filesystem::path& path, int class_threshold) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in)
+    throw TraceError(TraceError::Kind::MalformedRow, "cannot open trace file: " + path.string());
+  const std::string bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  size_t cap = bytes.size() / 6 + 1;  // a valid row holds >= 6 bytes; retried if malformed
+  for (int attempt = 0;; ++attempt) {
+    Call call;
+    const size_t ob = call.in(bytes.data(), bytes.size());
+    const size_t oa = call.out(cap * 8), op = call.out(cap * 4), oo = call.out(cap * 4),
+                 oc = call.out(cap);
+    call.commit();
+    gsb_trace_parse_result res;
+    const int rc = gsb_trace_parse(call.ctx(), call.dev<char>(ob), static_cast<int64_t>(bytes.size()),
+                                   class_threshold, static_cast<int64_t>(cap), call.dev<int64_t>(oa),
+                                   call.dev<int32_t>(op), call.dev<int32_t>(oo),
+                                   call.dev<uint8_t>(oc), &res, nullptr);
+    if (rc == GSB_TRACE_ERROR)
+      throw TraceError(static_cast<TraceError::Kind>(res.kind), gsb_last_error(call.ctx()));
+    if (rc == GSB_INVALID_ARGUMENT && res.n_rows > static_cast<int64_t>(cap) && attempt == 0) {
+      cap = static_cast<size_t>(res.n_rows);
+      continue;
+    }
+    check(call.ctx(), rc);
+    call.fetch();
+    Trace t;
+    const size_t n = static_cast<size_t>(res.n_rows);
+    t.requests.resize(n);
+    const int64_t* a = call.host<int64_t>(oa);
+    const int32_t* p = call.host<int32_t>(op);
+    const int32_t* o = call.host<int32_t>(oo);
+    const uint8_t* c = call.host<uint8_t>(oc);
+    for (size_t i = 0; i < n; ++i) {
+      Request& r = t.requests[i];
+      r.id = static_cast<int64_t>(i);
+      r.arrival_ms = a[i];
+      r.prompt_tokens = p[i];
+      r.output_tokens = o[i];
+      r.cls = static_cast<PromptClass>(c[i]);
+    }
+    // finalize_meta (trace.cpp:36-45) with duration 0: the largest arrival
+    t.meta.name = path.stem().string();
+    t.meta.duration_ms = std::max<int64_t>(0, res.max_arrival_ms);
+    t.meta.nominal_qps = t.meta.duration_ms > 0 ? 1000.0 * static_cast<double>(n) /
+                                                      static_cast<double>(t.meta.duration_ms)
+                                                : 0.0;
+    return t;
+  }
+}
+
+// save_trace_csv (trace.cpp:131-145): the SoA goes up in one copy, K6 renders the text, one
+// copy brings it back.
+void save_trace_csv(const Trace& trace, const std::filesystem::path& path) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot write trace file: " + path.string());
+  const size_t n = trace.requests.size();
+  const bool has_class = std::all_of(trace.requests.begin(), trace.requests.end(),
+                                     [](const Request& r) { return r.cls.has_value(); });
+  std::vector<int64_t> a(n);
+  std::vector<int32_t> p(n), o(n);
+  std::vector<uint8_t> c(n);
+  for (size_t i = 0; i < n; ++i) {
+    const Request& r = trace.requests[i];
+    a[i] = r.arrival_ms;
+    p[i] = r.prompt_tokens;
+    o[i] = r.output_tokens;
+    c[i] = r.cls ? static_cast<uint8_t>(*r.cls) : 0;
+  }
+  // upper bound of the text: 20 + 11 + 11 digits/signs, 3 commas, "SM", '\n' per row
+  const size_t cap = 64 + n * 48;
+  Call call;
+  const size_t oa = call.in_vec(a), op = call.in_vec(p), oo = call.in_vec(o), oc = call.in_vec(c);
+  const size_t ot = call.out(cap);
+  call.commit();
+  int64_t bytes = 0;
+  check(call.ctx(), gsb_trace_format(call.ctx(), static_cast<int64_t>(n), call.dev<int64_t>(oa),
+                                     call.dev<int32_t>(op), call.dev<int32_t>(oo),
+                                     has_class ? call.dev<uint8_t>(oc) : nullptr, call.dev<char>(ot),
+                                     static_cast<int64_t>(cap), &bytes, nullptr));
+  call.fetch();
+  out.write(call.host<char>(ot), bytes);
 }
 
 }  // namespace greensim

@@ -528,7 +528,8 @@ int gsb_trace_format(gsb_ctx* ctx, int64_t n, const int64_t* d_arrival, const in
                      int64_t cap_bytes, int64_t* h_bytes, void* stream) {
   if (!ctx || !h_bytes || n < 0) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_format: bad arguments");
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  const char* hdr = d_slo_class ? kHdr4 : kHdr3;
+  // has_class = all_of(requests, has cls): vacuously true for an empty trace (trace.cpp:134-137)
+  const char* hdr = (d_slo_class || n == 0) ? kHdr4 : kHdr3;
   const int64_t hl = static_cast<int64_t>(strlen(hdr)) + 1;
   if (n == 0) {
     *h_bytes = hl;

@@ -22,7 +22,7 @@ LIB = os.path.join(ROOT, "paper_2508_16449_b200", "lib")
 REF_BINS = [os.path.join(ROOT, "oracle", "_ref", "dropin", n)
             for n in ("test_prefill_opt", "test_decode_ctl", "test_router", "test_simkernel")]
 OWN_BINS = [os.path.join(ROOT, "tests", "cpp", "bin", n)
-            for n in ("test_router_dropin", "test_acceptance_dropin")]
+            for n in ("test_router_dropin", "test_acceptance_dropin", "test_trace_dropin")]
 ALL_BINS = REF_BINS + OWN_BINS
 
 
@@ -44,12 +44,14 @@ def test_dropin_library_exports_reference_api():
                 "greensim::DecodeController::on_coarse_tick(",
                 "greensim::DecodeController::on_adapt_tick(", "greensim::audit_decision_log(",
                 "greensim::decision_log_csv", "greensim::TbtWindow::p95()",
-                "greensim::TpsWindow::tps(", "greensim::quantile("]:
+                "greensim::TpsWindow::tps(", "greensim::quantile(", "greensim::load_trace(",
+                "greensim::save_trace_csv("]:
         assert sym in out, sym
     # and it is a client of the C ABI, not a second implementation
     dyn = subprocess.run(["nm", "-D", "--undefined-only", so], capture_output=True, text=True,
                          check=True).stdout
-    for sym in ["gsb_select_batches", "gsb_decode_script", "gsb_build_band_tables", "gsb_classify"]:
+    for sym in ["gsb_select_batches", "gsb_decode_script", "gsb_build_band_tables", "gsb_classify",
+                "gsb_trace_parse", "gsb_trace_format"]:
         assert sym in dyn, sym
 
 

@@ -111,7 +111,9 @@ def test_format_equals_restated_writer(gsb, restate):
     for cls in (None, c):
         assert gsb.format_trace(a, p, o, cls) == restate.trace_format(a, p, o, cls)
     assert gsb.format_trace(a[:0], p[:0], o[:0], c[:0]) == H4 + b"\n"
-    assert gsb.format_trace(a[:0], p[:0], o[:0]) == H3 + b"\n"
+    assert gsb.format_trace(a[:0], p[:0], o[:0]) == H4 + b"\n"  # all_of over nothing
+    assert gsb.format_trace(a[:1], p[:1], o[:1]) == H3 + b"\n" + restate.trace_format(
+        a[:1], p[:1], o[:1]).split(b"\n", 1)[1]
 
 
 def test_round_trip_and_route(gsb, restate, tmp_path):
