@@ -49,22 +49,6 @@ __device__ __forceinline__ unsigned char byte_at(const unsigned char* __restrict
   return (i >= 0 && i < n) ? __ldg(b + i) : static_cast<unsigned char>(0);
 }
 
-// a line ends at b: a '\n' byte, or the end of a file whose last byte is not '\n'
-__device__ __forceinline__ bool is_end(const unsigned char* s, int64_t s0, int64_t n, int64_t b,
-                                       bool last_is_nl) {
-  if (b < n) return s[b - s0] == '\n';
-  return b == n && n > 0 && !last_is_nl;
-}
-
-// the line ending at b is empty after the '\r' strip
-__device__ __forceinline__ bool empty_line(const unsigned char* s, int64_t s0, int64_t b) {
-  if (b == 0) return true;
-  const unsigned char c1 = s[b - 1 - s0];
-  if (c1 == '\n') return true;
-  if (c1 == '\r') return b - 1 == 0 || s[b - 2 - s0] == '\n';
-  return false;
-}
-
 // stage [t*kTile - kPre, (t+1)*kTile) (bytes outside the file read as 0)
 __device__ __forceinline__ void stage_tile(const TraceParams& tp, int64_t t, unsigned char* sm) {
   const int64_t s0 = t * kTile - kPre;
@@ -82,6 +66,49 @@ __device__ __forceinline__ void stage_tile(const TraceParams& tp, int64_t t, uns
     *reinterpret_cast<uint4*>(sm + 16 * i) = v;
   }
 }
+
+// bit k of the result: byte k of the 16 bytes q equals c (SIMD byte compare + MSB gather)
+__device__ __forceinline__ unsigned eq_mask16(const uint4& q, unsigned c4) {
+  unsigned m = 0;
+  const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned e = __vcmpeq4(w[i], c4) & 0x80808080u;  // 0x80 per matching byte
+    m |= ((e * 0x00204081u) >> 28) << (4 * i);              // gather the 4 MSBs
+  }
+  return m;
+}
+
+// Line ends and non-empty line ends among the 16 bytes [b0, b0 + 16) of a staged tile:
+// bit k <-> byte b0 + k. A line ends at each '\n' and at n when the file does not end with
+// '\n'; the line ending at b is empty iff byte b-1 is '\n' (or b is the file start) or byte
+// b-1 is '\r' preceded by '\n' or the file start (one '\r' is stripped).
+__device__ __forceinline__ void line_ends16(const unsigned char* sm, int64_t s0, int64_t n,
+                                            int64_t b0, bool last_is_nl, unsigned* ends,
+                                            unsigned* nonempty) {
+  const uint4 q = *reinterpret_cast<const uint4*>(sm + (b0 - s0));
+  const unsigned char p1 = sm[b0 - 1 - s0], p2 = sm[b0 - 2 - s0];
+  unsigned nl = eq_mask16(q, 0x0a0a0a0au), cr = eq_mask16(q, 0x0d0d0d0du);
+  const int64_t live = n - b0;  // bytes of this chunk inside the file
+  const unsigned in = live >= 16 ? 0xffffu : (live <= 0 ? 0u : (1u << live) - 1u);
+  nl &= in;
+  cr &= in;
+  // 18-bit windows, bit j <-> byte b0 - 2 + j; the byte before the file start acts as '\n'
+  unsigned nlx = (nl << 2) | (p1 == '\n' ? 2u : 0u) | (p2 == '\n' ? 1u : 0u);
+  const unsigned crx = (cr << 2) | (p1 == '\r' ? 2u : 0u) | (p2 == '\r' ? 1u : 0u);
+  if (b0 == 0) nlx |= 2u;
+  unsigned e = nl;
+  if (!last_is_nl && n > 0 && live >= 0 && live < 16) e |= 1u << live;  // the virtual end at n
+  const unsigned empty = ((nlx >> 1) | ((crx >> 1) & nlx)) & 0xffffu;
+  *ends = e;
+  *nonempty = e & ~empty;
+}
+
+struct MaxI64 {
+  __device__ __forceinline__ long long operator()(long long a, long long b) const {
+    return a > b ? a : b;
+  }
+};
 
 struct MinU64 {
   __device__ __forceinline__ unsigned long long operator()(unsigned long long a,
@@ -101,19 +128,11 @@ k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt,
   __syncthreads();
   const int64_t s0 = t * kTile - kPre;
   const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
-  unsigned nl = 0, ne = 0;
-  int64_t first = INT64_MAX;
   const int64_t b0 = t * kTile + 16 * threadIdx.x;
-#pragma unroll 4
-  for (int k = 0; k < 16; ++k) {
-    const int64_t b = b0 + k;
-    if (b > tp.n) break;
-    if (is_end(sm, s0, tp.n, b, last_is_nl)) {
-      ++nl;
-      ne += empty_line(sm, s0, b) ? 0u : 1u;
-      first = min(first, b);
-    }
-  }
+  unsigned ends, nonempty;
+  line_ends16(sm, s0, tp.n, b0, last_is_nl, &ends, &nonempty);
+  const unsigned nl = __popc(ends), ne = __popc(nonempty);
+  const int64_t first = ends ? b0 + __ffs(static_cast<int>(ends)) - 1 : INT64_MAX;
   const unsigned long long packed =
       (static_cast<unsigned long long>(nl) << 32) | static_cast<unsigned long long>(ne);
   const unsigned long long tot = BR(tmp).Sum(packed);
@@ -124,31 +143,6 @@ k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt,
     tile_cnt[t] = tot;
     if (fmin != static_cast<unsigned long long>(INT64_MAX)) atomicMin(first_end, fmin);
   }
-}
-
-// std::from_chars<int64_t> over [p, p+len): optional '-', >= 1 digits, whole field, no
-// overflow (trace.cpp:84-91)
-__device__ __forceinline__ bool parse_i64(const unsigned char* p, int len, int64_t* out) {
-  int i = 0;
-  bool neg = false;
-  if (len > 0 && p[0] == '-') {
-    neg = true;
-    i = 1;
-  }
-  if (i >= len) return false;
-  unsigned long long v = 0;
-  int sig = 0;
-  for (; i < len; ++i) {
-    const unsigned d = static_cast<unsigned>(p[i]) - '0';
-    if (d > 9) return false;
-    if (v == 0 && d == 0) continue;  // leading zeros
-    if (++sig > 19) return false;    // > 19 significant digits overflows int64
-    v = v * 10 + d;
-  }
-  const unsigned long long lim = neg ? 0x8000000000000000ull : 0x7fffffffffffffffull;
-  if (v > lim) return false;
-  *out = neg ? static_cast<int64_t>(0ull - v) : static_cast<int64_t>(v);
-  return true;
 }
 
 __device__ __forceinline__ unsigned long long err_key(int64_t line, int detail) {
@@ -162,102 +156,133 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
             uint32_t* __restrict__ line_of_row, unsigned long long* __restrict__ err) {
   __shared__ __align__(16) unsigned char sm[kTile + kPre];
   using BS = cub::BlockScan<unsigned long long, kTrThreads>;
+  using BS2 = cub::BlockScan<long long, kTrThreads>;
   __shared__ typename BS::TempStorage tmp;
+  __shared__ typename BS2::TempStorage tmp2;
   const int64_t t = blockIdx.x;
   stage_tile(tp, t, sm);
   __syncthreads();
   const int64_t s0 = t * kTile - kPre;
   const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
   const int64_t b0 = t * kTile + 16 * threadIdx.x;
-  unsigned nl = 0, ne = 0;
-  uint32_t ends = 0, nonempty = 0;  // bit k: byte b0 + k ends a (non-empty) line
-#pragma unroll 4
-  for (int k = 0; k < 16; ++k) {
-    const int64_t b = b0 + k;
-    if (b > tp.n) break;
-    if (is_end(sm, s0, tp.n, b, last_is_nl)) {
-      ends |= 1u << k;
-      ++nl;
-      if (!empty_line(sm, s0, b)) {
-        nonempty |= 1u << k;
-        ++ne;
-      }
-    }
-  }
+  unsigned ends, nonempty;  // bit k: byte b0 + k ends a (non-empty) line
+  line_ends16(sm, s0, tp.n, b0, last_is_nl, &ends, &nonempty);
+  const unsigned nl = __popc(ends), ne = __popc(nonempty);
   unsigned long long pre;
   BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre);
+  __syncthreads();
+  // the previous line end before this thread's bytes: exclusive max-scan of the threads' last
+  // ends; the tile's first line looks back into the previous tile (one thread per tile)
+  long long prev;
+  BS2(tmp2).ExclusiveScan(ends ? static_cast<long long>(b0 + 31 - __clz(ends)) : -1LL, prev,
+                          -1LL, MaxI64{});
+  if (threadIdx.x == 0) prev = -1;
   const unsigned long long tp0 = tile_pref[t];
   int64_t line = static_cast<int64_t>(tp0 >> 32) + static_cast<int64_t>(pre >> 32);
   int64_t nonempty_before = static_cast<int64_t>(tp0 & 0xffffffffull) +
                             static_cast<int64_t>(pre & 0xffffffffull);
   const int expect = tp.has_class ? 4 : 3;
+  if (ends && prev < 0) {  // this thread holds the tile's first line end
+    int64_t st = b0 + __ffs(static_cast<int>(ends)) - 2;
+    while (st >= 0) {
+      const unsigned char c = st >= s0 ? sm[st - s0] : __ldg(tp.bytes + st);
+      if (c == '\n') break;
+      --st;
+    }
+    prev = st;  // -1 at the file start
+  }
   while (ends) {
     const int k = __ffs(static_cast<int>(ends)) - 1;
     ends &= ends - 1;
     const int64_t b = b0 + k;
+    const int64_t st = prev + 1;
+    prev = b;
     const bool ne_line = (nonempty >> k) & 1u;
     const int64_t my_line = line++;
     if (!ne_line) continue;  // empty line: skipped (the row counter still advanced)
     const int64_t ne_idx = nonempty_before++;
     if (b <= tp.header_end) continue;  // the header
     const int64_t row = ne_idx - 1;    // the header is the first non-empty line
-    // line start: one past the previous '\n'
-    int64_t st = b - 1;
-    while (st >= 0) {
-      const unsigned char c = st >= s0 ? sm[st - s0] : __ldg(tp.bytes + st);
-      if (c == '\n') break;
-      --st;
-    }
-    ++st;
-    int64_t en = b;
-    if (en > st && (en - 1 >= s0 ? sm[en - 1 - s0] : __ldg(tp.bytes + en - 1)) == '\r') --en;
-    const int len = static_cast<int>(min(en - st, static_cast<int64_t>(INT32_MAX)));
     const bool in_sm = st >= s0;
-    // fields: split on ',', a trailing ',' adds no empty column (std::getline(ss, col, ','))
-    int fs[4], fl[4];
-    int ncols = 0, f0 = 0;
-    unsigned char local[64];
-    const unsigned char* p;
-    if (in_sm) {
-      p = sm + (st - s0);
-    } else if (len <= 64) {
-      for (int i = 0; i < len; ++i) local[i] = __ldg(tp.bytes + st + i);
-      p = local;
-    } else {
-      p = tp.bytes + st;  // long line (rare): read from global
-    }
-    for (int i = 0; i <= len; ++i) {
-      if (i == len || p[i] == ',') {
-        if (i == len && i == f0 && ncols > 0) break;  // trailing ',' (or empty line, not here)
-        if (ncols < 4) {
-          fs[ncols] = f0;
-          fl[ncols] = i - f0;
-        }
-        ++ncols;
-        f0 = i + 1;
+    auto at = [&](int64_t i) -> unsigned char { return in_sm ? sm[i - s0] : __ldg(tp.bytes + i); };
+    int64_t en = b;
+    if (en > st && at(en - 1) == '\r') --en;
+    // one pass over the line: columns split on ',' (a trailing ',' adds no column,
+    // std::getline(ss, col, ',')), from_chars<int64> on columns 0-2 (optional '-', >= 1
+    // digit, the whole column, no overflow), the class column's bytes
+    // one pass over the line: columns split on ',' (a trailing ',' adds no column,
+    // std::getline(ss, col, ',')), from_chars<int64> on columns 0-2 (optional '-', >= 1
+    // digit, the whole column, no overflow), the class column's bytes
+    unsigned long long v0 = 0, v1 = 0, v2 = 0, cur = 0;  // registers, no indexed arrays
+    bool ok0 = false, ok1 = false, ok2 = false;
+    int col = 0, flen = 0, sig = 0;
+    bool neg = false, bad = false;
+    unsigned char c0 = 0, c1 = 0;
+    int clen = 0;
+    auto close_field = [&]() {
+      if (col < 3) {
+        const unsigned long long lim = neg ? 0x8000000000000000ull : 0x7fffffffffffffffull;
+        const bool ok = !bad && flen > (neg ? 1 : 0) && cur <= lim;
+        const unsigned long long val = neg ? 0ull - cur : cur;
+        if (col == 0) { v0 = val; ok0 = ok; }
+        if (col == 1) { v1 = val; ok1 = ok; }
+        if (col == 2) { v2 = val; ok2 = ok; }
+      } else if (col == 3) {
+        clen = flen;
       }
+      ++col;
+      cur = 0;
+      flen = sig = 0;
+      neg = bad = false;
+    };
+    bool last_comma = false;
+    for (int64_t i = st; i < en; ++i) {
+      const unsigned char c = at(i);
+      last_comma = c == ',';
+      if (c == ',') {
+        close_field();
+        continue;
+      }
+      if (col < 3) {
+        if (flen == 0 && c == '-') {
+          neg = true;
+        } else {
+          const unsigned d = static_cast<unsigned>(c) - '0';
+          if (d > 9) {
+            bad = true;
+          } else if (cur != 0 || d != 0) {  // leading zeros are free
+            if (++sig > 19) bad = true;     // > 19 significant digits overflows int64
+            else cur = cur * 10 + d;
+          }
+        }
+      } else if (col == 3) {
+        if (flen == 0) c0 = c;
+        if (flen == 1) c1 = c;
+      }
+      ++flen;
+    }
+    int ncols;
+    if (last_comma) {
+      ncols = col;  // the empty text after the final ',' is not a column
+    } else {
+      close_field();
+      ncols = col;
     }
     int detail = 0;
-    int64_t a = 0, pr = 0, ou = 0;
-    if (ncols != expect) {
-      detail = GSB_TRACE_DETAIL_COLUMNS;
-    } else if (!parse_i64(p + fs[0], fl[0], &a)) {
-      detail = GSB_TRACE_DETAIL_ARRIVAL;
-    } else if (!parse_i64(p + fs[1], fl[1], &pr)) {
-      detail = GSB_TRACE_DETAIL_PROMPT;
-    } else if (!parse_i64(p + fs[2], fl[2], &ou)) {
-      detail = GSB_TRACE_DETAIL_OUTPUT;
-    }
+    if (ncols != expect) detail = GSB_TRACE_DETAIL_COLUMNS;
+    else if (!ok0) detail = GSB_TRACE_DETAIL_ARRIVAL;
+    else if (!ok1) detail = GSB_TRACE_DETAIL_PROMPT;
+    else if (!ok2) detail = GSB_TRACE_DETAIL_OUTPUT;
+    const int64_t a = static_cast<int64_t>(v0);
     // static_cast<int>(int64) (trace.cpp:98-99): two's-complement truncation
-    const int32_t pi = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(pr)));
-    const int32_t oi = static_cast<int32_t>(static_cast<uint32_t>(static_cast<uint64_t>(ou)));
+    const int32_t pi = static_cast<int32_t>(static_cast<uint32_t>(v1));
+    const int32_t oi = static_cast<int32_t>(static_cast<uint32_t>(v2));
     if (!detail && (a < 0 || pi < 1 || oi < 1)) detail = GSB_TRACE_DETAIL_RANGE;
     const uint8_t cls = pi <= tp.threshold ? 0 : 1;  // classify_by_threshold, trace.cpp:32-34
     if (!detail && tp.has_class) {
-      const unsigned char* c = p + fs[3];
       int fc = -1;
-      if (fl[3] == 2 && c[0] == 'S' && c[1] == 'M') fc = 0;
-      if (fl[3] == 1 && c[0] == 'L') fc = 1;
+      if (clen == 2 && c0 == 'S' && c1 == 'M') fc = 0;
+      if (clen == 1 && c0 == 'L') fc = 1;
       if (fc < 0)
         detail = GSB_TRACE_DETAIL_CLASS;
       else if (fc != cls)
