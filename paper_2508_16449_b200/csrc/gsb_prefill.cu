@@ -9,6 +9,7 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "gsb_common.cuh"
@@ -129,14 +130,15 @@ __device__ __forceinline__ int classify_c(const int32_t (&t)[GSB_MAX_CLASSES - 1
 //   A. each warp takes a contiguous quarter of the chunk: classify() (router.cpp:26-31), write
 //      the class, key = (window g, class c), per-warp key histogram (match.any + leader add),
 //      min of prefill deadlines (simkernel.cpp:499-501) per key (order-free: min is exact);
-//   B. stable counting sort of the chunk by key: warp w scatters the prompts of its quarter
-//      from cursor off[key] + (counts of warps < w), rank among the round's lanes by lane
-//      order, so every (g, c) run is in ARRIVAL order;
+//      phase A also records each request's rank among its warp's requests of the same key
+//      (the running per-warp count + its lane rank in the round);
+//   B. stable counting sort of the chunk by key: request j goes to cursor off[key] + (counts
+//      of warps < w) + its rank, so every (g, c) run is in ARRIVAL order (no second match);
 //   C. fold: lane (g, p) of warp w walks window g's runs of the classes c = w (mod warps) and
 //      extends T[g][c][p] += (a_p L + b_p) L + c_p left to right, exactly prefill_opt.cpp:9-14.
 //      The P lanes of a window read the same entry (broadcast); run lengths of a class are
 //      similar across windows, so lanes stay busy, and the warps fold different classes.
-// Shared memory is 9 B per chunk slot (prompt, key, sorted prompt), so nine CTAs share an SM and
+// Shared memory is 8 B per chunk slot (prompt, key|rank, sorted index), so nine CTAs share an SM and
 // the C4 grid (1,250 CTAs) is one wave (P = 1 holds 32 windows x C keys per CTA: fewer CTAs).
 constexpr int kRouteWarps = 4;
 constexpr int kRouteCap = 2544;  // requests per chunk
@@ -158,9 +160,13 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 template <int K, bool DL>
 struct RouteSmem {  // one CTA
+  // key (window g, class c) in the low kKeyBits, the request's rank among its warp's requests
+  // of that key above them
+  static constexpr int kKeyBits = K <= 64 ? 6 : 8;
+  using KR = typename std::conditional<K <= 64, uint16_t, uint32_t>::type;
   alignas(16) int32_t stage[kRouteCap + 4];  // prompts of [c0 & ~3, c1)
-  int32_t srt[kRouteCap];                    // the chunk's prompts sorted by key (stable)
-  uint8_t key[kRouteCap];
+  uint16_t srt[kRouteCap];                   // stage index of the chunk's requests, by key (stable)
+  KR kr[kRouteCap];
   uint64_t bar;
   int64_t bnd[33];
   int32_t lb[33];  // chunk-local window starts, lb[G] = "never"
@@ -254,10 +260,13 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
         }
         const int key = g * C + cl;
         const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
+        const unsigned below = m & lt;
+        const int base = hist_w[valid ? key : 0];
+        __syncwarp();
         if (valid) {
           *cls_p = static_cast<uint8_t>(cl);
-          s.key[j] = static_cast<uint8_t>(key);
-          if ((m & lt) == 0) hist_w[key] += __popc(m);
+          s.kr[j] = static_cast<typename S::KR>(key | ((base + __popc(below)) << S::kKeyBits));
+          if (below == 0) hist_w[key] = base + __popc(m);
           if (DL) {
             const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
             const double dl = static_cast<double>(__ldg(arrival + c0 + j)) + ttft - rp.allowance;
@@ -310,21 +319,12 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
       if (lane == 31) s.off[K] = incl;
     }
     __syncthreads();
-    // ---- B: stable scatter of the prompts by key (arrival order inside each key)
-    for (int r = j0; r < j1; r += 32) {
-      const int j = r + lane;
-      const bool valid = j < j1;
-      const int key = valid ? static_cast<int>(s.key[j]) : 0;
-      const int32_t L = st[valid ? j : j0];
-      const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
-      const int base = hist_w[key];
-      __syncwarp();
-      const unsigned below = m & lt;
-      if (valid) {
-        s.srt[base + __popc(below)] = L;
-        if (below == 0) hist_w[key] = base + __popc(m);
-      }
-      __syncwarp();
+    // ---- B: stable scatter of the stage indices by key (arrival order inside each key): the
+    //      warp's cursor for the key plus the rank phase A recorded
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const unsigned v = s.kr[j];
+      const int key = static_cast<int>(v & ((1u << S::kKeyBits) - 1u));
+      s.srt[hist_w[key] + static_cast<int>(v >> S::kKeyBits)] = static_cast<uint16_t>(sb + j);
     }
     __syncthreads();
     // ---- C: ordered fold, lane (window fg, profile fp) of warp w, classes c = w (mod NW)
@@ -334,11 +334,11 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
         const int c = wib + k * NW;
         if (c >= C) break;
         const int o = s.off[fg * C + c], n = s.off[fg * C + c + 1] - o;
-        const int32_t* run = s.srt + o;
+        const uint16_t* run = s.srt + o;
         double a = acc[k];
 #pragma unroll 4
         for (int j = 0; j < n; ++j) {
-          const double Ld = static_cast<double>(run[j]);
+          const double Ld = static_cast<double>(s.stage[run[j]]);
           a = a + 1.0 * ((la * Ld + lb) * Ld + lc);
         }
         acc[k] = a;
