@@ -701,8 +701,10 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
     int best = -1;
     double be = 0.0;
     if (cell_fast(TF, W, p_idle, P_min, P_max)) {
-      // unrolled 9x, not 81x: the table operands become indexed constant loads, and the four
-      // profile variants stay small enough for the instruction cache
+      // unrolled 9x, not 81x: the table operands become uniform constant loads, and the four
+      // profile variants stay small enough for the instruction cache (a fully unrolled 81-clock
+      // scan is ~26 KB of SASS per profile: 2x slower on B200 from instruction-fetch stalls,
+      // even with every profile of a cell in one thread walking the variants in order)
 #pragma unroll 9
       for (int i = 0; i < G; ++i) {
         const double f = cc.f[i], r = cc.r[i];
