@@ -701,6 +701,9 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
     int best = -1;
     double be = 0.0;
     if (cell_fast(TF, W, p_idle, P_min, P_max)) {
+      // every energy is finite here (the range guard), so "nothing taken yet or E < best"
+      // is exactly "E < be" with be starting at +inf: one compare per clock
+      be = INFINITY;
       // unrolled 9x, not 81x: the table operands become uniform constant loads, and the four
       // profile variants stay small enough for the instruction cache (a fully unrolled 81-clock
       // scan is ~26 KB of SASS per profile: 2x slower on B200 from instruction-fetch stalls,
@@ -720,7 +723,7 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
         e = __fma_rn(-1000.0, q, y);
         const double idle = __fma_rn(gsb::kRcp1000, e, q);
         const double E = __dadd_rn(active, idle);
-        const bool take = (busy <= W) && (best < 0 || E < be);
+        const bool take = (busy <= W) && (E < be);
         best = take ? i : best;
         be = take ? E : be;
       }
