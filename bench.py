@@ -372,10 +372,16 @@ def run_gsb(args, rank, world, dist):
     ms_e2e = max_over_ranks(statistics.mean(e2e_ms))
     ms_pool = max_over_ranks(statistics.mean(pool_ms))
     ms_ing = max_over_ranks(statistics.mean(ing_ms))
+    from paper_2508_16449_b200 import distributed as Dd
     psum = api.Engine.pool_summary(pplan)
+    # decode-side end-of-run reduction: per-rank tally of the pool scenarios (global index =
+    # rank * n + i), NCCL all-gather, rank-order combine (identical bytes on every rank)
+    my_tally = Dd.tally_pool(psum, rank * len(pcfg))
+    tallies = (Dd.gather_records(np.array([my_tally], Dd.DECODE_TALLY_DTYPE), "cuda")
+               if world > 1 else np.array([my_tally], Dd.DECODE_TALLY_DTYPE))
+    gtally = Dd.combine_tallies(tallies)
 
     # global per-(profile, class) result: every rank's summary, combined in rank order
-    from paper_2508_16449_b200 import distributed as Dd
     if world > 1:
         per_rank = gathered.cpu().numpy().reshape(world, -1).view(Dd.SUMMARY_DTYPE)
     else:
@@ -459,7 +465,10 @@ def run_gsb(args, rank, world, dist):
                  "workload": "C3 sinusoid 1500+-1000 tps, 150 s, 4 decode workers x max_batch 64; "
                              "sweep hysteresis x step x TBT target x margin x bias; K5 "
                              "k_decode_pool, one warp per scenario",
-                 "mean_decode_pool_j": float(psum["decode_pool_j"].mean())},
+                 "mean_decode_pool_j": float(psum["decode_pool_j"].mean()),
+                 "global_tally": {k: (int(gtally[k]) if gtally.dtype[k].kind in "iu"
+                                      else float(gtally[k])) for k in gtally.dtype.names},
+                 "reduction": "per-rank scenario tallies, NCCL all-gather, rank-order combine"},
         "roofline": {"bound": "fp64", "kernel": "k_prefill_select (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,

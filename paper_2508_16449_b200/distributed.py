@@ -75,3 +75,84 @@ def combine_summaries(per_rank: np.ndarray, cell_offsets) -> np.ndarray:
         out["min_energy_j"] = np.where(better, s["min_energy_j"], out["min_energy_j"])
         out["argmin_cell"] = np.where(better, g_cell, out["argmin_cell"])
     return out
+
+
+# ------------------------------------------------------------------ decode pool (K5) tallies
+# The end-of-run decode reductions of SURVEY.md 8(e) item 4: per rank, the per-scenario
+# gsb_pool_summary records (energy, SLO counts, trajectory digests) are folded in scenario
+# order into one DECODE_TALLY record; the records of all ranks are all-gathered (NCCL) and
+# combined in rank order, so every rank holds the same bytes.
+DECODE_TALLY_DTYPE = np.dtype([
+    ("n_scenarios", "<i8"), ("decode_pool_j", "<f8"), ("min_decode_pool_j", "<f8"),
+    ("argmin_scenario", "<i8"), ("n_completed", "<i8"), ("n_rejected", "<i8"),
+    ("n_ttft_ok", "<i8"), ("n_tbt_ok", "<i8"), ("tbt_samples", "<i8"),
+    ("tbt_samples_ok", "<i8"), ("n_decisions", "<i8"), ("n_freq_changes", "<i8"),
+    ("digest", "<u8")])
+_COUNTS = ("n_completed", "n_rejected", "n_ttft_ok", "n_tbt_ok", "tbt_samples",
+           "tbt_samples_ok", "n_decisions", "n_freq_changes")
+_M64 = (1 << 64) - 1
+
+
+def _mix64(x: int) -> int:  # splitmix64 finaliser
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def tally_pool(summary: np.ndarray, scen0: int) -> np.ndarray:
+    """Fold the per-scenario pool summaries of global scenarios [scen0, scen0 + N) in order.
+    digest = sum over scenarios of mix(decision ^ freq ^ request digest ^ global index)
+    (mod 2^64): independent of how the scenarios are split over ranks."""
+    out = np.zeros(1, DECODE_TALLY_DTYPE)[0]
+    out["n_scenarios"] = len(summary)
+    out["min_decode_pool_j"] = np.inf
+    out["argmin_scenario"] = -1
+    e = 0.0
+    dig = 0
+    for i, s in enumerate(summary):
+        x = float(s["decode_pool_j"])
+        e = e + x
+        if x < out["min_decode_pool_j"]:
+            out["min_decode_pool_j"] = x
+            out["argmin_scenario"] = scen0 + i
+        d = int(s["decision_digest"]) ^ int(s["freq_digest"]) ^ int(s["request_digest"])
+        dig = (dig + _mix64(d ^ (scen0 + i))) & _M64
+    out["decode_pool_j"] = e
+    for k in _COUNTS:
+        out[k] = int(summary[k].sum())
+    out["digest"] = dig
+    return out
+
+
+def combine_tallies(per_rank: np.ndarray) -> np.ndarray:
+    """Rank-order combine of [R] DECODE_TALLY records (ranks hold consecutive scenario ranges):
+    counts and digests add exactly, energies fold left to right, the argmin keeps the lowest
+    energy, then the lowest global scenario."""
+    per_rank = np.asarray(per_rank, DECODE_TALLY_DTYPE)
+    out = np.zeros(1, DECODE_TALLY_DTYPE)[0]
+    out["min_decode_pool_j"] = np.inf
+    out["argmin_scenario"] = -1
+    e = 0.0
+    dig = 0
+    for s in per_rank:
+        out["n_scenarios"] += s["n_scenarios"]
+        e = e + float(s["decode_pool_j"])
+        if s["argmin_scenario"] >= 0 and (
+                out["argmin_scenario"] < 0 or s["min_decode_pool_j"] < out["min_decode_pool_j"]):
+            out["min_decode_pool_j"] = s["min_decode_pool_j"]
+            out["argmin_scenario"] = s["argmin_scenario"]
+        dig = (dig + int(s["digest"])) & _M64
+        for k in _COUNTS:
+            out[k] += s[k]
+    out["decode_pool_j"] = e
+    out["digest"] = dig
+    return out
+
+
+def gather_records(rec: np.ndarray, device, group=None) -> np.ndarray:
+    """All-gather one numpy record per rank (as bytes) and return the [world] records."""
+    import torch
+    t = torch.from_numpy(np.frombuffer(rec.tobytes(), np.uint8).copy()).to(device)
+    g = gather_summaries(t, group)
+    return g.cpu().numpy().reshape(g.shape[0], -1).view(rec.dtype).reshape(-1)

@@ -114,3 +114,49 @@ def test_two_rank_gloo_combine_matches_single_pass(restate, prof, tmp_path):
         np.testing.assert_array_equal(comb[k], single[k])
     np.testing.assert_allclose(comb["sum_energy_j"], single["sum_energy_j"], rtol=1e-9)
     assert comb["n_infeasible"].sum() > 0 and comb["n_empty"].sum() >= 0
+
+
+def _pool_records(n, seed):
+    """Synthetic per-scenario gsb_pool_summary records (the K5 output format)."""
+    from paper_2508_16449_b200.api import POOL_SUMMARY_DTYPE
+    rng = np.random.default_rng(seed)
+    sm = np.zeros(n, POOL_SUMMARY_DTYPE)
+    sm["decode_pool_j"] = rng.uniform(1e5, 2e5, n)
+    for k in ("n_completed", "n_rejected", "n_ttft_ok", "n_tbt_ok", "tbt_samples",
+              "tbt_samples_ok", "n_decisions", "n_freq_changes"):
+        sm[k] = rng.integers(0, 10_000, n)
+    for k in ("decision_digest", "freq_digest", "request_digest"):
+        sm[k] = rng.integers(0, 2**63, n, dtype=np.int64).astype(np.uint64)
+    sm["decode_pool_j"][n // 3] = 50_000.0  # a unique minimum
+    return sm
+
+
+def _pool_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sm = _pool_records(1000, 3)
+    lo, n = D.scenario_shard(len(sm), world, rank)
+    mine = D.tally_pool(sm[lo:lo + n], lo)
+    per_rank = D.gather_records(np.array([mine], D.DECODE_TALLY_DTYPE), "cpu")
+    np.save(os.path.join(out_dir, f"pool{rank}.npy"), np.array([D.combine_tallies(per_rank)]))
+    dist.destroy_process_group()
+
+
+def test_decode_pool_tallies_gloo_world2(tmp_path):
+    """Decode-side end-of-run reduction: two ranks tally their scenario
+    ranges, all-gather, combine in rank order: identical bytes on both ranks; counts, digest
+    and argmin equal the single-process tally exactly, energy within 1e-12."""
+    import torch.multiprocessing as mp
+    mp.spawn(_pool_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    r0 = np.load(tmp_path / "pool0.npy")
+    r1 = np.load(tmp_path / "pool1.npy")
+    assert r0.tobytes() == r1.tobytes()
+    single = D.tally_pool(_pool_records(1000, 3), 0)
+    g = r0[0]
+    for k in D.DECODE_TALLY_DTYPE.names:
+        if k == "decode_pool_j":
+            assert abs(g[k] - single[k]) <= 1e-12 * abs(single[k])
+        else:
+            assert g[k] == single[k], k
+    assert g["argmin_scenario"] == 1000 // 3
