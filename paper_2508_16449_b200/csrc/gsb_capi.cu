@@ -113,17 +113,20 @@ cudaStream_t gsb_pick_stream(gsb_ctx* ctx, void* stream) {
   return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
 }
 
+// Grow-only scratch. An outgrown buffer is retired, not freed: a CUDA graph captured with it
+// (or work still in flight on any stream) keeps a valid address; retired buffers are freed
+// in gsb_ctx_destroy. Growth is geometric, so the retired total stays below the live size.
 void* gsb_scratch(gsb_ctx* ctx, size_t bytes) {
   if (bytes <= ctx->scratch_bytes) return ctx->d_scratch;
-  if (ctx->d_scratch) {
-    cudaStreamSynchronize(ctx->stream);
-    cudaDeviceSynchronize();
-    cudaFree(ctx->d_scratch);
+  const size_t want = std::max(bytes, ctx->scratch_bytes * 2);
+  void* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
   }
-  ctx->d_scratch = nullptr;
-  ctx->scratch_bytes = 0;
-  if (cudaMalloc(&ctx->d_scratch, bytes) != cudaSuccess) return nullptr;
-  ctx->scratch_bytes = bytes;
+  if (ctx->d_scratch) ctx->retired_scratch.push_back(ctx->d_scratch);
+  ctx->d_scratch = p;
+  ctx->scratch_bytes = want;
   return ctx->d_scratch;
 }
 
@@ -181,6 +184,7 @@ void gsb_ctx_destroy(gsb_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->stage_free) cudaEventDestroy(c->stage_free);
   cudaFree(c->d_scratch);
+  for (void* p : c->retired_scratch) cudaFree(p);
   cudaFree(c->d_ticks);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;

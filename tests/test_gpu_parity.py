@@ -501,6 +501,36 @@ def test_fused_select_summary_equals_standalone(eng, restate, thr):
                 assert s["argmin_cell"] == -1
 
 
+@pytest.mark.parametrize("mode,n_prof,minutes,thr", [
+    ("deadline", 1, 7, [1024]),          # DEADLINE_SLACK, one profile, 7 windows (< one tile)
+    ("fixed", 2, 301, []),               # routing disabled (C = 1), tile tail of 45 cells
+    ("fixed", 3, 90, [256, 512, 1024, 2048]),
+])
+def test_fused_summary_modes_and_shapes(eng, restate, mode, n_prof, minutes, thr):
+    """The fused K2 + summary path on small / ragged shapes, DEADLINE_SLACK windows, 1-3
+    profiles and routing off: per-cell results equal the unfused kernel, summary bytes equal
+    gsb_prefill_summary."""
+    api = _api()
+    profs = synth_profiles(api)[:n_prof]
+    eng.set_profiles(profs)
+    C = len(thr) + 1
+    a, p, _ = restate.gen_poisson_trace(2.0, minutes * 60_000, seed=5 + minutes)
+    routing = api.RoutingConfig(bool(thr), thr or [1024], list(range(C)) if thr else [0, 0])
+    rr = eng.route_bin(a, p, routing, 60_000, want_deadline=(mode == "deadline"))
+    kw = dict(fixed_window_ms=0.95 * 60_000) if mode == "fixed" else {}
+    m = api.L.FIXED_WINDOW if mode == "fixed" else api.L.DEADLINE_SLACK
+    ref = eng.prefill_select(rr, m, **kw)
+    summ = eng.summary_buffer(rr.n_classes)
+    sel = eng.prefill_select(rr, m, summary_out=summ, **kw)
+    assert torch.equal(sel.f_idx, ref.f_idx)
+    assert torch.equal(sel.energy_j.view(torch.int64), ref.energy_j.view(torch.int64))
+    busy = rr.count.view(torch.int32) != 0  # PrefillFreqCommand::window_ms exists per command
+    assert torch.equal(sel.window_ms.view(torch.int64)[busy], ref.window_ms.view(torch.int64)[busy])
+    fused = summ.cpu().numpy().view(eng.SUMMARY_DTYPE).reshape(n_prof, rr.n_classes)
+    assert fused.tobytes() == eng.prefill_summary(sel, rr.n_classes).tobytes()
+    assert int(fused["n_cmd"].sum() + fused["n_empty"].sum()) == n_prof * rr.n_cells
+
+
 def test_summary_is_deterministic_and_exact_counts(eng, restate):
     api = _api()
     eng.set_profiles([api.GpuProfile.default_profile()])
