@@ -768,6 +768,8 @@ k_prefill_select_c(const __grid_constant__ SelectParams sp, const __grid_constan
 #undef GSB_SEL
 }
 
+// (Measured and rejected: two cells per thread sharing the per-clock table loads — 47 vs 28 us,
+// more code and half the busy warps; 6 CTAs/SM at 40 registers — no change.)
 // K2 with the per-class summary fused: CTA (x, p) owns the 256-cell tile x of profile p. It
 // compacts the tile's NON-EMPTY cells onto its first threads (ballot + warp-offset scan), so
 // the 81-clock loop runs with every lane busy; warps with nothing to evaluate (and not needed
