@@ -120,7 +120,7 @@ struct MinU64 {
 __global__ void __launch_bounds__(kTrThreads)
 k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt,
             unsigned long long* __restrict__ first_end) {
-  __shared__ __align__(16) unsigned char sm[kTile + kPre];
+  __shared__ __align__(16) unsigned char sm[kTile + kPre + 16];
   using BR = cub::BlockReduce<unsigned long long, kTrThreads>;
   __shared__ typename BR::TempStorage tmp;
   const int64_t t = blockIdx.x;
@@ -154,7 +154,7 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
             int64_t* __restrict__ arrival, int32_t* __restrict__ prompt,
             int32_t* __restrict__ output, uint8_t* __restrict__ slo_cls,
             uint32_t* __restrict__ line_of_row, unsigned long long* __restrict__ err) {
-  __shared__ __align__(16) unsigned char sm[kTile + kPre];
+  __shared__ __align__(16) unsigned char sm[kTile + kPre + 16];
   using BS = cub::BlockScan<unsigned long long, kTrThreads>;
   using BS2 = cub::BlockScan<long long, kTrThreads>;
   __shared__ typename BS::TempStorage tmp;
@@ -210,15 +210,75 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
     // one pass over the line: columns split on ',' (a trailing ',' adds no column,
     // std::getline(ss, col, ',')), from_chars<int64> on columns 0-2 (optional '-', >= 1
     // digit, the whole column, no overflow), the class column's bytes
-    // one pass over the line: columns split on ',' (a trailing ',' adds no column,
-    // std::getline(ss, col, ',')), from_chars<int64> on columns 0-2 (optional '-', >= 1
-    // digit, the whole column, no overflow), the class column's bytes
-    unsigned long long v0 = 0, v1 = 0, v2 = 0, cur = 0;  // registers, no indexed arrays
+    unsigned long long v0 = 0, v1 = 0, v2 = 0;
     bool ok0 = false, ok1 = false, ok2 = false;
+    unsigned char c0 = 0, c1 = 0;
+    int clen = 0, ncols;
+    const int len = static_cast<int>(min(en - st, static_cast<int64_t>(INT32_MAX)));
+    bool general = !(in_sm && len <= 64);
+    if (!general) {
+      // fast path: the line's comma mask from 4-byte SIMD compares, then one tight digit loop
+      // per column (no per-byte branching)
+      const unsigned char* q = sm + (st - s0);
+      const int o = static_cast<int>(reinterpret_cast<uintptr_t>(q) & 3);
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(q - o);
+      unsigned long long cm = 0;
+      const int nw = (len + o + 3) >> 2;
+      for (int k = 0; k < nw; ++k) {
+        const uint32_t e = __vcmpeq4(w[k], 0x2c2c2c2cu) & 0x80808080u;
+        const unsigned long long bits = (e * 0x00204081u) >> 28;  // bit j: byte j is ','
+        const int sh = 4 * k - o;
+        cm |= sh >= 64 ? 0ull : (sh >= 0 ? (bits << sh) : (bits >> -sh));
+      }
+      if (len < 64) cm &= (1ull << len) - 1ull;
+      const bool trailing = (cm >> (len - 1)) & 1ull;
+      ncols = __popcll(cm) + (trailing ? 0 : 1);  // a final ',' adds no column
+      int fs[4], fe[4];
+      unsigned long long m = cm;
+      int f0 = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = m ? __ffsll(static_cast<long long>(m)) - 1 : len;
+        m &= m - 1ull;
+        fs[k] = f0;
+        fe[k] = e;
+        f0 = min(e + 1, len);
+      }
+      // <= 18 digits cannot overflow int64, so the digit loop is a plain multiply-add; longer
+      // columns (leading zeros, overflow candidates) send the line to the general path
+      auto num = [&](int a0, int a1, unsigned long long& v, bool& ok) {
+        const bool neg = a1 > a0 && q[a0] == '-';
+        const int d0 = a0 + (neg ? 1 : 0);
+        if (a1 - d0 > 18) general = true;
+        bool good = a1 > d0;
+        unsigned long long val = 0;
+        for (int i = d0; i < a1; ++i) {
+          const unsigned d = static_cast<unsigned>(q[i]) - '0';
+          good = good && d <= 9;
+          val = val * 10ull + d;
+        }
+        ok = good;
+        v = neg ? 0ull - val : val;
+      };
+      if (ncols == expect) {
+        num(fs[0], fe[0], v0, ok0);
+        num(fs[1], fe[1], v1, ok1);
+        num(fs[2], fe[2], v2, ok2);
+        if (expect == 4) {
+          clen = fe[3] - fs[3];
+          c0 = clen > 0 ? q[fs[3]] : 0;
+          c1 = clen > 1 ? q[fs[3] + 1] : 0;
+        }
+      }
+    }
+    if (general) {
+    // general path (long lines or columns, lines starting before the staged bytes): one
+    // scalar pass
+    c0 = c1 = 0;
+    clen = 0;
+    unsigned long long cur = 0;
     int col = 0, flen = 0, sig = 0;
     bool neg = false, bad = false;
-    unsigned char c0 = 0, c1 = 0;
-    int clen = 0;
     auto close_field = [&]() {
       if (col < 3) {
         const unsigned long long lim = neg ? 0x8000000000000000ull : 0x7fffffffffffffffull;
@@ -261,12 +321,12 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
       }
       ++flen;
     }
-    int ncols;
     if (last_comma) {
       ncols = col;  // the empty text after the final ',' is not a column
     } else {
       close_field();
       ncols = col;
+    }
     }
     int detail = 0;
     if (ncols != expect) detail = GSB_TRACE_DETAIL_COLUMNS;
