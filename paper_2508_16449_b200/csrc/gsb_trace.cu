@@ -83,11 +83,9 @@ __device__ __forceinline__ unsigned eq_mask16(const uint4& q, unsigned c4) {
 // bit k <-> byte b0 + k. A line ends at each '\n' and at n when the file does not end with
 // '\n'; the line ending at b is empty iff byte b-1 is '\n' (or b is the file start) or byte
 // b-1 is '\r' preceded by '\n' or the file start (one '\r' is stripped).
-__device__ __forceinline__ void line_ends16(const unsigned char* sm, int64_t s0, int64_t n,
-                                            int64_t b0, bool last_is_nl, unsigned* ends,
-                                            unsigned* nonempty) {
-  const uint4 q = *reinterpret_cast<const uint4*>(sm + (b0 - s0));
-  const unsigned char p1 = sm[b0 - 1 - s0], p2 = sm[b0 - 2 - s0];
+__device__ __forceinline__ void line_ends16_q(const uint4& q, unsigned char p1, unsigned char p2,
+                                              int64_t n, int64_t b0, bool last_is_nl,
+                                              unsigned* ends, unsigned* nonempty) {
   unsigned nl = eq_mask16(q, 0x0a0a0a0au), cr = eq_mask16(q, 0x0d0d0d0du);
   const int64_t live = n - b0;  // bytes of this chunk inside the file
   const unsigned in = live >= 16 ? 0xffffu : (live <= 0 ? 0u : (1u << live) - 1u);
@@ -104,45 +102,50 @@ __device__ __forceinline__ void line_ends16(const unsigned char* sm, int64_t s0,
   *nonempty = e & ~empty;
 }
 
+__device__ __forceinline__ void line_ends16(const unsigned char* sm, int64_t s0, int64_t n,
+                                            int64_t b0, bool last_is_nl, unsigned* ends,
+                                            unsigned* nonempty) {
+  const uint4 q = *reinterpret_cast<const uint4*>(sm + (b0 - s0));
+  line_ends16_q(q, sm[b0 - 1 - s0], sm[b0 - 2 - s0], n, b0, last_is_nl, ends, nonempty);
+}
+
 struct MaxI64 {
   __device__ __forceinline__ long long operator()(long long a, long long b) const {
     return a > b ? a : b;
   }
 };
 
-struct MinU64 {
-  __device__ __forceinline__ unsigned long long operator()(unsigned long long a,
-                                                           unsigned long long b) const {
-    return a < b ? a : b;
-  }
-};
 
+// Count pass: no staging and no block barrier. Thread g reads the 16 bytes [16g, 16g + 16) with
+// one vector load and takes the two bytes before them from its left neighbour (a shuffle); the
+// warp's packed (line ends << 32 | non-empty lines) sum goes to its 4 KB tile with one atomic
+// add (integer, so the per-tile totals are exact and order-free).
 __global__ void __launch_bounds__(kTrThreads)
-k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt,
-            unsigned long long* __restrict__ first_end) {
-  __shared__ __align__(16) unsigned char sm[kTile + kPre + 16];
-  using BR = cub::BlockReduce<unsigned long long, kTrThreads>;
-  __shared__ typename BR::TempStorage tmp;
-  const int64_t t = blockIdx.x;
-  stage_tile(tp, t, sm);
-  __syncthreads();
-  const int64_t s0 = t * kTile - kPre;
-  const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
-  const int64_t b0 = t * kTile + 16 * threadIdx.x;
-  unsigned ends, nonempty;
-  line_ends16(sm, s0, tp.n, b0, last_is_nl, &ends, &nonempty);
-  const unsigned nl = __popc(ends), ne = __popc(nonempty);
-  const int64_t first = ends ? b0 + __ffs(static_cast<int>(ends)) - 1 : INT64_MAX;
-  const unsigned long long packed =
-      (static_cast<unsigned long long>(nl) << 32) | static_cast<unsigned long long>(ne);
-  const unsigned long long tot = BR(tmp).Sum(packed);
-  __syncthreads();
-  const unsigned long long fmin = BR(tmp).Reduce(static_cast<unsigned long long>(first),
-                                                 MinU64{});
-  if (threadIdx.x == 0) {
-    tile_cnt[t] = tot;
-    if (fmin != static_cast<unsigned long long>(INT64_MAX)) atomicMin(first_end, fmin);
+k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b0 = (static_cast<int64_t>(blockIdx.x) * kTrThreads + threadIdx.x) * 16;
+  uint4 q;
+  if (b0 + 16 <= tp.n && (reinterpret_cast<uintptr_t>(tp.bytes + b0) & 15) == 0) {
+    q = __ldg(reinterpret_cast<const uint4*>(tp.bytes + b0));
+  } else {
+    unsigned char c[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) c[k] = byte_at(tp.bytes, tp.n, b0 + k);
+    memcpy(&q, c, 16);
   }
+  const unsigned left = __shfl_up_sync(0xffffffffu, q.w, 1);
+  unsigned char p1 = static_cast<unsigned char>(left >> 24), p2 = static_cast<unsigned char>(left >> 16);
+  if (lane == 0) {
+    p1 = byte_at(tp.bytes, tp.n, b0 - 1);
+    p2 = byte_at(tp.bytes, tp.n, b0 - 2);
+  }
+  const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
+  unsigned ends, nonempty;
+  line_ends16_q(q, p1, p2, tp.n, b0, last_is_nl, &ends, &nonempty);
+  unsigned long long v = (static_cast<unsigned long long>(__popc(ends)) << 32) | __popc(nonempty);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0 && v) atomicAdd(tile_cnt + b0 / kTile, v);
 }
 
 __device__ __forceinline__ unsigned long long err_key(int64_t line, int detail) {
@@ -366,6 +369,26 @@ __global__ void k_csv_monotone(int64_t n_rows, const int64_t* __restrict__ arriv
   if (arrival[r] < arrival[r - 1]) atomicMin(err, err_key(line_of_row[r], GSB_TRACE_DETAIL_MONOTONE));
 }
 
+// the header's end (line 0): one warp walks the file from byte 0, 32 bytes per step (ballot of
+// the line-end bytes), so the usual short header costs one coalesced load
+__global__ void k_csv_header_end(const TraceParams tp, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x;
+  const bool last_is_nl = tp.n > 0 && tp.bytes[tp.n - 1] == '\n';
+  for (int64_t b0 = 0;; b0 += 32) {
+    const int64_t b = b0 + lane;
+    const bool e = b < tp.n ? tp.bytes[b] == '\n' : (b == tp.n && tp.n > 0 && !last_is_nl);
+    const unsigned m = __ballot_sync(0xffffffffu, e);
+    if (m) {
+      if (lane == 0) out[1] = b0 + __ffs(static_cast<int>(m)) - 1;
+      return;
+    }
+    if (b0 + 32 > tp.n) {  // no end at all (n == 0)
+      if (lane == 0) out[1] = tp.n;
+      return;
+    }
+  }
+}
+
 // the byte range of line L (error reporting): one thread, binary search of the tile prefix
 __global__ void k_csv_locate(const TraceParams tp, const unsigned long long* __restrict__ tile_pref,
                              int64_t L, int64_t* __restrict__ out /* [2]: start, end */) {
@@ -490,7 +513,7 @@ int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t 
   tp.n = n_bytes;
   tp.n_tiles = n_bytes / kTile + 1;  // the virtual end at n may open a tile
   tp.threshold = class_threshold;
-  // scratch: [tile counts + 1][prefix + 1][first_end][err][locate 2][line_of_row (cap)][cub tmp]
+  // scratch: [tile counts + 1][prefix + 1][spare][err][locate 2][line_of_row (cap)][cub tmp]
   const size_t nt = static_cast<size_t>(tp.n_tiles) + 1;
   size_t cub_tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_tmp, static_cast<unsigned long long*>(nullptr),
@@ -507,11 +530,12 @@ int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t 
   auto* line_of_row = reinterpret_cast<uint32_t*>(scr + head);
   void* d_cub = scr + ((head + lor + 255) / 256) * 256;
   cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s);
-  cudaMemsetAsync(first_end, 0xff, 2 * sizeof(unsigned long long), s);  // first_end, err = max
-  k_csv_count<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(tp, cnt, first_end);
+  cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);  // err = none
+  k_csv_count<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(tp, cnt);
   cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, cnt, pref, static_cast<int>(nt), s);
+  k_csv_header_end<<<1, 32, 0, s>>>(tp, loc);  // line 0 (the header): its end
   unsigned long long h[2];
-  cudaMemcpyAsync(&h[0], first_end, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&h[0], loc + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&h[1], pref + nt - 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_parse");
   const int64_t header_end = static_cast<int64_t>(h[0]);
