@@ -62,6 +62,8 @@ constexpr unsigned kFull = 0xffffffffu;
 __global__ void __launch_bounds__(256)
 k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms, int64_t w0,
                 int64_t n_windows, int64_t* __restrict__ bounds) {
+  gsb::grid_dep_wait();    // the arrivals may come from the previous launch (e.g. a copy)
+  gsb::grid_dep_launch();  // K1b may be scheduled now; it waits for this grid's bounds
   const double rd = 1.0 / static_cast<double>(window_ms);
   const int lane = threadIdx.x & 31;
   const int64_t span = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) *
@@ -193,6 +195,8 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
 #pragma unroll
   for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) th[k] = rp.thr[k];
   const int64_t w_first = static_cast<int64_t>(blockIdx.x) * G;
+  gsb::grid_dep_wait();  // K1a's bounds (programmatic dependent launch)
+  gsb::grid_dep_launch();
   for (int k = tid; k <= G; k += NW * 32) s.bnd[k] = bounds[min(w_first + k, rp.n_windows)];
   for (int k = tid; k < K; k += NW * 32) {
     s.cnt[k] = 0;
@@ -379,9 +383,10 @@ int launch_route_bin(const RouteParams& rp, const int64_t* d_arrival, const int3
                            static_cast<int>(smem)) != cudaSuccess)
     return -1;
   const unsigned blocks = static_cast<unsigned>((rp.n_windows + G - 1) / G);
-  k_route_bin<C, P, DL><<<blocks, kRouteWarps * 32, smem, s>>>(rp, d_arrival, d_prompt, d_bounds,
-                                                               d_class, d_count, d_t_ref,
-                                                               d_min_deadline);
+  if (gsb::launch_pdl(k_route_bin<C, P, DL>, dim3(blocks), dim3(kRouteWarps * 32), smem, s, rp,
+                      d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref,
+                      d_min_deadline) != cudaSuccess)
+    return -1;
   return 0;
 }
 
@@ -496,6 +501,7 @@ __device__ __forceinline__ Part part_shfl_down(const Part& v, int o) {
 __global__ void __launch_bounds__(32)
 k_summary_final(const Part* __restrict__ parts, int nx, gsb_class_summary* __restrict__ out) {
   const int pc = blockIdx.x, lane = threadIdx.x;
+  gsb::grid_dep_wait();  // the tile partials (programmatic dependent launch)
   Part a = part_identity();
   const Part* src = parts + static_cast<long long>(pc) * nx;
 #pragma unroll 4
@@ -789,6 +795,8 @@ k_prefill_select_sum(const __grid_constant__ SelectParams sp, const __grid_const
   const int64_t n = sp.n_cells;
   const int p = static_cast<int>(blockIdx.y), x = static_cast<int>(blockIdx.x);
   const int64_t cell = static_cast<int64_t>(x) * kSumCta + t;
+  gsb::grid_dep_wait();  // K1's cells (programmatic dependent launch)
+  gsb::grid_dep_launch();
   const bool live = cell < n;
   const bool busy = live && (!count || count[cell] != 0);
   if (live && !busy) {  // empty queue: no command
@@ -1300,10 +1308,11 @@ int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t 
       SumArgs sa{static_cast<Part*>(gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(tiles) *
                                                          static_cast<size_t>(cfg->n_classes)))};
       if (!sa.parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "select: scratch allocation failed");
-      k_prefill_select_sum<81><<<grid, kSumCta, 0, s>>>(sp, cs, d_t_ref, d_count, d_min_deadline,
-                                                         d_window, d_f_idx, d_energy, sa);
-      k_summary_final<<<static_cast<unsigned>(ctx->n_profiles * cfg->n_classes), 32, 0, s>>>(
-          sa.parts, static_cast<int>(want), d_summary);
+      gsb::launch_pdl(k_prefill_select_sum<81>, grid, dim3(kSumCta), 0, s, sp, cs, d_t_ref,
+                      d_count, d_min_deadline, d_window, d_f_idx, d_energy, sa);
+      gsb::launch_pdl(k_summary_final, dim3(static_cast<unsigned>(ctx->n_profiles * cfg->n_classes)),
+                      dim3(32), 0, s, static_cast<const Part*>(sa.parts), static_cast<int>(want),
+                      d_summary);
       return gsb_check_launch(ctx, "prefill_select");
     }
     k_prefill_select_c<81><<<grid, 256, 0, s>>>(sp, cs, d_t_ref, d_count, d_min_deadline,
