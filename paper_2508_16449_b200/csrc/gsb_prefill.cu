@@ -178,13 +178,13 @@ struct RouteSmem {  // one CTA
   unsigned long long mdl[DL ? K : 1];
 };
 
-template <int C, int P, bool DL>
-__global__ void __launch_bounds__(kRouteWarps * 32, P == 1 ? 6 : kRouteMinBlocks)
+template <int C, int P, bool DL, int GW>
+__global__ void __launch_bounds__(kRouteWarps * 32, GW * C > 64 ? 6 : kRouteMinBlocks)
 k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
             const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
             uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
             double* __restrict__ t_ref, double* __restrict__ min_deadline) {
-  constexpr int G = 32 / P, K = G * C, E = (K + 31) / 32, NW = kRouteWarps;
+  constexpr int G = GW, K = G * C, E = (K + 31) / 32, NW = kRouteWarps;
   constexpr int kNever = 0x3fffffff;
   using S = RouteSmem<K, DL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -373,21 +373,36 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
   }
 }
 
-template <int C, int P, bool DL>
-int launch_route_bin(const RouteParams& rp, const int64_t* d_arrival, const int32_t* d_prompt,
-                     const int64_t* d_bounds, uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
-                     double* d_min_deadline, cudaStream_t s) {
-  constexpr int G = 32 / P;
+template <int C, int P, bool DL, int G>
+int launch_route_bin_g(const RouteParams& rp, const int64_t* d_arrival, const int32_t* d_prompt,
+                       const int64_t* d_bounds, uint8_t* d_class, uint32_t* d_count,
+                       double* d_t_ref, double* d_min_deadline, cudaStream_t s) {
   const size_t smem = sizeof(RouteSmem<G * C, DL>);
-  if (cudaFuncSetAttribute(k_route_bin<C, P, DL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_route_bin<C, P, DL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
     return -1;
   const unsigned blocks = static_cast<unsigned>((rp.n_windows + G - 1) / G);
-  if (gsb::launch_pdl(k_route_bin<C, P, DL>, dim3(blocks), dim3(kRouteWarps * 32), smem, s, rp,
+  if (gsb::launch_pdl(k_route_bin<C, P, DL, G>, dim3(blocks), dim3(kRouteWarps * 32), smem, s, rp,
                       d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref,
                       d_min_deadline) != cudaSuccess)
     return -1;
   return 0;
+}
+
+// G = 32 / P windows per CTA (lanes (window, profile) fill the fold warp). With one profile and
+// dense windows (32 windows would not fit one chunk) G = 8: four times the CTAs, one chunk each,
+// for small traces that would otherwise run a few long CTAs (fold lanes are cheap at P = 1).
+template <int C, int P, bool DL>
+int launch_route_bin(const RouteParams& rp, int64_t n_req, const int64_t* d_arrival,
+                     const int32_t* d_prompt, const int64_t* d_bounds, uint8_t* d_class,
+                     uint32_t* d_count, double* d_t_ref, double* d_min_deadline, cudaStream_t s) {
+  if constexpr (P == 1) {
+    if (n_req > rp.n_windows * (kRouteCap / 32))
+      return launch_route_bin_g<C, P, DL, 8>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,
+                                             d_t_ref, d_min_deadline, s);
+  }
+  return launch_route_bin_g<C, P, DL, 32 / P>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,
+                                              d_t_ref, d_min_deadline, s);
 }
 
 // ---------------------------------------------------------------- K1c: Dispatcher FIFO
@@ -1203,7 +1218,6 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const i
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
   if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "route: no profiles set");
-  (void)n_req;
   RouteParams rp = make_route_params(ctx, cfg);
   rp.want_deadline = d_min_deadline != nullptr;
   const int P = ctx->n_profiles;
@@ -1214,12 +1228,12 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const i
   switch (key) {
 #define GSB_RB(CC, PP)                                                                          \
   case ((CC)-1) * 8 + ((PP)-1) * 2:                                                            \
-    lrc = launch_route_bin<CC, PP, false>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count, \
-                                          d_t_ref, d_min_deadline, s);                         \
+    lrc = launch_route_bin<CC, PP, false>(rp, n_req, d_arrival, d_prompt, d_bounds, d_class,   \
+                                          d_count, d_t_ref, d_min_deadline, s);                \
     break;                                                                                      \
   case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                        \
-    lrc = launch_route_bin<CC, PP, true>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,  \
-                                         d_t_ref, d_min_deadline, s);                          \
+    lrc = launch_route_bin<CC, PP, true>(rp, n_req, d_arrival, d_prompt, d_bounds, d_class,    \
+                                         d_count, d_t_ref, d_min_deadline, s);                 \
     break;
 #define GSB_RB_P(CC) GSB_RB(CC, 1) GSB_RB(CC, 2) GSB_RB(CC, 3) GSB_RB(CC, 4)
     GSB_RB_P(1) GSB_RB_P(2) GSB_RB_P(3) GSB_RB_P(4) GSB_RB_P(5) GSB_RB_P(6) GSB_RB_P(7) GSB_RB_P(8)
