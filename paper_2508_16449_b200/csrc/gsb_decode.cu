@@ -117,7 +117,7 @@ struct ReplayParams {
 };
 
 template <bool COUNTS, bool RECORDS>
-__global__ void __launch_bounds__(128) k_decode_replay(const __grid_constant__ ReplayParams rp) {
+__global__ void __launch_bounds__(128, 5) k_decode_replay(const __grid_constant__ ReplayParams rp) {
   const gsb_replay_args& a = rp.a;
   const int64_t n = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (n >= a.n_traj) return;
