@@ -131,3 +131,36 @@ def test_round_trip_and_route(gsb, restate, tmp_path):
     rr_np = gsb.route_bin(a, p, api.RoutingConfig(True, [512, 1024], [0, 1, 2]), 60_000)
     assert torch.equal(rr_csv.cls, rr_np.cls) and torch.equal(rr_csv.count, rr_np.count)
     assert torch.equal(rr_csv.t_ref.view(torch.int64), rr_np.t_ref.view(torch.int64))
+
+
+def test_graph_survives_scratch_growth(gsb, restate):
+    """A CUDA graph captured over the fused K2 (which uses the context's scratch) stays valid
+    after a later call grows the scratch (a large trace parse): outgrown scratch buffers are
+    retired, not freed, so the graph's addresses remain live."""
+    from paper_2508_16449_b200 import api
+    gsb.set_profiles([api.GpuProfile.default_profile()])
+    a, p, _ = restate.gen_poisson_trace(5.0, 3_600_000, seed=8)
+    d_a = torch.as_tensor(a, device="cuda")
+    d_p = torch.as_tensor(p, device="cuda")
+    routing = api.RoutingConfig(True, [512, 1024], [0, 1, 2])
+    rr = gsb.route_bin(d_a, d_p, routing, 60_000)
+    summ = gsb.summary_buffer(3)
+    sel = gsb.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=57_000.0, summary_out=summ)
+    want_f, want_s = sel.f_idx.clone(), summ.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gsb.route_bin(d_a, d_p, routing, 60_000, 0, rr.n_windows, out=rr)  # no host reads
+            gsb.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=57_000.0, out=sel,
+                               summary_out=summ)
+    torch.cuda.current_stream().wait_stream(s)
+    _, _, _, _, text = _day_trace(restate)
+    gsb.parse_trace(text)  # grows the scratch well past the graph's partial buffer
+    sel.f_idx.zero_()
+    summ.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(sel.f_idx, want_f)
+    assert torch.equal(summ, want_s)
