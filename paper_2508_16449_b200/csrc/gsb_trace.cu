@@ -30,8 +30,9 @@
 
 namespace {
 
-constexpr int kTile = 4096;
-constexpr int kTrThreads = 256;  // x 16 bytes = one tile
+constexpr int kTrThreads = 256;
+constexpr int kPerThread = 32;  // parse: bytes per thread (two 16-byte groups)
+constexpr int kTile = kTrThreads * kPerThread;  // 8 KB
 constexpr int kPre = 256;        // bytes staged before the tile (line starts)
 constexpr unsigned long long kNoErr = ~0ull;
 
@@ -167,9 +168,15 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
   __syncthreads();
   const int64_t s0 = t * kTile - kPre;
   const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
-  const int64_t b0 = t * kTile + 16 * threadIdx.x;
+  const int64_t b0 = t * kTile + kPerThread * threadIdx.x;
   unsigned ends, nonempty;  // bit k: byte b0 + k ends a (non-empty) line
-  line_ends16(sm, s0, tp.n, b0, last_is_nl, &ends, &nonempty);
+  {
+    unsigned e0, n0, e1, n1;
+    line_ends16(sm, s0, tp.n, b0, last_is_nl, &e0, &n0);
+    line_ends16(sm, s0, tp.n, b0 + 16, last_is_nl, &e1, &n1);
+    ends = e0 | (e1 << 16);
+    nonempty = n0 | (n1 << 16);
+  }
   const unsigned nl = __popc(ends), ne = __popc(nonempty);
   unsigned long long pre;
   BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre);
@@ -531,7 +538,8 @@ int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t 
   void* d_cub = scr + ((head + lor + 255) / 256) * 256;
   cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s);
   cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);  // err = none
-  k_csv_count<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(tp, cnt);
+  k_csv_count<<<static_cast<unsigned>((n_bytes / 16 + 1 + kTrThreads - 1) / kTrThreads), kTrThreads,
+                0, s>>>(tp, cnt);
   cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, cnt, pref, static_cast<int>(nt), s);
   k_csv_header_end<<<1, 32, 0, s>>>(tp, loc);  // line 0 (the header): its end
   unsigned long long h[2];
