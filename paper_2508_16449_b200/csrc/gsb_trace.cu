@@ -31,7 +31,7 @@
 namespace {
 
 constexpr int kTrThreads = 256;
-constexpr int kPerThread = 32;  // parse: bytes per thread (two 16-byte groups)
+constexpr int kPerThread = 64;  // parse: bytes per thread (four 16-byte groups)
 constexpr int kTile = kTrThreads * kPerThread;  // 8 KB
 constexpr int kPre = 256;        // bytes staged before the tile (line starts)
 constexpr unsigned long long kNoErr = ~0ull;
@@ -169,22 +169,22 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
   const int64_t s0 = t * kTile - kPre;
   const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
   const int64_t b0 = t * kTile + kPerThread * threadIdx.x;
-  unsigned ends, nonempty;  // bit k: byte b0 + k ends a (non-empty) line
-  {
-    unsigned e0, n0, e1, n1;
-    line_ends16(sm, s0, tp.n, b0, last_is_nl, &e0, &n0);
-    line_ends16(sm, s0, tp.n, b0 + 16, last_is_nl, &e1, &n1);
-    ends = e0 | (e1 << 16);
-    nonempty = n0 | (n1 << 16);
+  unsigned long long ends = 0, nonempty = 0;  // bit k: byte b0 + k ends a (non-empty) line
+#pragma unroll
+  for (int h = 0; h < kPerThread / 16; ++h) {
+    unsigned e, ne16;
+    line_ends16(sm, s0, tp.n, b0 + 16 * h, last_is_nl, &e, &ne16);
+    ends |= static_cast<unsigned long long>(e) << (16 * h);
+    nonempty |= static_cast<unsigned long long>(ne16) << (16 * h);
   }
-  const unsigned nl = __popc(ends), ne = __popc(nonempty);
+  const unsigned nl = __popcll(ends), ne = __popcll(nonempty);
   unsigned long long pre;
   BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre);
   __syncthreads();
   // the previous line end before this thread's bytes: exclusive max-scan of the threads' last
   // ends; the tile's first line looks back into the previous tile (one thread per tile)
   long long prev;
-  BS2(tmp2).ExclusiveScan(ends ? static_cast<long long>(b0 + 31 - __clz(ends)) : -1LL, prev,
+  BS2(tmp2).ExclusiveScan(ends ? static_cast<long long>(b0 + 63 - __clzll(ends)) : -1LL, prev,
                           -1LL, MaxI64{});
   if (threadIdx.x == 0) prev = -1;
   const unsigned long long tp0 = tile_pref[t];
@@ -193,7 +193,7 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
                             static_cast<int64_t>(pre & 0xffffffffull);
   const int expect = tp.has_class ? 4 : 3;
   if (ends && prev < 0) {  // this thread holds the tile's first line end
-    int64_t st = b0 + __ffs(static_cast<int>(ends)) - 2;
+    int64_t st = b0 + __ffsll(static_cast<long long>(ends)) - 2;
     while (st >= 0) {
       const unsigned char c = st >= s0 ? sm[st - s0] : __ldg(tp.bytes + st);
       if (c == '\n') break;
@@ -202,12 +202,12 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
     prev = st;  // -1 at the file start
   }
   while (ends) {
-    const int k = __ffs(static_cast<int>(ends)) - 1;
-    ends &= ends - 1;
+    const int k = __ffsll(static_cast<long long>(ends)) - 1;
+    ends &= ends - 1ull;
     const int64_t b = b0 + k;
     const int64_t st = prev + 1;
     prev = b;
-    const bool ne_line = (nonempty >> k) & 1u;
+    const bool ne_line = (nonempty >> k) & 1ull;
     const int64_t my_line = line++;
     if (!ne_line) continue;  // empty line: skipped (the row counter still advanced)
     const int64_t ne_idx = nonempty_before++;
