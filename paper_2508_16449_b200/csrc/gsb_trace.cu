@@ -117,33 +117,92 @@ struct MaxI64 {
 };
 
 
-// Count pass: no staging and no block barrier. Thread g reads the 16 bytes [16g, 16g + 16) with
-// one vector load and takes the two bytes before them from its left neighbour (a shuffle); the
-// warp's packed (line ends << 32 | non-empty lines) sum goes to its 4 KB tile with one atomic
-// add (integer, so the per-tile totals are exact and order-free).
+// line ends and empty lines among the 16 bytes q = [b0, b0 + 16), counts only: exact per-byte
+// match masks (0x80 in each matching byte of a 64-bit word), one-byte shifts across the two
+// words for the "previous byte" tests, popcounts. p1, p2: bytes b0-1, b0-2.
+__device__ __forceinline__ void count16(const TraceParams& tp, const uint4& q, unsigned char p1,
+                                        unsigned char p2, int64_t b0, bool last_is_nl,
+                                        unsigned& n_end, unsigned& n_emp) {
+  const unsigned long long w0 = (static_cast<unsigned long long>(q.y) << 32) | q.x;
+  const unsigned long long w1 = (static_cast<unsigned long long>(q.w) << 32) | q.z;
+  auto match = [](unsigned long long w, unsigned long long c8) {
+    const unsigned long long x = w ^ c8;
+    return ~(((x & 0x7f7f7f7f7f7f7f7full) + 0x7f7f7f7f7f7f7f7full) | x | 0x7f7f7f7f7f7f7f7full);
+  };
+  const int64_t live = tp.n - b0;  // bytes of this chunk inside the file
+  unsigned long long in0 = ~0ull, in1 = ~0ull;
+  if (live < 16) {
+    in0 = live >= 8 ? ~0ull : (live <= 0 ? 0ull : (1ull << (8 * live)) - 1ull);
+    in1 = live <= 8 ? 0ull : (1ull << (8 * (live - 8))) - 1ull;
+  }
+  const unsigned long long nl0 = match(w0, 0x0a0a0a0a0a0a0a0aull) & in0,
+                           nl1 = match(w1, 0x0a0a0a0a0a0a0a0aull) & in1;
+  const unsigned long long cr0 = match(w0, 0x0d0d0d0d0d0d0d0dull) & in0,
+                           cr1 = match(w1, 0x0d0d0d0d0d0d0d0dull) & in1;
+  // previous-byte masks (byte j <-> byte j-1 of the chunk); the byte before the file start
+  // acts as '\n'
+  const unsigned long long p1nl = (p1 == '\n' || b0 == 0) ? 0x80ull : 0ull;
+  const unsigned long long p1cr = p1 == '\r' ? 0x80ull : 0ull;
+  const unsigned long long p2nl = p2 == '\n' ? 0x80ull : 0ull;
+  const unsigned long long nlm1_0 = (nl0 << 8) | p1nl, nlm1_1 = (nl1 << 8) | (nl0 >> 56);
+  const unsigned long long crm1_0 = (cr0 << 8) | p1cr, crm1_1 = (cr1 << 8) | (cr0 >> 56);
+  const unsigned long long nlm2_0 = (nl0 << 16) | (p1nl << 8) | p2nl,
+                           nlm2_1 = (nl1 << 16) | (nl0 >> 48);
+  const unsigned long long emp0 = nl0 & (nlm1_0 | (crm1_0 & nlm2_0));
+  const unsigned long long emp1 = nl1 & (nlm1_1 | (crm1_1 & nlm2_1));
+  n_end = __popcll(nl0) + __popcll(nl1);
+  n_emp = __popcll(emp0) + __popcll(emp1);
+  if (!last_is_nl && tp.n > 0 && live >= 0 && live < 16) {  // the virtual end at n
+    ++n_end;
+    // the last line is empty iff its only content is one '\r' after a line start
+    const int64_t b = tp.n;
+    const unsigned char c1 = byte_at(tp.bytes, tp.n, b - 1), c2 = byte_at(tp.bytes, tp.n, b - 2);
+    if (c1 == '\r' && (b - 1 == 0 || c2 == '\n')) ++n_emp;
+  }
+}
+
+// Count pass: no staging and no block barrier. Thread g reads the 64 bytes [64g, 64g + 64)
+// with four independent 16-byte vector loads, takes the two bytes before them from its left
+// neighbour (a shuffle), and the warp's packed (line ends << 32 | non-empty lines) sum goes to
+// its tile with one atomic add (integer, so the per-tile totals are exact and order-free).
+constexpr int kCountChunks = 4;
 __global__ void __launch_bounds__(kTrThreads)
 k_csv_count(const TraceParams tp, unsigned long long* __restrict__ tile_cnt) {
   const int lane = threadIdx.x & 31;
-  const int64_t b0 = (static_cast<int64_t>(blockIdx.x) * kTrThreads + threadIdx.x) * 16;
-  uint4 q;
-  if (b0 + 16 <= tp.n && (reinterpret_cast<uintptr_t>(tp.bytes + b0) & 15) == 0) {
-    q = __ldg(reinterpret_cast<const uint4*>(tp.bytes + b0));
-  } else {
-    unsigned char c[16];
+  const int64_t b0 =
+      (static_cast<int64_t>(blockIdx.x) * kTrThreads + threadIdx.x) * (16 * kCountChunks);
+  uint4 q[kCountChunks];
+  const bool fast = b0 + 16 * kCountChunks <= tp.n &&
+                    (reinterpret_cast<uintptr_t>(tp.bytes + b0) & 15) == 0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) c[k] = byte_at(tp.bytes, tp.n, b0 + k);
-    memcpy(&q, c, 16);
+  for (int k = 0; k < kCountChunks; ++k) {
+    if (fast) {
+      q[k] = __ldg(reinterpret_cast<const uint4*>(tp.bytes + b0) + k);
+    } else {
+      unsigned char c[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) c[j] = byte_at(tp.bytes, tp.n, b0 + 16 * k + j);
+      memcpy(&q[k], c, 16);
+    }
   }
-  const unsigned left = __shfl_up_sync(0xffffffffu, q.w, 1);
+  const unsigned left = __shfl_up_sync(0xffffffffu, q[kCountChunks - 1].w, 1);
   unsigned char p1 = static_cast<unsigned char>(left >> 24), p2 = static_cast<unsigned char>(left >> 16);
   if (lane == 0) {
     p1 = byte_at(tp.bytes, tp.n, b0 - 1);
     p2 = byte_at(tp.bytes, tp.n, b0 - 2);
   }
   const bool last_is_nl = tp.n > 0 && __ldg(tp.bytes + tp.n - 1) == '\n';
-  unsigned ends, nonempty;
-  line_ends16_q(q, p1, p2, tp.n, b0, last_is_nl, &ends, &nonempty);
-  unsigned long long v = (static_cast<unsigned long long>(__popc(ends)) << 32) | __popc(nonempty);
+  unsigned tot_end = 0, tot_emp = 0;
+#pragma unroll
+  for (int k = 0; k < kCountChunks; ++k) {
+    unsigned e, m;
+    count16(tp, q[k], p1, p2, b0 + 16 * k, last_is_nl, e, m);
+    tot_end += e;
+    tot_emp += m;
+    p1 = static_cast<unsigned char>(q[k].w >> 24);
+    p2 = static_cast<unsigned char>(q[k].w >> 16);
+  }
+  unsigned long long v = (static_cast<unsigned long long>(tot_end) << 32) | (tot_end - tot_emp);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0 && v) atomicAdd(tile_cnt + b0 / kTile, v);
@@ -538,8 +597,9 @@ int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t 
   void* d_cub = scr + ((head + lor + 255) / 256) * 256;
   cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s);
   cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);  // err = none
-  k_csv_count<<<static_cast<unsigned>((n_bytes / 16 + 1 + kTrThreads - 1) / kTrThreads), kTrThreads,
-                0, s>>>(tp, cnt);
+  k_csv_count<<<static_cast<unsigned>((n_bytes / (16 * kCountChunks) + 1 + kTrThreads - 1) /
+                                      kTrThreads),
+                kTrThreads, 0, s>>>(tp, cnt);
   cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, cnt, pref, static_cast<int>(nt), s);
   k_csv_header_end<<<1, 32, 0, s>>>(tp, loc);  // line 0 (the header): its end
   unsigned long long h[2];
