@@ -4,4 +4,4 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1;
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo rc=$? >> gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo rc=$? >> gpurun_out/bench_ref.log
-timeout 900 bash tools/profile_round.sh ${ROUND:-r1g} > gpurun_out/prof.log 2>&1
+timeout 900 bash tools/profile_round.sh ${ROUND:-r1h} > gpurun_out/prof.log 2>&1
