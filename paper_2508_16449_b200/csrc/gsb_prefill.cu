@@ -250,6 +250,7 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
       while (s.lb[g_lo + 1] <= j0) ++g_lo;
       int nb = s.lb[g_lo + 1];
       uint8_t* cls_p = cls_out + c0 + j0 + lane;
+#pragma unroll 2
       for (int r = j0; r < j1; r += 32, cls_p += 32) {
         const int j = r + lane;
         const bool valid = j < j1;
@@ -325,6 +326,7 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
     __syncthreads();
     // ---- B: stable scatter of the stage indices by key (arrival order inside each key): the
     //      warp's cursor for the key plus the rank phase A recorded
+#pragma unroll 4
     for (int j = j0 + lane; j < j1; j += 32) {
       const unsigned v = s.kr[j];
       const int key = static_cast<int>(v & ((1u << S::kKeyBits) - 1u));
