@@ -750,6 +750,8 @@ __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const Clo
         e = __fma_rn(-1000.0, q, y);
         const double idle = __fma_rn(gsb::kRcp1000, e, q);
         const double E = __dadd_rn(active, idle);
+        // (integer-pipe compares of the bit patterns were measured slower: the kernel is
+        // issue-bound as much as FP64-bound, and they add instructions)
         const bool take = (busy <= W) && (E < be);
         best = take ? i : best;
         be = take ? E : be;
