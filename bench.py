@@ -728,7 +728,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        if torch.cuda.is_available():  # the reference arm is host-only
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl" if args.impl == "gsb" else "gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
