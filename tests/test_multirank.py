@@ -160,3 +160,21 @@ def test_decode_pool_tallies_gloo_world2(tmp_path):
         else:
             assert g[k] == single[k], k
     assert g["argmin_scenario"] == 1000 // 3
+
+
+def test_decode_tallies_split_invariance():
+    """tally_pool/combine_tallies: any split of the scenarios over ranks (including empty
+    ranks) gives the same counts, digest and argmin as one tally; energy within 1e-12."""
+    sm = _pool_records(257, 11)
+    single = D.tally_pool(sm, 0)
+    for world in (1, 2, 3, 8, 300):
+        parts = []
+        for r in range(world):
+            lo, n = D.scenario_shard(len(sm), world, r)
+            parts.append(D.tally_pool(sm[lo:lo + n], lo))
+        g = D.combine_tallies(np.array(parts, D.DECODE_TALLY_DTYPE))
+        for k in D.DECODE_TALLY_DTYPE.names:
+            if k == "decode_pool_j":
+                assert abs(g[k] - single[k]) <= 1e-12 * abs(single[k])
+            else:
+                assert g[k] == single[k], (world, k)
