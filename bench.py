@@ -424,8 +424,9 @@ def run_gsb(args, rank, world, dist):
     # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
     # with the fused summary partials + summary final (4); decode step = tbt_p95 + tps +
     # decode_replay (3); e2e = 4
-    # + ingest (K6: count, parse, monotone per call; the CUB scan is library code)
-    launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4) + 3 * max(3, args.steps // 4)
+    # + pool (1 per step) + ingest (K6: count, header end, parse, monotone per call; the CUB
+    # scan is library code)
+    launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4) + 4 * max(3, args.steps // 4)
     line = {
         "metric": METRIC,
         "value": world * evals / (ms_pre / 1e3),
