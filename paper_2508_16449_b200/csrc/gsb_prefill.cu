@@ -344,7 +344,7 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
         double a = acc[k];
         // arithmetic, not a table: a per-profile (a L + b) L + c lookup table gathered from
         // L1/L2 measured 2x slower (latency-bound at 31% issue) than these 5 DP operations
-#pragma unroll 4
+#pragma unroll 8
         for (int j = 0; j < n; ++j) {
           const double Ld = static_cast<double>(s.stage[run[j]]);
           a = a + 1.0 * ((la * Ld + lb) * Ld + lc);
