@@ -250,7 +250,7 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
       while (s.lb[g_lo + 1] <= j0) ++g_lo;
       int nb = s.lb[g_lo + 1];
       uint8_t* cls_p = cls_out + c0 + j0 + lane;
-#pragma unroll 2
+#pragma unroll 4
       for (int r = j0; r < j1; r += 32, cls_p += 32) {
         const int j = r + lane;
         const bool valid = j < j1;
