@@ -250,6 +250,21 @@ def run_gsb(args, rank, world, dist):
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in ts]
 
+    def decode_split(n=3):
+        ka, kb = [], []
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        for _ in range(n):
+            flush.zero_()
+            e[0].record(stream)
+            eng.window_series(tel, 256, 20.0, 200.0, T_END, dev=tdev, out=(has, p95, tps))
+            e[1].record(stream)
+            eng.run_replay(plan)
+            e[2].record(stream)
+            torch.cuda.synchronize()
+            ka.append(e[0].elapsed_time(e[1]))
+            kb.append(e[1].elapsed_time(e[2]))
+        return statistics.median(ka), statistics.median(kb)
+
     # ---------------- closed-loop decode pool leg (K5): C3 sinusoid, controller sweep
     pa, pp, po = wl.sinusoid_decode_trace(1500.0, 1000.0, 120_000.0, 150_000, seed=11 + rank)
     pstream = wl.decode_stream(pa, pp, po)
@@ -359,6 +374,7 @@ def run_gsb(args, rank, world, dist):
         ing_ms = run_ingest(max(3, args.steps // 4), 3)
         barrier()
     k1_ms, k2_ms = kernel_split()
+    k3a_ms, k3b_ms = decode_split()
 
     def max_over_ranks(x):
         if world == 1:
@@ -389,47 +405,58 @@ def run_gsb(args, rank, world, dist):
     per_rank = per_rank.reshape(world, P, W["C"])
     glob = Dd.combine_summaries(per_rank, [r * nW * W["C"] for r in range(world)])
 
-    # ---------------- parity spot check + CPU baseline (rank 0, checker only)
+    # ---------------- CPU baseline + parity (rank 0, N = 1 only; the oracle is the checker)
     cpu = None
     parity = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        cpu, parity = cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep,
-                                   tel, plan, lo, hi, fo, T_END)
+        cpu, parity = cpu_baseline(args, sel, arrival, prompt, W, profs, thr, D, sweep, tel, plan,
+                                   lo, hi, fo, T_END)
         if cpu is not None:
             cpu["pool"], parity["pool"] = pool_cpu_baseline(args, pa, pp, po, pstream, pcfg,
                                                             psum)
             cpu["ingest"] = ingest_cpu_baseline(args, csv_text)
 
+    # executed K2 work, all ranks: every non-empty (cell, profile) pair runs the 81-clock scan
+    # (commands include the infeasible ones); empty queues give no command without evaluation
+    # (prefill_opt.cpp:64) and are not counted
+    pairs_rank = [int(per_rank[r]["n_cmd"].sum()) for r in range(world)]
+    evaluated_all = sum(pairs_rank) * 81
     if rank != 0:
         return
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)
-    traffic_k2 = traffic_k1 = None  # dram bytes per launch from the committed ncu capture
-    try:
-        import glob as _glob
-        tj = sorted(_glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))[-1]
-        tr = json.load(open(tj))
-        traffic_k2 = next((v["dram_bytes_per_launch"] for k, v in tr.items()
-                           if k.startswith("k_prefill_select")), None)
-        traffic_k1 = sum(v["dram_bytes_per_launch"] for k, v in tr.items()
-                         if k.startswith("k_route_bin") or k.startswith("k_window_bounds")) or None
-    except (IndexError, OSError, ValueError, KeyError):
-        pass
-    # executed K2 work: only non-empty (cell, profile) pairs run the 81-clock loop (empty
-    # queues give no command, prefill_opt.cpp:64, and are compacted away inside K2)
-    evaluated = int(per_rank[rank]["n_cmd"].sum()) * 81
+    prof_json = committed_profile()
+    evaluated = pairs_rank[0] * 81
     k2_tflops = evaluated * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
     peak_tflops = dfma_per_s * 2 / 1e12
-    k1_gbs = n_req * K1_BYTES_PER_REQ / (k1_ms / 1e3) / 1e9
-    # timed launches of our kernels: prefill step = window_bounds + route_bin + prefill_select
-    # with the fused summary partials + summary final (4); decode step = tbt_p95 + tps +
-    # decode_replay (3); e2e = 4
-    # + pool (1 per step) + ingest (K6: count, header end, parse, monotone per call; the CUB
-    # scan is library code)
+    # K1 (K1a window bounds + K1b route/bin) algorithmic bytes, FIXED_WINDOW mode:
+    # prompt i32 read + class u8 written per request, one arrival per 32-request tile (the
+    # window-edge search), count u32 + P t_ref f64 written per cell
+    cells = nW * W["C"]
+    k1_bytes = n_req * 5 + (n_req // 32) * 8 + cells * (4 + 8 * P)
+    k1_gbs = k1_bytes / (k1_ms / 1e3) / 1e9
+    clk = clk.summary()
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    issue_peak = 148 * 4 * sm_mhz * 1e6  # warp instructions / s (one per SMSP per cycle)
+
+    def issue_roof(kernel_prefix, units, ms):
+        rec = next((v for k, v in prof_json.items() if k.startswith(kernel_prefix)
+                    and v.get("warp_insts") and v.get("units")), None)
+        if rec is None:
+            return None
+        ach = rec["warp_insts"] / rec["units"] * units / (ms / 1e3)
+        return {"bound": "issue", "achieved": ach, "peak": issue_peak,
+                "unit": "warp-instr/s", "frac": ach / issue_peak, "kernel_ms": ms,
+                "warp_insts_per_unit": rec["warp_insts"] / rec["units"],
+                "fp64_pipe_pct_active": rec.get("fp64_pipe_pct_active"),
+                "dram_bytes_per_unit": rec.get("dram_bytes_per_launch", 0) / rec["units"],
+                "basis": "ncu smsp__inst_executed per unit (profiles/) x units / event time; "
+                         "peak = 592 SMSPs x 1 issue/cycle at the sampled SM clock"}
+
     launches = args.steps * (4 + 3 + 4) + max(3, args.steps // 4) + 4 * max(3, args.steps // 4)
     line = {
         "metric": METRIC,
-        "value": world * evals / (ms_pre / 1e3),
+        "value": evaluated_all / (ms_pre / 1e3),
         "unit": "window x class x clock evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_pre,
@@ -438,134 +465,147 @@ def run_gsb(args, rank, world, dist):
         "data": "synthetic (reference-shaped Poisson/bimodal traces; sinusoidal decode telemetry)",
         "config": {"workload": W["name"], "windows_per_gpu": nW, "window_ms": wms,
                    "classes": W["C"], "profiles": P, "clocks": 81, "requests_per_gpu": n_req,
-                   "evals_per_step_per_gpu": evals,
                    "evaluated_evals_per_step_per_gpu": evaluated,
-                   "value_counts": "every (window, class, profile, clock) triple of the grid is "
-                                   "decided each step; empty cells are decided as 'no command' "
-                                   "without evaluation (prefill_opt.cpp:64); the roofline counts "
-                                   "only the evaluated triples",
+                   "grid_evals_per_step_per_gpu": evals,
+                   "value_counts": "EVALUATED triples: non-empty (window, class, profile) x 81 "
+                                   "clocks (empty queues: no command, prefill_opt.cpp:64)",
                    "window_mode": "FIXED_WINDOW D=0.95*W",
                    "decode_scenarios_per_gpu": sweep.n_scenarios, "decode_horizon_ms": T_END,
                    "parallelism": f"dp{world} (windows/scenarios sharded, NCCL all-gather of "
                                   f"per-class summaries)",
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "cuda_graphs": use_graph},
-        "e2e": {"value": world * evals / (ms_e2e / 1e3), "unit": "window x class x clock evals/s",
+        "grid_value": world * evals / (ms_pre / 1e3),
+        "e2e": {"value": evaluated_all / (ms_e2e / 1e3), "unit": "window x class x clock evals/s",
                 "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "public API (Engine.route_bin/prefill_select) from pinned host buffers"},
-        "decode": {"value": world * sweep.n_scenarios / (ms_dec / 1e3),
-                   "unit": "decode-controller scenario replays/s",
-                   "fine_ticks_per_s": world * sweep.n_scenarios * 4 * 7500 / (ms_dec / 1e3),
-                   "ms_per_step": ms_dec, "trajectories_per_step": len(sweep.cfgs)},
-        "pool": {"value": world * len(pcfg) / (ms_pool / 1e3),
-                 "unit": "closed-loop decode-pool scenario replays/s",
-                 "decode_steps_per_s": world * float(psum["n_steps"].sum()) / (ms_pool / 1e3),
-                 "events_per_scenario": float((psum["n_steps"] + psum["n_decisions"]
-                                               + psum["n_freq_changes"]).mean() + len(pstream.t_ms)),
-                 "ms_per_step": ms_pool, "scenarios_per_step": len(pcfg),
-                 "workload": "C3 sinusoid 1500+-1000 tps, 150 s, 4 decode workers x max_batch 64; "
-                             "sweep hysteresis x step x TBT target x margin x bias; K5 "
-                             "k_decode_pool, one warp per scenario",
-                 "mean_decode_pool_j": float(psum["decode_pool_j"].mean()),
-                 "global_tally": {k: (int(gtally[k]) if gtally.dtype[k].kind in "iu"
-                                      else float(gtally[k])) for k in gtally.dtype.names},
-                 "reduction": "per-rank scenario tallies, NCCL all-gather, rank-order combine"},
+                "path": "Engine.route_bin/prefill_select from pinned host buffers"},
         "roofline": {"bound": "fp64", "kernel": "k_prefill_select (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,
-                     "basis": f"{K2_DP_OPS_PER_EVAL} DP-pipe instr per EVALUATED (non-empty "
-                              "cell, profile, clock) x 2 (DFMA-equivalent) vs DFMA throughput "
-                              "measured in this run (gsb_fp64_probe); kernel time includes the "
-                              "fused per-class summary and its final combine",
-                     "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre, "traffic": traffic_k2,
-                     "traffic_note": "dram__bytes_read+write per launch, profiles/ ncu capture"},
+                     "basis": f"{K2_DP_OPS_PER_EVAL} DP instr per evaluated triple x 2 vs DFMA "
+                              "rate measured in this run; K2 time incl. its fused summary",
+                     "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre,
+                     "traffic": prof_json.get("_k2_dram"),
+                     "fp64_warp_insts_ncu": prof_json.get("_k2_fp64_insts")},
+        "roofline_k1": {"bound": "hbm", "kernel": "k_window_bounds + k_route_bin (K1)",
+                        "achieved": k1_gbs, "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm,
+                        "kernel_ms": k1_ms, "algorithmic_bytes": k1_bytes,
+                        "basis": "5 B/request (prompt i32 in, class u8 out) + 8 B per 32-request "
+                                 "tile + (4 + 8P) B/cell",
+                        "traffic": prof_json.get("_k1_dram")},
         "ingest": {"value": world * len(csv_text) / (ms_ing / 1e3) / 1e9,
                    "unit": "GB/s of trace CSV parsed (load_trace semantics)",
                    "rows_per_s": world * n_req / (ms_ing / 1e3), "ms_per_step": ms_ing,
-                   "csv_bytes_per_step": len(csv_text), "rows_per_step": n_req,
-                   "workload": "this rank's trace rendered by save_trace_csv (4 columns), "
-                               "device-resident bytes -> SoA via gsb_trace_parse (K6: count, scan, "
-                               "parse, monotone check; two host syncs per call)",
                    "roofline": {"bound": "hbm", "achieved": (len(csv_text) * 2 + n_req * 21)
                                 / (ms_ing / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                                 "frac": (len(csv_text) * 2 + n_req * 21) / (ms_ing / 1e3) / 1e9
-                                / hbm,
-                                "basis": "CSV bytes read twice (count + parse passes) + 17 B/row "
-                                         "written + 4 B/row line index"}},
-        "roofline_k1": {"bound": "hbm", "kernel": "k_route_bin (K1)", "achieved": k1_gbs,
-                        "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm, "kernel_ms": k1_ms,
-                        "bytes_per_request": K1_BYTES_PER_REQ,
-                        "traffic": traffic_k1},
+                                / hbm}},
         "fp64_peak_measured_dfma_per_s": dfma_per_s,
         "result": {"commands": int(glob["n_cmd"].sum()),
                    "infeasible": int(glob["n_infeasible"].sum()),
                    "empty_cells": int(glob["n_empty"].sum()),
                    "sum_energy_j_per_profile": [float(x) for x in glob["sum_energy_j"].sum(axis=1)]},
-        "clocks": clk.summary(),
+        "clocks": clk,
         "gpu_launches": launches,
     }
     if cpu:
         line["cpu_baseline"] = cpu
     if parity:
         line["parity_sample"] = parity
+    # the decode half of the metric last: the driver keeps the tail of stdout
+    line["pool"] = {"value": world * len(pcfg) / (ms_pool / 1e3),
+                    "unit": "closed-loop decode-pool scenario replays/s",
+                    "ms_per_step": ms_pool, "scenarios_per_step": len(pcfg),
+                    "workload": "C3 sinusoid, 150 s, 4 decode workers x max_batch 64; K5 "
+                                "k_decode_pool, one warp per scenario",
+                    "roofline": issue_roof("k_decode_pool", len(pcfg), ms_pool),
+                    "global_digest": int(gtally["digest"]),
+                    "reduction": "per-rank scenario tallies, NCCL all-gather, rank-order combine"}
+    line["decode"] = {"value": world * sweep.n_scenarios / (ms_dec / 1e3),
+                      "unit": "decode-controller scenario replays/s",
+                      "kind": "open-loop DecodeController replay (4 workers per scenario) over "
+                              f"{tel.n_streams} shared telemetry streams: a controller "
+                              "state-machine rate",
+                      "ms_per_step": ms_dec, "k3a_ms": k3a_ms, "k3b_ms": k3b_ms,
+                      "trajectories_per_step": len(sweep.cfgs),
+                      "roofline": issue_roof("k_decode_replay", len(sweep.cfgs), k3b_ms)}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep, tel, plan, lo, hi,
-                 fo, T_END):
-    """Reference CPU path (oracle/_ref, the unmodified reference sources) on a bounded sample
-    of the same workload, all host threads; also bit-checks the GPU outputs on that sample."""
-    import torch
+def committed_profile():
+    """Per-kernel ncu numbers committed under profiles/ (latest round): dram bytes and warp
+    instructions per launch with the launch's work units (tools/summarize_profiles.py)."""
+    import glob as _glob
+    out = {}
+    try:
+        tj = sorted(_glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))[-1]
+        out = json.load(open(tj))
+    except (IndexError, OSError, ValueError):
+        return out
+    k2 = [v for k, v in out.items() if k.startswith("k_prefill_select")]
+    if k2:
+        out["_k2_dram"] = k2[0].get("dram_bytes_per_launch")
+        out["_k2_fp64_insts"] = k2[0].get("fp64_insts")
+    k1 = [v.get("dram_bytes_per_launch", 0) for k, v in out.items()
+          if k.startswith("k_route_bin") or k.startswith("k_window_bounds")]
+    out["_k1_dram"] = sum(k1) or None
+    return out
+
+
+def lscpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(args, sel, arrival, prompt, W, profs, thr, D, sweep, tel, plan, lo, hi, fo,
+                 T_END):
+    """The reference's CPU path (oracle/_ref, the unmodified reference sources) on this host:
+    Dispatcher routing + select_frequency for every (window, class, profile) of THIS rank's
+    whole trace with all host threads (the same config as the GPU arm), plus a 1-thread rate
+    on a prefix of the windows. Its outputs are compared with the GPU's for EVERY cell and
+    profile (grid index and energy bits)."""
     from oracle import oracle as O
 
     if not O.reference_available():
         return None, None
     ref = O.Reference()
     threads = os.cpu_count() or 1
-    C = W["C"]
-    # prefill sample: the FIFO job lists of the first windows (Dispatcher order)
-    cls = rr.cls.cpu().numpy()
-    cnt = rr.count.cpu().numpy().view(np.uint32)
-    bounds = rr.bounds.cpu().numpy()
-    n_w = 1
-    t_rate = None
-    res = {}
-    budget = args.cpu_seconds
-    while True:
-        s_end = bounds[n_w]
-        key = (arrival[:s_end] // W["window_ms"] - rr.w0) * C + cls[:s_end]
-        order = np.argsort(key, kind="stable")
-        ncell = n_w * C
-        off = np.concatenate([[0], np.cumsum(cnt[:ncell])]).astype(np.int64)
-        prompts = prompt[order].astype(np.int32)
-        nonempty = np.nonzero(cnt[:ncell])[0]
-        t0 = time.perf_counter()
-        f, e, found = ref.select_many(O.Profile(*profs[0].key()), off, prompts,
-                                      np.full(ncell, D), threads=threads)
-        dt = time.perf_counter() - t0
-        if dt > budget / 4 or n_w >= rr.n_windows:
-            break
-        n_w = min(rr.n_windows, int(n_w * max(2.0, min(16.0, budget / 2 / max(dt, 1e-4)))))
-    # repeat the sample until the time budget is used (bounded CPU work, stable rate)
-    reps, t_tot = 1, dt
-    while t_tot < budget / 2:
-        t0 = time.perf_counter()
-        ref.select_many(O.Profile(*profs[0].key()), off, prompts, np.full(ncell, D),
-                        threads=threads)
-        t_tot += time.perf_counter() - t0
-        reps += 1
-    dt = t_tot / reps
-    evals = ncell * 81
-    fi = sel.f_idx.cpu().numpy()[0, :ncell]
-    en = sel.energy_j.cpu().numpy()[0, :ncell]
-    gf = np.where(fi >= 0, 210.0 + 15.0 * fi, 0.0)
-    mism = int(((fi[nonempty] >= 0) != found[nonempty]).sum()
-               + (found[nonempty] & ((gf[nonempty] != f[nonempty])
-                                     | (en[nonempty] != e[nonempty]))).sum())
-    pre = {"value": evals / dt, "unit": "window x class x clock evals/s", "cores": threads,
-           "kind": "reference", "seconds": dt,
-           "sample": f"{n_w} windows x {C} classes (profile 0) of this rank's trace through "
-                     f"greensim::select_frequency on the FIFO job lists, {threads} std::threads"}
+    C, nW, wms = W["C"], W["W"], W["window_ms"]
+    rp = [O.Profile(*p.key()) for p in profs]
+    w0 = 0  # rank 0's windows (cpu_baseline runs at N = 1 only)
+    t0 = time.perf_counter()
+    fi_r, en_r, pairs = ref.prefill_pass(rp, thr, arrival, prompt, wms, w0, nW, D,
+                                         threads=threads)
+    dt_n = time.perf_counter() - t0
+    # 1-thread rate on the first windows (about a second of work)
+    n1 = max(1, min(nW, int(nW * min(1.0, 1.0 / max(dt_n * threads, 1e-3)))))
+    s_end = int(np.searchsorted(arrival, (w0 + n1) * wms))
+    t0 = time.perf_counter()
+    _, _, pairs1 = ref.prefill_pass(rp, thr, arrival[:s_end], prompt[:s_end], wms, w0, n1, D,
+                                    threads=1, outputs=False)
+    dt_1 = time.perf_counter() - t0
+    fi_g = sel.f_idx.cpu().numpy()
+    en_g = sel.energy_j.cpu().numpy()
+    per_prof = []
+    for p in range(len(profs)):
+        bad = (fi_g[p] != fi_r[p]) | (en_g[p].view(np.uint64) != en_r[p].view(np.uint64))
+        per_prof.append({"profile": p, "cells": int(fi_g.shape[1]),
+                         "commands": int((fi_r[p] != -2).sum()),
+                         "infeasible": int((fi_r[p] == -1).sum()),
+                         "mismatches": int(bad.sum())})
+    pre = {"value": pairs * 81 / dt_n, "unit": "window x class x clock evals/s",
+           "cores": threads, "kind": "reference", "seconds": dt_n,
+           "value_1thread": pairs1 * 81 / dt_1, "seconds_1thread": dt_1,
+           "cpu_model": lscpu_model(),
+           "sample": f"the whole GPU workload ({nW} windows x {C} classes x {len(profs)} "
+                     f"profiles, {len(arrival)} requests): Dispatcher::dispatch/pop + "
+                     f"select_frequency, one Dispatcher per std::thread over contiguous windows; "
+                     f"1-thread rate on the first {n1} windows"}
     # decode sample: full reference composition (windows + controller) per trajectory
     tels = []
     for s in range(tel.n_streams):
@@ -574,6 +614,7 @@ def cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep, t
         tels.append(O.TelemetryArrays(tel.t_ms[e0:e1].copy(), tel.tokens[e0:e1].copy(),
                                       (go - go[0]).astype(np.int64), tel.gaps[go[0]:go[-1]].copy()))
     lo_h, hi_h, fo_h = lo.cpu().numpy(), hi.cpu().numpy(), fo.cpu().numpy()
+    budget = args.cpu_seconds
     n_s = 8
     while True:
         idx = np.arange(min(len(sweep.cfgs), n_s * 4))
@@ -593,12 +634,12 @@ def cpu_baseline(args, eng, rr, sel, arrival, prompt, W, profs, thr, D, sweep, t
     gn = plan["n_rec"].cpu().numpy()[idx]
     dmism = int(((gd != dig) | (gn != nrec)).sum())
     scen = len(idx) / 4
-    dec = {"value": scen / ddt, "unit": "decode-controller scenario replays/s", "cores": threads,
-           "kind": "reference", "seconds": ddt,
-           "sample": f"{int(scen)} scenarios x 4 workers x 150 s: DecodeController + TbtWindow + "
-                     f"TpsWindow composed as Sim, {threads} std::threads"}
-    pre["decode"] = dec
-    parity = {"prefill_cells_checked": int(len(nonempty)), "prefill_mismatches": mism,
+    pre["decode"] = {"value": scen / ddt, "unit": "decode-controller scenario replays/s",
+                     "cores": threads, "kind": "reference", "seconds": ddt,
+                     "sample": f"{int(scen)} scenarios x 4 workers x 150 s: DecodeController + "
+                               f"TbtWindow + TpsWindow composed as Sim, {threads} std::threads"}
+    parity = {"prefill": per_prof,
+              "prefill_mismatches": int(sum(x["mismatches"] for x in per_prof)),
               "decode_trajectories_checked": int(len(idx)), "decode_digest_mismatches": dmism}
     return pre, parity
 
@@ -670,8 +711,11 @@ def pool_cpu_baseline(args, pa, pp, po, pstream, pcfg, psum):
 
 # ---------------------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
-    """The reference's own CPU implementation of the path (oracle/_ref) on the same config,
-    all host threads, each step a bounded sample."""
+    """The reference's own CPU implementation of the path (oracle/_ref, the unmodified reference
+    sources) on the SAME config as the gsb arm: rank 0's trace (same generator and seed), every
+    window x class x profile: Dispatcher::dispatch/pop routing + select_frequency per non-empty
+    (cell, profile), all host threads (one Dispatcher per thread over contiguous windows). The
+    metric counts evaluated triples exactly as the gsb arm does."""
     if rank != 0:
         return
     from oracle import oracle as O
@@ -683,40 +727,35 @@ def run_reference(args, rank, world):
     W = workload(args.config, args.windows)
     thr = wl.THRESHOLDS[W["C"]]
     threads = os.cpu_count() or 1
-    n_w = min(W["W"], 600)
+    nW, wms = W["W"], W["window_ms"]
     if W["shape"] == "mixed":
-        arrival, prompt, _ = wl.mixed_trace(W["qps"], n_w * W["window_ms"], seed=1000)
+        arrival, prompt, _ = wl.mixed_trace(W["qps"], nW * wms, seed=1000, t0_ms=0)
     else:
-        arrival, prompt, _ = wl.poisson_trace(W["qps"], n_w * W["window_ms"], W["shape"], seed=1000)
-    C = W["C"]
-    t_route0 = time.perf_counter()
-    q, _, _ = ref.dispatch(thr, prompt)
-    t_route = time.perf_counter() - t_route0
-    key = (arrival // W["window_ms"]) * C + q
-    order = np.argsort(key, kind="stable")
-    cnt = np.bincount(key, minlength=n_w * C)[: n_w * C]
-    off = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
-    prof = O.default_profile()
-    D = 0.95 * W["window_ms"]
-    times = []
+        arrival, prompt, _ = wl.poisson_trace(W["qps"], nW * wms, W["shape"], seed=1000, t0_ms=0)
+    profs = [O.Profile(*p.key()) for p in wl.synth_profiles(W["P"])]
+    D = 0.95 * wms
+    times, pairs = [], 0
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        ref.select_many(prof, off, prompt[order], np.full(n_w * C, D), threads=threads)
+        _, _, pairs = ref.prefill_pass(profs, thr, arrival, prompt, wms, 0, nW, D,
+                                       threads=threads, outputs=False)
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0 + t_route)
+            times.append(time.perf_counter() - t0)
     dt = statistics.mean(times)
-    evals = n_w * C * 81
-    v = evals / dt
+    v = pairs * 81 / dt
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "window x class x clock evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (same generator and config as the gsb arm)",
-        "config": {"workload": W["name"], "sample_windows": n_w, "classes": C, "profiles": 1},
+        "data": "synthetic (same generator, seed and config as the gsb arm's rank 0)",
+        "config": {"workload": W["name"], "windows": nW, "classes": W["C"],
+                   "profiles": W["P"], "clocks": 81, "requests": int(len(arrival)),
+                   "evaluated_evals_per_step": pairs * 81, "same_config": True},
         "cpu_baseline": {"value": v, "unit": "window x class x clock evals/s", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{n_w} one-minute windows x {C} classes per step: Dispatcher "
-                                   f"routing + select_frequency per cell, {threads} threads"},
+                         "kind": "reference", "cpu_model": lscpu_model(),
+                         "sample": "the whole workload per step: Dispatcher::dispatch/pop + "
+                                   "select_frequency per non-empty (window, class, profile), "
+                                   f"{threads} std::threads"},
         "e2e": {"value": v, "unit": "window x class x clock evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
 

@@ -398,8 +398,9 @@ int gsb_decode_script(gsb_ctx* ctx, const gsb_replay_args* a, const int64_t* d_e
                       const uint8_t* d_has, gsb_ctl_state* d_state, void* stream);
 
 /* Nearest-rank quantile (metrics.cpp:11-19) of each of n_sets sample sets
- * [d_off[s], d_off[s+1]), set sizes 1..4096 (TbtWindow::p95 is q = 0.95 over the ring). An
- * empty or oversized set yields NaN (the reference throws std::invalid_argument). */
+ * [d_off[s], d_off[s+1]) of any size (TbtWindow::p95 is q = 0.95 over the ring; sets up to 4096
+ * are sorted in shared memory, larger ones take an exact radix select). An empty set yields NaN
+ * (the reference throws std::invalid_argument). */
 int gsb_quantile_batch(gsb_ctx* ctx, double q, int64_t n_sets, const int64_t* d_off,
                        const double* d_samples, double* d_out, void* stream);
 

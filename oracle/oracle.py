@@ -605,6 +605,13 @@ class Reference:
         L.ref_energy_closed_form.restype = _d
         L.ref_select_frequency.argtypes = [P, _i64, _p, _p, _d, _p, _p]
         L.ref_select_frequency_many.argtypes = [P, _i64, _p, _p, _p, _p, C.c_int, _p, _p, _p]
+        L.ref_prefill_pass.argtypes = [C.c_int, _p, C.c_int, C.c_int, _p, _i64, _p, _p, _i64,
+                                       _i64, _i64, _d, C.c_int, _p, _p]
+        L.ref_prefill_pass.restype = _i64
+        L.ref_prefill_pass_ex.argtypes = [C.c_int, C.c_int, _p, C.c_int, C.c_int, _p, _i64, _p,
+                                          _p, _i64, _i64, _i64, _d, C.POINTER(QoptCfg), _d, _d,
+                                          C.c_int, _p, _p, _p]
+        L.ref_prefill_pass_ex.restype = _i64
         L.ref_queue_optimizer_tick.argtypes = [P, C.POINTER(QoptCfg), C.c_int, _p, _p, _p, _p, _p,
                                                _d, _p, _p, _p, _p]
         L.ref_classify.argtypes = [C.c_int, _p, _i32]
@@ -705,6 +712,45 @@ class Reference:
         self.lib.ref_select_frequency_many(C.byref(prof), nb, ptr(off), ptr(prompts), ptr(w),
                                            ptr(windows), threads, ptr(f), ptr(e), ptr(found))
         return f, e, found.astype(bool)
+
+    def prefill_pass(self, profs, thresholds, arrival, prompt, window_ms, w0, n_windows, D,
+                     threads=1, outputs=True, enabled=True):
+        """ref_prefill_pass: Dispatcher routing + select_frequency for every (window, class,
+        profile) of the trace (the reference's CPU path). Returns (f_idx [P, cells] or None,
+        energy [P, cells] or None, evaluated (cell, profile) pairs)."""
+        t = np.ascontiguousarray(thresholds, np.int32)
+        a = np.ascontiguousarray(arrival, np.int64)
+        p = np.ascontiguousarray(prompt, np.int32)
+        P = len(profs)
+        arr = (Profile * P)(*profs)
+        C_ = len(t) + 1 if enabled else 1
+        cells = n_windows * C_
+        fi = np.empty((P, cells), np.int16) if outputs else None
+        en = np.empty((P, cells), np.float64) if outputs else None
+        n = self.lib.ref_prefill_pass(P, C.cast(arr, _p), 1 if enabled else 0, len(t), ptr(t), len(a), ptr(a),
+                                      ptr(p), int(window_ms), int(w0), int(n_windows), float(D),
+                                      int(threads), ptr(fi), ptr(en))
+        return fi, en, int(n)
+
+    def prefill_pass_deadline(self, profs, thresholds, arrival, prompt, window_ms, w0, n_windows,
+                              qopt=None, ttft_sm=400.0, ttft_l=2000.0, threads=1):
+        """ref_prefill_pass_ex mode 1: queue_optimizer_tick per window at now = window start.
+        Returns (f_idx [P, cells] (-1 infeasible, -2 no command), window [cells] (profile 0),
+        number of commands)."""
+        t = np.ascontiguousarray(thresholds, np.int32)
+        a = np.ascontiguousarray(arrival, np.int64)
+        p = np.ascontiguousarray(prompt, np.int32)
+        P = len(profs)
+        arr = (Profile * P)(*profs)
+        cells = n_windows * (len(t) + 1)
+        fi = np.empty((P, cells), np.int16)
+        win = np.zeros(cells, np.float64)
+        q = qopt if qopt is not None else default_qopt_cfg()
+        n = self.lib.ref_prefill_pass_ex(1, P, C.cast(arr, _p), 1, len(t), ptr(t), len(a), ptr(a),
+                                         ptr(p), int(window_ms), int(w0), int(n_windows), 0.0,
+                                         C.byref(q), float(ttft_sm), float(ttft_l), int(threads),
+                                         ptr(fi), None, ptr(win))
+        return fi, win, int(n)
 
     def queue_optimizer_tick(self, prof, cfg, class_ids, off, prompts, deadlines, now, wf=None):
         class_ids = np.ascontiguousarray(class_ids, np.int32)

@@ -300,6 +300,135 @@ void ref_select_frequency_many(const gso_profile* c, int64_t n_batches, const in
   for (auto& th : pool) th.join();
 }
 
+// The reference's own CPU path for one offline prefill pass over a trace (bench.py's reference
+// arm and cpu_baseline; DESIGN.md offline window convention): window k covers arrivals in
+// [(w0+k)*window_ms, (w0+k+1)*window_ms). Per window, Dispatcher::dispatch (router.cpp:33-43)
+// routes its requests into per-class FIFOs, each non-empty queue is drained with
+// Dispatcher::pop into a PrefillBatch in FIFO order, and select_frequency (prefill_opt.cpp:45-56)
+// runs for every profile with window D. Windows are split into contiguous ranges, one std::thread
+// and one Dispatcher each (request ids are the trace indices, so no id repeats). Outputs per
+// (p, cell = k*C + c) at p*cells + cell, optional: grid index of the choice (-1 infeasible, -2
+// empty queue) and its energy (0 otherwise). Returns the number of (cell, profile) pairs that
+// ran select_frequency (each evaluates every grid clock).
+//
+// mode 1 (DEADLINE_SLACK) instead calls queue_optimizer_tick (prefill_opt.cpp:58-82) once per
+// window and profile at now = window start over the window's class snapshots, each job carrying
+// the simulator's prefill deadline arrival + ttft_for(request_class(r, 1024)) - allowance
+// (simkernel.cpp:113-116,298,499-501): f_idx -1 marks an infeasible command (pinned at f_max),
+// window_out[cell] receives the command's window (profile 0), energy is not produced.
+int64_t ref_prefill_pass_ex(int mode, int n_prof, const gso_profile* profs, int enabled, int n_thr,
+                            const int32_t* thr, int64_t n_req, const int64_t* arrival,
+                            const int32_t* prompt, int64_t window_ms, int64_t w0,
+                            int64_t n_windows, double D, const gso_qopt_cfg* qc, double ttft_sm,
+                            double ttft_l, int threads, int16_t* f_idx, double* energy,
+                            double* window_out) {
+  RoutingConfig cfg;
+  cfg.enabled = enabled != 0;
+  cfg.thresholds.assign(thr, thr + n_thr);
+  const int C = cfg.enabled ? n_thr + 1 : 1;
+  const int64_t cells = n_windows * C;
+  std::vector<GpuProfile> prof;
+  for (int p = 0; p < n_prof; ++p) prof.push_back(to_profile(&profs[p]));
+  threads = std::max(1, threads);
+  std::vector<int64_t> evaluated(static_cast<size_t>(threads), 0);
+  auto work = [&](int t) {
+    const int64_t k0 = n_windows * t / threads, k1 = n_windows * (t + 1) / threads;
+    Dispatcher d(cfg);
+    int64_t i = std::lower_bound(arrival, arrival + n_req, (w0 + k0) * window_ms) - arrival;
+    PrefillBatch b;
+    int64_t ev = 0;
+    for (int64_t k = k0; k < k1; ++k) {
+      const int64_t end_ms = (w0 + k + 1) * window_ms;
+      for (; i < n_req && arrival[i] < end_ms; ++i) {
+        Request r;
+        r.id = i;
+        r.arrival_ms = arrival[i];
+        r.prompt_tokens = prompt[i];
+        r.output_tokens = 1;
+        d.dispatch(r);
+      }
+      if (mode == 1) {
+        QueueOptimizerConfig qcfg;
+        qcfg.resolve_period_ms = qc->resolve_period_ms;
+        qcfg.margin_prefill = qc->margin_prefill;
+        qcfg.min_budget_ms = qc->min_budget_ms;
+        qcfg.first_token_allowance_ms = qc->first_token_allowance_ms;
+        std::vector<ClassQueueSnapshot> snaps(static_cast<size_t>(C));
+        for (int q = 0; q < C; ++q) {
+          snaps[static_cast<size_t>(q)].class_id = q;
+          for (int p = 0; p < n_prof && f_idx; ++p) f_idx[p * cells + k * C + q] = -2;
+          while (!d.empty(q)) {
+            const int64_t id = d.pop(q);
+            const double arr = static_cast<double>(arrival[id]);
+            const double ttft = prompt[id] <= 1024 ? ttft_sm : ttft_l;
+            snaps[static_cast<size_t>(q)].batch.jobs.push_back(
+                PrefillJob{id, prompt[id], arr + ttft - qcfg.first_token_allowance_ms, 1.0});
+          }
+        }
+        const double now = static_cast<double>((w0 + k) * window_ms);
+        for (int p = 0; p < n_prof; ++p) {
+          const auto cmds = queue_optimizer_tick(snaps, now, qcfg, prof[static_cast<size_t>(p)]);
+          ev += static_cast<int64_t>(cmds.size());
+          for (const auto& c : cmds) {
+            const int64_t cell = k * C + c.class_id;
+            if (f_idx)
+              f_idx[p * cells + cell] =
+                  c.infeasible ? int16_t{-1}
+                               : static_cast<int16_t>(std::llround(
+                                     (c.f_mhz - profs[p].f_min_mhz) / profs[p].step_mhz));
+            if (window_out && p == 0) window_out[cell] = c.window_ms;
+          }
+        }
+        continue;
+      }
+      for (int q = 0; q < C; ++q) {
+        const int64_t cell = k * C + q;
+        if (d.empty(q)) {
+          for (int p = 0; p < n_prof; ++p) {
+            if (f_idx) f_idx[p * cells + cell] = -2;
+            if (energy) energy[p * cells + cell] = 0.0;
+          }
+          continue;
+        }
+        b.jobs.clear();
+        while (!d.empty(q)) {
+          const int64_t id = d.pop(q);
+          b.jobs.push_back(PrefillJob{id, prompt[id], 0.0, 1.0});
+        }
+        for (int p = 0; p < n_prof; ++p) {
+          const auto r = select_frequency(b, D, prof[static_cast<size_t>(p)]);
+          ++ev;
+          if (f_idx)
+            f_idx[p * cells + cell] = r ? static_cast<int16_t>(std::llround(
+                                              (r->f_mhz - profs[p].f_min_mhz) / profs[p].step_mhz))
+                                        : int16_t{-1};
+          if (energy) energy[p * cells + cell] = r ? r->energy_j : 0.0;
+        }
+      }
+    }
+    evaluated[static_cast<size_t>(t)] = ev;
+  };
+  if (threads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+  }
+  int64_t total = 0;
+  for (int64_t e : evaluated) total += e;
+  return total;
+}
+
+int64_t ref_prefill_pass(int n_prof, const gso_profile* profs, int enabled, int n_thr,
+                         const int32_t* thr, int64_t n_req, const int64_t* arrival,
+                         const int32_t* prompt, int64_t window_ms, int64_t w0, int64_t n_windows,
+                         double D, int threads, int16_t* f_idx, double* energy) {
+  return ref_prefill_pass_ex(0, n_prof, profs, enabled, n_thr, thr, n_req, arrival, prompt,
+                             window_ms, w0, n_windows, D, nullptr, 0.0, 0.0, threads, f_idx,
+                             energy, nullptr);
+}
+
 // queue_optimizer_tick over n_queues snapshots at one instant; returns #commands.
 int ref_queue_optimizer_tick(const gso_profile* c, const gso_qopt_cfg* qc, int n_queues,
                              const int32_t* class_ids, const int64_t* off, const int32_t* prompt,

@@ -235,10 +235,18 @@ class RoutingConfig:
                                   >= n_prefill_workers else self.worker_map, np.int32)
         msg = C.create_string_buffer(256)
         cfg = _route_cfg(self, 1, 0, 1)
+        thr = [int(t) for t in self.thresholds]
+        # the reference's order (router.cpp:8-13) over the WHOLE list, then this ABI's cap
+        if not thr:
+            raise RouterError("routing: need at least one threshold")
+        if any(a >= b for a, b in zip(thr, thr[1:])):
+            raise RouterError("routing: thresholds must be ascending and distinct")
+        if any(t < 1 for t in thr):
+            raise RouterError("routing: thresholds must be >= 1")
+        if len(thr) > L.GSB_MAX_CLASSES - 1:
+            raise RouterError("routing: more than 7 thresholds")
         if self.enabled and len(self.worker_map) != n_prefill_workers:
             raise RouterError("routing: worker_map must name a class per prefill worker")
-        if len(self.thresholds) > L.GSB_MAX_CLASSES - 1:
-            raise RouterError("routing: more than 7 thresholds")
         rc = L.load().gsb_routing_validate(C.byref(cfg), n_prefill_workers,
                                            wm.ctypes.data_as(C.c_void_p), msg, 256)
         if rc != L.OK:
@@ -413,6 +421,7 @@ class RouteResult:
     min_deadline: Optional[torch.Tensor]   # f64 [cells]
     cell_off: Optional[torch.Tensor] = None  # i64 [cells+1]
     fifo: Optional[torch.Tensor] = None      # i64 [n_req] cell-major FIFO order
+    profile_gen: int = -1                    # Engine.profile_gen its t_ref rows were built under
 
     @property
     def n_cells(self) -> int:
@@ -516,15 +525,26 @@ class Engine:
 
     def set_profiles(self, profiles: Sequence[GpuProfile]) -> None:
         arr = (L.CProfile * len(profiles))(*[p.to_c() for p in profiles])
+        # (gsb_set_profiles orders the upload after every kernel already issued on the device)
         self._check(self.lib.gsb_set_profiles(self.ctx, len(profiles), C.cast(arr, C.c_void_p)))
         self.profiles = list(profiles)
+        self.profile_gen = getattr(self, "profile_gen", 0) + 1
 
     def _profile_index(self, profile: GpuProfile) -> int:
+        """Index of `profile` in the installed set. The reference's free functions take the
+        profile as an argument (prefill_opt.hpp:40-57), so a profile outside the set is
+        installed (a new generation); RouteResults built under the previous set are then
+        rejected by prefill_select instead of being read against the wrong tables."""
         for i, p in enumerate(self.profiles):
             if p.key() == profile.key():
                 return i
         self.set_profiles([profile])
         return 0
+
+    def _check_gen(self, rr: "RouteResult") -> None:
+        if rr.profile_gen != self.profile_gen:
+            raise ModelError("RouteResult was built under another profile set (set_profiles was "
+                             "called since); re-run route_bin")
 
     # ---------------------------------------------------------------- K1
     def window_bounds(self, arrival: torch.Tensor, rc: RoutingConfig, window_ms: int, w0: int,
@@ -562,6 +582,7 @@ class Engine:
         self._check(self.lib.gsb_route_bin(self.ctx, C.byref(cfg), n, _ptr(arrival), _ptr(prompt),
                                            _ptr(out.bounds), _ptr(out.cls), _ptr(out.count),
                                            _ptr(out.t_ref), _ptr(out.min_deadline), s))
+        out.profile_gen = self.profile_gen
         if want_fifo:
             out.cell_off = self._empty(cells + 1, torch.int64)
             out.fifo = self._empty(n, torch.int64)
@@ -648,6 +669,7 @@ class Engine:
         """K2: energy_total at every (cell, profile, clock) + deterministic argmin. With
         summary_out (a [P*C, 48] byte tensor, see prefill_summary_dev) the per-(profile,
         class) summary is folded into the same launch (gsb_prefill_select_summary)."""
+        self._check_gen(rr)
         cfg = L.CSelectCfg(mode, rr.n_classes, fixed_window_ms, rr.w0, rr.window_ms, qopt.to_c())
         P, cells = len(self.profiles), rr.n_cells
         if out is None:
@@ -843,7 +865,7 @@ class Engine:
 
     # ---------------------------------------------------------------- window statistics
     def quantile_batch(self, off, samples, q: float) -> torch.Tensor:
-        """Nearest-rank quantile (metrics.cpp:11-19) of every CSR sample set (<= 4096 each)."""
+        """Nearest-rank quantile (metrics.cpp:11-19) of every CSR sample set (any size)."""
         off = self._dev(off, torch.int64)
         s = self._dev(samples, torch.float64)
         out = self._empty(off.numel() - 1, torch.float64)

@@ -577,12 +577,11 @@ std::vector<PrefillFreqCommand> queue_optimizer_tick(const std::vector<ClassQueu
 }
 
 // ================================================================== metrics.hpp
-// Nearest-rank quantile (metrics.cpp:11-19) through gsb_quantile_batch (sets up to 4096).
+// Nearest-rank quantile (metrics.cpp:11-19) through gsb_quantile_batch (any set size: sets up
+// to 4096 samples are sorted in shared memory, larger ones take an exact radix select).
 double quantile(std::span<const double> samples, double q) {
   if (samples.empty()) throw std::invalid_argument("quantile: empty sample set");
   if (q < 0.0 || q > 1.0) throw std::invalid_argument("quantile: q outside [0, 1]");
-  if (samples.size() > 4096)
-    throw std::length_error("quantile: the B200 kernel takes at most 4096 samples per set");
   const int64_t off[2] = {0, static_cast<int64_t>(samples.size())};
   Call call;
   const size_t o_off = call.in(off, sizeof off);

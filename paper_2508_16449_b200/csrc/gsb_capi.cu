@@ -275,11 +275,14 @@ int gsb_routing_validate(const gsb_route_cfg* cfg, int n_prefill_workers,
                          const int32_t* worker_map, char* msg, size_t cap) {
   std::string m;
   const int nt = cfg->n_thresholds;
+  // thresholds[] holds GSB_MAX_CLASSES - 1 entries: read no further, reject longer lists after
+  // the order / positivity checks (the reference's check order, router.cpp:8-13)
+  const int nt_seen = std::min(nt, GSB_MAX_CLASSES - 1);
   if (nt < 1) m = "routing: need at least one threshold";
-  for (int i = 0; m.empty() && i + 1 < nt; ++i)
+  for (int i = 0; m.empty() && i + 1 < nt_seen; ++i)
     if (cfg->thresholds[i] >= cfg->thresholds[i + 1])
       m = "routing: thresholds must be ascending and distinct";
-  for (int i = 0; m.empty() && i < nt; ++i)
+  for (int i = 0; m.empty() && i < nt_seen; ++i)
     if (cfg->thresholds[i] < 1) m = "routing: thresholds must be >= 1";
   if (m.empty() && nt > GSB_MAX_CLASSES - 1) m = "routing: more than 7 thresholds";
   if (m.empty() && cfg->enabled) {
@@ -316,6 +319,12 @@ int gsb_set_profiles_ex(gsb_ctx* ctx, int n, const gsb_profile* profiles, int fl
   // the pinned staging area is reused: wait until the previous upload has read it
   if (cudaEventSynchronize(ctx->stage_free) != cudaSuccess)
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "set_profiles: staging wait failed");
+  // d_tabs is read by kernels launched on ANY stream (k_select_batches, k_energy_batches, ...):
+  // without GSB_PROFILES_ASYNC (whose contract is "every launch on the context's stream", where
+  // stream order already serialises the upload behind them) the new tables may only land once
+  // every kernel already issued on the device has finished reading the old ones
+  if (!(flags & GSB_PROFILES_ASYNC) && cudaDeviceSynchronize() != cudaSuccess)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "set_profiles: device sync failed");
   for (int p = 0; p < n; ++p) {
     const gsb_profile& pr = profiles[p];
     gsb::ProfTab& t = ctx->h_stage[p];

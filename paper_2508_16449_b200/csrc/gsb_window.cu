@@ -225,6 +225,57 @@ namespace {
 
 constexpr int kQMax = 4096;
 
+// Sets larger than kQMax (the reference takes any size, metrics.cpp:11-19): the element of
+// 0-based rank r = max(ceil(q n), 1) - 1 in ascending order, found by an 8-pass radix select
+// (8-bit digits, most significant first) over order-preserving 64-bit keys of the doubles
+// (negative: all bits flipped, else the sign bit set), each pass one read of the set. Ties
+// (equal keys) are the same double, so the result is the value std::sort would put there.
+__device__ __forceinline__ uint64_t q_key(double v) {
+  const uint64_t u = static_cast<uint64_t>(__double_as_longlong(v));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__device__ void quantile_radix_select(double q, const double* __restrict__ x, int64_t n,
+                                      double* __restrict__ out) {
+  __shared__ unsigned long long hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ long long s_k;
+  const int64_t rank = static_cast<int64_t>(ceil(q * static_cast<double>(n)));
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_k = rank == 0 ? 0 : rank - 1;
+  }
+  uint64_t mask = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint64_t prefix = s_prefix;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t k = q_key(x[i]);
+      if ((k & mask) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1ull);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long k = s_k;
+      int b = 0;
+      for (; b < 255; ++b) {
+        const long long h = static_cast<long long>(hist[b]);
+        if (k < h) break;
+        k -= h;
+      }
+      s_k = k;
+      s_prefix = prefix | (static_cast<uint64_t>(b) << shift);
+    }
+    mask |= 0xffull << shift;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t k = s_prefix;
+    const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    *out = __longlong_as_double(static_cast<long long>(u));
+  }
+}
+
 // One CTA per set: stage <= 4096 samples in shared memory (padded with +inf to a power of two),
 // bitonic sort, read sorted[ceil(q n) - 1] (rank 0 -> minimum), metrics.cpp:14-18.
 __global__ void __launch_bounds__(256) k_quantile(double q, int64_t n_sets,
@@ -235,8 +286,12 @@ __global__ void __launch_bounds__(256) k_quantile(double q, int64_t n_sets,
   const int64_t set = blockIdx.x;
   if (set >= n_sets) return;
   const int64_t b0 = off[set], n64 = off[set + 1] - b0;
-  if (n64 <= 0 || n64 > kQMax) {
+  if (n64 <= 0) {
     if (threadIdx.x == 0) out[set] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  if (n64 > kQMax) {  // any larger set: exact radix select of the same rank
+    quantile_radix_select(q, x + b0, n64, out + set);
     return;
   }
   const int n = static_cast<int>(n64);

@@ -132,4 +132,10 @@ TEST_CASE("decode controller: quantile and window helpers") {
   CHECK(quantile(v, 1.0) == 100.0);
   CHECK_THROWS_AS(quantile(std::vector<double>{}, 0.5), std::invalid_argument);
   CHECK_THROWS_AS(quantile(v, 1.5), std::invalid_argument);
+  // any set size, as metrics.cpp:11-19 (io.cpp's tbt_digest passes a request's whole TBT list)
+  std::vector<double> big;
+  for (int i = 0; i < 50000; ++i) big.push_back(static_cast<double>((i * 7919) % 50000) * 0.5 - 3.0);
+  CHECK(quantile(big, 0.0) == -3.0);
+  CHECK(quantile(big, 0.95) == 47500.0 * 0.5 - 3.0 - 0.5);
+  CHECK(quantile(big, 1.0) == 49999.0 * 0.5 - 3.0);
 }

@@ -145,8 +145,10 @@ def test_decode_script_resumed_state_equals_one_shot(gsb, ref):
 
 def test_quantile_batch_matches_reference(gsb, ref):
     rng = np.random.default_rng(5)
-    sizes = np.concatenate([[1, 2, 3, 4, 5, 19, 20, 21, 255, 256, 257, 1024, 4095, 4096],
-                            rng.integers(1, 4097, 30)])
+    # > 4096 samples: the radix-select path (the reference takes any size; io.cpp's tbt_digest
+    # feeds it a request's whole TBT list)
+    sizes = np.concatenate([[1, 2, 3, 4, 5, 19, 20, 21, 255, 256, 257, 1024, 4095, 4096, 4097,
+                             9000, 70_001, 300_000], rng.integers(1, 4097, 30)])
     sets = []
     for n in sizes:
         kind = rng.integers(0, 3)

@@ -75,21 +75,27 @@ def test_fast_division_equals_ieee(eng):
     # sparse: most windows empty, window edges far apart
     ([512, 1024, 4096], 2, 0.02, 1_000),
 ])
-def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms):
+# want_deadline False selects the FIXED-mode K1b instances (k_route_bin<C, P, DL=0, G>), the ones
+# the bench times; True the deadline instances
+@pytest.mark.parametrize("want_deadline", [True, False])
+def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms, want_deadline):
     api = _api()
     profs = synth_profiles(api)[:P]
     eng.set_profiles(profs)
     a, p, _ = restate.gen_poisson_trace(qps, 1_800_000, 768.0, 3072.0, 0.15, 128.0, seed=len(thr))
     nw = int(a[-1] // wms) + 1
     rr = eng.route_bin(a, p, api.RoutingConfig(True, thr, list(range(len(thr) + 1))), wms, 0, nw,
-                       want_deadline=True, want_fifo=True)
+                       want_deadline=want_deadline, want_fifo=True)
     torch.cuda.synchronize()
     cls, cnt, tref, mdl, fifo = restate.route_bin(a, p, thr, wms, 0, nw,
                                                   [to_oracle(x) for x in profs])
     np.testing.assert_array_equal(rr.cls.cpu().numpy(), cls)
     np.testing.assert_array_equal(rr.count.cpu().numpy().view(np.uint32), cnt)
     np.testing.assert_array_equal(u64(rr.t_ref.cpu().numpy()), u64(tref))
-    np.testing.assert_array_equal(u64(rr.min_deadline.cpu().numpy()), u64(mdl))
+    if want_deadline:
+        np.testing.assert_array_equal(u64(rr.min_deadline.cpu().numpy()), u64(mdl))
+    else:
+        assert rr.min_deadline is None
     np.testing.assert_array_equal(rr.fifo.cpu().numpy(), fifo)
     eng.set_profiles([api.GpuProfile.default_profile()])
 

@@ -30,6 +30,8 @@ METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
     "launch__registers_per_thread": "regs",
     "smsp__inst_executed.sum": "warp_insts",
+    "smsp__inst_executed_pipe_fp64.sum": "fp64_insts",
+    "sm__cycles_active.avg": "sm_cycles_active",
 }
 UNIT_SCALE = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
               "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6,
@@ -82,7 +84,7 @@ def main(rnd):
     os.makedirs(PROF, exist_ok=True)
     launch_summary(rnd)
     recs = []
-    for part in ("prefill", "decode"):
+    for part in ("prefill", "decode", "pool"):
         rep = os.path.join(OUT, f"{rnd}_{part}.ncu-rep")
         if os.path.exists(rep):
             recs += rep_metrics(rep)
@@ -90,6 +92,8 @@ def main(rnd):
              "| kernel | us | DRAM R+W MB | DRAM % | SM % | FP64 pipe % (active) | issue % (active) | occupancy % | regs | warp insts |",
              "|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
+    units_path = os.path.join(OUT, f"{rnd}_units.json")
+    units = json.load(open(units_path)) if os.path.exists(units_path) else {}
     for r in recs:
         mb = (r.get("dram_read", 0) + r.get("dram_write", 0)) / 1e6
         lines.append(f"| `{r['kernel']}` | {r.get('duration', 0):.1f} | {mb:.2f} | "
@@ -97,8 +101,14 @@ def main(rnd):
                      f"{r.get('fp64_pipe_pct_active', 0):.1f} | {r.get('issue_pct_active', 0):.1f} | "
                      f"{r.get('occupancy_pct', 0):.1f} | {r.get('regs', 0):.0f} | "
                      f"{r.get('warp_insts', 0):.3g} |")
-        traffic.setdefault(r["kernel"], {"dram_bytes_per_launch": mb * 1e6,
-                                         "duration_us": r.get("duration", 0)})
+        rec = {"dram_bytes_per_launch": mb * 1e6, "duration_us": r.get("duration", 0),
+               "warp_insts": r.get("warp_insts"), "fp64_insts": r.get("fp64_insts"),
+               "fp64_pipe_pct_active": r.get("fp64_pipe_pct_active"),
+               "issue_pct_active": r.get("issue_pct_active")}
+        u = next((v for k, v in units.items() if r["kernel"].startswith(k)), None)
+        if u:
+            rec["units"] = u
+        traffic.setdefault(r["kernel"], rec)
     open(os.path.join(PROF, f"{rnd}_kernels.md"), "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(os.path.join(PROF, f"{rnd}_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
