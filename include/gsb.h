@@ -165,6 +165,25 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
                   uint8_t* d_class, uint32_t* d_count, double* d_t_ref, double* d_min_deadline,
                   void* stream);
 
+/* The non-empty cells of a pass (count > 0) in ascending order, as K1b emits them in the same
+ * pass as gsb_route_bin (decoupled look-back across its CTAs): K2 then runs as one wave of fully
+ * populated warps over the list (an empty queue gives no command, prefill_opt.cpp:64). The
+ * per-cell inputs K2 needs are also written in list order, so K2 reads them coalesced. */
+typedef struct gsb_cell_list {
+  uint32_t* d_cells;        /* [capacity] ascending non-empty cells (cells < 2^32) */
+  int64_t* d_n;             /* [1] entries, written on the device */
+  double* d_t_ref;          /* optional [P][capacity]: t_ref of the listed cells, per profile */
+  double* d_min_deadline;   /* optional [capacity]: min_deadline of the listed cells */
+  int64_t capacity;         /* >= cells of the pass */
+} gsb_cell_list;
+
+/* gsb_route_bin plus the cell list. Uses per-context sync words: calls on one context must be
+ * stream-ordered. */
+int gsb_route_bin_list(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
+                       const int64_t* d_arrival, const int32_t* d_prompt, const int64_t* d_bounds,
+                       uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                       double* d_min_deadline, const gsb_cell_list* list, void* stream);
+
 /* Dispatcher queue contents: stable per-cell FIFO of request indices (cell-major), i.e.
  * Dispatcher::queue(q) of every window (router.cpp:37-43). d_cell_off[cells+1] receives
  * the exclusive prefix of d_count. */
@@ -249,7 +268,7 @@ int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_c
                         gsb_class_summary* d_out /* [n_profiles*n_classes] */, void* stream);
 
 /* K2 with the per-class summary fused: gsb_prefill_select's outputs plus the
- * gsb_prefill_summary record of every (profile, class). The per-CTA partials are folded in
+ * gsb_prefill_summary record of every (profile, class). The per-chunk partials are folded in
  * K2's epilogue and one small kernel combines them. Same fixed-shape tree as
  * gsb_prefill_summary, so the two paths give identical bytes. Needs cfg->n_classes with n_cells = windows x classes.
  * Replaces the reference's end-of-run energy / SLO tallies over queue_optimizer_tick's
@@ -258,6 +277,16 @@ int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t 
                                const double* d_t_ref, const uint32_t* d_count,
                                const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
                                double* d_energy, gsb_class_summary* d_summary, void* stream);
+
+/* gsb_prefill_select_summary over a cell list from gsb_route_bin_list (its d_t_ref /
+ * d_min_deadline are used when present, else d_t_ref / d_min_deadline are gathered per cell;
+ * list == NULL: the list is built from d_count first). d_summary may be NULL. Results are
+ * identical to gsb_prefill_select_summary's. */
+int gsb_prefill_select_list(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                            const double* d_t_ref, const uint32_t* d_count,
+                            const gsb_cell_list* list, const double* d_min_deadline,
+                            double* d_window, int16_t* d_f_idx, double* d_energy,
+                            gsb_class_summary* d_summary, void* stream);
 
 /* ---------------------------------------------------------------- K6: trace CSV ingest */
 /* greensim::TraceError::Kind (trace.hpp:36-40), in the reference's enum order */

@@ -31,6 +31,12 @@ class CTraceResult(C.Structure):
                 ("line", C.c_char * 1024)]
 
 
+class CCellList(C.Structure):
+    """gsb_cell_list (include/gsb.h)."""
+    _fields_ = [("d_cells", _p), ("d_n", _p), ("d_t_ref", _p), ("d_min_deadline", _p),
+                ("capacity", _i64)]
+
+
 class CProfile(C.Structure):
     _fields_ = [(n, _d) for n in (
         "f_min_mhz", "f_max_mhz", "step_mhz", "f_ref_mhz",
@@ -132,7 +138,7 @@ EXPORTS = (
     "gsb_memcpy", "gsb_classify",
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
-    "gsb_trace_parse", "gsb_trace_format",
+    "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
 )
 
 _lib = None
@@ -173,6 +179,10 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_prefill_summary.argtypes = [_p, C.c_int, C.c_int, _i64, _p, _p, _p, _p]
     L.gsb_prefill_select_summary.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, _p, _p, _p, _p,
                                              _p, _p]
+    L.gsb_route_bin_list.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p,
+                                     P(CCellList), _p]
+    L.gsb_prefill_select_list.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, P(CCellList), _p, _p,
+                                          _p, _p, _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]
     L.gsb_n_ticks.restype = _i64
     L.gsb_window_series.argtypes = [_p, P(CTelemetry), C.c_int, _d, _d, _d, _p, _p, _p, _p]

@@ -422,6 +422,17 @@ class RouteResult:
     cell_off: Optional[torch.Tensor] = None  # i64 [cells+1]
     fifo: Optional[torch.Tensor] = None      # i64 [n_req] cell-major FIFO order
     profile_gen: int = -1                    # Engine.profile_gen its t_ref rows were built under
+    nonempty: Optional[torch.Tensor] = None  # u32 (as i32) [cells]: non-empty cells, ascending
+    n_nonempty: Optional[torch.Tensor] = None  # i64 [1]: entries of nonempty (device)
+    t_ref_list: Optional[torch.Tensor] = None  # f64 [P, cells]: t_ref of the listed cells
+    min_deadline_list: Optional[torch.Tensor] = None  # f64 [cells]: min_deadline, list order
+
+    def cell_list(self) -> Optional["L.CCellList"]:
+        """The gsb_cell_list K1b wrote (None: no list)."""
+        if self.nonempty is None:
+            return None
+        return L.CCellList(_ptr(self.nonempty), _ptr(self.n_nonempty), _ptr(self.t_ref_list),
+                           _ptr(self.min_deadline_list), self.nonempty.numel())
 
     @property
     def n_cells(self) -> int:
@@ -576,12 +587,21 @@ class Engine:
                               self._empty(n, torch.uint8), self._empty(cells, torch.int32),
                               self._empty((P, cells), torch.float64),
                               self._empty(cells, torch.float64) if want_deadline else None)
+            if cells < 2 ** 32:  # K1b also emits the non-empty cell list K2 runs over
+                out.nonempty = self._empty(cells, torch.int32)
+                out.n_nonempty = self._empty(1, torch.int64)
+                out.t_ref_list = self._empty((P, cells), torch.float64)
+                if want_deadline:
+                    out.min_deadline_list = self._empty(cells, torch.float64)
         s = self.stream()
         self._check(self.lib.gsb_window_bounds(self.ctx, C.byref(cfg), n, _ptr(arrival),
                                                _ptr(out.bounds), s))
-        self._check(self.lib.gsb_route_bin(self.ctx, C.byref(cfg), n, _ptr(arrival), _ptr(prompt),
-                                           _ptr(out.bounds), _ptr(out.cls), _ptr(out.count),
-                                           _ptr(out.t_ref), _ptr(out.min_deadline), s))
+        cl = out.cell_list()
+        self._check(self.lib.gsb_route_bin_list(self.ctx, C.byref(cfg), n, _ptr(arrival),
+                                                _ptr(prompt), _ptr(out.bounds), _ptr(out.cls),
+                                                _ptr(out.count), _ptr(out.t_ref),
+                                                _ptr(out.min_deadline),
+                                                C.byref(cl) if cl is not None else None, s))
         out.profile_gen = self.profile_gen
         if want_fifo:
             out.cell_off = self._empty(cells + 1, torch.int64)
@@ -676,11 +696,13 @@ class Engine:
             out = SelectResult(self._empty((P, cells), torch.int16),
                                self._empty((P, cells), torch.float64),
                                window if window is not None else self._empty(cells, torch.float64))
-        if summary_out is not None:
-            self._check(self.lib.gsb_prefill_select_summary(
+        if summary_out is not None or rr.nonempty is not None:
+            cl = rr.cell_list()
+            self._check(self.lib.gsb_prefill_select_list(
                 self.ctx, C.byref(cfg), cells, _ptr(rr.t_ref), _ptr(rr.count),
-                _ptr(rr.min_deadline), _ptr(out.window_ms), _ptr(out.f_idx), _ptr(out.energy_j),
-                _ptr(summary_out), self.stream()))
+                C.byref(cl) if cl is not None else None, _ptr(rr.min_deadline),
+                _ptr(out.window_ms), _ptr(out.f_idx), _ptr(out.energy_j), _ptr(summary_out),
+                self.stream()))
             return out
         self._check(self.lib.gsb_prefill_select(self.ctx, C.byref(cfg), cells, _ptr(rr.t_ref),
                                                 _ptr(rr.count), _ptr(rr.min_deadline),

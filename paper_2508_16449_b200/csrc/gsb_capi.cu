@@ -130,6 +130,27 @@ void* gsb_scratch(gsb_ctx* ctx, size_t bytes) {
   return ctx->d_scratch;
 }
 
+void* gsb_sync_words(gsb_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->sync_bytes) return ctx->d_sync;
+  const size_t want = std::max(bytes, ctx->sync_bytes * 2);
+  void* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  // zeroed before any kernel of the context's stream can use it; the old words (epochs,
+  // statuses) are not carried over: a fresh zero state is a valid state
+  if (cudaMemsetAsync(p, 0, want, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    cudaFree(p);
+    return nullptr;
+  }
+  if (ctx->d_sync) ctx->retired_scratch.push_back(ctx->d_sync);
+  ctx->d_sync = p;
+  ctx->sync_bytes = want;
+  return ctx->d_sync;
+}
+
 extern "C" {
 
 const char* gsb_version(void) { return "gsb 0.1 (sm_100a, abi 1)"; }
@@ -184,6 +205,7 @@ void gsb_ctx_destroy(gsb_ctx* c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   if (c->stage_free) cudaEventDestroy(c->stage_free);
   cudaFree(c->d_scratch);
+  cudaFree(c->d_sync);
   for (void* p : c->retired_scratch) cudaFree(p);
   cudaFree(c->d_ticks);
   if (c->stream) cudaStreamDestroy(c->stream);

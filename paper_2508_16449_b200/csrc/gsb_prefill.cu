@@ -176,6 +176,23 @@ struct RouteSmem {  // one CTA
   int32_t hist[kRouteWarps][K];  // per-warp key counts, then per-warp scatter cursors
   uint32_t cnt[K];
   unsigned long long mdl[DL ? K : 1];
+  int32_t lwarp[kRouteWarps];  // non-empty list: per-warp counts, the CTA's prefix, the epoch
+  long long lexcl;
+  unsigned lepoch;
+  int32_t lpos[K];             // list position of cell k relative to lexcl (-1: empty)
+};
+
+// Optional output of K1b: the ascending list of non-empty cells (count > 0) for K2, built in
+// the same pass by the decoupled look-back (gsb::lookback_prefix) over the CTAs in launch
+// order (CTA b owns cells [b*G*C, (b+1)*G*C), so CTA order is cell order).
+struct ListOut {
+  uint32_t* list;            // [cells] (NULL: no list)
+  int64_t* n_list;
+  double* t_ref;             // optional [P][cap]: t_ref in list order
+  double* min_deadline;      // optional [cap]
+  int64_t cap;
+  gsb::CompactHdr* hdr;
+  unsigned long long* status;  // [gridDim.x]
 };
 
 template <int C, int P, bool DL, int GW>
@@ -183,7 +200,7 @@ __global__ void __launch_bounds__(kRouteWarps * 32, GW * C > 64 ? 6 : kRouteMinB
 k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
             const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
             uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
-            double* __restrict__ t_ref, double* __restrict__ min_deadline) {
+            double* __restrict__ t_ref, double* __restrict__ min_deadline, ListOut lo) {
   constexpr int G = GW, K = G * C, E = (K + 31) / 32, NW = kRouteWarps;
   constexpr int kNever = 0x3fffffff;
   using S = RouteSmem<K, DL>;
@@ -202,7 +219,11 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
     s.cnt[k] = 0;
     if (DL) s.mdl[k] = ~0ull;
   }
-  if (tid == 0) gsb::mbar_init(&s.bar, 1);
+  unsigned epoch = 0;  // read now, used in the epilogue (the load's latency hides behind the pass)
+  if (tid == 0) {
+    gsb::mbar_init(&s.bar, 1);
+    if (lo.list) epoch = __ldcg(&lo.hdr->epoch);
+  }
   __syncthreads();
   const int64_t b0 = s.bnd[0], bG = s.bnd[G];
   const bool tma = (reinterpret_cast<uintptr_t>(prompt) & 15) == 0;
@@ -373,12 +394,74 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
       min_deadline[cell] = v == ~0ull ? INFINITY : unord_f64(v);
     }
   }
+  if (lo.list) {  // this CTA's non-empty cells, in cell order, at their global list positions
+    constexpr int KT = (K + NW * 32 - 1) / (NW * 32);  // consecutive cells per thread
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const int k = tid * KT + j;
+      if (k < K && w_first + k / C < rp.n_windows && s.cnt[k] != 0) m |= 1u << j;
+    }
+    const int c = __popc(m);
+    int incl = c;  // (this thread's cells' positions: below, once the warp prefix is known)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s.lwarp[wib] = incl;
+    if (tid == 0) s.lepoch = epoch;
+    __syncthreads();
+    int wbase = 0, agg = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      wbase += k < wib ? s.lwarp[k] : 0;
+      agg += s.lwarp[k];
+    }
+    if (wib == 0) {
+      const long long excl = gsb::lookback_prefix(lo.status, blockIdx.x, s.lepoch, agg);
+      if (lane == 0) s.lexcl = excl;
+    }
+    __syncthreads();
+    int rel = wbase + incl - c;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const int k = tid * KT + j;
+      if (k >= K) break;
+      const bool ne = (m >> j) & 1u;
+      s.lpos[k] = ne ? rel : -1;
+      if (ne) {
+        lo.list[s.lexcl + rel] = static_cast<uint32_t>(w_first * C + k);
+        if (DL && lo.min_deadline) {
+          const unsigned long long v = s.mdl[DL ? k : 0];
+          lo.min_deadline[s.lexcl + rel] = v == ~0ull ? INFINITY : unord_f64(v);
+        }
+        ++rel;
+      }
+    }
+    if (tid == 0 && blockIdx.x == gridDim.x - 1) {
+      *lo.n_list = s.lexcl + agg;
+      gsb::lookback_finish(lo.hdr, s.lepoch);
+    }
+    if (lo.t_ref) {  // the fold lanes' T_ref, in list order
+      __syncthreads();
+      if (folder && w_first + fg < rp.n_windows) {
+#pragma unroll
+        for (int k = 0; k < CPW; ++k) {
+          const int c = wib + k * NW;
+          if (c >= C) continue;
+          const int r = s.lpos[fg * C + c];
+          if (r >= 0) lo.t_ref[fp * lo.cap + s.lexcl + r] = acc[k];
+        }
+      }
+    }
+  }
 }
 
 template <int C, int P, bool DL, int G>
 int launch_route_bin_g(const RouteParams& rp, const int64_t* d_arrival, const int32_t* d_prompt,
                        const int64_t* d_bounds, uint8_t* d_class, uint32_t* d_count,
-                       double* d_t_ref, double* d_min_deadline, cudaStream_t s) {
+                       double* d_t_ref, double* d_min_deadline, const ListOut& lo, cudaStream_t s) {
   const size_t smem = sizeof(RouteSmem<G * C, DL>);
   if (cudaFuncSetAttribute(k_route_bin<C, P, DL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
@@ -386,7 +469,7 @@ int launch_route_bin_g(const RouteParams& rp, const int64_t* d_arrival, const in
   const unsigned blocks = static_cast<unsigned>((rp.n_windows + G - 1) / G);
   if (gsb::launch_pdl(k_route_bin<C, P, DL, G>, dim3(blocks), dim3(kRouteWarps * 32), smem, s, rp,
                       d_arrival, d_prompt, d_bounds, d_class, d_count, d_t_ref,
-                      d_min_deadline) != cudaSuccess)
+                      d_min_deadline, lo) != cudaSuccess)
     return -1;
   return 0;
 }
@@ -397,14 +480,15 @@ int launch_route_bin_g(const RouteParams& rp, const int64_t* d_arrival, const in
 template <int C, int P, bool DL>
 int launch_route_bin(const RouteParams& rp, int64_t n_req, const int64_t* d_arrival,
                      const int32_t* d_prompt, const int64_t* d_bounds, uint8_t* d_class,
-                     uint32_t* d_count, double* d_t_ref, double* d_min_deadline, cudaStream_t s) {
+                     uint32_t* d_count, double* d_t_ref, double* d_min_deadline,
+                     const ListOut& lo, cudaStream_t s) {
   if constexpr (P == 1) {
     if (n_req > rp.n_windows * (kRouteCap / 32))
       return launch_route_bin_g<C, P, DL, 8>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,
-                                             d_t_ref, d_min_deadline, s);
+                                             d_t_ref, d_min_deadline, lo, s);
   }
   return launch_route_bin_g<C, P, DL, 32 / P>(rp, d_arrival, d_prompt, d_bounds, d_class, d_count,
-                                              d_t_ref, d_min_deadline, s);
+                                              d_t_ref, d_min_deadline, lo, s);
 }
 
 // ---------------------------------------------------------------- K1c: Dispatcher FIFO
@@ -529,10 +613,34 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
 int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const int64_t* d_arrival,
                   const int32_t* d_prompt, const int64_t* d_bounds, uint8_t* d_class,
                   uint32_t* d_count, double* d_t_ref, double* d_min_deadline, void* stream) {
+  return gsb_route_bin_list(ctx, cfg, n_req, d_arrival, d_prompt, d_bounds, d_class, d_count,
+                            d_t_ref, d_min_deadline, nullptr, stream);
+}
+
+int gsb_route_bin_list(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
+                       const int64_t* d_arrival, const int32_t* d_prompt, const int64_t* d_bounds,
+                       uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                       double* d_min_deadline, const gsb_cell_list* list, void* stream) {
   if (!ctx) return GSB_INVALID_ARGUMENT;
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
   if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "route: no profiles set");
+  ListOut lo{};
+  if (list && list->d_cells) {
+    const int C = cfg->enabled ? cfg->n_thresholds + 1 : 1;
+    const int64_t cells = cfg->n_windows * C;
+    if (!list->d_n || cells >= (int64_t{1} << 32) || list->capacity < cells)
+      return gsb_set_error(ctx, GSB_INVALID_ARGUMENT,
+                           "route: list needs d_n, capacity >= cells and < 2^32 cells");
+    // K1b CTAs own >= 8 windows each: one look-back status per CTA after the 256-byte header
+    char* sy = static_cast<char*>(gsb_sync_words(
+        ctx, 256 + sizeof(unsigned long long) * static_cast<size_t>(cfg->n_windows / 8 + 2)));
+    if (!sy) return gsb_set_error(ctx, GSB_CUDA_ERROR, "route: sync allocation failed");
+    lo = ListOut{list->d_cells, list->d_n, list->d_t_ref,
+                 d_min_deadline ? list->d_min_deadline : nullptr, list->capacity,
+                 reinterpret_cast<gsb::CompactHdr*>(sy),
+                 reinterpret_cast<unsigned long long*>(sy + 256)};
+  }
   RouteParams rp = make_route_params(ctx, cfg);
   rp.want_deadline = d_min_deadline != nullptr;
   const int P = ctx->n_profiles;
@@ -544,11 +652,11 @@ int gsb_route_bin(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const i
 #define GSB_RB(CC, PP)                                                                          \
   case ((CC)-1) * 8 + ((PP)-1) * 2:                                                            \
     lrc = launch_route_bin<CC, PP, false>(rp, n_req, d_arrival, d_prompt, d_bounds, d_class,   \
-                                          d_count, d_t_ref, d_min_deadline, s);                \
+                                          d_count, d_t_ref, d_min_deadline, lo, s);            \
     break;                                                                                      \
   case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                        \
     lrc = launch_route_bin<CC, PP, true>(rp, n_req, d_arrival, d_prompt, d_bounds, d_class,    \
-                                         d_count, d_t_ref, d_min_deadline, s);                 \
+                                         d_count, d_t_ref, d_min_deadline, lo, s);             \
     break;
 #define GSB_RB_P(CC) GSB_RB(CC, 1) GSB_RB(CC, 2) GSB_RB(CC, 3) GSB_RB(CC, 4)
     GSB_RB_P(1) GSB_RB_P(2) GSB_RB_P(3) GSB_RB_P(4) GSB_RB_P(5) GSB_RB_P(6) GSB_RB_P(7) GSB_RB_P(8)

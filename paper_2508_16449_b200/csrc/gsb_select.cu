@@ -19,32 +19,36 @@ constexpr unsigned kFull = 0xffffffffu;
 
 // ---------------------------------------------------------------- per-class summary
 // Per (profile, class) reduction of a K2 pass (n_cmd, n_infeasible, n_empty, sum E, argmin
-// cell). Fixed-shape tree, so bitwise identical on every run and every rank:
-//   CTA (x, p) owns cells [256x, 256x+256) of profile p: slot t = cell - 256x;
-//   level 1: thread (segment s < 8, class c) folds the class-c slots of [32s, 32s+32) in slot
-//            order; level 2: thread c folds its 8 segments in order -> parts[p][c][x];
-//   final:   k_summary_final, one warp per (p, c): lane l folds x = l, l+32, ... in order,
-//            then a fixed 5-level shuffle tree.
-// K2 runs levels 1-2 in its own epilogue (gsb_prefill_select_summary: the objective, argmin
-// and partial reduction are one launch); gsb_prefill_summary runs the same tree from the
-// stored f_idx / energy, so both give identical bytes.
-constexpr int kSumCta = 256;  // (128-cell tiles measured slower: 30-32 vs 28 us, 2x partials)
+// cell); the fixed-shape tree is described at k_cells_finish.
+// The argmin travels as an order-preserving 64-bit key of the energy (negative: all bits
+// flipped, else the sign bit set), so combining two parts compares integers on the ALU pipe
+// instead of issuing quarter-rate DSETPs on the FP64 pipe K2 is bound by.
+__device__ __forceinline__ unsigned long long e_key(double x) {
+  unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+  if ((u << 1) == 0) u = 0;  // -0 == +0, as the double compare has it
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double e_unkey(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+constexpr unsigned long long kKeyInf = 0xfff0000000000000ull;  // e_key(+inf)
 
-struct Part {
-  double sum, mn;
-  long long cmd, inf, emp, arg;
+struct alignas(16) Part {  // 32 bytes: two 16-byte loads
+  double sum;
+  unsigned long long mnk;  // e_key of the minimum energy (kKeyInf: none)
+  long long arg;           // its cell (lowest on ties), -1: none
+  int cmd, inf;
 };
 
-__device__ __forceinline__ Part part_identity() { return Part{0.0, INFINITY, 0, 0, 0, -1}; }
+__device__ __forceinline__ Part part_identity() { return Part{0.0, kKeyInf, -1, 0, 0}; }
 
-// one cell's contribution: f_idx -2 empty, -1 infeasible (a command pinned at f_max), else a
-// choice with energy e (the argmin skips non-finite energies, as a '<' scan from +inf does)
+// one non-empty cell's contribution: f_idx -1 infeasible (a command pinned at f_max), else a
+// choice with energy e (the argmin skips non-finite energies, as a '<' scan from +inf does);
+// empty cells are not listed (n_empty = windows - commands)
 __device__ __forceinline__ Part part_of_cell(int fi, double e, long long cell) {
   Part v = part_identity();
-  if (fi == -2) {
-    v.emp = 1;
-    return v;
-  }
+  if (fi == -2) return v;
   v.cmd = 1;
   if (fi < 0) {
     v.inf = 1;
@@ -52,7 +56,7 @@ __device__ __forceinline__ Part part_of_cell(int fi, double e, long long cell) {
   }
   v.sum = e;
   if (e < INFINITY) {
-    v.mn = e;
+    v.mnk = e_key(e);
     v.arg = cell;
   }
   return v;
@@ -62,96 +66,10 @@ __device__ __forceinline__ void part_combine(Part& x, const Part& y) {
   x.sum = x.sum + y.sum;
   x.cmd += y.cmd;
   x.inf += y.inf;
-  x.emp += y.emp;
-  if (y.arg >= 0 && (x.arg < 0 || y.mn < x.mn || (y.mn == x.mn && y.arg < x.arg))) {
-    x.mn = y.mn;
+  if (y.arg >= 0 && (x.arg < 0 || y.mnk < x.mnk || (y.mnk == x.mnk && y.arg < x.arg))) {
+    x.mnk = y.mnk;
     x.arg = y.arg;
   }
-}
-
-struct SumArgs {
-  Part* parts;  // [P][C][gridDim.x]
-};
-
-struct SumSmem {
-  Part s1[kSumCta];  // slot t's contribution
-  Part s2[8 * GSB_MAX_CLASSES];
-};
-
-// Levels 1-2 of the tree for tile (x, p) once sm.s1 holds every slot's contribution (the
-// caller synchronises before and after).
-__device__ __forceinline__ void summary_tile(SumSmem& sm, int C, const SumArgs& sa, int x, int p,
-                                             int nx) {
-  const int t = threadIdx.x;
-  const long long cell0 = static_cast<long long>(x) * kSumCta;
-  if (t < 8 * C) {
-    const int c = t % C, seg = t / C;
-    const int r0 = static_cast<int>((cell0 + seg * 32) % C);
-    Part a = part_identity();
-    for (int j = seg * 32 + (c - r0 + C) % C; j < seg * 32 + 32; j += C) part_combine(a, sm.s1[j]);
-    sm.s2[seg * C + c] = a;
-  }
-  __syncthreads();
-  if (t < C) {
-    Part a = sm.s2[t];
-    for (int seg = 1; seg < 8; ++seg) part_combine(a, sm.s2[seg * C + t]);
-    sa.parts[(static_cast<long long>(p) * C + t) * nx + x] = a;
-  }
-}
-
-__device__ __forceinline__ Part part_shfl_down(const Part& v, int o) {
-  Part r;
-  r.sum = __shfl_down_sync(kFull, v.sum, o);
-  r.mn = __shfl_down_sync(kFull, v.mn, o);
-  r.cmd = __shfl_down_sync(kFull, v.cmd, o);
-  r.inf = __shfl_down_sync(kFull, v.inf, o);
-  r.emp = __shfl_down_sync(kFull, v.emp, o);
-  r.arg = __shfl_down_sync(kFull, v.arg, o);
-  return r;
-}
-
-// one warp per (profile, class) pc: lane l folds the partials x = l, l+32, ... in x order,
-// then a fixed 5-level shuffle tree
-__global__ void __launch_bounds__(32)
-k_summary_final(const Part* __restrict__ parts, int nx, gsb_class_summary* __restrict__ out) {
-  const int pc = blockIdx.x, lane = threadIdx.x;
-  gsb::grid_dep_wait();  // the tile partials (programmatic dependent launch)
-  Part a = part_identity();
-  const Part* src = parts + static_cast<long long>(pc) * nx;
-#pragma unroll 4
-  for (int x = lane; x < nx; x += 32) part_combine(a, src[x]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const Part y = part_shfl_down(a, o);
-    if (lane < o) part_combine(a, y);
-  }
-  if (lane == 0) {
-    gsb_class_summary o;
-    o.n_cmd = a.cmd;
-    o.n_infeasible = a.inf;
-    o.n_empty = a.emp;
-    o.sum_energy_j = a.sum;
-    o.min_energy_j = a.mn;
-    o.argmin_cell = a.arg;
-    out[pc] = o;
-  }
-}
-
-// gsb_prefill_summary: the same tree from stored f_idx / energy
-__global__ void __launch_bounds__(kSumCta)
-k_summary(int C, int64_t n_cells, const int16_t* __restrict__ f_idx,
-          const double* __restrict__ energy, SumArgs sa) {
-  __shared__ SumSmem sm;
-  const int64_t cell = static_cast<int64_t>(blockIdx.x) * kSumCta + threadIdx.x;
-  Part v = part_identity();
-  if (cell < n_cells) {
-    const int64_t o = static_cast<int64_t>(blockIdx.y) * n_cells + cell;
-    v = part_of_cell(f_idx[o], energy[o], cell);
-  }
-  sm.s1[threadIdx.x] = v;
-  __syncthreads();
-  summary_tile(sm, C, sa, static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
-               static_cast<int>(gridDim.x));
 }
 
 // ---------------------------------------------------------------- K2: objective + argmin
@@ -283,7 +201,7 @@ __device__ __forceinline__ bool cell_fast(double TF, double W, double p_idle, do
   const double x_lo = TF * P_min * 0x1p-12, x_hi = TF * P_max;
   const double y_lo = p_idle * fmin(W, TF * 0x1p-12) * 0x1p-53, y_hi = p_idle * fmax(W, TF);
   return TF >= lo && TF <= hi && W >= lo && W <= hi && x_lo >= lo && x_hi <= hi && y_lo >= lo &&
-         y_hi <= hi;
+         y_hi <= hi && P_min > 0.0 && p_idle > 0.0;
 }
 
 template <int G>
@@ -295,79 +213,93 @@ struct ClockSet {  // every profile of the pass, one kernel-parameter block (<= 
 
 // cells first, first + stride, ... of profile PI; SUM: one cell (stride = n) and its summary
 // contribution in *part
-template <int G, int PI, bool SUM>
+// The exhaustive scan of one (cell, profile PI): returns the grid index of the choice (-1:
+// nothing feasible) and its energy in *be_out.
+template <int G, int PI>
+__device__ __forceinline__ int scan_clocks_c(const ClockSet<G>& cs, double T, double W,
+                                             double* be_out) {
+  const ClockConst<G>& cc = cs.c[PI];
+  const double f_ref = cs.f_ref[PI], p_idle = cs.p_idle[PI], P_min = cs.P_min[PI],
+               P_max = cs.P_max[PI];
+  const double TF = T * f_ref;
+  int best = -1;
+  double be = 0.0;
+  if (cell_fast(TF, W, p_idle, P_min, P_max)) {
+    // every energy is finite here (the range guard), so "nothing taken yet or E < best" is
+    // exactly "E < be" with be starting at +inf
+    be = INFINITY;
+    // (Starting each lane's scan at its first feasible clock — busy_i is monotone — was
+    // measured 6x slower: per-lane trip counts break the unrolled loop into divergent code.
+    // A fully unrolled scan with constant-bank operands runs at the same rate in isolation,
+    // tools/micro/k2_loop.cu, but is 26 KB of SASS per profile.)
+#pragma unroll 9
+    for (int i = 0; i < G; ++i) {
+      const double f = cc.f[i], r = cc.r[i];
+      double q = __dmul_rn(TF, r);
+      double e = __fma_rn(-f, q, TF);
+      const double busy = __fma_rn(r, e, q);
+      const double x = __dmul_rn(cc.P[i], busy);
+      q = __dmul_rn(x, gsb::kRcp1000);
+      e = __fma_rn(-1000.0, q, x);
+      const double active = __fma_rn(gsb::kRcp1000, e, q);
+      const double wb = __dsub_rn(W, busy);
+      const double y = __dmul_rn(p_idle, wb);
+      q = __dmul_rn(y, gsb::kRcp1000);
+      e = __fma_rn(-1000.0, q, y);
+      const double idle = __fma_rn(gsb::kRcp1000, e, q);
+      const double E = __dadd_rn(active, idle);
+      // The two compares without DSETP (a quarter-rate FP64-pipe instruction on B200,
+      // tools/micro/fp64_mix.cu): busy <= W  <=>  RN(W - busy) >= +0 (equal operands give +0),
+      // a value the idle term needs anyway; E < be  <=>  RN(E - be) < 0 (finite operands: a
+      // nonzero difference never rounds to zero; E - inf = -inf). Both are sign tests of a high
+      // word on the integer pipe. Fast cells have P_i > 0 and p_idle > 0, so a feasible E is > 0
+      // and no signed-zero case arises.
+      const double d = __dsub_rn(E, be);
+      const bool take = (__double2hiint(wb) >= 0) & (__double2hiint(d) < 0);
+      best = take ? i : best;
+      be = take ? E : be;
+    }
+  } else {
+#pragma unroll 1
+    for (int i = 0; i < G; ++i) {
+      const double busy = __ddiv_rn(TF, cc.f[i]);
+      const double active = __ddiv_rn(__dmul_rn(cc.P[i], busy), 1000.0);
+      const double idle = __ddiv_rn(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0);
+      const double E = __dadd_rn(active, idle);
+      const bool take = (busy <= W) && (best < 0 || E < be);
+      best = take ? i : best;
+      be = take ? E : be;
+    }
+  }
+  *be_out = be;
+  return best;
+}
+
+// cells first, first + stride, ... of profile PI
+template <int G, int PI>
 __device__ __forceinline__ void select_cells_c(const SelectParams& sp, const ClockSet<G>& cs,
                                                const double* __restrict__ t_ref,
                                                const uint32_t* __restrict__ count,
                                                const double* __restrict__ min_deadline,
                                                double* __restrict__ window,
                                                int16_t* __restrict__ f_idx,
-                                               double* __restrict__ energy, Part* part,
-                                               int64_t first, int64_t stride) {
-  const ClockConst<G>& cc = cs.c[PI];
+                                               double* __restrict__ energy, int64_t first,
+                                               int64_t stride) {
   const int p = PI;
-  const double f_ref = cs.f_ref[PI], p_idle = cs.p_idle[PI], P_min = cs.P_min[PI],
-               P_max = cs.P_max[PI];
   const int64_t n = sp.n_cells;
   for (int64_t cell = first; cell < n; cell += stride) {
     const int64_t o = p * n + cell;
     if (count && count[cell] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
       f_idx[o] = -2;
       energy[o] = 0.0;
-      if (SUM) *part = part_of_cell(-2, 0.0, cell);
       continue;
     }
     const double W = cell_window(sp, cell, min_deadline, window);
     if (p == 0 && window && sp.mode != GSB_PER_CELL_WINDOW) window[cell] = W;
-    const double TF = t_ref[o] * f_ref;
-    int best = -1;
-    double be = 0.0;
-    if (cell_fast(TF, W, p_idle, P_min, P_max)) {
-      // every energy is finite here (the range guard), so "nothing taken yet or E < best"
-      // is exactly "E < be" with be starting at +inf: one compare per clock
-      be = INFINITY;
-      // (Starting each lane's scan at its first feasible clock — busy_i is monotone — was
-      // measured 6x slower: per-lane trip counts break the unrolled loop into divergent code.)
-      // unrolled 9x, not 81x: the table operands become uniform constant loads, and the four
-      // profile variants stay small enough for the instruction cache (a fully unrolled 81-clock
-      // scan is ~26 KB of SASS per profile: 2x slower on B200 from instruction-fetch stalls,
-      // even with every profile of a cell in one thread walking the variants in order)
-#pragma unroll 9
-      for (int i = 0; i < G; ++i) {
-        const double f = cc.f[i], r = cc.r[i];
-        double q = __dmul_rn(TF, r);
-        double e = __fma_rn(-f, q, TF);
-        const double busy = __fma_rn(r, e, q);
-        const double x = __dmul_rn(cc.P[i], busy);
-        q = __dmul_rn(x, gsb::kRcp1000);
-        e = __fma_rn(-1000.0, q, x);
-        const double active = __fma_rn(gsb::kRcp1000, e, q);
-        const double y = __dmul_rn(p_idle, __dsub_rn(W, busy));
-        q = __dmul_rn(y, gsb::kRcp1000);
-        e = __fma_rn(-1000.0, q, y);
-        const double idle = __fma_rn(gsb::kRcp1000, e, q);
-        const double E = __dadd_rn(active, idle);
-        // (integer-pipe compares of the bit patterns were measured slower: the kernel is
-        // issue-bound as much as FP64-bound, and they add instructions)
-        const bool take = (busy <= W) && (E < be);
-        best = take ? i : best;
-        be = take ? E : be;
-      }
-    } else {
-#pragma unroll 1
-      for (int i = 0; i < G; ++i) {
-        const double busy = __ddiv_rn(TF, cc.f[i]);
-        const double active = __ddiv_rn(__dmul_rn(cc.P[i], busy), 1000.0);
-        const double idle = __ddiv_rn(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0);
-        const double E = __dadd_rn(active, idle);
-        const bool take = (busy <= W) && (best < 0 || E < be);
-        best = take ? i : best;
-        be = take ? E : be;
-      }
-    }
+    double be;
+    const int best = scan_clocks_c<G, PI>(cs, t_ref[o], W, &be);
     f_idx[o] = static_cast<int16_t>(best);
     energy[o] = best >= 0 ? be : 0.0;
-    if (SUM) *part = part_of_cell(best, be, cell);
   }
 }
 
@@ -381,8 +313,7 @@ k_prefill_select_c(const __grid_constant__ SelectParams sp, const __grid_constan
   const int64_t first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
 #define GSB_SEL(PI)                                                                             \
-  select_cells_c<G, PI, false>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy, nullptr, \
-                               first, stride)
+  select_cells_c<G, PI>(sp, cs, t_ref, count, min_deadline, window, f_idx, energy, first, stride)
   switch (blockIdx.y) {
     case 0: GSB_SEL(0); break;
     case 1: GSB_SEL(1); break;
@@ -393,71 +324,285 @@ k_prefill_select_c(const __grid_constant__ SelectParams sp, const __grid_constan
 }
 
 // (Measured and rejected: two cells per thread sharing the per-clock table loads — 47 vs 28 us,
-// more code and half the busy warps; 6 CTAs/SM at 40 registers — no change.)
-// K2 with the per-class summary fused: CTA (x, p) owns the 256-cell tile x of profile p. It
-// compacts the tile's NON-EMPTY cells onto its first threads (ballot + warp-offset scan), so
-// the 81-clock loop runs with every lane busy; warps with nothing to evaluate (and not needed
-// by the summary tree) exit at once and free their slots for the next CTAs. Empty queues give
-// no command (prefill_opt.cpp:64) and cost no FP64 issue slots. Each cell's result goes to its
-// own slot, so the summary tree (summary_tile) is the one gsb_prefill_summary runs, bit for bit.
-template <int G>
-__global__ void __launch_bounds__(kSumCta, 5)
-k_prefill_select_sum(const __grid_constant__ SelectParams sp, const __grid_constant__ ClockSet<G> cs,
-                     const double* __restrict__ t_ref, const uint32_t* __restrict__ count,
-                     const double* __restrict__ min_deadline, double* __restrict__ window,
-                     int16_t* __restrict__ f_idx, double* __restrict__ energy, SumArgs sa) {
-  __shared__ SumSmem sm;
-  __shared__ int s_slot[kSumCta];
-  __shared__ int s_wcnt[kSumCta / 32 + 1];
-  const int t = threadIdx.x, lane = t & 31, wib = t >> 5;
-  const int64_t n = sp.n_cells;
-  const int p = static_cast<int>(blockIdx.y), x = static_cast<int>(blockIdx.x);
-  const int64_t cell = static_cast<int64_t>(x) * kSumCta + t;
-  gsb::grid_dep_wait();  // K1's cells (programmatic dependent launch)
+// more code and half the busy warps; 6 CTAs/SM at 40 registers — no change; round 1's per-tile
+// compaction of 256-cell tiles: 1.7 waves of ragged warps, replaced by the global list below.)
+
+// ---------------------------------------------------------------- non-empty cell lists
+// K2 evaluates only non-empty (cell, profile) pairs (an empty queue gives no command,
+// prefill_opt.cpp:64). Compacting the non-empty cells into ONE ascending list lets K2 run as a
+// single wave of fully populated warps (one lane per (listed cell, profile)) instead of
+// per-tile compaction with ragged warps and a 1.7-wave tail.
+//
+// k_compact: one pass with decoupled look-back. A CTA takes the next 2048-item tile by ticket
+// (so every tile it waits on belongs to a CTA that is already running), publishes its count,
+// and its first warp sums its predecessors' published counts 32 tiles at a time until it
+// reaches a published inclusive prefix. Status word: launch epoch (24 bits) | flag (2 bits:
+// 1 = tile count, 2 = inclusive prefix) | value (38 bits). The epoch advances once per launch
+// (the last CTA to finish bumps it and rewinds the ticket counters), so no reset pass is
+// needed and a captured graph can replay the kernel.
+constexpr int kCompactThreads = 256, kCompactItems = 8;
+constexpr int kCompactTile = kCompactThreads * kCompactItems;
+
+using gsb::CompactHdr;
+
+struct NonEmptyCount {  // K1's queue sizes: non-empty iff count != 0
+  const uint32_t* p;
+  __device__ __forceinline__ unsigned mask8(int64_t i0, int64_t n) const {
+    unsigned m = 0;
+    if (i0 + 8 <= n && (reinterpret_cast<uintptr_t>(p + i0) & 15) == 0) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(p + i0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(p + i0) + 1);
+      m = (a.x != 0) | (a.y != 0) << 1 | (a.z != 0) << 2 | (a.w != 0) << 3 | (b.x != 0) << 4 |
+          (b.y != 0) << 5 | (b.z != 0) << 6 | (b.w != 0) << 7;
+    } else {
+      for (int j = 0; j < 8; ++j)
+        if (i0 + j < n && p[i0 + j] != 0) m |= 1u << j;
+    }
+    return m;
+  }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kCompactThreads)
+k_compact(Src src, int64_t n, CompactHdr* __restrict__ hdr,
+          unsigned long long* __restrict__ status, uint32_t* __restrict__ list,
+          int64_t* __restrict__ n_list) {
+  __shared__ unsigned s_tile, s_epoch;
+  __shared__ int s_warp[kCompactThreads / 32];
+  __shared__ long long s_excl;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  gsb::grid_dep_wait();  // the producer of src (K1) has finished
   gsb::grid_dep_launch();
-  const bool live = cell < n;
-  const bool busy = live && (!count || count[cell] != 0);
-  if (live && !busy) {  // empty queue: no command
-    const int64_t o = p * n + cell;
-    f_idx[o] = -2;
-    energy[o] = 0.0;
-  }
-  sm.s1[t] = live ? part_of_cell(-2, 0.0, cell) : part_identity();
-  const unsigned b = __ballot_sync(kFull, busy);
-  if (lane == 0) s_wcnt[wib] = __popc(b);
-  __syncthreads();
   if (t == 0) {
-    int run = 0;
-    for (int w = 0; w < kSumCta / 32; ++w) {
-      const int c = s_wcnt[w];
-      s_wcnt[w] = run;
-      run += c;
-    }
-    s_wcnt[kSumCta / 32] = run;
+    s_epoch = *reinterpret_cast<volatile unsigned*>(&hdr->epoch);
+    s_tile = atomicAdd(&hdr->ticket, 1u);
   }
   __syncthreads();
-  if (busy) s_slot[s_wcnt[wib] + __popc(b & ((1u << lane) - 1u))] = t;
+  const unsigned tile = s_tile, ep = s_epoch & 0xffffffu;
+  const unsigned n_tiles = static_cast<unsigned>((n + kCompactTile - 1) / kCompactTile);
+  const int64_t i0 = static_cast<int64_t>(tile) * kCompactTile + t * kCompactItems;
+  const unsigned m = src.mask8(i0, n);
+  const int c = __popc(m);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[w] = incl;
   __syncthreads();
-  const int n_busy = s_wcnt[kSumCta / 32];
-  // warps past the compacted work and the summary tree's 8 x C threads leave now
-  if ((wib << 5) >= max(n_busy, 8 * sp.C)) return;
-  if (t < n_busy) {
-    const int slot = s_slot[t];
-    Part v;
-#define GSB_SEL(PI)                                                                            \
-  select_cells_c<G, PI, true>(sp, cs, t_ref, nullptr, min_deadline, window, f_idx, energy, &v, \
-                              static_cast<int64_t>(x) * kSumCta + slot, n)
+  int wbase = 0, agg = 0;
+#pragma unroll
+  for (int k = 0; k < kCompactThreads / 32; ++k) {
+    wbase += k < w ? s_warp[k] : 0;
+    agg += s_warp[k];
+  }
+  if (w == 0) {
+    const long long excl = gsb::lookback_prefix(status, tile, ep, agg);
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  int64_t pos = s_excl + wbase + incl - c;
+  for (unsigned mm = m; mm; mm &= mm - 1) list[pos++] = static_cast<uint32_t>(i0 + __ffs(mm) - 1);
+  if (t == 0 && tile == n_tiles - 1) {
+    *n_list = s_excl + agg;
+    gsb::lookback_finish(hdr, s_epoch);
+  }
+}
+
+// ---------------------------------------------------------------- per-class summary tree
+// The per-(profile, class) summary of a pass, over the DENSE cell array (cell = w*C + c, so the
+// class-c cells are every C-th cell: no list, no per-class routing). Fixed shape, hence bitwise
+// identical on every run and rank, whichever entry point runs it:
+//   level 1  CTA (x, p) owns cells [x*T*K, (x+1)*T*K) with T = 32*C threads: thread t folds
+//            cells base + t + k*T, k = 0..K-1 (class t % C, windows in order); the same kernel
+//            writes the empty cells' "no command" outputs (-2, 0) when it is given the counts
+//   level 2  class c: slot j = t / C (0..31); (c, s) folds slots [8s, 8s+8) in order, then
+//            (s0 + s1) + (s2 + s3)                                          -> block part
+//   final    k_summary_final (one CTA per (profile, class)): thread q folds block parts q,
+//            q + 256, ... in order, then a fixed 256-wide tree
+// Empty cells only count (n_empty = windows - commands). Round 1's per-tile tree (and a list-
+// ordered one measured this round: ~15 extra instructions per cell inside the FP64-bound K2,
+// 4 us) are replaced by this memory-bound pass over 10 B per (cell, profile).
+constexpr int kSumK = 4;        // cells per thread in level 1
+constexpr int kFinalCta = 256;
+
+__device__ __forceinline__ Part part_shfl_down_w(const Part& v, int o, int width) {
+  Part r;
+  r.sum = __shfl_down_sync(kFull, v.sum, o, width);
+  r.mnk = __shfl_down_sync(kFull, v.mnk, o, width);
+  r.cmd = __shfl_down_sync(kFull, v.cmd, o, width);
+  r.inf = __shfl_down_sync(kFull, v.inf, o, width);
+  r.arg = __shfl_down_sync(kFull, v.arg, o, width);
+  return r;
+}
+
+__device__ __forceinline__ Part ld_part_cg(const Part* p) {  // L2 (written by other CTAs)
+  const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+  const longlong2 b = __ldcg(reinterpret_cast<const longlong2*>(p) + 1);
+  Part r;
+  r.sum = a.x;
+  r.mnk = static_cast<unsigned long long>(__double_as_longlong(a.y));
+  r.arg = b.x;
+  r.cmd = static_cast<int>(b.y & 0xffffffffll);
+  r.inf = static_cast<int>(b.y >> 32);
+  return r;
+}
+
+// Level 1 + 2 (and the empty-cell fill): grid (X, P), 32*C threads. count != NULL: cells with
+// count 0 get f_idx -2 / energy 0 (K2 evaluates only the listed, non-empty cells); else the
+// emptiness is read from f_idx (gsb_prefill_summary over stored results). parts == NULL: fill only.
+template <int C>
+__global__ void __launch_bounds__(32 * C)
+k_cells_finish(int64_t n_cells, const uint32_t* __restrict__ count, int16_t* __restrict__ f_idx,
+               double* __restrict__ energy, Part* __restrict__ parts, int64_t n_blocks) {
+  constexpr int T = 32 * C;
+  __shared__ Part sl[32][C];
+  __shared__ Part s2[4][C];
+  const int t = threadIdx.x, p = blockIdx.y;
+  gsb::grid_dep_wait();  // K2's results
+  gsb::grid_dep_launch();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * T * kSumK;
+  int16_t* fi = f_idx + p * n_cells;
+  double* en = energy + p * n_cells;
+  Part a = part_identity();
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int64_t cell = base + t + k * T;
+    if (cell >= n_cells) break;
+    if (count) {
+      if (count[cell] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
+        fi[cell] = -2;
+        en[cell] = 0.0;
+        continue;
+      }
+      if (parts) part_combine(a, part_of_cell(fi[cell], en[cell], cell));
+    } else if (parts) {
+      part_combine(a, part_of_cell(fi[cell], en[cell], cell));
+    }
+  }
+  if (!parts) return;
+  const int c = t % C, j = t / C;
+  sl[j][c] = a;
+  __syncthreads();
+  if (t < 4 * C) {  // (c, s): slots [8s, 8s+8) of class c
+    const int cc = t % C, ss = t / C;
+    Part b = sl[8 * ss][cc];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) part_combine(b, sl[8 * ss + i][cc]);
+    s2[ss][cc] = b;
+  }
+  __syncthreads();
+  if (t < C) {
+    Part b0 = s2[0][t], b2 = s2[2][t];
+    part_combine(b0, s2[1][t]);
+    part_combine(b2, s2[3][t]);
+    part_combine(b0, b2);
+    parts[(static_cast<int64_t>(p) * C + t) * n_blocks + blockIdx.x] = b0;
+  }
+}
+
+// final level: CTA (p, c) over the n_blocks block parts of (p, c)
+__global__ void __launch_bounds__(kFinalCta)
+k_summary_final(const Part* __restrict__ parts, int C, int64_t n_blocks, int64_t n_windows,
+                gsb_class_summary* __restrict__ out) {
+  __shared__ Part red[kFinalCta / 32];
+  const int pc = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  gsb::grid_dep_wait();  // the block parts
+  const Part* src = parts + static_cast<int64_t>(pc) * n_blocks;
+  Part a = part_identity();
+  int64_t x = t;
+  for (; x + kFinalCta < n_blocks; x += 2 * kFinalCta) {  // two loads in flight, in order
+    const Part p0 = ld_part_cg(src + x), p1 = ld_part_cg(src + x + kFinalCta);
+    part_combine(a, p0);
+    part_combine(a, p1);
+  }
+  for (; x < n_blocks; x += kFinalCta) part_combine(a, ld_part_cg(src + x));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const Part y = part_shfl_down_w(a, o, 32);
+    if (lane < o) part_combine(a, y);
+  }
+  if (lane == 0) red[w] = a;
+  __syncthreads();
+  if (w == 0) {
+    a = lane < kFinalCta / 32 ? red[lane] : part_identity();
+#pragma unroll
+    for (int o = kFinalCta / 64; o > 0; o >>= 1) {
+      const Part y = part_shfl_down_w(a, o, 32);
+      if (lane < o) part_combine(a, y);
+    }
+    if (lane == 0) {
+      gsb_class_summary o;
+      o.n_cmd = a.cmd;
+      o.n_infeasible = a.inf;
+      o.n_empty = n_windows - a.cmd;
+      o.sum_energy_j = a.sum;
+      o.min_energy_j = a.arg >= 0 ? e_unkey(a.mnk) : INFINITY;
+      o.argmin_cell = a.arg;
+      out[pc] = o;
+    }
+  }
+}
+
+// K2 over the non-empty list: CTA unit (profile p, chunk ch) evaluates list positions
+// [128 ch, 128 ch + 128) of profile p, one lane each (the profile is uniform per CTA, so the
+// per-profile constant-operand instantiation runs with no divergence). Persistent grid: units
+// b = blockIdx.x, + gridDim.x, ... (one wave at C4). Inputs in list order when K1b wrote them
+// (T_ref / min_deadline: coalesced, no dependent gather). Empty cells are finished by
+// k_cells_finish (their "no command" outputs and the summary), not here.
+struct ListIn {
+  const uint32_t* list;
+  const int64_t* n_list;
+  const double* t_ref;         // [P][cap] in list order, or NULL (gather t_ref[p][cell])
+  const double* min_deadline;  // [cap] in list order, or NULL (gather)
+  int64_t cap;
+};
+
+constexpr int kListCta = 128;
+
+template <int G>
+__global__ void __launch_bounds__(kListCta, 10)
+k_prefill_select_list(const __grid_constant__ SelectParams sp, const __grid_constant__ ClockSet<G> cs,
+                      int P, ListIn li, const double* __restrict__ t_ref,
+                      const double* __restrict__ min_deadline, double* __restrict__ window,
+                      int16_t* __restrict__ f_idx, double* __restrict__ energy) {
+  const int t = threadIdx.x;
+  gsb::grid_dep_wait();  // the list and K1's cells
+  gsb::grid_dep_launch();
+  const int64_t n = sp.n_cells;
+  const int64_t nl = *li.n_list;  // one list for every profile (emptiness is per cell); < 2^32
+  const unsigned nch = static_cast<unsigned>((nl + kListCta - 1) / kListCta);
+  const unsigned units = nch * static_cast<unsigned>(P);
+  for (unsigned b = blockIdx.x; b < units; b += gridDim.x) {
+    const int p = static_cast<int>(b / nch);
+    const int64_t k = static_cast<int64_t>(b - static_cast<unsigned>(p) * nch) * kListCta + t;
+    if (k >= nl) continue;
+    const int64_t cell = li.list[k];
+    const double T = li.t_ref ? li.t_ref[p * li.cap + k] : t_ref[p * n + cell];
+    double W;
+    if (sp.mode == GSB_FIXED_WINDOW) {
+      W = sp.fixed_window;
+    } else if (sp.mode == GSB_DEADLINE_SLACK) {
+      const double mdl = li.min_deadline ? li.min_deadline[k] : min_deadline[cell];
+      const double now = static_cast<double>((sp.w0 + cell / sp.C) * sp.window_ms);
+      W = std_max(sp.margin * (mdl - now), sp.min_budget);
+    } else {
+      W = window[cell];
+    }
+    if (p == 0 && window && sp.mode != GSB_PER_CELL_WINDOW) window[cell] = W;
+    double be;
+    int best;
     switch (p) {
-      case 0: GSB_SEL(0); break;
-      case 1: GSB_SEL(1); break;
-      case 2: GSB_SEL(2); break;
-      default: GSB_SEL(3); break;
+      case 0: best = scan_clocks_c<G, 0>(cs, T, W, &be); break;
+      case 1: best = scan_clocks_c<G, 1>(cs, T, W, &be); break;
+      case 2: best = scan_clocks_c<G, 2>(cs, T, W, &be); break;
+      default: best = scan_clocks_c<G, 3>(cs, T, W, &be); break;
     }
-#undef GSB_SEL
-    sm.s1[slot] = v;
+    const int64_t o = p * n + cell;
+    f_idx[o] = static_cast<int16_t>(best);
+    energy[o] = best >= 0 ? be : 0.0;
   }
-  __syncthreads();
-  summary_tile(sm, sp.C, sa, x, p, static_cast<int>(gridDim.x));
 }
 
 __global__ void __launch_bounds__(256)
@@ -691,6 +836,86 @@ __global__ void k_energy_closed_form(const ProfTab* __restrict__ tab, int64_t n_
   out[b] = active + idle;
 }
 
+// The non-empty list of a pass built by k_compact (when K1b did not emit one): the list and its
+// count in the context scratch, the look-back statuses in the context's zeroed sync words.
+struct ListPass {
+  uint32_t* list;
+  int64_t* n_list;
+  CompactHdr* hdr;
+  unsigned long long* status;
+  int64_t n_tiles;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t{255}; }
+
+bool list_pass_buffers(gsb_ctx* ctx, int64_t n_cells, size_t scratch_offset, ListPass* lp) {
+  lp->n_tiles = (n_cells + kCompactTile - 1) / kCompactTile;
+  char* sc = static_cast<char*>(gsb_scratch(
+      ctx, scratch_offset + align_up(sizeof(uint32_t) * n_cells) + sizeof(int64_t)));
+  char* sy = static_cast<char*>(gsb_sync_words(
+      ctx, 256 + align_up(sizeof(unsigned long long) * std::max<int64_t>(1, lp->n_tiles))));
+  if (!sc || !sy) return false;
+  lp->list = reinterpret_cast<uint32_t*>(sc + scratch_offset);
+  lp->n_list = reinterpret_cast<int64_t*>(sc + scratch_offset + align_up(sizeof(uint32_t) * n_cells));
+  lp->hdr = reinterpret_cast<CompactHdr*>(sy);
+  lp->status = reinterpret_cast<unsigned long long*>(sy + 256);
+  return true;
+}
+
+template <class Src>
+cudaError_t launch_compact(const ListPass& lp, Src src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaMemsetAsync(lp.n_list, 0, sizeof(int64_t), s);
+  return gsb::launch_pdl(k_compact<Src>, dim3(static_cast<unsigned>(lp.n_tiles)),
+                         dim3(kCompactThreads), 0, s, src, n, lp.hdr, lp.status, lp.list,
+                         lp.n_list);
+}
+
+// Block parts of the summary tree (placed at the start of the context scratch).
+int64_t finish_blocks(int C, int64_t n_cells) {
+  const int64_t per = static_cast<int64_t>(32) * C * kSumK;
+  return std::max<int64_t>(1, (n_cells + per - 1) / per);
+}
+
+size_t finish_scratch_bytes(int P, int C, int64_t n_cells) {
+  return align_up(sizeof(Part) * static_cast<size_t>(P) * C * finish_blocks(C, n_cells));
+}
+
+// k_cells_finish (+ k_summary_final when out != NULL) for a [P][n_cells] result.
+cudaError_t launch_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uint32_t* count,
+                          int16_t* f_idx, double* energy, gsb_class_summary* out, Part* parts,
+                          cudaStream_t s) {
+  (void)ctx;
+  const int64_t nb = finish_blocks(C, n_cells);
+  if (nb > 65535LL * 1024) return cudaErrorInvalidValue;
+  Part* pp = out ? parts : nullptr;
+  const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(P));
+  cudaError_t e = cudaSuccess;
+  if (n_cells > 0) {
+    switch (C) {
+#define GSB_FIN(CC)                                                                             \
+  case CC:                                                                                    \
+    e = gsb::launch_pdl(k_cells_finish<CC>, grid, dim3(32 * CC), 0, s, n_cells, count, f_idx,  \
+                        energy, pp, nb);                                                      \
+    break;
+      GSB_FIN(1) GSB_FIN(2) GSB_FIN(3) GSB_FIN(4) GSB_FIN(5) GSB_FIN(6) GSB_FIN(7) GSB_FIN(8)
+#undef GSB_FIN
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  if (e != cudaSuccess || !out) return e;
+  return gsb::launch_pdl(k_summary_final, dim3(static_cast<unsigned>(P * C)), dim3(kFinalCta), 0,
+                         s, static_cast<const Part*>(parts), C, n_cells > 0 ? nb : int64_t{0},
+                         n_cells / C, out);
+}
+
+template <class K>
+int resident_ctas(gsb_ctx* ctx, K kernel, int threads) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess || nb < 1)
+    nb = 1;
+  return nb * ctx->n_sms;
+}
+
 }  // namespace
 
 extern "C" {
@@ -714,6 +939,18 @@ int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t 
                                const double* d_t_ref, const uint32_t* d_count,
                                const double* d_min_deadline, double* d_window, int16_t* d_f_idx,
                                double* d_energy, gsb_class_summary* d_summary, void* stream) {
+  return gsb_prefill_select_list(ctx, cfg, n_cells, d_t_ref, d_count, nullptr, d_min_deadline,
+                                 d_window, d_f_idx, d_energy, d_summary, stream);
+}
+
+int gsb_prefill_select_list(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_cells,
+                            const double* d_t_ref, const uint32_t* d_count,
+                            const gsb_cell_list* list, const double* d_min_deadline,
+                            double* d_window, int16_t* d_f_idx, double* d_energy,
+                            gsb_class_summary* d_summary, void* stream) {
+  const uint32_t* d_list = list ? list->d_cells : nullptr;
+  if (d_list && (!list->d_n || list->capacity < n_cells))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: bad cell list");
   if (!ctx || !cfg) return GSB_INVALID_ARGUMENT;
   if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select: no profiles set");
   if (cfg->mode == GSB_DEADLINE_SLACK && (!d_min_deadline || cfg->n_classes < 1 || cfg->window_ms <= 0))
@@ -759,19 +996,35 @@ int gsb_prefill_select_summary(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t 
       cs.P_min[p] = t.P_min;
       cs.P_max[p] = t.P_max;
     }
-    const dim3 grid(gx, static_cast<unsigned>(ctx->n_profiles));
-    const int64_t tiles = want * ctx->n_profiles;
-    if (d_summary && want == static_cast<int64_t>(gx)) {  // one CTA per 256-cell tile
-      SumArgs sa{static_cast<Part*>(gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(tiles) *
-                                                         static_cast<size_t>(cfg->n_classes)))};
-      if (!sa.parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "select: scratch allocation failed");
-      gsb::launch_pdl(k_prefill_select_sum<81>, grid, dim3(kSumCta), 0, s, sp, cs, d_t_ref,
-                      d_count, d_min_deadline, d_window, d_f_idx, d_energy, sa);
-      gsb::launch_pdl(k_summary_final, dim3(static_cast<unsigned>(ctx->n_profiles * cfg->n_classes)),
-                      dim3(32), 0, s, static_cast<const Part*>(sa.parts), static_cast<int>(want),
-                      d_summary);
+    if (d_count && n_cells < (int64_t{1} << 32)) {
+      // non-empty list (K1b's, or k_compact's) + one wave of K2 over it, then the empty cells'
+      // outputs and the summary in one memory-bound pass
+      const int P = ctx->n_profiles, Cn = std::max(1, cfg->n_classes);
+      const size_t fin_bytes = d_summary ? finish_scratch_bytes(P, Cn, n_cells) : 0;
+      ListPass lp{};
+      ListIn li{};
+      if (d_list) {  // K1b's list (gsb_route_bin_list) and its list-order inputs
+        li = ListIn{d_list, list->d_n, list->d_t_ref, list->d_min_deadline, list->capacity};
+        if (fin_bytes && !gsb_scratch(ctx, fin_bytes))
+          return gsb_set_error(ctx, GSB_CUDA_ERROR, "select: scratch allocation failed");
+      } else {
+        if (!list_pass_buffers(ctx, n_cells, fin_bytes, &lp))
+          return gsb_set_error(ctx, GSB_CUDA_ERROR, "select: scratch allocation failed");
+        if (launch_compact(lp, NonEmptyCount{d_count}, n_cells, s) != cudaSuccess)
+          return gsb_check_launch(ctx, "prefill_select (compact)");
+        li = ListIn{lp.list, lp.n_list, nullptr, nullptr, n_cells};
+      }
+      static int grid_k2 = 0;
+      if (!grid_k2) grid_k2 = resident_ctas(ctx, k_prefill_select_list<81>, kListCta);
+      gsb::launch_pdl(k_prefill_select_list<81>, dim3(static_cast<unsigned>(grid_k2)),
+                      dim3(kListCta), 0, s, sp, cs, P, li, d_t_ref, d_min_deadline, d_window,
+                      d_f_idx, d_energy);
+      if (launch_finish(ctx, P, Cn, n_cells, d_count, d_f_idx, d_energy, d_summary,
+                        static_cast<Part*>(ctx->d_scratch), s) != cudaSuccess)
+        return gsb_check_launch(ctx, "prefill_select (finish)");
       return gsb_check_launch(ctx, "prefill_select");
     }
+    const dim3 grid(gx, static_cast<unsigned>(ctx->n_profiles));
     k_prefill_select_c<81><<<grid, 256, 0, s>>>(sp, cs, d_t_ref, d_count, d_min_deadline,
                                                 d_window, d_f_idx, d_energy);
     const int rc = gsb_check_launch(ctx, "prefill_select");
@@ -846,16 +1099,16 @@ int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_c
   if (!ctx || n_profiles < 1 || n_profiles > GSB_MAX_PROFILES || n_classes < 1 ||
       n_classes > GSB_MAX_CLASSES || n_cells < 0 || n_cells % n_classes)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: bad shape");
-  const int64_t gx = std::max<int64_t>(1, (n_cells + kSumCta - 1) / kSumCta);
-  if (gx > 65535LL * 16) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: too many cells");
-  SumArgs sa{static_cast<Part*>(gsb_scratch(ctx, sizeof(Part) * static_cast<size_t>(gx) *
-                                                     n_profiles * n_classes))};
-  if (!sa.parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "summary: scratch allocation failed");
+  if (n_cells >= (int64_t{1} << 32))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: too many cells");
+  // the same tree as the K2 path (k_cells_finish, emptiness read from f_idx), identical bytes
+  void* parts = gsb_scratch(ctx, finish_scratch_bytes(n_profiles, n_classes, n_cells));
+  if (!parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "summary: scratch allocation failed");
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  k_summary<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(n_profiles)), kSumCta, 0, s>>>(
-      n_classes, n_cells, d_f_idx, d_energy, sa);
-  k_summary_final<<<static_cast<unsigned>(n_profiles * n_classes), 32, 0, s>>>(
-      sa.parts, static_cast<int>(gx), d_out);
+  if (launch_finish(ctx, n_profiles, n_classes, n_cells, nullptr, const_cast<int16_t*>(d_f_idx),
+                    const_cast<double*>(d_energy), d_out, static_cast<Part*>(parts), s) !=
+      cudaSuccess)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: too many cells");
   return gsb_check_launch(ctx, "prefill_summary");
 }
 

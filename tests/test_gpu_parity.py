@@ -96,6 +96,10 @@ def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms, want_deadline)
         np.testing.assert_array_equal(u64(rr.min_deadline.cpu().numpy()), u64(mdl))
     else:
         assert rr.min_deadline is None
+    # the non-empty cell list K1b emits in the same pass (decoupled look-back across CTAs)
+    n_ne = int(rr.n_nonempty.item())
+    np.testing.assert_array_equal(rr.nonempty.cpu().numpy()[:n_ne].view(np.uint32),
+                                  np.flatnonzero(cnt).astype(np.uint32))
     np.testing.assert_array_equal(rr.fifo.cpu().numpy(), fifo)
     eng.set_profiles([api.GpuProfile.default_profile()])
 
