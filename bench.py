@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 K2_DP_OPS_PER_EVAL = 14  # DP-pipe instructions per (cell, clock) in K2 (SASS, profiles/r2_k2_sass.txt)
-K1_BYTES_PER_REQ = 8 + 4 + 1  # arrival i64 + prompt i32 read, class u8 written
+K1_DP_OPS_PER_REQ_PROFILE = 5  # (a L + b) L + c and the chain add (prefill_opt.cpp:9-14)
 
 
 def parse():
@@ -160,16 +160,15 @@ def run_gsb(args, rank, world, dist):
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
-    def prefill_step(mark=False):
-        if mark:
-            ev[0].record(stream)
+    def prefill_step():
+        # K1 (window bounds, route + bin + T_ref fold + the non-empty cell list), then K2 over
+        # the list, the empty cells' outputs and the per-class summary
         eng.route_bin(d_arr, d_prm, routing, wms, w0, nW, out=rr)
-        if mark:
-            ev[1].record(stream)
-        # K2 + the per-class summary: one launch (objective, argmin, reduction)
         eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel, summary_out=summ)
-        if mark:
-            ev[2].record(stream)
+
+    def fused_step():  # the same pass with K1b and K2 in one persistent kernel (gsb_prefill_pass)
+        eng.prefill_pass(d_arr, d_prm, routing, wms, w0, nW, api.L.FIXED_WINDOW,
+                         fixed_window_ms=D, rr=rr, sel=sel, summary_out=summ)
 
     use_graph = not args.no_graph
     graphs = {}
@@ -221,13 +220,15 @@ def run_gsb(args, rank, world, dist):
         torch.cuda.synchronize()
         return statistics.mean(a.elapsed_time(b) for a, b in ts[2:])
 
-    # per-kernel split: K1 alone and K1 + K2 as CUDA graphs (the step's own launch sequence),
-    # K2 = the difference (device time only; eager events would include host launch gaps)
+    # per-kernel split of the two-call path: K1 alone and K1 + K2 as CUDA graphs, K2 = the
+    # difference (device time only; eager events would include host launch gaps); and the
+    # fused pass alone
     def kernel_split(n=10):
         g1 = graph_of(lambda: eng.route_bin(d_arr, d_prm, routing, wms, w0, nW, out=rr))
         g12 = graph_of(prefill_step)
+        gp = graph_of(fused_step)
         k1 = graph_ms(g1, n)
-        return k1, max(graph_ms(g12, n) - k1, 1e-6)
+        return k1, max(graph_ms(g12, n) - k1, 1e-6), graph_ms(gp, n)
 
     # ---------------- decode leg setup
     T_END = 150_000.0
@@ -381,7 +382,7 @@ def run_gsb(args, rank, world, dist):
         barrier()
         ing_ms = run_ingest(max(3, args.steps // 4), 3)
         barrier()
-    k1_ms, k2_ms = kernel_split()
+    k1_ms, k2_ms, pass_ms = kernel_split()
     k3a_ms, k3b_ms = decode_split()
 
     def max_over_ranks(x):
@@ -436,6 +437,8 @@ def run_gsb(args, rank, world, dist):
     prof_json = committed_profile()
     evaluated = pairs_rank[0] * 81
     k2_tflops = evaluated * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
+    pass_tflops = ((evaluated * K2_DP_OPS_PER_EVAL + n_req * P * K1_DP_OPS_PER_REQ_PROFILE) * 2
+                   / (pass_ms / 1e3) / 1e12)
     peak_tflops = dfma_per_s * 2 / 1e12
     # K1 (K1a window bounds + K1b route/bin) algorithmic bytes, FIXED_WINDOW mode:
     # prompt i32 read + class u8 written per request, one arrival per 32-request tile (the
@@ -487,7 +490,8 @@ def run_gsb(args, rank, world, dist):
         "e2e": {"value": evaluated_all / (ms_e2e / 1e3), "unit": "window x class x clock evals/s",
                 "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "Engine.route_bin/prefill_select from pinned host buffers"},
-        "roofline": {"bound": "fp64", "kernel": "k_prefill_select (K2)",
+        "roofline": {"bound": "fp64", "kernel": "k_prefill_select_list (K2) + k_cells_finish + "
+                                                "k_summary_final",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,
                      "basis": f"{K2_DP_OPS_PER_EVAL} DP instr per evaluated triple x 2 vs DFMA "
@@ -496,6 +500,14 @@ def run_gsb(args, rank, world, dist):
                      "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre,
                      "traffic": prof_json.get("_k2_dram"),
                      "fp64_warp_insts_ncu": prof_json.get("_k2_fp64_insts")},
+        "roofline_pass": {"bound": "fp64", "kernel": "gsb_prefill_pass: K1a, k_prefill_pass "
+                                                     "(K1b + K2 in one persistent kernel), "
+                                                     "finish, summary",
+                          "achieved": pass_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                          "frac": pass_tflops / peak_tflops, "kernel_ms": pass_ms,
+                          "basis": f"{K2_DP_OPS_PER_EVAL} DP instr/evaluated triple + "
+                                   f"{K1_DP_OPS_PER_REQ_PROFILE}/(request, profile) of K1b's "
+                                   "ordered T_ref fold, x 2, vs the measured DFMA rate"},
         "roofline_k1": {"bound": "hbm", "kernel": "k_window_bounds + k_route_bin (K1)",
                         "achieved": k1_gbs, "peak": hbm, "unit": "GB/s", "frac": k1_gbs / hbm,
                         "kernel_ms": k1_ms, "algorithmic_bytes": k1_bytes,

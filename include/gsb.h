@@ -288,6 +288,19 @@ int gsb_prefill_select_list(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_c
                             double* d_window, int16_t* d_f_idx, double* d_energy,
                             gsb_class_summary* d_summary, void* stream);
 
+/* The whole offline prefill pass in one call: gsb_window_bounds + gsb_route_bin_list +
+ * gsb_prefill_select_list (+ the per-class summary when d_summary != NULL), with identical
+ * outputs, where K1b and K2 run as ONE persistent kernel (routing tiles first, then K2 chunks
+ * of the cell list as soon as their entries are written). scfg->mode: FIXED_WINDOW or
+ * DEADLINE_SLACK (the latter needs d_min_deadline and list->d_min_deadline); list->d_t_ref is
+ * required. Profiles whose grid is not 81 short-divisor clocks take the two-call path. */
+int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
+                     const int64_t* d_arrival, const int32_t* d_prompt, int64_t* d_bounds,
+                     uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                     double* d_min_deadline, const gsb_cell_list* list,
+                     const gsb_select_cfg* scfg, double* d_window, int16_t* d_f_idx,
+                     double* d_energy, gsb_class_summary* d_summary, void* stream);
+
 /* ---------------------------------------------------------------- K6: trace CSV ingest */
 /* greensim::TraceError::Kind (trace.hpp:36-40), in the reference's enum order */
 enum {

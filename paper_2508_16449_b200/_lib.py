@@ -139,6 +139,7 @@ EXPORTS = (
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
     "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
+    "gsb_prefill_pass",
 )
 
 _lib = None
@@ -183,6 +184,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                                      P(CCellList), _p]
     L.gsb_prefill_select_list.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, P(CCellList), _p, _p,
                                           _p, _p, _p, _p]
+    L.gsb_prefill_pass.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p,
+                                   P(CCellList), P(CSelectCfg), _p, _p, _p, _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]
     L.gsb_n_ticks.restype = _i64
     L.gsb_window_series.argtypes = [_p, P(CTelemetry), C.c_int, _d, _d, _d, _p, _p, _p, _p]

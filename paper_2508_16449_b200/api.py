@@ -611,6 +611,47 @@ class Engine:
                                                 _ptr(out.cell_off), _ptr(out.fifo), s))
         return out
 
+    def prefill_pass(self, arrival, prompt, routing: RoutingConfig, window_ms: int, w0: int,
+                     n_windows: int, mode: int = L.FIXED_WINDOW, fixed_window_ms: float = 0.0,
+                     qopt: QueueOptimizerConfig = QueueOptimizerConfig(),
+                     slo: SloConfig = SloConfig(), allowance_ms: float = 100.0,
+                     rr: Optional[RouteResult] = None, sel: Optional["SelectResult"] = None,
+                     summary_out: Optional[torch.Tensor] = None):
+        """route_bin + prefill_select (+ the per-class summary) as ONE fused pass
+        (gsb_prefill_pass: K1b and K2 in one persistent kernel). Returns (RouteResult,
+        SelectResult), identical to the two-call path's."""
+        arrival = self._dev(arrival, torch.int64)
+        prompt = self._dev(prompt, torch.int32)
+        n = arrival.numel()
+        Cn = routing.n_classes() if routing.enabled else 1
+        cells = n_windows * Cn
+        P = len(self.profiles)
+        dl = mode == L.DEADLINE_SLACK
+        if rr is None:
+            rr = RouteResult(Cn, n_windows, window_ms, w0, self._empty(n_windows + 1, torch.int64),
+                             self._empty(n, torch.uint8), self._empty(cells, torch.int32),
+                             self._empty((P, cells), torch.float64),
+                             self._empty(cells, torch.float64) if dl else None)
+            rr.nonempty = self._empty(cells, torch.int32)
+            rr.n_nonempty = self._empty(1, torch.int64)
+            rr.t_ref_list = self._empty((P, cells), torch.float64)
+            if dl:
+                rr.min_deadline_list = self._empty(cells, torch.float64)
+        if sel is None:
+            sel = SelectResult(self._empty((P, cells), torch.int16),
+                               self._empty((P, cells), torch.float64),
+                               self._empty(cells, torch.float64))
+        rcfg = _route_cfg(routing, window_ms, w0, n_windows, slo, allowance_ms)
+        scfg = L.CSelectCfg(mode, Cn, fixed_window_ms, w0, window_ms, qopt.to_c())
+        cl = rr.cell_list()
+        self._check(self.lib.gsb_prefill_pass(
+            self.ctx, C.byref(rcfg), n, _ptr(arrival), _ptr(prompt), _ptr(rr.bounds), _ptr(rr.cls),
+            _ptr(rr.count), _ptr(rr.t_ref), _ptr(rr.min_deadline), C.byref(cl), C.byref(scfg),
+            _ptr(sel.window_ms), _ptr(sel.f_idx), _ptr(sel.energy_j), _ptr(summary_out),
+            self.stream()))
+        rr.profile_gen = self.profile_gen
+        return rr, sel
+
     # ---------------------------------------------------------------- K6: trace CSV
     def parse_trace(self, data, class_threshold: int = 1024, name: str = "trace") -> "TraceArrays":
         """greensim::load_trace (trace.cpp:56-129) of a CSV image (bytes, a uint8 numpy array

@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "gsb_common.cuh"
+#include "gsb_scan.cuh"
 
 using gsb::ProfTab;
 using gsb::std_max;
@@ -61,9 +62,14 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __global__ void __launch_bounds__(256)
 k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms, int64_t w0,
-                int64_t n_windows, int64_t* __restrict__ bounds) {
+                int64_t n_windows, int64_t* __restrict__ bounds, unsigned* __restrict__ zero_words,
+                int64_t n_zero) {
   gsb::grid_dep_wait();    // the arrivals may come from the previous launch (e.g. a copy)
   gsb::grid_dep_launch();  // K1b may be scheduled now; it waits for this grid's bounds
+  // the fused pass's counters (tickets, per-chunk readiness) start every pass at zero
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_zero;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    zero_words[i] = 0;
   const double rd = 1.0 / static_cast<double>(window_ms);
   const int lane = threadIdx.x & 31;
   const int64_t span = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) *
@@ -185,6 +191,8 @@ struct RouteSmem {  // one CTA
 // Optional output of K1b: the ascending list of non-empty cells (count > 0) for K2, built in
 // the same pass by the decoupled look-back (gsb::lookback_prefix) over the CTAs in launch
 // order (CTA b owns cells [b*G*C, (b+1)*G*C), so CTA order is cell order).
+constexpr long long kChunk = 128;  // list positions per K2 chunk (the fused pass's readiness unit)
+
 struct ListOut {
   uint32_t* list;            // [cells] (NULL: no list)
   int64_t* n_list;
@@ -192,42 +200,39 @@ struct ListOut {
   double* min_deadline;      // optional [cap]
   int64_t cap;
   gsb::CompactHdr* hdr;
-  unsigned long long* status;  // [gridDim.x]
+  unsigned long long* status;  // [tiles]
+  unsigned* ready;           // fused pass only: entries written per chunk of kChunk positions
+  unsigned* nl_known;        // fused pass only: set once *n_list is final
 };
 
+// One K1b tile (windows [tile*G, tile*G + G)), run by all threads of a CTA whose s.bar was
+// initialised (parity: the barrier's phase, carried across the tiles of a persistent CTA).
 template <int C, int P, bool DL, int GW>
-__global__ void __launch_bounds__(kRouteWarps * 32, GW * C > 64 ? 6 : kRouteMinBlocks)
-k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
-            const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
-            uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
-            double* __restrict__ t_ref, double* __restrict__ min_deadline, ListOut lo) {
+__device__ __forceinline__ void route_bin_tile(
+    const RouteParams& rp, const int64_t* __restrict__ arrival, const int32_t* __restrict__ prompt,
+    const int64_t* __restrict__ bounds, uint8_t* __restrict__ cls_out,
+    uint32_t* __restrict__ count, double* __restrict__ t_ref, double* __restrict__ min_deadline,
+    const ListOut& lo, RouteSmem<GW * C, DL>& s, unsigned tile, unsigned n_tiles,
+    uint32_t& parity) {
   constexpr int G = GW, K = G * C, E = (K + 31) / 32, NW = kRouteWarps;
   constexpr int kNever = 0x3fffffff;
   using S = RouteSmem<K, DL>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  S& s = *reinterpret_cast<S*>(smem_raw);
   const int tid = threadIdx.x, wib = tid >> 5, lane = tid & 31;
   const unsigned lt = lanemask_lt();
   int32_t th[GSB_MAX_CLASSES - 1];
 #pragma unroll
   for (int k = 0; k < GSB_MAX_CLASSES - 1; ++k) th[k] = rp.thr[k];
-  const int64_t w_first = static_cast<int64_t>(blockIdx.x) * G;
-  gsb::grid_dep_wait();  // K1a's bounds (programmatic dependent launch)
-  gsb::grid_dep_launch();
+  const int64_t w_first = static_cast<int64_t>(tile) * G;
   for (int k = tid; k <= G; k += NW * 32) s.bnd[k] = bounds[min(w_first + k, rp.n_windows)];
   for (int k = tid; k < K; k += NW * 32) {
     s.cnt[k] = 0;
     if (DL) s.mdl[k] = ~0ull;
   }
   unsigned epoch = 0;  // read now, used in the epilogue (the load's latency hides behind the pass)
-  if (tid == 0) {
-    gsb::mbar_init(&s.bar, 1);
-    if (lo.list) epoch = __ldcg(&lo.hdr->epoch);
-  }
+  if (tid == 0 && lo.list) epoch = __ldcg(&lo.hdr->epoch);
   __syncthreads();
   const int64_t b0 = s.bnd[0], bG = s.bnd[G];
   const bool tma = (reinterpret_cast<uintptr_t>(prompt) & 15) == 0;
-  uint32_t parity = 0;
   // fold role: lane (fg, fp) = (window, profile)
   const int fg = lane / P, fp = lane - (lane / P) * P;
   const bool folder = lane < G * P;
@@ -419,7 +424,7 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
       agg += s.lwarp[k];
     }
     if (wib == 0) {
-      const long long excl = gsb::lookback_prefix(lo.status, blockIdx.x, s.lepoch, agg);
+      const long long excl = gsb::lookback_prefix(lo.status, tile, s.lepoch, agg);
       if (lane == 0) s.lexcl = excl;
     }
     __syncthreads();
@@ -439,10 +444,6 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
         ++rel;
       }
     }
-    if (tid == 0 && blockIdx.x == gridDim.x - 1) {
-      *lo.n_list = s.lexcl + agg;
-      gsb::lookback_finish(lo.hdr, s.lepoch);
-    }
     if (lo.t_ref) {  // the fold lanes' T_ref, in list order
       __syncthreads();
       if (folder && w_first + fg < rp.n_windows) {
@@ -455,7 +456,194 @@ k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ 
         }
       }
     }
+    if (lo.ready) __threadfence();  // this thread's list entries before the chunk counters
+    __syncthreads();
+    if (tid == 0) {
+      if (lo.ready && agg > 0) {  // the fused pass: count this tile's entries into their chunks
+        const long long e0 = s.lexcl, e1 = s.lexcl + agg;
+        for (long long ch = e0 / kChunk; ch * kChunk < e1; ++ch) {
+          const long long lo_ = max(e0, ch * kChunk), hi_ = min(e1, (ch + 1) * kChunk);
+          atomicAdd(lo.ready + ch, static_cast<unsigned>(hi_ - lo_));
+        }
+      }
+      if (tile == n_tiles - 1) {
+        *lo.n_list = s.lexcl + agg;
+        if (lo.ready) {
+          __threadfence();
+          atomicExch(lo.nl_known, 1u);
+        }
+        gsb::lookback_finish(lo.hdr, s.lepoch);
+      }
+    }
   }
+  __syncthreads();  // the next tile of a persistent CTA reuses the shared memory
+}
+
+template <int C, int P, bool DL, int GW>
+__global__ void __launch_bounds__(kRouteWarps * 32, GW * C > 64 ? 6 : kRouteMinBlocks)
+k_route_bin(const __grid_constant__ RouteParams rp, const int64_t* __restrict__ arrival,
+            const int32_t* __restrict__ prompt, const int64_t* __restrict__ bounds,
+            uint8_t* __restrict__ cls_out, uint32_t* __restrict__ count,
+            double* __restrict__ t_ref, double* __restrict__ min_deadline, ListOut lo) {
+  using S = RouteSmem<GW * C, DL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& s = *reinterpret_cast<S*>(smem_raw);
+  gsb::grid_dep_wait();  // K1a's bounds (programmatic dependent launch)
+  gsb::grid_dep_launch();
+  if (threadIdx.x == 0) gsb::mbar_init(&s.bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
+  route_bin_tile<C, P, DL, GW>(rp, arrival, prompt, bounds, cls_out, count, t_ref, min_deadline,
+                               lo, s, blockIdx.x, gridDim.x, parity);
+}
+
+// ---------------------------------------------------------------- the fused prefill pass
+// K1b and K2 in ONE persistent kernel (gsb_prefill_pass): every CTA first takes K1b tiles by
+// ticket (route, bin, ordered T_ref fold, list entries by look-back) and, once no tile is left,
+// K2 chunks (128 listed cells x one profile) in list order, each as soon as the tiles that
+// write its entries have counted them in (per-chunk readiness counters). The FP64-bound scan of
+// the early chunks so runs beside the issue-bound routing of the late tiles on the same SMs, and
+// neither kernel boundary nor one-wave ramp/tail separates the two halves. Forward progress:
+// every tile is taken by a running CTA before any CTA waits on a chunk, and a tile waits only on
+// lower tiles (look-back).
+struct PassHdr {
+  unsigned tile_ticket, chunk_ticket, pad0, pad1;
+};
+
+struct PassK2 {
+  gsb_k2::SelectParams sp;
+  double* window;
+  int16_t* f_idx;
+  double* energy;
+  PassHdr* ph;
+};
+
+template <int C, int P, bool DL, int GW>
+__global__ void __launch_bounds__(kRouteWarps * 32, GW * C > 64 ? 6 : kRouteMinBlocks)
+k_prefill_pass(const __grid_constant__ RouteParams rp, const __grid_constant__ gsb_k2::ClockSet<81> cs,
+               const int64_t* __restrict__ arrival, const int32_t* __restrict__ prompt,
+               const int64_t* __restrict__ bounds, uint8_t* __restrict__ cls_out,
+               uint32_t* __restrict__ count, double* __restrict__ t_ref,
+               double* __restrict__ min_deadline, ListOut lo, PassK2 pk) {
+  using S = RouteSmem<GW * C, DL>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  S& s = *reinterpret_cast<S*>(smem_raw);
+  __shared__ unsigned s_work;
+  __shared__ int s_avail;
+  const int tid = threadIdx.x;
+  gsb::grid_dep_wait();  // K1a's bounds and zeroed counters
+  gsb::grid_dep_launch();
+  if (tid == 0) gsb::mbar_init(&s.bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
+  const unsigned n_tiles = static_cast<unsigned>((rp.n_windows + GW - 1) / GW);
+  for (;;) {  // ---- K1b tiles
+    if (tid == 0) s_work = atomicAdd(&pk.ph->tile_ticket, 1u);
+    __syncthreads();
+    const unsigned t = s_work;
+    __syncthreads();
+    if (t >= n_tiles) break;
+    route_bin_tile<C, P, DL, GW>(rp, arrival, prompt, bounds, cls_out, count, t_ref,
+                                 min_deadline, lo, s, t, n_tiles, parity);
+  }
+  const gsb_k2::SelectParams& sp = pk.sp;
+  const int64_t n = sp.n_cells;
+  for (;;) {  // ---- K2 chunks, list order (chunk-major, profile-minor)
+    if (tid == 0) {
+      const unsigned c = atomicAdd(&pk.ph->chunk_ticket, 1u);
+      const long long ch = c / P;
+      int avail = -1;
+      if (ch * kChunk < n) {
+        const volatile unsigned* rd = lo.ready + ch;
+        for (;;) {
+          const unsigned r = *rd;
+          if (r == kChunk) {
+            avail = static_cast<int>(kChunk);
+            break;
+          }
+          if (*reinterpret_cast<volatile unsigned*>(lo.nl_known)) {
+            const long long nl = *reinterpret_cast<volatile long long*>(lo.n_list);
+            if (ch * kChunk >= nl) break;  // past the end of the list
+            if (r == static_cast<unsigned>(nl - ch * kChunk)) {
+              avail = static_cast<int>(r);
+              break;
+            }
+          }
+          __nanosleep(64);
+        }
+        __threadfence();  // acquire: the entries the counter covers
+      }
+      s_work = c;
+      s_avail = avail;
+    }
+    __syncthreads();
+    const unsigned c = s_work;
+    const int avail = s_avail;
+    __syncthreads();
+    if (avail < 0) break;
+    if (tid >= avail) continue;
+    const int p = static_cast<int>(c % P);
+    const long long k = static_cast<long long>(c / P) * kChunk + tid;
+    const int64_t cell = __ldcg(lo.list + k);
+    const double T = __ldcg(lo.t_ref + p * lo.cap + k);
+    double W;
+    if (sp.mode == GSB_FIXED_WINDOW) {
+      W = sp.fixed_window;
+    } else {  // GSB_DEADLINE_SLACK (the pass takes FIXED or DEADLINE_SLACK)
+      const double mdl = __ldcg(lo.min_deadline + k);
+      const double now = static_cast<double>((sp.w0 + cell / sp.C) * sp.window_ms);
+      W = gsb::std_max(sp.margin * (mdl - now), sp.min_budget);
+    }
+    if (p == 0 && pk.window) pk.window[cell] = W;
+    double be;
+    int best;
+    switch (p) {
+      case 0: best = gsb_k2::scan_clocks_c<81, 0>(cs, T, W, &be); break;
+      case 1: best = gsb_k2::scan_clocks_c<81, 1>(cs, T, W, &be); break;
+      case 2: best = gsb_k2::scan_clocks_c<81, 2>(cs, T, W, &be); break;
+      default: best = gsb_k2::scan_clocks_c<81, 3>(cs, T, W, &be); break;
+    }
+    const int64_t o = p * n + cell;
+    pk.f_idx[o] = static_cast<int16_t>(best);
+    pk.energy[o] = best >= 0 ? be : 0.0;
+  }
+}
+
+template <int C, int P, bool DL, int G>
+int launch_pass_g(gsb_ctx* ctx, const RouteParams& rp, const gsb_k2::ClockSet<81>& cs,
+                  const int64_t* d_arrival, const int32_t* d_prompt, const int64_t* d_bounds,
+                  uint8_t* d_class, uint32_t* d_count, double* d_t_ref, double* d_min_deadline,
+                  const ListOut& lo, const PassK2& pk, cudaStream_t s) {
+  const size_t smem = sizeof(RouteSmem<G * C, DL>);
+  auto kern = k_prefill_pass<C, P, DL, G>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return -1;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRouteWarps * 32, smem) !=
+          cudaSuccess || per_sm < 1)
+    return -1;
+  // persistent: every CTA resident (the chunk waits rely on it)
+  const unsigned blocks = static_cast<unsigned>(per_sm * ctx->n_sms);
+  if (gsb::launch_pdl(kern, dim3(blocks), dim3(kRouteWarps * 32), smem, s, rp, cs, d_arrival,
+                      d_prompt, d_bounds, d_class, d_count, d_t_ref, d_min_deadline, lo,
+                      pk) != cudaSuccess)
+    return -1;
+  return 0;
+}
+
+template <int C, int P, bool DL>
+int launch_pass(gsb_ctx* ctx, const RouteParams& rp, int64_t n_req,
+                const gsb_k2::ClockSet<81>& cs, const int64_t* d_arrival, const int32_t* d_prompt,
+                const int64_t* d_bounds, uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                double* d_min_deadline, const ListOut& lo, const PassK2& pk, cudaStream_t s) {
+  if constexpr (P == 1) {
+    if (n_req > rp.n_windows * (kRouteCap / 32))
+      return launch_pass_g<C, P, DL, 8>(ctx, rp, cs, d_arrival, d_prompt, d_bounds, d_class,
+                                        d_count, d_t_ref, d_min_deadline, lo, pk, s);
+  }
+  return launch_pass_g<C, P, DL, 32 / P>(ctx, rp, cs, d_arrival, d_prompt, d_bounds, d_class,
+                                         d_count, d_t_ref, d_min_deadline, lo, pk, s);
 }
 
 template <int C, int P, bool DL, int G>
@@ -606,7 +794,7 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   const int64_t blocks = (warps + 7) / 8;
   k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
                     gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms, cfg->w0,
-                                                    cfg->n_windows, d_bounds);
+                                                    cfg->n_windows, d_bounds, nullptr, 0);
   return gsb_check_launch(ctx, "window_bounds");
 }
 
@@ -639,7 +827,7 @@ int gsb_route_bin_list(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
     lo = ListOut{list->d_cells, list->d_n, list->d_t_ref,
                  d_min_deadline ? list->d_min_deadline : nullptr, list->capacity,
                  reinterpret_cast<gsb::CompactHdr*>(sy),
-                 reinterpret_cast<unsigned long long*>(sy + 256)};
+                 reinterpret_cast<unsigned long long*>(sy + 256), nullptr, nullptr};
   }
   RouteParams rp = make_route_params(ctx, cfg);
   rp.want_deadline = d_min_deadline != nullptr;
@@ -667,6 +855,101 @@ int gsb_route_bin_list(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   }
   if (lrc) return gsb_set_error(ctx, GSB_CUDA_ERROR, "route: shared-memory attribute refused");
   return gsb_check_launch(ctx, "route_bin");
+}
+
+int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
+                     const int64_t* d_arrival, const int32_t* d_prompt, int64_t* d_bounds,
+                     uint8_t* d_class, uint32_t* d_count, double* d_t_ref,
+                     double* d_min_deadline, const gsb_cell_list* list,
+                     const gsb_select_cfg* scfg, double* d_window, int16_t* d_f_idx,
+                     double* d_energy, gsb_class_summary* d_summary, void* stream) {
+  if (!ctx || !scfg || !list) return GSB_INVALID_ARGUMENT;
+  int rc = check_route_cfg(ctx, rcfg);
+  if (rc) return rc;
+  if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass: no profiles set");
+  const int C = rcfg->enabled ? rcfg->n_thresholds + 1 : 1;
+  const int64_t cells = rcfg->n_windows * C;
+  const bool dl = scfg->mode == GSB_DEADLINE_SLACK;
+  if (scfg->mode != GSB_FIXED_WINDOW && !dl)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass: FIXED_WINDOW or DEADLINE_SLACK only");
+  if (!list->d_cells || !list->d_n || !list->d_t_ref || list->capacity < cells ||
+      cells >= (int64_t{1} << 32) || (dl && (!d_min_deadline || !list->d_min_deadline)))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT,
+                         "pass: needs a full cell list (cells, n, t_ref, min_deadline when "
+                         "DEADLINE_SLACK) and < 2^32 cells");
+  if (d_summary && scfg->n_classes != C)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass: summary needs n_classes = C");
+  gsb_k2::ClockSet<81> cs{};
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  if (!gsb_k2::make_clockset81(ctx, &cs)) {  // generic grids: the two-call path
+    rc = gsb_window_bounds(ctx, rcfg, n_req, d_arrival, d_bounds, stream);
+    if (!rc)
+      rc = gsb_route_bin_list(ctx, rcfg, n_req, d_arrival, d_prompt, d_bounds, d_class, d_count,
+                              d_t_ref, dl ? d_min_deadline : nullptr, list, stream);
+    if (!rc)
+      rc = gsb_prefill_select_list(ctx, scfg, cells, d_t_ref, d_count, list,
+                                   dl ? d_min_deadline : nullptr, d_window, d_f_idx, d_energy,
+                                   d_summary, stream);
+    return rc;
+  }
+  // sync words: [0,256) look-back header, [256,512) pass header, the per-chunk readiness
+  // counters, then the look-back statuses (one per K1b tile, tiles own >= 8 windows)
+  const int64_t max_chunks = (cells + kChunk - 1) / kChunk;
+  const size_t o_rd = 512, o_st = (o_rd + sizeof(unsigned) * max_chunks + 255) & ~size_t{255};
+  char* sy = static_cast<char*>(gsb_sync_words(
+      ctx, o_st + sizeof(unsigned long long) * static_cast<size_t>(rcfg->n_windows / 8 + 2)));
+  if (!sy) return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass: sync allocation failed");
+  PassHdr* ph = reinterpret_cast<PassHdr*>(sy + 256);
+  unsigned* ready = reinterpret_cast<unsigned*>(sy + o_rd);
+  // K1a (window bounds), which also zeroes the pass header and the readiness counters
+  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
+  const int64_t blocks = (warps + 7) / 8;
+  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, s>>>(
+      d_arrival, n_req, rcfg->window_ms, rcfg->w0, rcfg->n_windows, d_bounds,
+      reinterpret_cast<unsigned*>(ph), static_cast<int64_t>((o_st - 256) / sizeof(unsigned)));
+  RouteParams rp = make_route_params(ctx, rcfg);
+  rp.want_deadline = dl ? 1 : 0;
+  const ListOut lo{list->d_cells, list->d_n, list->d_t_ref, dl ? list->d_min_deadline : nullptr,
+                   list->capacity, reinterpret_cast<gsb::CompactHdr*>(sy),
+                   reinterpret_cast<unsigned long long*>(sy + o_st), ready, &ph->pad0};
+  PassK2 pk{};
+  pk.sp.mode = scfg->mode;
+  pk.sp.C = C;
+  pk.sp.fixed_window = scfg->fixed_window_ms;
+  pk.sp.w0 = rcfg->w0;
+  pk.sp.window_ms = rcfg->window_ms;
+  pk.sp.margin = scfg->qopt.margin_prefill;
+  pk.sp.min_budget = scfg->qopt.min_budget_ms;
+  pk.sp.n_cells = cells;
+  pk.window = d_window;
+  pk.f_idx = d_f_idx;
+  pk.energy = d_energy;
+  pk.ph = ph;
+  const int P = ctx->n_profiles;
+  const int key = (C - 1) * 8 + (P - 1) * 2 + (dl ? 1 : 0);
+  int lrc = 0;
+  double* mdl = dl ? d_min_deadline : nullptr;
+  switch (key) {
+#define GSB_PS(CC, PP)                                                                           \
+  case ((CC)-1) * 8 + ((PP)-1) * 2:                                                             \
+    lrc = launch_pass<CC, PP, false>(ctx, rp, n_req, cs, d_arrival, d_prompt, d_bounds, d_class, \
+                                     d_count, d_t_ref, mdl, lo, pk, s);                         \
+    break;                                                                                       \
+  case ((CC)-1) * 8 + ((PP)-1) * 2 + 1:                                                         \
+    lrc = launch_pass<CC, PP, true>(ctx, rp, n_req, cs, d_arrival, d_prompt, d_bounds, d_class,  \
+                                    d_count, d_t_ref, mdl, lo, pk, s);                          \
+    break;
+#define GSB_PS_P(CC) GSB_PS(CC, 1) GSB_PS(CC, 2) GSB_PS(CC, 3) GSB_PS(CC, 4)
+    GSB_PS_P(1) GSB_PS_P(2) GSB_PS_P(3) GSB_PS_P(4) GSB_PS_P(5) GSB_PS_P(6) GSB_PS_P(7) GSB_PS_P(8)
+#undef GSB_PS_P
+#undef GSB_PS
+    default:
+      return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass: need 1..8 classes, 1..4 profiles");
+  }
+  if (lrc) return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass: launch configuration refused");
+  rc = gsb_check_launch(ctx, "prefill_pass");
+  if (rc) return rc;
+  return gsb_internal_finish(ctx, P, C, cells, d_count, d_f_idx, d_energy, d_summary, s);
 }
 
 int gsb_fifo_order(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const uint8_t* d_class,

@@ -8,12 +8,19 @@
 #include <cmath>
 
 #include "gsb_common.cuh"
+#include "gsb_scan.cuh"
 
 using gsb::ProfTab;
 using gsb::std_max;
 using gsb::std_min;
 
 namespace {
+
+using gsb_k2::SelectParams;
+using gsb_k2::ClockConst;
+using gsb_k2::ClockSet;
+using gsb_k2::cell_fast;
+using gsb_k2::scan_clocks_c;
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -73,14 +80,6 @@ __device__ __forceinline__ void part_combine(Part& x, const Part& y) {
 }
 
 // ---------------------------------------------------------------- K2: objective + argmin
-struct SelectParams {
-  int32_t mode, C;
-  double fixed_window;
-  int64_t w0, window_ms;
-  double margin, min_budget;
-  int64_t n_cells;
-};
-
 // energy_total at every grid clock (prefill_opt.cpp:16-31) and the ascending strict-'<'
 // argmin over feasible clocks (prefill_opt.cpp:45-56). One lane per (cell, profile); the
 // clock loop runs over the profile's tables staged in shared memory (uniform broadcast
@@ -176,103 +175,6 @@ __device__ __forceinline__ double cell_window(const SelectParams& sp, int64_t ce
     return std_max(sp.margin * (min_deadline[cell] - now), sp.min_budget);
   }
   return window[cell];
-}
-
-// Specialisation for a G-clock grid whose every clock is a short divisor: the clock tables are
-// KERNEL PARAMETERS (constant-bank operands of the DFMA/DMUL themselves, no shared-memory loads)
-// and the clock loop is fully unrolled: 15 DP-pipe instructions per (cell, clock), nothing else
-// but two selects. The three division range guards of div_pre are hoisted to ONE per-cell test:
-// with 1 <= f_i <= 4096 and TF = T*f_ref,
-//   busy_i   = TF / f_i                 dividend TF
-//   active_i = (P_i*busy_i) / 1000      dividend in [TF*P_min/4096*(1-u), TF*P_max]
-//   idle_i   = (p_idle*(W-busy_i))/1000 dividend 0, or |.| in
-//              [p_idle*min(W, TF/4096)*2^-53*(1-u), p_idle*max(W, TF)]
-// (W - busy is a multiple of 2^(e-52), e the smaller exponent, hence >= min * 2^-53 unless 0;
-// a zero dividend is exact on the fast path too). All of these inside [2^-900, 2^1000] keeps
-// every dividend in div_pre's fast range [2^-959, 2^1023]; otherwise the cell takes IEEE '/'.
-template <int G>
-struct ClockConst {
-  double f[G], r[G], P[G];
-};
-
-__device__ __forceinline__ bool cell_fast(double TF, double W, double p_idle, double P_min,
-                                          double P_max) {
-  const double lo = 0x1p-900, hi = 0x1p+1000;
-  const double x_lo = TF * P_min * 0x1p-12, x_hi = TF * P_max;
-  const double y_lo = p_idle * fmin(W, TF * 0x1p-12) * 0x1p-53, y_hi = p_idle * fmax(W, TF);
-  return TF >= lo && TF <= hi && W >= lo && W <= hi && x_lo >= lo && x_hi <= hi && y_lo >= lo &&
-         y_hi <= hi && P_min > 0.0 && p_idle > 0.0;
-}
-
-template <int G>
-struct ClockSet {  // every profile of the pass, one kernel-parameter block (<= 32 KB)
-  ClockConst<G> c[GSB_MAX_PROFILES];
-  double f_ref[GSB_MAX_PROFILES], p_idle[GSB_MAX_PROFILES];
-  double P_min[GSB_MAX_PROFILES], P_max[GSB_MAX_PROFILES];
-};
-
-// cells first, first + stride, ... of profile PI; SUM: one cell (stride = n) and its summary
-// contribution in *part
-// The exhaustive scan of one (cell, profile PI): returns the grid index of the choice (-1:
-// nothing feasible) and its energy in *be_out.
-template <int G, int PI>
-__device__ __forceinline__ int scan_clocks_c(const ClockSet<G>& cs, double T, double W,
-                                             double* be_out) {
-  const ClockConst<G>& cc = cs.c[PI];
-  const double f_ref = cs.f_ref[PI], p_idle = cs.p_idle[PI], P_min = cs.P_min[PI],
-               P_max = cs.P_max[PI];
-  const double TF = T * f_ref;
-  int best = -1;
-  double be = 0.0;
-  if (cell_fast(TF, W, p_idle, P_min, P_max)) {
-    // every energy is finite here (the range guard), so "nothing taken yet or E < best" is
-    // exactly "E < be" with be starting at +inf
-    be = INFINITY;
-    // (Starting each lane's scan at its first feasible clock — busy_i is monotone — was
-    // measured 6x slower: per-lane trip counts break the unrolled loop into divergent code.
-    // A fully unrolled scan with constant-bank operands runs at the same rate in isolation,
-    // tools/micro/k2_loop.cu, but is 26 KB of SASS per profile.)
-#pragma unroll 9
-    for (int i = 0; i < G; ++i) {
-      const double f = cc.f[i], r = cc.r[i];
-      double q = __dmul_rn(TF, r);
-      double e = __fma_rn(-f, q, TF);
-      const double busy = __fma_rn(r, e, q);
-      const double x = __dmul_rn(cc.P[i], busy);
-      q = __dmul_rn(x, gsb::kRcp1000);
-      e = __fma_rn(-1000.0, q, x);
-      const double active = __fma_rn(gsb::kRcp1000, e, q);
-      const double wb = __dsub_rn(W, busy);
-      const double y = __dmul_rn(p_idle, wb);
-      q = __dmul_rn(y, gsb::kRcp1000);
-      e = __fma_rn(-1000.0, q, y);
-      const double idle = __fma_rn(gsb::kRcp1000, e, q);
-      const double E = __dadd_rn(active, idle);
-      // The two compares without DSETP (a quarter-rate FP64-pipe instruction on B200,
-      // tools/micro/fp64_mix.cu): busy <= W  <=>  RN(W - busy) >= +0 (equal operands give +0),
-      // a value the idle term needs anyway; E < be  <=>  RN(E - be) < 0 (finite operands: a
-      // nonzero difference never rounds to zero; E - inf = -inf). Both are sign tests of a high
-      // word on the integer pipe. Fast cells have P_i > 0 and p_idle > 0, so a feasible E is > 0
-      // and no signed-zero case arises.
-      const double d = __dsub_rn(E, be);
-      const bool take = (__double2hiint(wb) >= 0) & (__double2hiint(d) < 0);
-      best = take ? i : best;
-      be = take ? E : be;
-    }
-  } else {
-#pragma unroll 1
-    for (int i = 0; i < G; ++i) {
-      const double busy = __ddiv_rn(TF, cc.f[i]);
-      const double active = __ddiv_rn(__dmul_rn(cc.P[i], busy), 1000.0);
-      const double idle = __ddiv_rn(__dmul_rn(p_idle, __dsub_rn(W, busy)), 1000.0);
-      const double E = __dadd_rn(active, idle);
-      const bool take = (busy <= W) && (best < 0 || E < be);
-      best = take ? i : best;
-      be = take ? E : be;
-    }
-  }
-  *be_out = be;
-  return best;
 }
 
 // cells first, first + stride, ... of profile PI
@@ -918,6 +820,17 @@ int resident_ctas(gsb_ctx* ctx, K kernel, int threads) {
 
 }  // namespace
 
+// for the fused pass (gsb_prefill.cu): the empty cells' outputs and the summary
+int gsb_internal_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uint32_t* count,
+                        int16_t* f_idx, double* energy, gsb_class_summary* out, cudaStream_t s) {
+  void* parts = out ? gsb_scratch(ctx, finish_scratch_bytes(P, C, n_cells)) : nullptr;
+  if (out && !parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass: scratch allocation failed");
+  if (launch_finish(ctx, P, C, n_cells, count, f_idx, energy, out, static_cast<Part*>(parts), s) !=
+      cudaSuccess)
+    return gsb_check_launch(ctx, "prefill_pass (finish)");
+  return GSB_OK;
+}
+
 extern "C" {
 
 int gsb_energy_closed_form_batches(gsb_ctx* ctx, int profile, int64_t n_batches,
@@ -977,25 +890,9 @@ int gsb_prefill_select_list(gsb_ctx* ctx, const gsb_select_cfg* cfg, int64_t n_c
   const int64_t want = (n_cells + 255) / 256;
   const unsigned gx = static_cast<unsigned>(std::min<int64_t>(want, 65535LL * 16));
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  bool all_c = true;
-  for (int p = 0; p < ctx->n_profiles; ++p) {
-    const ProfTab& t = ctx->h_tabs[p];
-    all_c = all_c && t.G == 81 && t.all_fast && t.f_min >= 1.0 && t.f_max <= 4096.0;
-  }
+  ClockSet<81> cs{};  // filled per call (host), passed by value as the kernel parameter
+  const bool all_c = gsb_k2::make_clockset81(ctx, &cs);
   if (all_c) {
-    ClockSet<81> cs{};  // filled per call (host), passed by value as the kernel parameter
-    for (int p = 0; p < ctx->n_profiles; ++p) {
-      const ProfTab& t = ctx->h_tabs[p];
-      for (int i = 0; i < 81; ++i) {
-        cs.c[p].f[i] = t.f[i];
-        cs.c[p].r[i] = t.rcp_f[i];
-        cs.c[p].P[i] = t.P[i];
-      }
-      cs.f_ref[p] = t.f_ref;
-      cs.p_idle[p] = t.p_idle;
-      cs.P_min[p] = t.P_min;
-      cs.P_max[p] = t.P_max;
-    }
     if (d_count && n_cells < (int64_t{1} << 32)) {
       // non-empty list (K1b's, or k_compact's) + one wave of K2 over it, then the empty cells'
       // outputs and the summary in one memory-bound pass

@@ -68,6 +68,15 @@ def main():
     out["K2 compact + list + summary"] = timed(lambda: eng.prefill_select(rr_nolist, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel, summary_out=summ), flush=flush)
     out["K2 compact + list, no summary"] = timed(lambda: eng.prefill_select(rr_nolist, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel), flush=flush)
     out["summary standalone"] = timed(lambda: eng.prefill_summary_dev(sel, C), flush=flush)
+    prr, psel = eng.prefill_pass(da, dp, routing, wms, 0, nW, api.L.FIXED_WINDOW,
+                                 fixed_window_ms=D, summary_out=summ)
+    out["fused pass (K1a + K1b/K2 + finish + summary)"] = timed(
+        lambda: eng.prefill_pass(da, dp, routing, wms, 0, nW, api.L.FIXED_WINDOW, fixed_window_ms=D,
+                                 rr=prr, sel=psel, summary_out=summ), flush=flush)
+    out["two-call path (K1 + K2 + finish + summary)"] = timed(
+        lambda: (eng.route_bin(da, dp, routing, wms, 0, nW, out=rr),
+                 eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel,
+                                    summary_out=summ)), flush=flush)
     if NCU:
         return
     for k, v in out.items():
