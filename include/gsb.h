@@ -231,6 +231,28 @@ int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int
                        const double* d_deadline, const double* d_now, double* d_window,
                        int16_t* d_f_idx, double* d_energy, double* d_t_ref_out, void* stream);
 
+/* The raw state of the running prefill job in a snapshot (the fields simkernel.cpp:476-479
+ * reads): job j with d_running[j] != 0 gets
+ *   work_fraction = max(remaining_ref - ((now - updated) * freq) / f_ref, 0) / t_ref
+ * in the reference's operation order (now = the batch's d_now, f_ref = the profile's grid
+ * f_ref); every other job 1.0 (or d_wf[j]). */
+typedef struct gsb_running_jobs {
+  const uint8_t* d_running;          /* [jobs] */
+  const double* d_remaining_ref_ms;  /* PrefillWorker::job_remaining_ref */
+  const double* d_updated_ms;        /* PrefillWorker::job_updated_ms */
+  const double* d_freq_mhz;          /* PrefillWorker::freq (the applied clock) */
+  const double* d_t_ref_ms;          /* PrefillWorker::job_t_ref_ms */
+} gsb_running_jobs;
+
+/* gsb_select_batches with the running jobs' work_fraction computed on the device from their raw
+ * state (queue_optimizer_tick snapshots exactly as Sim::on_optimizer_tick builds them). */
+int gsb_select_batches_running(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile,
+                               int64_t n_batches, const int64_t* d_off, const int32_t* d_prompt,
+                               const double* d_wf, const gsb_running_jobs* run,
+                               const double* d_deadline, const double* d_now, double* d_window,
+                               int16_t* d_f_idx, double* d_energy, double* d_t_ref_out,
+                               void* stream);
+
 /* busy_time_ms + energy_total at one given clock per batch (prefill_opt.cpp:16-31): full
  * breakdown. d_feasible[b] = 2 marks the reference's ModelError (empty batch or off-grid
  * clock, prefill_opt.cpp:17-18). */

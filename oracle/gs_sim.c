@@ -172,6 +172,16 @@ typedef struct {
   int64_t rejected_total, n_steps;
   VEC(fc_t) timeline;
   VEC(pc_t) commands;
+  /* optimizer snapshots with the RAW running-job state (simkernel.cpp:470-480), for the
+     device-side work_fraction test: per non-empty queue snapshot now, class, job range; per
+     job prompt, deadline, running flag, remaining_ref, updated_ms, freq, t_ref, and the wf
+     the simulator computed from them */
+  VEC(double) sn_now;
+  VEC(int32_t) sn_cls;
+  VEC(int64_t) sn_off;
+  VEC(int32_t) sj_prompt;
+  VEC(uint8_t) sj_run;
+  VEC(double) sj_dl, sj_rem, sj_upd, sj_freq, sj_tref, sj_wf;
   VEC(double) enq_t;
   VEC(int64_t) enq_req;
   gso_decision* decisions;
@@ -445,14 +455,32 @@ static void on_optimizer_tick(sim_t* s) { /* :466-497 */
       VPUSH(prompt, s->prompt[pw->job]);
       VPUSH(dl, prefill_deadline(s, pw->job));
       VPUSH(wf, remaining / pw->job_t_ref);
+      VPUSH(s->sj_run, 1);
+      VPUSH(s->sj_rem, pw->job_rem);
+      VPUSH(s->sj_upd, pw->job_upd);
+      VPUSH(s->sj_freq, pw->freq);
+      VPUSH(s->sj_tref, pw->job_t_ref);
     }
     for (int64_t k = s->q_head[q]; k < s->q[q].n; ++k) {
       const int64_t id = s->q[q].v[k];
       VPUSH(prompt, s->prompt[id]);
       VPUSH(dl, prefill_deadline(s, id));
       VPUSH(wf, 1.0);
+      VPUSH(s->sj_run, 0);
+      VPUSH(s->sj_rem, 0.0);
+      VPUSH(s->sj_upd, 0.0);
+      VPUSH(s->sj_freq, 0.0);
+      VPUSH(s->sj_tref, 0.0);
     }
     if (prompt.n == 0) continue; /* queue_optimizer_tick skips empty queues, prefill_opt.cpp:64 */
+    VPUSH(s->sn_now, s->now);
+    VPUSH(s->sn_cls, q);
+    VPUSH(s->sn_off, s->sj_prompt.n);
+    for (int64_t k = 0; k < prompt.n; ++k) {
+      VPUSH(s->sj_prompt, prompt.v[k]);
+      VPUSH(s->sj_dl, dl.v[k]);
+      VPUSH(s->sj_wf, wf.v[k]);
+    }
     double f, window, e;
     int infeasible, fidx;
     gso_queue_tick_one(&s->prof, &s->pol.prefill_opt, prompt.n, prompt.v, dl.v, wf.v, s->now, &f,
@@ -705,8 +733,39 @@ void gso_sim_free(void* h) {
   }
   free(s->dw); free(s->pled); free(s->dled); free(s->f_opt_table); free(s->tps_lo); free(s->tps_hi);
   free(s->heap.v); free(s->timeline.v); free(s->commands.v); free(s->enq_t.v); free(s->enq_req.v);
+  free(s->sn_now.v); free(s->sn_cls.v); free(s->sn_off.v); free(s->sj_prompt.v); free(s->sj_run.v);
+  free(s->sj_dl.v); free(s->sj_rem.v); free(s->sj_upd.v); free(s->sj_freq.v); free(s->sj_tref.v);
+  free(s->sj_wf.v);
   free(s->decisions);
   free(s);
+}
+
+void gso_sim_snapshot_sizes(void* h, int64_t* n_snap, int64_t* n_jobs) {
+  const sim_t* s = (const sim_t*)h;
+  *n_snap = s->sn_now.n;
+  *n_jobs = s->sj_prompt.n;
+}
+
+void gso_sim_snapshots(void* h, double* now, int32_t* cls, int64_t* off, int32_t* prompt,
+                       double* deadline, uint8_t* running, double* rem_ref, double* upd_ms,
+                       double* freq, double* t_ref, double* wf) {
+  const sim_t* s = (const sim_t*)h;
+  for (int64_t i = 0; i < s->sn_now.n; ++i) {
+    now[i] = s->sn_now.v[i];
+    cls[i] = s->sn_cls.v[i];
+    off[i] = s->sn_off.v[i];
+  }
+  off[s->sn_now.n] = s->sj_prompt.n;
+  for (int64_t j = 0; j < s->sj_prompt.n; ++j) {
+    prompt[j] = s->sj_prompt.v[j];
+    deadline[j] = s->sj_dl.v[j];
+    running[j] = s->sj_run.v[j];
+    rem_ref[j] = s->sj_rem.v[j];
+    upd_ms[j] = s->sj_upd.v[j];
+    freq[j] = s->sj_freq.v[j];
+    t_ref[j] = s->sj_tref.v[j];
+    wf[j] = s->sj_wf.v[j];
+  }
 }
 
 void gso_sim_sizes(void* h, int64_t* z) {

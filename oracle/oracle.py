@@ -307,6 +307,8 @@ class Restatement:
                                         C.c_size_t]
         L.gso_pool_run.restype = _p
         L.gso_sim_free.argtypes = [_p]
+        L.gso_sim_snapshot_sizes.argtypes = [_p, _p, _p]
+        L.gso_sim_snapshots.argtypes = [_p] + [_p] * 11
         for f, k in (("sizes", 1), ("requests", 10), ("tbt", 2), ("ledgers", 3), ("decisions", 1),
                      ("timeline", 4), ("commands", 6), ("enqueue", 2), ("scalars", 1)):
             getattr(L, "gso_sim_" + f).argtypes = [_p] + [_p] * k
@@ -543,9 +545,24 @@ class Restatement:
             sm = PoolSummary()
             self.lib.gso_sim_summary(h, C.byref(slo), C.byref(sm))
             out["summary"] = sm.as_dict()
+            out["snapshots"] = self._snapshots(h)
             return out
         finally:
             self.lib.gso_sim_free(h)
+
+    def _snapshots(self, h) -> dict:
+        """The optimizer snapshots with the raw running-job state (gs_sim.c on_optimizer_tick)."""
+        ns, nj = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        self.lib.gso_sim_snapshot_sizes(h, ptr(ns), ptr(nj))
+        ns, nj = int(ns[0]), int(nj[0])
+        o = {"now": np.zeros(ns), "cls": np.zeros(ns, np.int32), "off": np.zeros(ns + 1, np.int64),
+             "prompt": np.zeros(nj, np.int32), "deadline": np.zeros(nj),
+             "running": np.zeros(nj, np.uint8), "rem_ref": np.zeros(nj), "upd_ms": np.zeros(nj),
+             "freq": np.zeros(nj), "t_ref": np.zeros(nj), "wf": np.zeros(nj)}
+        self.lib.gso_sim_snapshots(h, *(ptr(o[k]) for k in (
+            "now", "cls", "off", "prompt", "deadline", "running", "rem_ref", "upd_ms", "freq",
+            "t_ref", "wf")))
+        return o
 
     def pool_run(self, prof, policy: "PolicyHolder", slo, cfg, arrival, prompt, output, enq_t,
                  enq_req, end_floor, cls=None) -> dict:
@@ -608,6 +625,10 @@ class Reference:
         L.ref_prefill_pass.argtypes = [C.c_int, _p, C.c_int, C.c_int, _p, _i64, _p, _p, _i64,
                                        _i64, _i64, _d, C.c_int, _p, _p]
         L.ref_prefill_pass.restype = _i64
+        L.ref_freq_timeline_csv.argtypes = [_i64, _p, _p, _p, _p, _p, _i64]
+        L.ref_freq_timeline_csv.restype = _i64
+        L.ref_prefill_commands_csv.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _i64]
+        L.ref_prefill_commands_csv.restype = _i64
         L.ref_prefill_pass_ex.argtypes = [C.c_int, C.c_int, _p, C.c_int, C.c_int, _p, _i64, _p,
                                           _p, _i64, _i64, _i64, _d, C.POINTER(QoptCfg), _d, _d,
                                           C.c_int, _p, _p, _p]
@@ -712,6 +733,25 @@ class Reference:
         self.lib.ref_select_frequency_many(C.byref(prof), nb, ptr(off), ptr(prompts), ptr(w),
                                            ptr(windows), threads, ptr(f), ptr(e), ptr(found))
         return f, e, found.astype(bool)
+
+    def freq_timeline_csv(self, applied, pool, worker, f) -> bytes:
+        a = [np.ascontiguousarray(applied, np.float64), np.ascontiguousarray(pool, np.uint8),
+             np.ascontiguousarray(worker, np.int32), np.ascontiguousarray(f, np.float64)]
+        n = len(a[0])
+        cap = 64 * n + 64
+        buf = C.create_string_buffer(cap)
+        k = self.lib.ref_freq_timeline_csv(n, *(ptr(x) for x in a), buf, cap)
+        return buf.raw[:k]
+
+    def prefill_commands_csv(self, tick, cls, worker, f, window, infeasible) -> bytes:
+        a = [np.ascontiguousarray(tick, np.float64), np.ascontiguousarray(cls, np.int32),
+             np.ascontiguousarray(worker, np.int32), np.ascontiguousarray(f, np.float64),
+             np.ascontiguousarray(window, np.float64), np.ascontiguousarray(infeasible, np.uint8)]
+        n = len(a[0])
+        cap = 96 * n + 64
+        buf = C.create_string_buffer(cap)
+        k = self.lib.ref_prefill_commands_csv(n, *(ptr(x) for x in a), buf, cap)
+        return buf.raw[:k]
 
     def prefill_pass(self, profs, thresholds, arrival, prompt, window_ms, w0, n_windows, D,
                      threads=1, outputs=True, enabled=True):

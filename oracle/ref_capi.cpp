@@ -429,6 +429,30 @@ int64_t ref_prefill_pass(int n_prof, const gso_profile* profs, int enabled, int 
                              energy, nullptr);
 }
 
+// freq_timeline_csv / prefill_commands_csv (simkernel.cpp:686-714) over SoA records; returns
+// the byte count, copying at most cap bytes into out.
+int64_t ref_freq_timeline_csv(int64_t n, const double* applied, const uint8_t* pool,
+                              const int32_t* worker, const double* f, char* out, int64_t cap) {
+  std::vector<FreqChangeRecord> r(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    r[static_cast<size_t>(i)] = FreqChangeRecord{applied[i], pool[i] != 0, worker[i], f[i]};
+  const std::string s = freq_timeline_csv(r);
+  std::memcpy(out, s.data(), static_cast<size_t>(std::min<int64_t>(cap, s.size())));
+  return static_cast<int64_t>(s.size());
+}
+
+int64_t ref_prefill_commands_csv(int64_t n, const double* tick, const int32_t* cls,
+                                 const int32_t* worker, const double* f, const double* window,
+                                 const uint8_t* infeasible, char* out, int64_t cap) {
+  std::vector<PrefillCommandRecord> r(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i)
+    r[static_cast<size_t>(i)] =
+        PrefillCommandRecord{tick[i], cls[i], worker[i], f[i], window[i], infeasible[i] != 0};
+  const std::string s = prefill_commands_csv(r);
+  std::memcpy(out, s.data(), static_cast<size_t>(std::min<int64_t>(cap, s.size())));
+  return static_cast<int64_t>(s.size());
+}
+
 // queue_optimizer_tick over n_queues snapshots at one instant; returns #commands.
 int ref_queue_optimizer_tick(const gso_profile* c, const gso_qopt_cfg* qc, int n_queues,
                              const int32_t* class_ids, const int64_t* off, const int32_t* prompt,

@@ -37,6 +37,12 @@ class CCellList(C.Structure):
                 ("capacity", _i64)]
 
 
+class CRunningJobs(C.Structure):
+    """gsb_running_jobs (include/gsb.h)."""
+    _fields_ = [("d_running", _p), ("d_remaining_ref_ms", _p), ("d_updated_ms", _p),
+                ("d_freq_mhz", _p), ("d_t_ref_ms", _p)]
+
+
 class CProfile(C.Structure):
     _fields_ = [(n, _d) for n in (
         "f_min_mhz", "f_max_mhz", "step_mhz", "f_ref_mhz",
@@ -139,7 +145,8 @@ EXPORTS = (
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
     "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
-    "gsb_prefill_pass",
+    "gsb_prefill_pass", "gsb_select_batches_running", "gsb_freq_timeline_csv",
+    "gsb_prefill_commands_csv", "gsb_format_g10",
 )
 
 _lib = None
@@ -184,6 +191,12 @@ def load(path: str = LIB_PATH) -> C.CDLL:
                                      P(CCellList), _p]
     L.gsb_prefill_select_list.argtypes = [_p, P(CSelectCfg), _i64, _p, _p, P(CCellList), _p, _p,
                                           _p, _p, _p, _p]
+    L.gsb_select_batches_running.argtypes = [_p, P(CSelectCfg), C.c_int, _i64, _p, _p, _p,
+                                             P(CRunningJobs), _p, _p, _p, _p, _p, _p, _p]
+    L.gsb_freq_timeline_csv.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _i64, P(_i64), _p]
+    L.gsb_prefill_commands_csv.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, P(_i64),
+                                           _p]
+    L.gsb_format_g10.argtypes = [_p, _i64, _p, _p, _p, _p]
     L.gsb_prefill_pass.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p,
                                    P(CCellList), P(CSelectCfg), _p, _p, _p, _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]

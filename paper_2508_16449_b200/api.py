@@ -652,6 +652,42 @@ class Engine:
         rr.profile_gen = self.profile_gen
         return rr, sel
 
+    # ---------------------------------------------------------------- simulator wire formats
+    def _render(self, fn, n, arrays) -> bytes:
+        nb = C.c_int64(0)
+        self._check(fn(self.ctx, n, *[_ptr(a) for a in arrays], None, 0, C.byref(nb),
+                       self.stream()))
+        buf = self._empty(max(int(nb.value), 1), torch.uint8)
+        self._check(fn(self.ctx, n, *[_ptr(a) for a in arrays], _ptr(buf), int(nb.value),
+                       C.byref(nb), self.stream()))
+        return bytes(buf[:int(nb.value)].cpu().numpy().tobytes())
+
+    def freq_timeline_csv(self, applied_ms, prefill_pool, worker, f_mhz) -> bytes:
+        """freq_timeline_csv (simkernel.cpp:686-697) of FreqChangeRecords given as arrays
+        (host or device), rendered on the GPU: '%.10g' numbers, byte-identical."""
+        a = [self._dev(applied_ms, torch.float64), self._dev(prefill_pool, torch.uint8),
+             self._dev(worker, torch.int32), self._dev(f_mhz, torch.float64)]
+        return self._render(self.lib.gsb_freq_timeline_csv, a[0].numel(), a)
+
+    def prefill_commands_csv(self, tick_ms, class_id, worker, f_mhz, window_ms,
+                             infeasible) -> bytes:
+        """prefill_commands_csv (simkernel.cpp:699-714) of PrefillCommandRecords, on the GPU."""
+        a = [self._dev(tick_ms, torch.float64), self._dev(class_id, torch.int32),
+             self._dev(worker, torch.int32), self._dev(f_mhz, torch.float64),
+             self._dev(window_ms, torch.float64), self._dev(infeasible, torch.uint8)]
+        return self._render(self.lib.gsb_prefill_commands_csv, a[0].numel(), a)
+
+    def format_g10(self, values) -> list:
+        """snprintf("%.10g") of every value, on the GPU (the reference's fmt_g)."""
+        v = self._dev(values, torch.float64)
+        n = v.numel()
+        out = self._empty((max(n, 1), 32), torch.uint8)
+        ln = self._empty(max(n, 1), torch.int32)
+        self._check(self.lib.gsb_format_g10(self.ctx, n, _ptr(v), _ptr(out), _ptr(ln),
+                                            self.stream()))
+        o, l = out.cpu().numpy(), ln.cpu().numpy()
+        return [bytes(o[i, :l[i]]).decode() for i in range(n)]
+
     # ---------------------------------------------------------------- K6: trace CSV
     def parse_trace(self, data, class_threshold: int = 1024, name: str = "trace") -> "TraceArrays":
         """greensim::load_trace (trace.cpp:56-129) of a CSV image (bytes, a uint8 numpy array
@@ -779,9 +815,11 @@ class Engine:
     def select_batches(self, off, prompt, windows=None, profile: Optional[GpuProfile] = None,
                        wf=None, mode: int = L.PER_CELL_WINDOW, fixed_window_ms: float = 0.0,
                        deadline=None, now=None,
-                       qopt: QueueOptimizerConfig = QueueOptimizerConfig()):
+                       qopt: QueueOptimizerConfig = QueueOptimizerConfig(), running=None):
         """select_frequency / queue_optimizer_tick over CSR batches. Returns device tensors
-        (f_idx i16, energy f64, window f64, t_ref f64)."""
+        (f_idx i16, energy f64, window f64, t_ref f64). running: optional dict of per-job
+        arrays (running u8, remaining_ref_ms, updated_ms, freq_mhz, t_ref_ms): the running jobs'
+        work_fraction is then computed on the device (simkernel.cpp:476-479; needs now)."""
         pi = 0 if profile is None else self._profile_index(profile)
         off = self._dev(off, torch.int64)
         nb = off.numel() - 1
@@ -794,10 +832,16 @@ class Engine:
         energy = self._empty(nb, torch.float64)
         t_ref = self._empty(nb, torch.float64)
         cfg = L.CSelectCfg(mode, 1, fixed_window_ms, 0, 1, qopt.to_c())
-        self._check(self.lib.gsb_select_batches(self.ctx, C.byref(cfg), pi, nb, _ptr(off),
-                                                _ptr(prompt), _ptr(wf_t), _ptr(dl), _ptr(nw),
-                                                _ptr(win), _ptr(f_idx), _ptr(energy),
-                                                _ptr(t_ref), self.stream()))
+        rj, keep = None, None
+        if running is not None:
+            keep = [self._dev(running["running"], torch.uint8)] + [
+                self._dev(running[k], torch.float64)
+                for k in ("remaining_ref_ms", "updated_ms", "freq_mhz", "t_ref_ms")]
+            rj = L.CRunningJobs(*[_ptr(t) for t in keep])
+        self._check(self.lib.gsb_select_batches_running(
+            self.ctx, C.byref(cfg), pi, nb, _ptr(off), _ptr(prompt), _ptr(wf_t),
+            C.byref(rj) if rj is not None else None, _ptr(dl), _ptr(nw), _ptr(win), _ptr(f_idx),
+            _ptr(energy), _ptr(t_ref), self.stream()))
         return f_idx, energy, win, t_ref
 
     def energy_batches(self, off, prompt, f_mhz, windows, profile: Optional[GpuProfile] = None,

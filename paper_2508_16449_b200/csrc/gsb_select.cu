@@ -563,7 +563,7 @@ k_select_batches(const __grid_constant__ SelectParams sp, const ProfTab* __restr
                  const int32_t* __restrict__ prompt, const double* __restrict__ wf,
                  const double* __restrict__ deadline, const double* __restrict__ now_ms,
                  double* __restrict__ window, int16_t* __restrict__ f_idx,
-                 double* __restrict__ energy, double* __restrict__ t_out) {
+                 double* __restrict__ energy, double* __restrict__ t_out, gsb_running_jobs run) {
   __shared__ double s_f[GSB_MAX_GRID], s_r[GSB_MAX_GRID], s_P[GSB_MAX_GRID];
   __shared__ int s_fast;
   const int G = tab->G;
@@ -595,7 +595,14 @@ k_select_batches(const __grid_constant__ SelectParams sp, const ProfTab* __restr
   const double now = (sp.mode == GSB_DEADLINE_SLACK) ? now_ms[b] : 0.0;
   for (int64_t j = j0; j < j1; ++j) {
     const double L = static_cast<double>(prompt[j]);
-    const double w = wf ? wf[j] : 1.0;
+    double w = wf ? wf[j] : 1.0;
+    if (run.d_running && run.d_running[j]) {
+      // the running job's outstanding share at the snapshot (simkernel.cpp:476-479): work done
+      // since its last update at the applied clock, in reference time, off its remaining work
+      const double done = (now_ms[b] - run.d_updated_ms[j]) * run.d_freq_mhz[j] / tab->f_ref;
+      const double remaining = std_max(run.d_remaining_ref_ms[j] - done, 0.0);
+      w = remaining / run.d_t_ref_ms[j];
+    }
     T = T + w * ((tab->lat_a * L + tab->lat_b) * L + tab->lat_c);
     if (sp.mode == GSB_DEADLINE_SLACK) min_slack = std_min(min_slack, deadline[j] - now);
   }
@@ -956,7 +963,26 @@ int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int
                        const int64_t* d_off, const int32_t* d_prompt, const double* d_wf,
                        const double* d_deadline, const double* d_now, double* d_window,
                        int16_t* d_f_idx, double* d_energy, double* d_t_ref_out, void* stream) {
+  return gsb_select_batches_running(ctx, cfg, profile, n_batches, d_off, d_prompt, d_wf, nullptr,
+                                    d_deadline, d_now, d_window, d_f_idx, d_energy, d_t_ref_out,
+                                    stream);
+}
+
+int gsb_select_batches_running(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile,
+                               int64_t n_batches, const int64_t* d_off, const int32_t* d_prompt,
+                               const double* d_wf, const gsb_running_jobs* run,
+                               const double* d_deadline, const double* d_now, double* d_window,
+                               int16_t* d_f_idx, double* d_energy, double* d_t_ref_out,
+                               void* stream) {
   if (!ctx || !cfg) return GSB_INVALID_ARGUMENT;
+  gsb_running_jobs rj{};
+  if (run && run->d_running) {
+    if (!run->d_remaining_ref_ms || !run->d_updated_ms || !run->d_freq_mhz || !run->d_t_ref_ms ||
+        !d_now)
+      return gsb_set_error(ctx, GSB_INVALID_ARGUMENT,
+                           "select_batches: running jobs need their state and the snapshot now");
+    rj = *run;
+  }
   if (profile < 0 || profile >= ctx->n_profiles)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "select_batches: bad profile index");
   if (cfg->mode == GSB_DEADLINE_SLACK && (!d_deadline || !d_now))
@@ -972,7 +998,7 @@ int gsb_select_batches(gsb_ctx* ctx, const gsb_select_cfg* cfg, int profile, int
   sp.n_cells = n_batches;
   k_select_batches<<<static_cast<unsigned>((n_batches + 7) / 8), 256, 0, gsb_pick_stream(ctx, stream)>>>(
       sp, static_cast<const ProfTab*>(ctx->d_tabs) + profile, n_batches, d_off, d_prompt, d_wf,
-      d_deadline, d_now, d_window, d_f_idx, d_energy, d_t_ref_out);
+      d_deadline, d_now, d_window, d_f_idx, d_energy, d_t_ref_out, rj);
   return gsb_check_launch(ctx, "select_batches");
 }
 

@@ -276,6 +276,41 @@ def test_online_snapshots_reproduce_reference_commands(eng, ref, prof):
     assert r["cmd_infeasible"].sum() > 1000
 
 
+def test_online_snapshots_work_fraction_on_device(eng, ref, restate, prof):
+    """a5: the running prefill job's work_fraction computed ON THE DEVICE from the raw worker
+    state (remaining_ref, updated_ms, applied clock, t_ref; simkernel.cpp:476-479), as the
+    (reference-pinned) restated simulator records it at every optimizer tick of the C1 run:
+    the device's T_ref bits equal the host-side fraction's, and the commands equal the ones
+    the unmodified reference simulator issued."""
+    api = _api()
+    from oracle import oracle as O
+    a, p, o = ref.gen_poisson_trace(5.0, 3_600_000, seed=7)
+    r = ref.run_capture(a, p, o, prof, "greenllm", thresholds=(512, 1024), worker_map=(0, 1, 2))
+    pol = O.PolicyHolder("greenllm", thresholds=(512, 1024), worker_map=(0, 1, 2))
+    sn = restate.sim_run(prof, pol, O.default_slo(), O.default_sim_cfg(n_prefill_workers=3),
+                         a, p, o)["snapshots"]
+    assert len(sn["now"]) == len(r["cmd_f"]) and sn["running"].sum() > 10_000
+    gp = api.GpuProfile.default_profile()
+    running = {"running": sn["running"], "remaining_ref_ms": sn["rem_ref"],
+               "updated_ms": sn["upd_ms"], "freq_mhz": sn["freq"], "t_ref_ms": sn["t_ref"]}
+    f_idx, en, win, t_dev = eng.select_batches(sn["off"], sn["prompt"], None, gp, None,
+                                               api.L.DEADLINE_SLACK, 0.0, sn["deadline"],
+                                               sn["now"], api.QueueOptimizerConfig(),
+                                               running=running)
+    # the same batches with the host-computed fractions: identical T_ref bits
+    _, _, _, t_host = eng.select_batches(sn["off"], sn["prompt"], None, gp, sn["wf"],
+                                         api.L.DEADLINE_SLACK, 0.0, sn["deadline"], sn["now"],
+                                         api.QueueOptimizerConfig())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(u64(t_dev.cpu().numpy()), u64(t_host.cpu().numpy()))
+    fi = f_idx.cpu().numpy()
+    f = np.where(fi >= 0, 210.0 + 15.0 * fi, 1410.0)
+    np.testing.assert_array_equal(sn["cls"], r["cmd_class"])
+    np.testing.assert_array_equal(f, r["cmd_f"])
+    np.testing.assert_array_equal(u64(win.cpu().numpy()), u64(r["cmd_window"]))
+    np.testing.assert_array_equal((fi < 0).astype(np.uint8), r["cmd_infeasible"])
+
+
 def test_band_tables_vs_reference(eng, ref):
     api = _api()
     rng = np.random.default_rng(3)

@@ -118,3 +118,29 @@ def test_enqueue_stream_is_parameter_independent(restate, prof, sinus):
         assert g["enq_t"].tobytes() == g0["enq_t"].tobytes()
         assert g["enq_req"].tobytes() == g0["enq_req"].tobytes()
         assert g["scalars"][2] == g0["scalars"][2]
+
+
+def test_restated_snapshots_match_reference_capture(restate, ref, prof):
+    """The restated simulator's optimizer snapshots (with the raw running-job state the device
+    work_fraction test replays) are the reference simulator's own: same queues, prompts,
+    deadlines and work_fraction bits (simkernel.cpp:466-501)."""
+    from oracle import oracle as O
+    a, p, o = ref.gen_poisson_trace(5.0, 1_200_000, seed=7)
+    r = ref.run_capture(a, p, o, prof, "greenllm", thresholds=(512, 1024), worker_map=(0, 1, 2))
+    pol = O.PolicyHolder("greenllm", thresholds=(512, 1024), worker_map=(0, 1, 2))
+    sn = restate.sim_run(prof, pol, O.default_slo(), O.default_sim_cfg(n_prefill_workers=3),
+                         a, p, o)["snapshots"]
+    off = r["snap_off"]
+    idx = np.nonzero(np.diff(off) > 0)[0]
+    sel = np.concatenate([np.arange(off[i], off[i + 1]) for i in idx])
+    np.testing.assert_array_equal(sn["now"], r["snap_now"][idx])
+    np.testing.assert_array_equal(sn["cls"], r["snap_class"][idx])
+    np.testing.assert_array_equal(sn["prompt"], r["job_prompt"][sel])
+    np.testing.assert_array_equal(sn["deadline"].view(np.uint64), r["job_deadline"][sel].view(np.uint64))
+    np.testing.assert_array_equal(sn["wf"].view(np.uint64), r["job_wf"][sel].view(np.uint64))
+    # the raw state reproduces the fraction in the reference's operation order
+    run = sn["running"] != 0
+    done = (np.repeat(sn["now"], np.diff(sn["off"]))[run] - sn["upd_ms"][run]) * sn["freq"][run] / 1410.0
+    wf = np.maximum(sn["rem_ref"][run] - done, 0.0) / sn["t_ref"][run]
+    np.testing.assert_array_equal(wf.view(np.uint64), sn["wf"][run].view(np.uint64))
+    assert run.sum() > 1000
