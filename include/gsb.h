@@ -369,6 +369,25 @@ int gsb_trace_format(gsb_ctx* ctx, int64_t n, const int64_t* d_arrival, const in
                      const int32_t* d_output, const uint8_t* d_slo_class, char* d_out,
                      int64_t cap_bytes, int64_t* h_bytes, void* stream);
 
+/* ---------------------------------------------------------------- simulator wire formats */
+/* greensim::freq_timeline_csv / prefill_commands_csv (simkernel.cpp:686-714) rendered on the
+ * GPU from device-resident SoA records (FreqChangeRecord / PrefillCommandRecord,
+ * simkernel.hpp:131-146): header + one line per record, numbers as snprintf("%.10g") from the
+ * exact binary value (simkernel.cpp:679-683), integers as std::to_string. d_out == NULL: size
+ * query; *h_bytes = bytes. Synchronous. */
+int gsb_freq_timeline_csv(gsb_ctx* ctx, int64_t n, const double* d_applied_ms,
+                          const uint8_t* d_prefill_pool, const int32_t* d_worker,
+                          const double* d_f_mhz, char* d_out, int64_t cap_bytes, int64_t* h_bytes,
+                          void* stream);
+int gsb_prefill_commands_csv(gsb_ctx* ctx, int64_t n, const double* d_tick_ms,
+                             const int32_t* d_class, const int32_t* d_worker,
+                             const double* d_f_mhz, const double* d_window_ms,
+                             const uint8_t* d_infeasible, char* d_out, int64_t cap_bytes,
+                             int64_t* h_bytes, void* stream);
+/* snprintf("%.10g") of n values: value i's text at d_out32 + 32*i, its length in d_len[i]. */
+int gsb_format_g10(gsb_ctx* ctx, int64_t n, const double* d_values, char* d_out32,
+                   int32_t* d_len, void* stream);
+
 /* ---------------------------------------------------------------- K3/K4: decode control */
 /* Raw decode telemetry of S streams (one decode worker each), CSR layout:
  * events of stream s are [d_ev_off[s], d_ev_off[s+1]) sorted by time; event j emitted
