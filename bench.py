@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: ONE global trace of the config's windows, sliced per "
+                         "rank (distributed.window_shard / trace_slice), scenarios split too")
     return ap.parse_args()
 
 
@@ -136,13 +139,26 @@ def run_gsb(args, rank, world, dist):
     thr = wl.THRESHOLDS[W["C"]]
     routing = api.RoutingConfig(True, thr, list(range(W["C"])))
     nW, wms = W["W"], W["window_ms"]
-    w0 = rank * nW
-    t0 = w0 * wms
-    if W["shape"] == "mixed":
-        arrival, prompt, _ = wl.mixed_trace(W["qps"], nW * wms, seed=1000 + rank, t0_ms=t0)
+    from paper_2508_16449_b200 import distributed as Dd
+    if args.strong:  # one global trace (rank 0's weak-scaling trace), this rank's window slice
+        total_w = nW
+        if W["shape"] == "mixed":
+            ga, gp, _ = wl.mixed_trace(W["qps"], total_w * wms, seed=1000, t0_ms=0)
+        else:
+            ga, gp, _ = wl.poisson_trace(W["qps"], total_w * wms, W["shape"], seed=1000, t0_ms=0)
+        w0, nW = Dd.window_shard(total_w, world, rank)
+        lo, hi = Dd.trace_slice(ga, wms, w0, nW)
+        arrival, prompt = ga[lo:hi].copy(), gp[lo:hi].copy()
+        args.scenarios = Dd.scenario_shard(args.scenarios, world, rank)[1]
+        args.pool_scenarios = max(1, Dd.scenario_shard(args.pool_scenarios, world, rank)[1])
     else:
-        arrival, prompt, _ = wl.poisson_trace(W["qps"], nW * wms, W["shape"], seed=1000 + rank,
-                                              t0_ms=t0)
+        w0 = rank * nW
+        t0 = w0 * wms
+        if W["shape"] == "mixed":
+            arrival, prompt, _ = wl.mixed_trace(W["qps"], nW * wms, seed=1000 + rank, t0_ms=t0)
+        else:
+            arrival, prompt, _ = wl.poisson_trace(W["qps"], nW * wms, W["shape"],
+                                                  seed=1000 + rank, t0_ms=t0)
     n_req = len(arrival)
     cells = nW * W["C"]
     P = W["P"]
@@ -412,7 +428,12 @@ def run_gsb(args, rank, world, dist):
     else:
         per_rank = summ.cpu().numpy().reshape(1, -1).view(Dd.SUMMARY_DTYPE)
     per_rank = per_rank.reshape(world, P, W["C"])
-    glob = Dd.combine_summaries(per_rank, [r * nW * W["C"] for r in range(world)])
+    if args.strong:
+        cell_off = [Dd.window_shard(W["W"], world, r)[0] * W["C"] for r in range(world)]
+    else:
+        cell_off = [r * nW * W["C"] for r in range(world)]
+    # the rank-order combine through the C ABI (gsb_combine_summaries)
+    glob = Dd.combine_summaries_c(per_rank, cell_off)
 
     # ---------------- CPU baseline + parity (rank 0, N = 1 only; the oracle is the checker)
     cpu = None
@@ -471,8 +492,8 @@ def run_gsb(args, rank, world, dist):
         "unit": "window x class x clock evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_pre,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference-shaped Poisson/bimodal traces; sinusoidal decode telemetry)",
         "config": {"workload": W["name"], "windows_per_gpu": nW, "window_ms": wms,
                    "classes": W["C"], "profiles": P, "clocks": 81, "requests_per_gpu": n_req,

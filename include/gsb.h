@@ -323,6 +323,18 @@ int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
                      const gsb_select_cfg* scfg, double* d_window, int16_t* d_f_idx,
                      double* d_energy, gsb_class_summary* d_summary, void* stream);
 
+/* M/G/1 side output of a pass (BASELINE north_star (2)): per (profile, cell) the utilisation
+ * rho = lambda E[s], the Pollaczek-Khinchine mean wait Wq = lambda E[s^2] / (2 (1 - rho)) in ms
+ * (+inf when rho >= 1) and the energy per request E / n, with service times s_j = (f_ref / f)
+ * t_j at the command's clock (f_max when infeasible) and lambda = jobs / window_ms.
+ * PARITY-UNPINNED: the reference has no M/G/1 term; never an input of the
+ * bit-exact decisions. Outputs [P][cells]; empty cells 0. d_bounds / d_class from K1,
+ * d_f_idx / d_energy from K2. */
+int gsb_mg1_side_output(gsb_ctx* ctx, int n_classes, int64_t n_windows, double window_ms,
+                        const int32_t* d_prompt, const uint8_t* d_class, const int64_t* d_bounds,
+                        const int16_t* d_f_idx, const double* d_energy, double* d_wq_ms,
+                        double* d_rho, double* d_energy_per_request, void* stream);
+
 /* ---------------------------------------------------------------- K6: trace CSV ingest */
 /* greensim::TraceError::Kind (trace.hpp:36-40), in the reference's enum order */
 enum {
@@ -579,6 +591,48 @@ int gsb_decode_pool_tps_cap(const gsb_profile* prof, int32_t max_batch, double c
 /* prof is a HOST pointer (passed as a kernel parameter); everything in st / a is device memory. */
 int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* cfg,
                     const gsb_pool_stream* st, const gsb_pool_args* a, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU reductions */
+/* The path shards with no data exchange (windows / scenarios per rank); the
+ * only collective is the end-of-run gather of small records, combined on every rank in RANK
+ * ORDER, so the global result is bitwise identical everywhere (an fp64 all-reduce would not be).
+ * The transport is the caller's: gather(d_send, d_recv, bytes, stream, user) must place every
+ * rank's `bytes` from d_send into d_recv in rank order (device memory, on `stream`) and return 0
+ * -- e.g. ncclAllGather(d_send, d_recv, bytes, ncclUint8, comm, stream) with comm in user
+ * (INTEGRATION.md). This replaces the reference's serial sweep (simkernel.cpp:663-676). */
+typedef int (*gsb_allgather_fn)(const void* d_send, void* d_recv, size_t bytes, void* stream,
+                                void* user);
+
+/* Rank-order combine of per-rank prefill summaries (host memory, [world][n_records], rank r's
+ * cells offset by h_cell_offsets[r]): counts add, energies fold left to right over ranks, the
+ * argmin keeps the lowest energy then the lowest global cell. No device needed. */
+int gsb_combine_summaries(int world, int n_records, const gsb_class_summary* h_per_rank,
+                          const int64_t* h_cell_offsets, gsb_class_summary* h_out);
+/* gather (the caller's transport) + gsb_combine_summaries: d_local = this rank's n_records
+ * summaries (device), h_out = the global records (host, identical on every rank). */
+int gsb_reduce_summaries(gsb_ctx* ctx, int world, int rank, int n_records,
+                         const gsb_class_summary* d_local, const int64_t* h_cell_offsets,
+                         gsb_allgather_fn gather, void* user, gsb_class_summary* h_out,
+                         void* stream);
+
+/* Decode-pool end-of-run tally (the K5 scenario summaries of one rank folded in order). */
+typedef struct gsb_decode_tally {
+  int64_t n_scenarios;
+  double decode_pool_j, min_decode_pool_j;
+  int64_t argmin_scenario;
+  int64_t n_completed, n_rejected, n_ttft_ok, n_tbt_ok, tbt_samples, tbt_samples_ok;
+  int64_t n_decisions, n_freq_changes;
+  uint64_t digest;  /* sum mod 2^64 of splitmix64(decision ^ freq ^ request digest ^ scenario) */
+} gsb_decode_tally;
+/* Fold n scenario summaries (host) of global scenarios [scen0, scen0 + n) in order. */
+int gsb_tally_pool(int64_t n, const gsb_pool_summary* h_summary, int64_t scen0,
+                   gsb_decode_tally* h_out);
+/* Rank-order combine of [world] tallies (host). */
+int gsb_combine_tallies(int world, const gsb_decode_tally* h_per_rank, gsb_decode_tally* h_out);
+/* gather (caller's transport, device staging in the context) + gsb_combine_tallies. */
+int gsb_reduce_tallies(gsb_ctx* ctx, int world, int rank, const gsb_decode_tally* h_local,
+                       gsb_allgather_fn gather, void* user, gsb_decode_tally* h_out,
+                       void* stream);
 
 /* ---------------------------------------------------------------- microbenchmarks */
 /* FP64 pipe peak probe: n_threads lanes each run `iters` independent DFMA chains;

@@ -146,8 +146,13 @@ EXPORTS = (
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
     "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
     "gsb_prefill_pass", "gsb_select_batches_running", "gsb_freq_timeline_csv",
-    "gsb_prefill_commands_csv", "gsb_format_g10",
+    "gsb_prefill_commands_csv", "gsb_format_g10", "gsb_mg1_side_output",
+    "gsb_combine_summaries", "gsb_reduce_summaries", "gsb_tally_pool", "gsb_combine_tallies",
+    "gsb_reduce_tallies",
 )
+
+# gsb_allgather_fn: int (*)(const void* d_send, void* d_recv, size_t bytes, void* stream, void* user)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
 _lib = None
 
@@ -197,6 +202,13 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_prefill_commands_csv.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, P(_i64),
                                            _p]
     L.gsb_format_g10.argtypes = [_p, _i64, _p, _p, _p, _p]
+    L.gsb_combine_summaries.argtypes = [C.c_int, C.c_int, _p, _p, _p]
+    L.gsb_reduce_summaries.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, ALLGATHER_FN, _p,
+                                       _p, _p]
+    L.gsb_tally_pool.argtypes = [_i64, _p, _i64, _p]
+    L.gsb_combine_tallies.argtypes = [C.c_int, _p, _p]
+    L.gsb_reduce_tallies.argtypes = [_p, C.c_int, C.c_int, _p, ALLGATHER_FN, _p, _p, _p]
+    L.gsb_mg1_side_output.argtypes = [_p, C.c_int, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p]
     L.gsb_prefill_pass.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p,
                                    P(CCellList), P(CSelectCfg), _p, _p, _p, _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]

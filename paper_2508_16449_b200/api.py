@@ -652,6 +652,20 @@ class Engine:
         rr.profile_gen = self.profile_gen
         return rr, sel
 
+    def mg1_side_output(self, rr: RouteResult, sel: "SelectResult", prompt):
+        """M/G/1 side output beside the decisions (gsb_mg1_side_output): dict of [P, cells]
+        device tensors rho, wq_ms, energy_per_request_j. PARITY-UNPINNED (the reference has no
+        M/G/1 term); never an input of the bit-exact argmin."""
+        prompt = self._dev(prompt, torch.int32)
+        P, cells = sel.f_idx.shape
+        out = {k: self._empty((P, cells), torch.float64)
+               for k in ("wq_ms", "rho", "energy_per_request_j")}
+        self._check(self.lib.gsb_mg1_side_output(
+            self.ctx, rr.n_classes, rr.n_windows, float(rr.window_ms), _ptr(prompt), _ptr(rr.cls),
+            _ptr(rr.bounds), _ptr(sel.f_idx), _ptr(sel.energy_j), _ptr(out["wq_ms"]),
+            _ptr(out["rho"]), _ptr(out["energy_per_request_j"]), self.stream()))
+        return out
+
     # ---------------------------------------------------------------- simulator wire formats
     def _render(self, fn, n, arrays) -> bytes:
         nb = C.c_int64(0)

@@ -391,6 +391,145 @@ int gsb_set_profiles_ex(gsb_ctx* ctx, int n, const gsb_profile* profiles, int fl
   return GSB_OK;
 }
 
+// ---------------------------------------------------------------- multi-GPU reductions
+int gsb_combine_summaries(int world, int n, const gsb_class_summary* per_rank,
+                          const int64_t* cell_off, gsb_class_summary* out) {
+  if (world < 1 || n < 0 || (n && (!per_rank || !out || !cell_off))) return GSB_INVALID_ARGUMENT;
+  for (int i = 0; i < n; ++i) {
+    gsb_class_summary o{};
+    o.min_energy_j = INFINITY;
+    o.argmin_cell = -1;
+    double e = 0.0;
+    for (int r = 0; r < world; ++r) {
+      const gsb_class_summary& x = per_rank[static_cast<size_t>(r) * n + i];
+      o.n_cmd += x.n_cmd;
+      o.n_infeasible += x.n_infeasible;
+      o.n_empty += x.n_empty;
+      e = e + x.sum_energy_j;
+      if (x.argmin_cell >= 0) {
+        const int64_t g = x.argmin_cell + cell_off[r];
+        if (o.argmin_cell < 0 || x.min_energy_j < o.min_energy_j ||
+            (x.min_energy_j == o.min_energy_j && g < o.argmin_cell)) {
+          o.min_energy_j = x.min_energy_j;
+          o.argmin_cell = g;
+        }
+      }
+    }
+    o.sum_energy_j = e;
+    out[i] = o;
+  }
+  return GSB_OK;
+}
+
+namespace {
+int gather_to_host(gsb_ctx* ctx, int world, const void* d_send, size_t bytes,
+                   gsb_allgather_fn gather, void* user, void* h_out, void* stream) {
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  char* d = static_cast<char*>(gsb_scratch(ctx, bytes * (static_cast<size_t>(world) + 1)));
+  if (!d) return gsb_set_error(ctx, GSB_CUDA_ERROR, "reduce: scratch allocation failed");
+  char* d_send_copy = d + bytes * static_cast<size_t>(world);
+  cudaMemcpyAsync(d_send_copy, d_send, bytes, cudaMemcpyDefault, s);
+  if (gather(d_send_copy, d, bytes, s, user) != 0)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "reduce: the all-gather callback failed");
+  cudaMemcpyAsync(h_out, d, bytes * static_cast<size_t>(world), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "reduce");
+  return GSB_OK;
+}
+inline uint64_t mix64(uint64_t x) {  // splitmix64 finaliser (distributed.py _mix64)
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+}  // namespace
+
+int gsb_reduce_summaries(gsb_ctx* ctx, int world, int rank, int n, const gsb_class_summary* d_local,
+                         const int64_t* cell_off, gsb_allgather_fn gather, void* user,
+                         gsb_class_summary* h_out, void* stream) {
+  if (!ctx || !gather || world < 1 || rank < 0 || rank >= world || n < 0)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "reduce_summaries: bad arguments");
+  std::vector<gsb_class_summary> all(static_cast<size_t>(world) * n);
+  const int rc = gather_to_host(ctx, world, d_local, sizeof(gsb_class_summary) * n, gather, user,
+                                all.data(), stream);
+  if (rc) return rc;
+  return gsb_combine_summaries(world, n, all.data(), cell_off, h_out);
+}
+
+int gsb_tally_pool(int64_t n, const gsb_pool_summary* sm, int64_t scen0, gsb_decode_tally* out) {
+  if (n < 0 || !out || (n && !sm)) return GSB_INVALID_ARGUMENT;
+  gsb_decode_tally t{};
+  t.n_scenarios = n;
+  t.min_decode_pool_j = INFINITY;
+  t.argmin_scenario = -1;
+  double e = 0.0;
+  uint64_t dig = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const gsb_pool_summary& s = sm[i];
+    const double x = s.decode_pool_j;
+    e = e + x;
+    if (x < t.min_decode_pool_j) {
+      t.min_decode_pool_j = x;
+      t.argmin_scenario = scen0 + i;
+    }
+    const uint64_t d = s.decision_digest ^ s.freq_digest ^ s.request_digest;
+    dig += mix64(d ^ static_cast<uint64_t>(scen0 + i));
+    t.n_completed += s.n_completed;
+    t.n_rejected += s.n_rejected;
+    t.n_ttft_ok += s.n_ttft_ok;
+    t.n_tbt_ok += s.n_tbt_ok;
+    t.tbt_samples += s.tbt_samples;
+    t.tbt_samples_ok += s.tbt_samples_ok;
+    t.n_decisions += s.n_decisions;
+    t.n_freq_changes += s.n_freq_changes;
+  }
+  t.decode_pool_j = e;
+  t.digest = dig;
+  *out = t;
+  return GSB_OK;
+}
+
+int gsb_combine_tallies(int world, const gsb_decode_tally* pr, gsb_decode_tally* out) {
+  if (world < 1 || !pr || !out) return GSB_INVALID_ARGUMENT;
+  gsb_decode_tally t{};
+  t.min_decode_pool_j = INFINITY;
+  t.argmin_scenario = -1;
+  double e = 0.0;
+  for (int r = 0; r < world; ++r) {
+    const gsb_decode_tally& s = pr[r];
+    t.n_scenarios += s.n_scenarios;
+    e = e + s.decode_pool_j;
+    if (s.argmin_scenario >= 0 &&
+        (t.argmin_scenario < 0 || s.min_decode_pool_j < t.min_decode_pool_j)) {
+      t.min_decode_pool_j = s.min_decode_pool_j;
+      t.argmin_scenario = s.argmin_scenario;
+    }
+    t.digest += s.digest;
+    t.n_completed += s.n_completed;
+    t.n_rejected += s.n_rejected;
+    t.n_ttft_ok += s.n_ttft_ok;
+    t.n_tbt_ok += s.n_tbt_ok;
+    t.tbt_samples += s.tbt_samples;
+    t.tbt_samples_ok += s.tbt_samples_ok;
+    t.n_decisions += s.n_decisions;
+    t.n_freq_changes += s.n_freq_changes;
+  }
+  t.decode_pool_j = e;
+  *out = t;
+  return GSB_OK;
+}
+
+int gsb_reduce_tallies(gsb_ctx* ctx, int world, int rank, const gsb_decode_tally* h_local,
+                       gsb_allgather_fn gather, void* user, gsb_decode_tally* h_out,
+                       void* stream) {
+  if (!ctx || !gather || !h_local || world < 1 || rank < 0 || rank >= world)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "reduce_tallies: bad arguments");
+  std::vector<gsb_decode_tally> all(static_cast<size_t>(world));
+  const int rc = gather_to_host(ctx, world, h_local, sizeof(gsb_decode_tally), gather, user,
+                                all.data(), stream);
+  if (rc) return rc;
+  return gsb_combine_tallies(world, all.data(), h_out);
+}
+
 int64_t gsb_n_ticks(double period_ms, double t_end_ms) {
   int64_t n = 0;
   for (double t = period_ms; t <= t_end_ms; t = t + period_ms) ++n;

@@ -661,6 +661,53 @@ __global__ void k_energy_batches(const ProfTab* __restrict__ tab, int64_t n_batc
   total[b] = a + d;
 }
 
+// ---------------------------------------------------------------- M/G/1 side output
+// BASELINE north_star (2) asks for an M/G/1-style waiting time and the energy per request beside
+// each decision. The reference has no such term (SPEC.md:294 lists it as a non-goal), so this is
+// a labelled, parity-UNPINNED side output, never an input of the bit-exact argmin: for cell
+// (window w, class c) of profile p with n jobs, service times s_j = (f_ref / f) t_j at the
+// command's clock f (f_max when infeasible), t_j = (a L_j + b) L_j + c, arrival rate
+// lambda = n / window_ms, Pollaczek-Khinchine: rho = lambda E[s], Wq = lambda E[s^2] /
+// (2 (1 - rho)) (+inf when rho >= 1), and E / n. One thread per (cell, profile) walks the window's
+// requests of its class in arrival order (deterministic sums).
+__global__ void k_mg1(int P, int C, int64_t n_windows, double window_ms,
+                      const ProfTab* __restrict__ tabs, const int32_t* __restrict__ prompt,
+                      const uint8_t* __restrict__ cls, const int64_t* __restrict__ bounds,
+                      const int16_t* __restrict__ f_idx, const double* __restrict__ energy,
+                      double* __restrict__ wq, double* __restrict__ rho,
+                      double* __restrict__ e_req) {
+  const int64_t cells = n_windows * C;
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= cells * P) return;
+  const int p = static_cast<int>(i / cells);
+  const int64_t cell = i - p * cells, w = cell / C;
+  const int c = static_cast<int>(cell - w * C);
+  const ProfTab& t = tabs[p];
+  const int fi = f_idx[i];
+  if (fi == -2) {  // empty queue: no command
+    wq[i] = rho[i] = e_req[i] = 0.0;
+    return;
+  }
+  double s1 = 0.0, s2 = 0.0;
+  int64_t n = 0;
+  for (int64_t j = bounds[w]; j < bounds[w + 1]; ++j) {
+    if (cls[j] != c) continue;
+    const double L = static_cast<double>(prompt[j]);
+    const double tj = (t.lat_a * L + t.lat_b) * L + t.lat_c;
+    s1 += tj;
+    s2 += tj * tj;
+    ++n;
+  }
+  const double f = fi >= 0 ? t.f[fi] : t.f_max;
+  const double k = t.f_ref / f;
+  const double lambda = static_cast<double>(n) / window_ms;
+  const double es = k * s1 / static_cast<double>(n), es2 = k * k * s2 / static_cast<double>(n);
+  const double r = lambda * es;
+  rho[i] = r;
+  wq[i] = r < 1.0 ? lambda * es2 / (2.0 * (1.0 - r)) : INFINITY;
+  e_req[i] = fi >= 0 ? energy[i] / static_cast<double>(n) : 0.0;
+}
+
 // ---------------------------------------------------------------- FP64 pipe probe
 __global__ void k_fp64_probe(int iters, double* sink) {
   double a0 = threadIdx.x * 1e-3, a1 = a0 + 1.0, a2 = a0 + 2.0, a3 = a0 + 3.0;
@@ -1033,6 +1080,20 @@ int gsb_prefill_summary(gsb_ctx* ctx, int n_profiles, int n_classes, int64_t n_c
       cudaSuccess)
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "summary: too many cells");
   return gsb_check_launch(ctx, "prefill_summary");
+}
+
+int gsb_mg1_side_output(gsb_ctx* ctx, int n_classes, int64_t n_windows, double window_ms,
+                        const int32_t* d_prompt, const uint8_t* d_class, const int64_t* d_bounds,
+                        const int16_t* d_f_idx, const double* d_energy, double* d_wq_ms,
+                        double* d_rho, double* d_energy_per_request, void* stream) {
+  if (!ctx || n_classes < 1 || n_windows < 0 || !(window_ms > 0.0))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "mg1: bad shape");
+  const int64_t total = n_windows * n_classes * ctx->n_profiles;
+  if (total == 0) return GSB_OK;
+  k_mg1<<<static_cast<unsigned>((total + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(
+      ctx->n_profiles, n_classes, n_windows, window_ms, static_cast<const ProfTab*>(ctx->d_tabs),
+      d_prompt, d_class, d_bounds, d_f_idx, d_energy, d_wq_ms, d_rho, d_energy_per_request);
+  return gsb_check_launch(ctx, "mg1_side_output");
 }
 
 int gsb_selftest_division(gsb_ctx* ctx, int64_t per_divisor, uint64_t seed,

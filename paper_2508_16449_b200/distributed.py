@@ -156,3 +156,97 @@ def gather_records(rec: np.ndarray, device, group=None) -> np.ndarray:
     t = torch.from_numpy(np.frombuffer(rec.tobytes(), np.uint8).copy()).to(device)
     g = gather_summaries(t, group)
     return g.cpu().numpy().reshape(g.shape[0], -1).view(rec.dtype).reshape(-1)
+
+
+# ------------------------------------------------------------------ the C-ABI reductions
+# gsb_combine_summaries / gsb_tally_pool / gsb_combine_tallies (host C, no device needed) and
+# gsb_reduce_summaries / gsb_reduce_tallies with a torch.distributed all-gather as the
+# transport callback (NCCL on GPU tensors, gloo otherwise): the same rank-order combine a C++
+# host runs with ncclAllGather.
+def _lib():
+    from . import _lib as L
+    return L.load()
+
+
+def combine_summaries_c(per_rank: np.ndarray, cell_offsets) -> np.ndarray:
+    """gsb_combine_summaries over [R, N] SUMMARY_DTYPE records."""
+    import ctypes as C
+    pr = np.ascontiguousarray(per_rank, SUMMARY_DTYPE).reshape(per_rank.shape[0], -1)
+    off = np.ascontiguousarray(cell_offsets, np.int64)
+    out = np.zeros(pr.shape[1], SUMMARY_DTYPE)
+    rc = _lib().gsb_combine_summaries(pr.shape[0], pr.shape[1], pr.ctypes.data_as(C.c_void_p),
+                                      off.ctypes.data_as(C.c_void_p),
+                                      out.ctypes.data_as(C.c_void_p))
+    assert rc == 0, rc
+    return out.reshape(per_rank.shape[1:])
+
+
+def tally_pool_c(summary: np.ndarray, scen0: int) -> np.ndarray:
+    """gsb_tally_pool over POOL_SUMMARY_DTYPE records."""
+    import ctypes as C
+    sm = np.ascontiguousarray(summary)
+    out = np.zeros(1, DECODE_TALLY_DTYPE)
+    rc = _lib().gsb_tally_pool(len(sm), sm.ctypes.data_as(C.c_void_p), int(scen0),
+                               out.ctypes.data_as(C.c_void_p))
+    assert rc == 0, rc
+    return out[0]
+
+
+def combine_tallies_c(per_rank: np.ndarray) -> np.ndarray:
+    import ctypes as C
+    pr = np.ascontiguousarray(per_rank, DECODE_TALLY_DTYPE)
+    out = np.zeros(1, DECODE_TALLY_DTYPE)
+    rc = _lib().gsb_combine_tallies(len(pr), pr.ctypes.data_as(C.c_void_p),
+                                    out.ctypes.data_as(C.c_void_p))
+    assert rc == 0, rc
+    return out[0]
+
+
+def torch_allgather_callback(engine, group=None):
+    """A gsb_allgather_fn that moves the bytes through torch.distributed (device staging via
+    gsb_memcpy, all_gather on tensors of the group's backend). Keep the returned object alive
+    while the library may call it."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from . import _lib as L
+
+    lib = engine.lib
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+    def cb(d_send, d_recv, nbytes, stream, user):
+        try:
+            world = dist.get_world_size(group)
+            lib.gsb_synchronize(engine.ctx)
+            torch.cuda.synchronize()
+            mine = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            host = torch.empty(nbytes, dtype=torch.uint8)
+            if lib.gsb_memcpy(engine.ctx, host.data_ptr(), d_send, nbytes, 1, None) != 0:
+                return 1
+            lib.gsb_synchronize(engine.ctx)
+            mine.copy_(host)
+            out = torch.empty(world * nbytes, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(out, mine, group=group)
+            outh = out.cpu()
+            if lib.gsb_memcpy(engine.ctx, d_recv, outh.data_ptr(), world * nbytes, 0, None) != 0:
+                return 1
+            lib.gsb_synchronize(engine.ctx)
+            return 0
+        except Exception:  # noqa: BLE001 - reported to the library as a failed transport
+            return 1
+
+    return L.ALLGATHER_FN(cb)
+
+
+def reduce_summaries(engine, summary_dev, n_records: int, cell_offsets, group=None) -> np.ndarray:
+    """gsb_reduce_summaries: this rank's device summaries -> the global records (host)."""
+    import ctypes as C
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    off = np.ascontiguousarray(cell_offsets, np.int64)
+    out = np.zeros(n_records, SUMMARY_DTYPE)
+    cb = torch_allgather_callback(engine, group)
+    engine._check(engine.lib.gsb_reduce_summaries(
+        engine.ctx, world, rank, n_records, summary_dev.data_ptr(), off.ctypes.data_as(C.c_void_p),
+        cb, None, out.ctypes.data_as(C.c_void_p), None))
+    return out

@@ -266,3 +266,45 @@ def test_unchecked_profiles_evaluate_like_the_reference(gsb, ref):
             else:
                 assert p.grid.at(int(f_idx[b])) == r[0] and u64([e[b]])[0] == u64([r[1]])[0], b
     gsb.set_profiles([api.GpuProfile.default_profile()])
+
+
+def test_mg1_side_output_formula(gsb):
+    """North_star (2)'s M/G/1 side output: PARITY-UNPINNED (the reference has no M/G/1 term,
+    SPEC.md:294), so it is pinned to its own definition (Pollaczek-Khinchine over the cell's
+    service times at the command's clock), computed here in float64 numpy, 1e-12 relative."""
+    import torch
+    from paper_2508_16449_b200 import api, workloads as wl
+    profs = wl.synth_profiles(2)
+    gsb.set_profiles(profs)
+    a, p, _ = wl.poisson_trace(5.0, 120 * 60_000, "alibaba_chat", seed=9)
+    routing = api.RoutingConfig(True, wl.THRESHOLDS[3], [0, 1, 2])
+    rr = gsb.route_bin(a, p, routing, 60_000, 0, 120)
+    sel = gsb.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=57_000.0)
+    out = gsb.mg1_side_output(rr, sel, p)
+    torch.cuda.synchronize()
+    cls = rr.cls.cpu().numpy()
+    fi, en = sel.f_idx.cpu().numpy(), sel.energy_j.cpu().numpy()
+    wq, rho, epr = (out[k].cpu().numpy() for k in ("wq_ms", "rho", "energy_per_request_j"))
+    win = a // 60_000
+    checked = 0
+    for pi, pr in enumerate(profs):
+        grid = np.array(pr.grid.frequencies())
+        for cell in range(0, 360, 7):
+            w, c = divmod(cell, 3)
+            m = (win == w) & (cls == c)
+            if fi[pi, cell] == -2:
+                assert m.sum() == 0 and wq[pi, cell] == 0.0
+                continue
+            L = p[m].astype(np.float64)
+            t = (pr.prefill.a * L + pr.prefill.b) * L + pr.prefill.c
+            f = grid[fi[pi, cell]] if fi[pi, cell] >= 0 else pr.grid.f_max_mhz
+            k = pr.grid.f_ref_mhz / f
+            lam = len(L) / 60_000.0
+            r = lam * k * t.sum() / len(L)
+            assert abs(rho[pi, cell] - r) <= 1e-12 * r
+            want = lam * k * k * (t * t).sum() / len(L) / (2 * (1 - r)) if r < 1 else np.inf
+            assert (wq[pi, cell] == want) if not np.isfinite(want) else abs(wq[pi, cell] - want) <= 1e-12 * want
+            if fi[pi, cell] >= 0:
+                assert abs(epr[pi, cell] - en[pi, cell] / len(L)) <= 1e-15 * en[pi, cell]
+            checked += 1
+    assert checked > 50

@@ -178,3 +178,24 @@ def test_decode_tallies_split_invariance():
                 assert abs(g[k] - single[k]) <= 1e-12 * abs(single[k])
             else:
                 assert g[k] == single[k], (world, k)
+
+
+def test_c_abi_reductions_equal_the_python_combine():
+    """gsb_combine_summaries / gsb_tally_pool / gsb_combine_tallies (host C over the C ABI, what
+    a C++ host calls after its ncclAllGather) give the Python reference combine's exact bytes."""
+    rng = np.random.default_rng(6)
+    R, N = 5, 24
+    pr = np.zeros((R, N), D.SUMMARY_DTYPE)
+    for k in ("n_cmd", "n_infeasible", "n_empty"):
+        pr[k] = rng.integers(0, 1000, (R, N))
+    pr["sum_energy_j"] = rng.uniform(0, 1e9, (R, N))
+    pr["min_energy_j"] = rng.choice([1.0, 2.0, 3.0, np.inf], (R, N))
+    pr["argmin_cell"] = np.where(np.isinf(pr["min_energy_j"]), -1, rng.integers(0, 500, (R, N)))
+    off = np.arange(R) * 1000
+    want = D.combine_summaries(pr.reshape(R, 1, N), off)[0]
+    got = D.combine_summaries_c(pr.reshape(R, 1, N), off)[0]
+    assert got.tobytes() == want.tobytes()
+    sm = _pool_records(301, 2)
+    assert D.tally_pool_c(sm, 17).tobytes() == D.tally_pool(sm, 17).tobytes()
+    parts = np.array([D.tally_pool(sm[i::3], 100 * i) for i in range(3)], D.DECODE_TALLY_DTYPE)
+    assert D.combine_tallies_c(parts).tobytes() == D.combine_tallies(parts).tobytes()
