@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${ROUND}_launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-graph > gpurun_out/${ROUND}_launch_bench.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_route_bin|k_prefill_select|k_window_bounds|k_summary" -s 10 -c 5 \
+    -k regex:"k_route_bin|k_prefill_select|k_window_bounds|k_summary|k_cells_finish|k_prefill_pass" -s 12 -c 7 \
     -o gpurun_out/${ROUND}_prefill python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-graph \
     --scenarios 2000 --pool-scenarios 64 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \

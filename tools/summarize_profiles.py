@@ -80,6 +80,30 @@ def rep_metrics(rep):
     return out
 
 
+def fp64_insts(rep, kernel):
+    """FP64-pipe warp instructions (DFMA/DMUL/DADD/DSETP executed) of the first captured launch
+    of `kernel`, summed from the report's per-SASS-instruction counts."""
+    raw = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kernel, "--page", "source", "--csv",
+                          "--print-source", "sass"], capture_output=True, text=True).stdout
+    lines = raw.splitlines()
+    heads = [i for i, ln in enumerate(lines) if ln.startswith('"Kernel Name"')]
+    if not heads:
+        return None
+    body = lines[heads[0] + 1:heads[1] if len(heads) > 1 else len(lines)]
+    rows = list(csv.reader(io.StringIO("\n".join(body))))
+    hdr = rows[0]
+    isrc, ie = hdr.index("Source"), hdr.index("Instructions Executed")
+    n = 0.0
+    for r in rows[1:]:
+        if len(r) <= ie:
+            continue
+        op = r[isrc].split()
+        op = (op[1] if op and op[0].startswith("@") and len(op) > 1 else (op[0] if op else ""))
+        if op.split(".")[0] in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX"):
+            n += float(r[ie] or 0)
+    return n
+
+
 def main(rnd):
     os.makedirs(PROF, exist_ok=True)
     launch_summary(rnd)
@@ -110,6 +134,11 @@ def main(rnd):
             rec["units"] = u
         traffic.setdefault(r["kernel"], rec)
     open(os.path.join(PROF, f"{rnd}_kernels.md"), "w").write("\n".join(lines) + "\n")
+    prep = os.path.join(OUT, f"{rnd}_prefill.ncu-rep")
+    for k in list(traffic):
+        if k.startswith("k_prefill_select") or k.startswith("k_route_bin"):
+            base = k.split("<")[0]
+            traffic[k]["fp64_insts"] = fp64_insts(prep, base) if os.path.exists(prep) else None
     json.dump(traffic, open(os.path.join(PROF, f"{rnd}_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
 
