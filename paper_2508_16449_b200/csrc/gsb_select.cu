@@ -357,33 +357,49 @@ __device__ __forceinline__ Part ld_part_cg(const Part* p) {  // L2 (written by o
 template <int C>
 __global__ void __launch_bounds__(32 * C)
 k_cells_finish(int64_t n_cells, const uint32_t* __restrict__ count, int16_t* __restrict__ f_idx,
-               double* __restrict__ energy, Part* __restrict__ parts, int64_t n_blocks) {
+               double* __restrict__ energy, Part* __restrict__ parts, int64_t n_blocks,
+               int early_fill) {
   constexpr int T = 32 * C;
   __shared__ Part sl[32][C];
   __shared__ Part s2[4][C];
   const int t = threadIdx.x, p = blockIdx.y;
-  gsb::grid_dep_wait();  // K2's results
-  gsb::grid_dep_launch();
   const int64_t base = static_cast<int64_t>(blockIdx.x) * T * kSumK;
   int16_t* fi = f_idx + p * n_cells;
   double* en = energy + p * n_cells;
-  Part a = part_identity();
+  // The empty cells' outputs need only K1's counts. early_fill: those were complete before K2
+  // started (K2 waits on K1 before it lets this grid launch), so they are written BEFORE the
+  // dependency wait and a programmatic launch overlaps them with K2's tail (K2 writes only the
+  // listed cells). The fused pass produces the counts in the primary kernel itself: no early fill.
+  if (!early_fill) gsb::grid_dep_wait();
+  uint32_t cnt[kSumK];
 #pragma unroll
   for (int k = 0; k < kSumK; ++k) {
     const int64_t cell = base + t + k * T;
-    if (cell >= n_cells) break;
-    if (count) {
-      if (count[cell] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
-        fi[cell] = -2;
-        en[cell] = 0.0;
-        continue;
-      }
-      if (parts) part_combine(a, part_of_cell(fi[cell], en[cell], cell));
-    } else if (parts) {
-      part_combine(a, part_of_cell(fi[cell], en[cell], cell));
+    cnt[k] = (count && cell < n_cells) ? __ldg(count + cell) : 1u;
+  }
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {
+    const int64_t cell = base + t + k * T;
+    if (cell < n_cells && cnt[k] == 0) {  // empty queue: no command (prefill_opt.cpp:64)
+      fi[cell] = -2;
+      en[cell] = 0.0;
     }
   }
+  gsb::grid_dep_launch();
+  gsb::grid_dep_wait();  // K2's results (also keeps this grid ordered after K2 when fill-only)
   if (!parts) return;
+  Part a = part_identity();
+  int16_t f[kSumK];
+  double e[kSumK];
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) {  // every load first, then the fold in cell order
+    const int64_t cell = base + t + k * T;
+    const bool live = cell < n_cells && cnt[k] != 0;
+    f[k] = live ? fi[cell] : int16_t{-2};
+    e[k] = live ? en[cell] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < kSumK; ++k) part_combine(a, part_of_cell(f[k], e[k], base + t + k * T));
   const int c = t % C, j = t / C;
   sl[j][c] = a;
   __syncthreads();
@@ -839,7 +855,7 @@ size_t finish_scratch_bytes(int P, int C, int64_t n_cells) {
 // k_cells_finish (+ k_summary_final when out != NULL) for a [P][n_cells] result.
 cudaError_t launch_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uint32_t* count,
                           int16_t* f_idx, double* energy, gsb_class_summary* out, Part* parts,
-                          cudaStream_t s) {
+                          cudaStream_t s, bool early_fill = true) {
   (void)ctx;
   const int64_t nb = finish_blocks(C, n_cells);
   if (nb > 65535LL * 1024) return cudaErrorInvalidValue;
@@ -851,7 +867,7 @@ cudaError_t launch_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uin
 #define GSB_FIN(CC)                                                                             \
   case CC:                                                                                    \
     e = gsb::launch_pdl(k_cells_finish<CC>, grid, dim3(32 * CC), 0, s, n_cells, count, f_idx,  \
-                        energy, pp, nb);                                                      \
+                        energy, pp, nb, early_fill ? 1 : 0);                                  \
     break;
       GSB_FIN(1) GSB_FIN(2) GSB_FIN(3) GSB_FIN(4) GSB_FIN(5) GSB_FIN(6) GSB_FIN(7) GSB_FIN(8)
 #undef GSB_FIN
@@ -879,8 +895,8 @@ int gsb_internal_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uint3
                         int16_t* f_idx, double* energy, gsb_class_summary* out, cudaStream_t s) {
   void* parts = out ? gsb_scratch(ctx, finish_scratch_bytes(P, C, n_cells)) : nullptr;
   if (out && !parts) return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass: scratch allocation failed");
-  if (launch_finish(ctx, P, C, n_cells, count, f_idx, energy, out, static_cast<Part*>(parts), s) !=
-      cudaSuccess)
+  if (launch_finish(ctx, P, C, n_cells, count, f_idx, energy, out, static_cast<Part*>(parts), s,
+                    /*early_fill=*/false) != cudaSuccess)
     return gsb_check_launch(ctx, "prefill_pass (finish)");
   return GSB_OK;
 }
