@@ -348,6 +348,18 @@ __device__ __forceinline__ void route_bin_tile(
         }
       }
       if (lane == 31) s.off[K] = incl;
+      if (lo.list && c1 == bG) {
+        // the counts are final after the last chunk's scan: publish this tile's non-empty cell
+        // count NOW, before the fold, so that successors' look-backs rarely wait on this tile
+        int ne = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int k = lane * E + e;
+          ne += (k < K && w_first + k / C < rp.n_windows && s.cnt[k] != 0) ? 1 : 0;
+        }
+        ne = __reduce_add_sync(kFull, static_cast<unsigned>(ne));
+        if (lane == 0) gsb::lookback_publish(lo.status, tile, epoch, ne);  // lane 0 = tid 0
+      }
     }
     __syncthreads();
     // ---- B: stable scatter of the stage indices by key (arrival order inside each key): the
@@ -423,8 +435,9 @@ __device__ __forceinline__ void route_bin_tile(
       wbase += k < wib ? s.lwarp[k] : 0;
       agg += s.lwarp[k];
     }
-    if (wib == 0) {
-      const long long excl = gsb::lookback_prefix(lo.status, tile, s.lepoch, agg);
+    if (wib == 0) {  // (the tile count was published after the last chunk's scan)
+      const long long excl = gsb::lookback_prefix(lo.status, tile, s.lepoch, agg,
+                                                  /*published=*/b0 < bG);
       if (lane == 0) s.lexcl = excl;
     }
     __syncthreads();
