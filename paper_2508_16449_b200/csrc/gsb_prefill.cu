@@ -50,67 +50,69 @@ __device__ __forceinline__ int64_t div_floor(int64_t a, int64_t d, double rd) {
 // first request of window k (arrivals are non-decreasing, trace.cpp:109-111). Request i owns
 // the entries k in (w(i-1), w(i)] (request 0 covers k <= w(0), a virtual request n the tail),
 // so every entry is written exactly once.
-// (Round 1 sampled one arrival per 32-request tile and resolved the edge tiles in a second
-// round: two dependent rounds of scattered 32-byte sectors, latency-bound at 7.4 us for C4.)
+// Lane l of a warp owns tile l of 32 requests. It reads only the LAST arrival of its tile (one
+// 32-byte sector per 32 requests) and takes the previous tile's from its neighbour: with sorted
+// arrivals a tile holds a window edge iff its two ends differ. The warp then resolves its edge
+// tiles cooperatively, up to four at a time: lane l loads element l of each of them (four
+// independent coalesced loads in flight), so a warp pays two dependent DRAM latencies in the
+// common case and the pass reads ~1/8 of the arrivals plus the edge tiles.
+constexpr int kBoundsTile = 32;
+constexpr int kBoundsBatch = 4;
 constexpr unsigned kFull = 0xffffffffu;
 
-// Streaming form (the one launched): thread g owns requests [8g, 8g + 8), read with four
-// coalesced 16-byte loads, and writes the entries k in (w(i-1), w(i)] of each of them; the
-// window of request 8g - 1 comes from the left neighbour lane (lane 0 loads it). One fully
-// coalesced read of the arrivals (24 MB at C4: ~3.7 us of HBM) replaces the sampled kernel's
-// two dependent rounds of scattered sectors (13.3 MB at 64 B granularity, latency-bound).
-constexpr int kBoundsPer = 8;
-
-__device__ __forceinline__ int64_t win_of(int64_t i, int64_t n, int64_t a, int64_t window_ms,
-                                          int64_t w0, int64_t n_windows, double rd) {
-  if (i >= n) return n_windows;  // the virtual request n
-  const int64_t w = div_floor(a, window_ms, rd) - w0;
-  return w < -1 ? -1 : (w > n_windows ? n_windows : w);
-}
-
 __global__ void __launch_bounds__(256)
-k_window_bounds_stream(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms,
-                       int64_t w0, int64_t n_windows, int64_t* __restrict__ bounds,
-                       unsigned* __restrict__ zero_words, int64_t n_zero) {
+k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms, int64_t w0,
+                int64_t n_windows, int64_t* __restrict__ bounds, unsigned* __restrict__ zero_words,
+                int64_t n_zero) {
   gsb::grid_dep_wait();    // the arrivals may come from the previous launch (e.g. a copy)
   gsb::grid_dep_launch();  // K1b may be scheduled now; it waits for this grid's bounds
+  // the fused pass's counters (tickets, per-chunk readiness) start every pass at zero
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_zero;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     zero_words[i] = 0;
   const double rd = 1.0 / static_cast<double>(window_ms);
   const int lane = threadIdx.x & 31;
-  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t i0 = g * kBoundsPer;  // lanes past n + 8 still join the shuffle below
-  int64_t a[kBoundsPer];
-  if (i0 + kBoundsPer <= n && (reinterpret_cast<uintptr_t>(arrival + i0) & 15) == 0) {
+  const int64_t span = ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) *
+                       (32 * kBoundsTile);
+  if (span > n) return;  // warp-uniform
+  auto win = [&](int64_t i) -> int64_t {
+    if (i < 0) return -1;
+    if (i >= n) return n_windows;
+    return div_floor(__ldg(arrival + i), window_ms, rd) - w0;
+  };
+  const int64_t t0 = span + static_cast<int64_t>(lane) * kBoundsTile;
+  const bool live = t0 <= n;
+  const int64_t wlast = live ? win(min(t0 + kBoundsTile - 1, n)) : 0;
+  int64_t wprev = __shfl_up_sync(kFull, wlast, 1);
+  if (lane == 0) wprev = win(t0 - 1);
+  unsigned edges = __ballot_sync(kFull, live && wlast != wprev);
+  while (edges) {
+    int src[kBoundsBatch];
+    int64_t a[kBoundsBatch];
 #pragma unroll
-    for (int k = 0; k < kBoundsPer / 2; ++k) {
-      const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(arrival + i0) + k);
-      a[2 * k] = v.x;
-      a[2 * k + 1] = v.y;
+    for (int k = 0; k < kBoundsBatch; ++k) {  // issue the batch's loads together
+      src[k] = edges ? __ffs(static_cast<int>(edges)) - 1 : -1;
+      edges &= edges - 1;
+      const int64_t i = span + static_cast<int64_t>(src[k]) * kBoundsTile + lane;
+      a[k] = (src[k] >= 0 && i < n) ? __ldg(arrival + i) : 0;
     }
-  } else {
 #pragma unroll
-    for (int k = 0; k < kBoundsPer; ++k) a[k] = i0 + k < n ? __ldg(arrival + i0 + k) : 0;
-  }
-  int64_t w[kBoundsPer];
-#pragma unroll
-  for (int k = 0; k < kBoundsPer; ++k) w[k] = win_of(i0 + k, n, a[k], window_ms, w0, n_windows, rd);
-  int64_t wp = __shfl_up_sync(kFull, w[kBoundsPer - 1], 1);
-  if (lane == 0 && i0 <= n)
-    wp = i0 == 0 ? -1 : win_of(i0 - 1, n, __ldg(arrival + i0 - 1), window_ms, w0, n_windows, rd);
-  if (i0 > n) return;
-#pragma unroll
-  for (int k = 0; k < kBoundsPer; ++k) {
-    const int64_t i = i0 + k;
-    if (i > n) break;
-    const int64_t hi = min(w[k], n_windows);
-    for (int64_t e = max(wp + 1, int64_t{0}); e <= hi; ++e) bounds[e] = i;
-    wp = w[k];
+    for (int k = 0; k < kBoundsBatch; ++k) {
+      if (src[k] < 0) break;  // warp-uniform
+      const int64_t wp0 = __shfl_sync(kFull, wprev, src[k]);
+      const int64_t i = span + static_cast<int64_t>(src[k]) * kBoundsTile + lane;
+      const int64_t wi = i < n ? div_floor(a[k], window_ms, rd) - w0 : n_windows;
+      int64_t wp = __shfl_up_sync(kFull, wi, 1);
+      if (lane == 0) wp = wp0;
+      if (i <= n && wi != wp) {
+        const int64_t hi = min(wi, n_windows);
+        for (int64_t k2 = max(wp + 1, int64_t{0}); k2 <= hi; ++k2) bounds[k2] = i;
+      }
+    }
   }
 }
 
-// classify(), router.cpp:26-31: number of thresholds strictly below the prompt.// classify(), router.cpp:26-31: number of thresholds strictly below the prompt. The thresholds
+// classify(), router.cpp:26-31: number of thresholds strictly below the prompt. The thresholds
 // are ascending and distinct (RoutingConfig::validate, router.cpp:7-11, checked host-side) and
 // padded with INT_MAX, so the count is a branch-free binary search: ceil(log2 C) compares on
 // thresholds held in registers.
@@ -801,12 +803,11 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   if (!ctx) return GSB_INVALID_ARGUMENT;
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
-  const int64_t threads = n_req / kBoundsPer + 1;  // request n (virtual) included
-  const int64_t blocks = (threads + 255) / 256;
-  k_window_bounds_stream<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
-                           gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms,
-                                                           cfg->w0, cfg->n_windows, d_bounds,
-                                                           nullptr, 0);
+  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
+  const int64_t blocks = (warps + 7) / 8;
+  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
+                    gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms, cfg->w0,
+                                                    cfg->n_windows, d_bounds, nullptr, 0);
   return gsb_check_launch(ctx, "window_bounds");
 }
 
@@ -914,9 +915,9 @@ int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
   PassHdr* ph = reinterpret_cast<PassHdr*>(sy + 256);
   unsigned* ready = reinterpret_cast<unsigned*>(sy + o_rd);
   // K1a (window bounds), which also zeroes the pass header and the readiness counters
-  const int64_t threads = n_req / kBoundsPer + 1;
-  const int64_t blocks = (threads + 255) / 256;
-  k_window_bounds_stream<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, s>>>(
+  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
+  const int64_t blocks = (warps + 7) / 8;
+  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, s>>>(
       d_arrival, n_req, rcfg->window_ms, rcfg->w0, rcfg->n_windows, d_bounds,
       reinterpret_cast<unsigned*>(ph), static_cast<int64_t>((o_st - 256) / sizeof(unsigned)));
   RouteParams rp = make_route_params(ctx, rcfg);
