@@ -26,6 +26,7 @@
 // Per-worker state lives in shared memory; the FIFO of waiting requests in a global
 // workspace slot owned by the warp (persistent grid, scenarios claimed by atomic counter).
 #include <cmath>
+#include <cstdlib>
 
 #include "gsb_common.cuh"
 #include "gsb_ctl.cuh"
@@ -52,9 +53,14 @@ struct PoolParams {
   gsb_pool_stream st;
   gsb_pool_args a;
   int W, MB, RC, TC;
+  int RC_full;          // TBT run capacity the configuration needs (max tbt_window_tokens)
   int64_t warp_bytes;
   int32_t* ws_pending;  // [n_warps][W][pending_cap]
   unsigned* counter;
+  unsigned* rerun_n;         // scenarios whose TBT runs outgrew RC < RC_full ...
+  uint32_t* rerun_list;      // ... replayed again by a second launch with RC = RC_full
+  const uint32_t* list_in;   // second launch: the scenarios to replay (count *list_n)
+  const unsigned* list_n;
 };
 
 // shared-memory carve-up of one warp's region
@@ -201,7 +207,8 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   const double end_floor = st.d_end_floor_ms ? st.d_end_floor_ms[sid] : 0.0;
   const double tbt_thr = cfg.tbt_p95_ms;
   int status = 0;
-  if (ccfg.tbt_window_tokens > RC) status |= ST_TBT;
+  if (ccfg.tbt_window_tokens > P.RC_full) status |= ST_TBT;
+  bool runs_full = false;  // lane ww: the run ring (RC < RC_full) could not take a new run
 
   // controller (lane w), DecodeController ctor (decode_ctl.cpp:130-140)
   double f_opt[GSB_MAX_BUCKETS];
@@ -459,13 +466,17 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
             }
           }
           const int g = min(g_total, tbt_cap);
-          int pos = wk.r_head + wk.r_n;
-          if (pos >= RC) pos -= RC;
-          s.rv[w * RC + pos] = gap;
-          s.rc[w * RC + pos] = static_cast<uint16_t>(g);
-          ++wk.r_n;
-          wk.r_total += g;
-          wk.p95_valid = false;
+          if (wk.r_n >= RC) {
+            runs_full = true;  // only when RC < tbt_cap: the scenario is replayed with RC_full
+          } else {
+            int pos = wk.r_head + wk.r_n;
+            if (pos >= RC) pos -= RC;
+            s.rv[w * RC + pos] = gap;
+            s.rc[w * RC + pos] = static_cast<uint16_t>(g);
+            ++wk.r_n;
+            wk.r_total += g;
+            wk.p95_valid = false;
+          }
         }
         // TpsWindow::record (decode_ctl.hpp:73); unobservable once no coarse tick is left
         if (!coarse_on) {
@@ -480,6 +491,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
         }
       }
       n_done += n_fin;
+      if (__shfl_sync(kFull, static_cast<int>(runs_full), ww)) break;
       __syncwarp();
       start_step(ww, now);
     } else if (kind == K_ENQ) {
@@ -603,6 +615,10 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
     __syncwarp();
   }
 
+  if (__any_sync(kFull, runs_full)) {  // hand the scenario to the full-capacity launch
+    if (lane == 0) P.rerun_list[atomicAdd(P.rerun_n, 1u)] = static_cast<uint32_t>(n);
+    return;
+  }
   // ---- finalize (simkernel.cpp:503-520) and the summary
   double end = std_max(end_floor, max_finish);
   end = std_max(end, is_w ? wk.last_applied : 0.0);
@@ -668,7 +684,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
 }
 
 template <bool REQ_OUT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_decode_pool(const __grid_constant__ PoolParams P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_decode_pool(const __grid_constant__ PoolParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -677,7 +693,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_decode_pool(const __gri
   int32_t* pend = P.ws_pending + slot * P.W * P.cfg.pending_cap;
   for (;;) {
     unsigned n = 0;
-    if (lane == 0) n = atomicAdd(P.counter, 1u);
+    if (lane == 0) {
+      n = atomicAdd(P.counter, 1u);
+      if (P.list_in) n = n < *P.list_n ? P.list_in[n] : 0xffffffffu;
+    }
     n = __shfl_sync(kFull, n, 0);
     if (n >= P.a.n_scen) break;
     run_scenario<REQ_OUT>(P, s, pend, static_cast<int64_t>(n), lane);
@@ -728,32 +747,64 @@ int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* c
   P.a = *a;
   P.W = W;
   P.MB = MB;
-  P.RC = cfg->tbt_cap;
+  P.RC_full = cfg->tbt_cap;
   P.TC = cfg->tps_cap;
-  P.warp_bytes = smem_bytes(W, MB, P.RC, P.TC);
-  const int64_t block_smem = P.warp_bytes * kWarpsPerBlock;
-  if (block_smem > 227 * 1024)
-    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
   auto kern = req_out ? k_decode_pool<true> : k_decode_pool<false>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(block_smem)) != cudaSuccess)
-    return gsb_check_launch(ctx, "decode_pool attr");
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarpsPerBlock * 32,
-                                                static_cast<size_t>(block_smem));
-  if (per_sm < 1) per_sm = 1;
-  int64_t blocks = static_cast<int64_t>(ctx->n_sms) * per_sm;
+  // First launch: a TBT run ring of at most kFastRuns runs per worker (a run is one step's
+  // equal gaps, so a 256-token window rarely holds more than a few dozen), which keeps four
+  // 4-scenario CTAs resident per SM; the scenarios whose ring fills are replayed by a second
+  // launch with the full capacity (runs <= tokens <= tbt_cap). Both launches are always
+  // enqueued (graph-capturable); the second exits at once when nothing overflowed.
+  int fast_runs = 128;
+  if (const char* e = std::getenv("GSB_POOL_RUN_CAP")) fast_runs = std::atoi(e);  // tests
+  if (fast_runs < 1) fast_runs = 1;
+  const int RC1 = fast_runs < P.RC_full ? fast_runs : P.RC_full;
+  const int RC2 = P.RC_full;
+  int per_sm[2] = {0, 0};
+  int64_t warp_bytes[2];
+  for (int i = 0; i < 2; ++i) {
+    warp_bytes[i] = smem_bytes(W, MB, i == 0 ? RC1 : RC2, P.TC);
+    const int64_t block_smem = warp_bytes[i] * kWarpsPerBlock;
+    if (block_smem > 227 * 1024)
+      return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(warp_bytes[1] * kWarpsPerBlock)) != cudaSuccess)
+      return gsb_check_launch(ctx, "decode_pool attr");
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[i], kern, kWarpsPerBlock * 32,
+                                                  static_cast<size_t>(block_smem));
+    if (per_sm[i] < 1) per_sm[i] = 1;
+  }
   const int64_t need = (a->n_scen + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  int64_t blocks = static_cast<int64_t>(ctx->n_sms) * per_sm[0];
   if (blocks > need) blocks = need;
+  int64_t blocks2 = static_cast<int64_t>(ctx->n_sms) * per_sm[1];
+  if (blocks2 > blocks) blocks2 = blocks;
   const int64_t ws_ints = blocks * kWarpsPerBlock * W * static_cast<int64_t>(cfg->pending_cap);
-  const size_t bytes = 256 + static_cast<size_t>(ws_ints) * 4;
+  const size_t bytes = 256 + static_cast<size_t>(ws_ints) * 4 + static_cast<size_t>(a->n_scen) * 4;
   char* scratch = static_cast<char*>(gsb_scratch(ctx, bytes));
   if (!scratch) return gsb_set_error(ctx, GSB_CUDA_ERROR, "decode pool: workspace allocation failed");
-  P.counter = reinterpret_cast<unsigned*>(scratch);
+  unsigned* hdr = reinterpret_cast<unsigned*>(scratch);  // [0] claims, [1] replay claims, [2] replays
   P.ws_pending = reinterpret_cast<int32_t*>(scratch + 256);
+  uint32_t* list = reinterpret_cast<uint32_t*>(scratch + 256 + ws_ints * 4);
   cudaStream_t s = gsb_pick_stream(ctx, stream);
-  cudaMemsetAsync(P.counter, 0, sizeof(unsigned), s);
-  kern<<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, static_cast<size_t>(block_smem), s>>>(P);
+  cudaMemsetAsync(hdr, 0, 4 * sizeof(unsigned), s);
+  P.rerun_n = hdr + 2;
+  P.rerun_list = list;
+  P.RC = RC1;
+  P.warp_bytes = warp_bytes[0];
+  P.counter = hdr;
+  P.list_in = nullptr;
+  P.list_n = nullptr;
+  kern<<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32,
+         static_cast<size_t>(warp_bytes[0] * kWarpsPerBlock), s>>>(P);
+  if (RC1 == RC2) return gsb_check_launch(ctx, "decode_pool");
+  P.RC = RC2;
+  P.warp_bytes = warp_bytes[1];
+  P.counter = hdr + 1;
+  P.list_in = list;
+  P.list_n = hdr + 2;
+  kern<<<static_cast<unsigned>(blocks2), kWarpsPerBlock * 32,
+         static_cast<size_t>(warp_bytes[1] * kWarpsPerBlock), s>>>(P);
   return gsb_check_launch(ctx, "decode_pool");
 }
 
