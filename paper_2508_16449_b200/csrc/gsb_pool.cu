@@ -762,14 +762,15 @@ int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* c
   const int RC2 = P.RC_full;
   int per_sm[2] = {0, 0};
   int64_t warp_bytes[2];
+  warp_bytes[0] = smem_bytes(W, MB, RC1, P.TC);
+  warp_bytes[1] = smem_bytes(W, MB, RC2, P.TC);
+  if (warp_bytes[1] * kWarpsPerBlock > 227 * 1024)
+    return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(warp_bytes[1] * kWarpsPerBlock)) != cudaSuccess)
+    return gsb_check_launch(ctx, "decode_pool attr");
   for (int i = 0; i < 2; ++i) {
-    warp_bytes[i] = smem_bytes(W, MB, i == 0 ? RC1 : RC2, P.TC);
     const int64_t block_smem = warp_bytes[i] * kWarpsPerBlock;
-    if (block_smem > 227 * 1024)
-      return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(warp_bytes[1] * kWarpsPerBlock)) != cudaSuccess)
-      return gsb_check_launch(ctx, "decode_pool attr");
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[i], kern, kWarpsPerBlock * 32,
                                                   static_cast<size_t>(block_smem));
     if (per_sm[i] < 1) per_sm[i] = 1;
