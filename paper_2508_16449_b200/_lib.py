@@ -6,7 +6,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgsb.so")
+# GSB_LIB: another build of the same library (tools/ A/B timing of two kernel variants)
+LIB_PATH = os.environ.get("GSB_LIB") or os.path.join(HERE, "lib", "libgsb.so")
 
 _d, _i32, _i64, _u64, _p = C.c_double, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
 

@@ -104,6 +104,39 @@ def test_route_bin_matches_oracle(eng, restate, thr, P, qps, wms, want_deadline)
     eng.set_profiles([api.GpuProfile.default_profile()])
 
 
+@pytest.mark.parametrize("want_deadline", [False, True])
+def test_route_bin_wide_prompts(eng, restate, want_deadline):
+    """K1b's fold reads 16-bit prompts straight from the sorted list when every prompt of a
+    staging chunk fits 16 bits, else through stage indices: windows mixing both kinds (prompts
+    up to INT32_MAX, zero and negative) must give the same bits as the oracle."""
+    api = _api()
+    profs = synth_profiles(api)[:4]
+    eng.set_profiles(profs)
+    a, p, _ = restate.gen_poisson_trace(5.0, 1_800_000, 768.0, 3072.0, 0.15, 128.0, seed=5)
+    rng = np.random.default_rng(5)
+    wms = 60_000
+    w = a // wms
+    wide = (w % 3) == 1  # every third window: some prompts beyond 16 bits
+    pick = wide & (rng.random(len(p)) < 0.2)
+    p = p.copy()
+    p[pick] = rng.integers(65_536, 2**31 - 1, int(pick.sum()))
+    p[wide & (rng.random(len(p)) < 0.05)] = 65_535
+    neg = (w % 3 == 2) & (rng.random(len(p)) < 0.02)
+    p[neg] = rng.integers(-(2**31), 1, int(neg.sum()))
+    thr = [128, 256, 512, 768, 1024, 2048, 4096]
+    nw = int(a[-1] // wms) + 1
+    rr = eng.route_bin(a, p, api.RoutingConfig(True, thr, list(range(len(thr) + 1))), wms, 0, nw,
+                       want_deadline=want_deadline)
+    torch.cuda.synchronize()
+    cls, cnt, tref, mdl, _ = restate.route_bin(a, p, thr, wms, 0, nw, [to_oracle(x) for x in profs])
+    np.testing.assert_array_equal(rr.cls.cpu().numpy(), cls)
+    np.testing.assert_array_equal(rr.count.cpu().numpy().view(np.uint32), cnt)
+    np.testing.assert_array_equal(u64(rr.t_ref.cpu().numpy()), u64(tref))
+    if want_deadline:
+        np.testing.assert_array_equal(u64(rr.min_deadline.cpu().numpy()), u64(mdl))
+    eng.set_profiles([api.GpuProfile.default_profile()])
+
+
 def test_route_bin_edges(eng, restate):
     """empty windows, a window offset (w0), requests outside the range, routing disabled."""
     api = _api()
