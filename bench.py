@@ -192,13 +192,23 @@ def run_gsb(args, rank, world, dist):
         for _ in range(2):
             prefill_step()
         torch.cuda.synchronize()
+        # timing events INSIDE the graph (external event-record nodes): the step's device time
+        # from its first kernel to its last, without the host's graph-launch latency that an
+        # event recorded before replay() also counts (kept as ms_per_step_replay)
+        g_e0 = torch.cuda.Event(enable_timing=True, external=True)
+        g_e1 = torch.cuda.Event(enable_timing=True, external=True)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
+            g_e0.record()
             prefill_step()
+            g_e1.record()
         graphs["prefill"] = g
 
     def run_prefill(timed_steps, warm):
-        t_step, t_k1, t_k2 = [], [], []
+        """per step: L2 flush (outside the timing), the step; returns (device ms from the
+        step's first to last kernel (+ the all-gather when world > 1), ms from an event
+        recorded before replay())"""
+        t_dev, t_rep = [], []
         for i in range(warm + timed_steps):
             flush.zero_()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -210,41 +220,57 @@ def run_gsb(args, rank, world, dist):
             if world > 1:
                 dist.all_gather_into_tensor(gathered, summ)
             s1.record(stream)
+            torch.cuda.synchronize()  # the in-graph events are re-recorded by the next replay
             if i >= warm:
-                t_step.append((s0, s1))
-        torch.cuda.synchronize()
-        return [a.elapsed_time(b) for a, b in t_step]
+                t_rep.append(s0.elapsed_time(s1))
+                if use_graph:
+                    t_dev.append(g_e0.elapsed_time(s1 if world > 1 else g_e1))
+                else:
+                    t_dev.append(s0.elapsed_time(s1))
+        return t_dev, t_rep
 
     def graph_of(fn):
-        fn()
+        """a graph of [L2 flush, fn]"""
+        if fn is not None:
+            fn()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn()
+            flush.zero_()
+            if fn is not None:
+                fn()
         return g
 
-    def graph_ms(g, n=10):
-        """mean device time of one replay, L2 flushed before each (no host launch gaps)"""
-        ts = []
-        for _ in range(n + 2):
-            flush.zero_()
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
+    def graph_ms(g, n=40):
+        """mean device time of one replay over n back-to-back replays (one event pair: the
+        per-replay launch latency overlaps, and the 2-us event granularity averages out)"""
+        for _ in range(3):
             g.replay()
-            s1.record(stream)
-            ts.append((s0, s1))
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(n):
+            g.replay()
+        s1.record(stream)
         torch.cuda.synchronize()
-        return statistics.mean(a.elapsed_time(b) for a, b in ts[2:])
+        return s0.elapsed_time(s1) / n
 
-    # per-kernel split of the two-call path: K1 alone and K1 + K2 as CUDA graphs, K2 = the
-    # difference (device time only; eager events would include host launch gaps); and the
-    # fused pass alone
-    def kernel_split(n=10):
+    # per-kernel split of the two-call path by graph differencing: [flush, K1], [flush, K1,
+    # K2 (+ its empty-cell fill)], [flush, K1, K2, finish, summary] and the fused pass, each
+    # minus [flush] (tools/k_ab.py resolves 0.1 us this way)
+    def kernel_split(n=40, reps=3):
+        g0 = graph_of(None)
         g1 = graph_of(lambda: eng.route_bin(d_arr, d_prm, routing, wms, w0, nW, out=rr))
+        g12k = graph_of(lambda: (eng.route_bin(d_arr, d_prm, routing, wms, w0, nW, out=rr),
+                                 eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D,
+                                                    out=sel)))
         g12 = graph_of(prefill_step)
         gp = graph_of(fused_step)
-        k1 = graph_ms(g1, n)
-        return k1, max(graph_ms(g12, n) - k1, 1e-6), graph_ms(gp, n)
+        res = []
+        for _ in range(reps):
+            t0 = graph_ms(g0, n)
+            res.append([graph_ms(g, n) - t0 for g in (g1, g12k, g12, gp)])
+        k1, k12k, k12, kp = (statistics.median(r[i] for r in res) for i in range(4))
+        return k1, max(k12k - k1, 1e-6), max(k12 - k1, 1e-6), kp
 
     # ---------------- decode leg setup
     T_END = 150_000.0
@@ -288,7 +314,8 @@ def run_gsb(args, rank, world, dist):
         ga = graph_of(lambda: eng.window_series(tel, 256, 20.0, 200.0, T_END, dev=tdev,
                                                 out=(has, p95, tps)))
         gb = graph_of(lambda: eng.run_replay(plan))
-        return graph_ms(ga, n), graph_ms(gb, n)
+        t0 = graph_ms(graph_of(None), n)
+        return graph_ms(ga, n) - t0, graph_ms(gb, n) - t0
 
     # ---------------- closed-loop decode pool leg (K5): C3 sinusoid, controller sweep
     pa, pp, po = wl.sinusoid_decode_trace(1500.0, 1000.0, 120_000.0, 150_000, seed=11 + rank)
@@ -388,7 +415,7 @@ def run_gsb(args, rank, world, dist):
     # ---------------- timed region
     with ClockSampler(dev) as clk:
         barrier()
-        pre_ms = run_prefill(args.steps, args.warmup)
+        pre_ms, pre_rep_ms = run_prefill(args.steps, args.warmup)
         barrier()
         dec_ms = run_decode(args.steps, max(3, args.warmup // 2))
         barrier()
@@ -398,7 +425,7 @@ def run_gsb(args, rank, world, dist):
         barrier()
         ing_ms = run_ingest(max(3, args.steps // 4), 3)
         barrier()
-    k1_ms, k2_ms, pass_ms = kernel_split()
+    k1_ms, k2_ms, k2_full_ms, pass_ms = kernel_split()
     k3a_ms, k3b_ms = decode_split()
 
     def max_over_ranks(x):
@@ -409,6 +436,7 @@ def run_gsb(args, rank, world, dist):
         return float(t.item())
 
     ms_pre = max_over_ranks(statistics.mean(pre_ms))
+    ms_pre_rep = max_over_ranks(statistics.mean(pre_rep_ms))
     ms_dec = max_over_ranks(statistics.mean(dec_ms))
     ms_e2e = max_over_ranks(statistics.mean(e2e_ms))
     ms_pool = max_over_ranks(statistics.mean(pool_ms))
@@ -458,6 +486,7 @@ def run_gsb(args, rank, world, dist):
     prof_json = committed_profile()
     evaluated = pairs_rank[0] * 81
     k2_tflops = evaluated * K2_DP_OPS_PER_EVAL * 2 / (k2_ms / 1e3) / 1e12
+    k2_full_tflops = evaluated * K2_DP_OPS_PER_EVAL * 2 / (k2_full_ms / 1e3) / 1e12
     pass_tflops = ((evaluated * K2_DP_OPS_PER_EVAL + n_req * P * K1_DP_OPS_PER_REQ_PROFILE) * 2
                    / (pass_ms / 1e3) / 1e12)
     peak_tflops = dfma_per_s * 2 / 1e12
@@ -492,6 +521,10 @@ def run_gsb(args, rank, world, dist):
         "unit": "window x class x clock evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_pre,
+        "ms_per_step_replay": ms_pre_rep,
+        "timing": "events inside the step's CUDA graph (first to last kernel; the all-gather "
+                  "too when N > 1); ms_per_step_replay: an event recorded before replay(), i.e. "
+                  "plus the host's graph-launch latency",
         "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference-shaped Poisson/bimodal traces; sinusoidal decode telemetry)",
@@ -511,14 +544,16 @@ def run_gsb(args, rank, world, dist):
         "e2e": {"value": evaluated_all / (ms_e2e / 1e3), "unit": "window x class x clock evals/s",
                 "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "Engine.route_bin/prefill_select from pinned host buffers"},
-        "roofline": {"bound": "fp64", "kernel": "k_prefill_select_list (K2) + k_cells_finish + "
-                                                "k_summary_final",
+        "roofline": {"bound": "fp64", "kernel": "k_prefill_select_list (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,
                      "basis": f"{K2_DP_OPS_PER_EVAL} DP instr per evaluated triple x 2 vs DFMA "
-                              "rate measured in this run; K2 time = graph(K1+K2) - graph(K1), "
-                              "incl. the per-class summary",
+                              "rate measured in this run; K2 time = graph(K1 + K2 + its "
+                              "empty-cell fill) - graph(K1), 40 back-to-back replays each",
                      "kernel_ms": k2_ms, "share_of_step": k2_ms / ms_pre,
+                     "with_finish_summary": {"kernel_ms": k2_full_ms,
+                                             "achieved": k2_full_tflops,
+                                             "frac": k2_full_tflops / peak_tflops},
                      "traffic": prof_json.get("_k2_dram"),
                      "fp64_warp_insts_ncu": prof_json.get("_k2_fp64_insts")},
         "roofline_pass": {"bound": "fp64", "kernel": "gsb_prefill_pass: K1a, k_prefill_pass "
