@@ -466,7 +466,15 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
             }
           }
           const int g = min(g_total, tbt_cap);
-          if (wk.r_n >= RC) {
+          int last = wk.r_head + wk.r_n - 1;
+          if (last >= RC) last -= RC;
+          if (wk.r_n > 0 && s.rv[w * RC + last] == gap) {
+            // the same gap as the newest run (same batch and clock): one run (the P95 only
+            // sees the multiset of gaps)
+            s.rc[w * RC + last] = static_cast<uint16_t>(s.rc[w * RC + last] + g);
+            wk.r_total += g;
+            wk.p95_valid = false;
+          } else if (wk.r_n >= RC) {
             runs_full = true;  // only when RC < tbt_cap: the scenario is replayed with RC_full
           } else {
             int pos = wk.r_head + wk.r_n;
@@ -750,12 +758,15 @@ int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* c
   P.RC_full = cfg->tbt_cap;
   P.TC = cfg->tps_cap;
   auto kern = req_out ? k_decode_pool<true> : k_decode_pool<false>;
-  // First launch: a TBT run ring of at most kFastRuns runs per worker (a run is one step's
-  // equal gaps, so a 256-token window rarely holds more than a few dozen), which keeps four
-  // 4-scenario CTAs resident per SM; the scenarios whose ring fills are replayed by a second
-  // launch with the full capacity (runs <= tokens <= tbt_cap). Both launches are always
-  // enqueued (graph-capturable); the second exits at once when nothing overflowed.
-  int fast_runs = 128;
+  // First launch: a TBT run ring of at most 32 runs per worker (a run is the equal gaps of
+  // consecutive steps with the same gap, so a 256-token window rarely holds more than a few),
+  // which keeps four 4-scenario CTAs resident per SM (the 128-register bound; 5 or 6 CTAs
+  // spill 0.5-0.8 KB and ran 27-42% slower) with the smallest shared-memory carve-out; the
+  // scenarios whose ring fills are replayed by a second launch with the full capacity
+  // (runs <= tokens <= tbt_cap). Both launches are always enqueued (graph-capturable); the
+  // second exits at once when nothing overflowed. Pool rate by first-launch ring (runs merged):
+  // 256: 6.5e4/s (3 CTAs/SM), 128: 7.8e4, 96-32: 8.1-8.2e4 (tools/k5_runcap_sweep.sh).
+  int fast_runs = 32;
   if (const char* e = std::getenv("GSB_POOL_RUN_CAP")) fast_runs = std::atoi(e);  // tests
   if (fast_runs < 1) fast_runs = 1;
   const int RC1 = fast_runs < P.RC_full ? fast_runs : P.RC_full;
