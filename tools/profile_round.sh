@@ -25,7 +25,7 @@ ncu --set full --clock-control none --import-source on \
     -o gpurun_out/${ROUND}_decode python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-graph \
     --scenarios ${DEC_SCEN} --pool-scenarios 64 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_decode_pool" -s 1 -c 1 \
+    -k regex:"k_decode_pool" -s 2 -c 2 \
     -o gpurun_out/${ROUND}_pool python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-graph \
     --scenarios 2000 --pool-scenarios ${POOL_SCEN} > /dev/null 2>&1
 ls -la gpurun_out/${ROUND}_*
