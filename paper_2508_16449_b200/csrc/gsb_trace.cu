@@ -34,15 +34,28 @@ constexpr int kTrThreads = 256;
 constexpr int kPerThread = 64;  // parse: bytes per thread (four 16-byte groups)
 constexpr int kTile = kTrThreads * kPerThread;  // 8 KB
 constexpr int kPre = 256;        // bytes staged before the tile (line starts)
+constexpr int kMaxLines = 1024;  // listed lines per tile (a denser tile parses in place)
 constexpr unsigned long long kNoErr = ~0ull;
 
 struct TraceParams {
   const unsigned char* bytes;
   int64_t n;
   int64_t n_tiles;
-  int64_t header_end;  // position of line 0's end
+  int64_t header_end;  // position of line 0's end (host-side uses; kernels read ParseState)
   int32_t has_class;
   int32_t threshold;
+  int64_t cap_rows;    // rows >= cap_rows are not written (the host reports the overflow)
+};
+
+// Written on the device by k_csv_header and read back ONCE at the end of gsb_trace_parse (the
+// header check, the row count and the first error all come back in one copy).
+struct ParseState {
+  int64_t header_end;  // line 0's end
+  int64_t n_rows;      // non-empty lines after the header
+  int64_t last_arrival;
+  unsigned long long err;  // (row << 4 | check), ~0: none
+  int32_t hdr;         // 3 / 4: a recognised header with that many columns; 0: unrecognised
+  int32_t pad;
 };
 
 __device__ __forceinline__ unsigned char byte_at(const unsigned char* __restrict__ b, int64_t n,
@@ -213,15 +226,23 @@ __device__ __forceinline__ unsigned long long err_key(int64_t line, int detail) 
 }
 
 __global__ void __launch_bounds__(kTrThreads)
-k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pref,
+k_csv_parse(TraceParams tp, const unsigned long long* __restrict__ tile_pref,
             int64_t* __restrict__ arrival, int32_t* __restrict__ prompt,
             int32_t* __restrict__ output, uint8_t* __restrict__ slo_cls,
-            uint32_t* __restrict__ line_of_row, unsigned long long* __restrict__ err) {
+            uint32_t* __restrict__ line_of_row, ParseState* __restrict__ ps) {
+  const int hdr = ps->hdr;
+  if (hdr == 0) return;  // unrecognised header: nothing is parsed (the host reports it)
+  tp.has_class = hdr == 4 ? 1 : 0;
+  tp.header_end = ps->header_end;
+  unsigned long long* err = &ps->err;
   __shared__ __align__(16) unsigned char sm[kTile + kPre + 16];
   using BS = cub::BlockScan<unsigned long long, kTrThreads>;
   using BS2 = cub::BlockScan<long long, kTrThreads>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ typename BS2::TempStorage tmp2;
+  __shared__ int64_t s_st[kMaxLines];  // the tile's non-empty lines: start, end (tile-relative),
+  __shared__ int32_t s_b[kMaxLines];   // line index (tile-relative)
+  __shared__ int32_t s_ln[kMaxLines];
   const int64_t t = blockIdx.x;
   stage_tile(tp, t, sm);
   __syncthreads();
@@ -237,8 +258,8 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
     nonempty |= static_cast<unsigned long long>(ne16) << (16 * h);
   }
   const unsigned nl = __popcll(ends), ne = __popcll(nonempty);
-  unsigned long long pre;
-  BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre);
+  unsigned long long pre, agg;
+  BS(tmp).ExclusiveSum((static_cast<unsigned long long>(nl) << 32) | ne, pre, agg);
   __syncthreads();
   // the previous line end before this thread's bytes: exclusive max-scan of the threads' last
   // ends; the tile's first line looks back into the previous tile (one thread per tile)
@@ -260,18 +281,11 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
     }
     prev = st;  // -1 at the file start
   }
-  while (ends) {
-    const int k = __ffsll(static_cast<long long>(ends)) - 1;
-    ends &= ends - 1ull;
-    const int64_t b = b0 + k;
-    const int64_t st = prev + 1;
-    prev = b;
-    const bool ne_line = (nonempty >> k) & 1ull;
-    const int64_t my_line = line++;
-    if (!ne_line) continue;  // empty line: skipped (the row counter still advanced)
-    const int64_t ne_idx = nonempty_before++;
-    if (b <= tp.header_end) continue;  // the header
-    const int64_t row = ne_idx - 1;    // the header is the first non-empty line
+  // one non-empty line [st, b) (st may precede the staged bytes): fields, checks, outputs
+  auto parse_one = [&](const int64_t st, const int64_t b, const int64_t my_line,
+                       const int64_t ne_idx) {
+    if (b <= tp.header_end) return;  // the header
+    const int64_t row = ne_idx - 1;  // the header is the first non-empty line
     const bool in_sm = st >= s0;
     auto at = [&](int64_t i) -> unsigned char { return in_sm ? sm[i - s0] : __ldg(tp.bytes + i); };
     int64_t en = b;
@@ -417,41 +431,101 @@ k_csv_parse(const TraceParams tp, const unsigned long long* __restrict__ tile_pr
       else if (fc != cls)
         detail = GSB_TRACE_DETAIL_MISMATCH;
     }
+    if (row >= tp.cap_rows) return;  // more rows than the caller's buffers: reported
     arrival[row] = a;
     prompt[row] = pi;
     output[row] = oi;
     slo_cls[row] = cls;
     line_of_row[row] = static_cast<uint32_t>(my_line);
     if (detail) atomicMin(err, err_key(my_line, detail));
+  };
+  const int64_t line0 = static_cast<int64_t>(tp0 >> 32);
+  const int64_t ne0 = static_cast<int64_t>(tp0 & 0xffffffffull);
+  const int n_ne = static_cast<int>(agg & 0xffffffffull);
+  if (n_ne <= kMaxLines) {
+    // the tile's non-empty lines listed in order, then parsed round-robin: every thread gets
+    // the same number of lines (+-1) instead of the lines ending in its own 64 bytes
+    int idx = static_cast<int>(pre & 0xffffffffull);
+    while (ends) {
+      const int k = __ffsll(static_cast<long long>(ends)) - 1;
+      ends &= ends - 1ull;
+      const int64_t b = b0 + k;
+      const int64_t st = prev + 1;
+      prev = b;
+      const int64_t my_line = line++;
+      if (!((nonempty >> k) & 1ull)) continue;  // empty line: skipped (still counted)
+      s_st[idx] = st;
+      s_b[idx] = static_cast<int32_t>(b - s0);
+      s_ln[idx] = static_cast<int32_t>(my_line - line0);
+      ++idx;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_ne; i += kTrThreads)
+      parse_one(s_st[i], s0 + s_b[i], line0 + s_ln[i], ne0 + i);
+  } else {
+    while (ends) {
+      const int k = __ffsll(static_cast<long long>(ends)) - 1;
+      ends &= ends - 1ull;
+      const int64_t b = b0 + k;
+      const int64_t st = prev + 1;
+      prev = b;
+      const int64_t my_line = line++;
+      if (!((nonempty >> k) & 1ull)) continue;  // empty line: skipped (still counted)
+      parse_one(st, b, my_line, nonempty_before++);
+    }
   }
 }
 
 // trace.cpp:108-111: arrivals non-decreasing (checked after the range checks of the same row)
-__global__ void k_csv_monotone(int64_t n_rows, const int64_t* __restrict__ arrival,
-                               const uint32_t* __restrict__ line_of_row,
-                               unsigned long long* __restrict__ err) {
-  const int64_t r = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (r >= n_rows) return;
-  if (arrival[r] < arrival[r - 1]) atomicMin(err, err_key(line_of_row[r], GSB_TRACE_DETAIL_MONOTONE));
+__global__ void k_csv_monotone(const int64_t* __restrict__ arrival,
+                               const uint32_t* __restrict__ line_of_row, int64_t cap_rows,
+                               ParseState* __restrict__ ps) {
+  if (ps->hdr == 0) return;
+  const int64_t n_rows = ps->n_rows;
+  if (n_rows <= 0 || n_rows > cap_rows) return;  // reported by the host before any row error
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = 1 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_rows;
+       r += stride)
+    if (arrival[r] < arrival[r - 1])
+      atomicMin(&ps->err, err_key(line_of_row[r], GSB_TRACE_DETAIL_MONOTONE));
+  if (blockIdx.x == 0 && threadIdx.x == 0) ps->last_arrival = arrival[n_rows - 1];
 }
 
 // the header's end (line 0): one warp walks the file from byte 0, 32 bytes per step (ballot of
 // the line-end bytes), so the usual short header costs one coalesced load
-__global__ void k_csv_header_end(const TraceParams tp, int64_t* __restrict__ out) {
+__constant__ char c_hdr4[] = "arrival_ms,prompt_tokens,output_tokens,class";
+
+// ...then (trace.cpp:63-74) line 0 after one '\r' strip against the two accepted headers, the
+// row count from the line scan, and the error key's reset: ParseState for the parse kernels
+__global__ void k_csv_header(const TraceParams tp, const unsigned long long* __restrict__ tile_pref,
+                             int64_t nt, ParseState* __restrict__ ps) {
   const int lane = threadIdx.x;
   const bool last_is_nl = tp.n > 0 && tp.bytes[tp.n - 1] == '\n';
+  int64_t he = tp.n;
   for (int64_t b0 = 0;; b0 += 32) {
     const int64_t b = b0 + lane;
     const bool e = b < tp.n ? tp.bytes[b] == '\n' : (b == tp.n && tp.n > 0 && !last_is_nl);
     const unsigned m = __ballot_sync(0xffffffffu, e);
     if (m) {
-      if (lane == 0) out[1] = b0 + __ffs(static_cast<int>(m)) - 1;
-      return;
+      he = b0 + __ffs(static_cast<int>(m)) - 1;
+      break;
     }
-    if (b0 + 32 > tp.n) {  // no end at all (n == 0)
-      if (lane == 0) out[1] = tp.n;
-      return;
-    }
+    if (b0 + 32 > tp.n) break;  // no end at all (n == 0)
+  }
+  int64_t hlen = he;
+  if (hlen > 0 && tp.bytes[hlen - 1] == '\r') --hlen;
+  constexpr int64_t k4 = sizeof(c_hdr4) - 1, k3 = k4 - 6;  // "...,class" / without ",class"
+  bool ok = true;
+  if (hlen == k4 || hlen == k3) {
+    for (int64_t i = lane; i < hlen; i += 32) ok = ok && tp.bytes[i] == c_hdr4[i];
+    ok = __all_sync(0xffffffffu, ok);
+  }
+  if (lane == 0) {
+    ps->header_end = he;
+    ps->hdr = (hlen == k4 && ok) ? 4 : ((hlen == k3 && ok) ? 3 : 0);
+    ps->n_rows = static_cast<int64_t>(tile_pref[nt - 1] & 0xffffffffull) - 1;  // minus the header
+    ps->last_arrival = 0;
+    ps->err = kNoErr;
   }
 }
 
@@ -579,76 +653,60 @@ int gsb_trace_parse(gsb_ctx* ctx, const char* d_bytes, int64_t n_bytes, int32_t 
   tp.n = n_bytes;
   tp.n_tiles = n_bytes / kTile + 1;  // the virtual end at n may open a tile
   tp.threshold = class_threshold;
-  // scratch: [tile counts + 1][prefix + 1][spare][err][locate 2][line_of_row (cap)][cub tmp]
+  tp.cap_rows = cap_rows;
+  // scratch: [tile counts + 1][prefix + 1][ParseState][locate 2][line_of_row (cap)][cub tmp]
   const size_t nt = static_cast<size_t>(tp.n_tiles) + 1;
   size_t cub_tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_tmp, static_cast<unsigned long long*>(nullptr),
                                 static_cast<unsigned long long*>(nullptr), static_cast<int>(nt), s);
-  const size_t head = (2 * nt + 4) * sizeof(unsigned long long);
+  const size_t head = 2 * nt * sizeof(unsigned long long) + sizeof(ParseState) + 32;
   const size_t lor = static_cast<size_t>(std::max<int64_t>(cap_rows, 1)) * sizeof(uint32_t);
   char* scr = static_cast<char*>(gsb_scratch(ctx, head + lor + cub_tmp + 256));
   if (!scr) return gsb_set_error(ctx, GSB_CUDA_ERROR, "trace_parse: scratch allocation failed");
   auto* cnt = reinterpret_cast<unsigned long long*>(scr);
   auto* pref = cnt + nt;
-  auto* first_end = pref + nt;
-  auto* err = first_end + 1;
-  auto* loc = reinterpret_cast<int64_t*>(err + 1);
+  auto* ps = reinterpret_cast<ParseState*>(pref + nt);
+  auto* loc = reinterpret_cast<int64_t*>(ps + 1);
   auto* line_of_row = reinterpret_cast<uint32_t*>(scr + head);
   void* d_cub = scr + ((head + lor + 255) / 256) * 256;
+  // everything on the stream, ONE read-back at the end: the header check (line 0 against the
+  // two accepted headers), the row count and the first failing row come back together
   cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s);
-  cudaMemsetAsync(err, 0xff, sizeof(unsigned long long), s);  // err = none
   k_csv_count<<<static_cast<unsigned>((n_bytes / (16 * kCountChunks) + 1 + kTrThreads - 1) /
                                       kTrThreads),
                 kTrThreads, 0, s>>>(tp, cnt);
   cub::DeviceScan::ExclusiveSum(d_cub, cub_tmp, cnt, pref, static_cast<int>(nt), s);
-  k_csv_header_end<<<1, 32, 0, s>>>(tp, loc);  // line 0 (the header): its end
-  unsigned long long h[2];
-  cudaMemcpyAsync(&h[0], loc + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(&h[1], pref + nt - 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  k_csv_header<<<1, 32, 0, s>>>(tp, pref, static_cast<int64_t>(nt), ps);
+  k_csv_parse<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(
+      tp, pref, d_arrival, d_prompt, d_output, d_slo_class, line_of_row, ps);
+  k_csv_monotone<<<static_cast<unsigned>(ctx->n_sms * 8), 256, 0, s>>>(d_arrival, line_of_row,
+                                                                       cap_rows, ps);
+  ParseState st{};
+  cudaMemcpyAsync(&st, ps, sizeof(st), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_parse");
-  const int64_t header_end = static_cast<int64_t>(h[0]);
-  // header (trace.cpp:63-74): line 0 after one '\r' strip
-  char hb[sizeof(res->line)];
-  const int64_t hl = std::min<int64_t>(header_end, static_cast<int64_t>(sizeof(hb) - 1));
-  cudaMemcpy(hb, d_bytes, static_cast<size_t>(hl), cudaMemcpyDeviceToHost);
-  int64_t hlen = header_end;
-  if (hlen > 0 && hlen <= hl && hb[hlen - 1] == '\r') --hlen;
-  const int64_t hshown = std::min<int64_t>(hlen, hl);
-  const std::string hdr(hb, static_cast<size_t>(hshown));
-  if (hlen == static_cast<int64_t>(sizeof(kHdr3) - 1) && hdr == kHdr3) {
-    tp.has_class = 0;
-  } else if (hlen == static_cast<int64_t>(sizeof(kHdr4) - 1) && hdr == kHdr4) {
-    tp.has_class = 1;
-  } else {
-    std::string full(static_cast<size_t>(header_end), '\0');  // the whole header line
+  const int rc = gsb_check_launch(ctx, "trace_parse");
+  if (rc) return rc;
+  const int64_t header_end = st.header_end;
+  if (st.hdr == 0) {  // trace.cpp:63-74: the whole header line in the message
+    std::string full(static_cast<size_t>(header_end), '\0');
     if (!full.empty()) cudaMemcpy(&full[0], d_bytes, full.size(), cudaMemcpyDeviceToHost);
     if (!full.empty() && full.back() == '\r') full.pop_back();
     set_result_line(res, full.data(), static_cast<int64_t>(full.size()));
     return fail(GSB_TRACE_KIND_BAD_HEADER, 0, 1, "unrecognized trace header: " + full);
   }
+  tp.has_class = st.hdr == 4 ? 1 : 0;
   res->has_class = tp.has_class;
   tp.header_end = header_end;
-  const int64_t n_rows = static_cast<int64_t>(h[1] & 0xffffffffull) - 1;  // minus the header
+  const int64_t n_rows = st.n_rows;
   if (n_rows <= 0) return fail(GSB_TRACE_KIND_EMPTY, 0, -1, "trace has no rows");
   if (n_rows > cap_rows) {
     res->n_rows = n_rows;
     return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "trace_parse: more rows than cap_rows");
   }
-  k_csv_parse<<<static_cast<unsigned>(tp.n_tiles), kTrThreads, 0, s>>>(
-      tp, pref, d_arrival, d_prompt, d_output, d_slo_class, line_of_row, err);
-  if (n_rows > 1)
-    k_csv_monotone<<<static_cast<unsigned>((n_rows - 1 + 255) / 256), 256, 0, s>>>(
-        n_rows, d_arrival, line_of_row, err);
-  unsigned long long ek = kNoErr;
-  cudaMemcpyAsync(&ek, err, sizeof(ek), cudaMemcpyDeviceToHost, s);
-  int64_t last = 0;
-  cudaMemcpyAsync(&last, d_arrival + n_rows - 1, sizeof(last), cudaMemcpyDeviceToHost, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) return gsb_check_launch(ctx, "trace_parse");
-  const int rc = gsb_check_launch(ctx, "trace_parse");
-  if (rc) return rc;
+  const unsigned long long ek = st.err;
   if (ek == kNoErr) {
     res->n_rows = n_rows;
-    res->max_arrival_ms = last;  // arrivals are non-decreasing: the last is the max
+    res->max_arrival_ms = st.last_arrival;  // arrivals are non-decreasing: the last is the max
     return GSB_OK;
   }
   // the earliest failing row: fetch its bytes, the host formats the reference's message

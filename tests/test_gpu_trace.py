@@ -164,3 +164,45 @@ def test_graph_survives_scratch_growth(gsb, restate):
     torch.cuda.synchronize()
     assert torch.equal(sel.f_idx, want_f)
     assert torch.equal(summ, want_s)
+
+
+def test_cap_rows_overflow_is_reported_then_parses(gsb, restate):
+    """gsb_trace_parse with cap_rows below the row count: INVALID_ARGUMENT with the true count
+    (rows past the cap are never written: the buffers below are guarded), then the same bytes
+    with room parse to the restated load_trace's rows; a bad header wins over the cap."""
+    import ctypes as C
+    from paper_2508_16449_b200 import _lib as L
+    rng = np.random.default_rng(3)
+    n = 5000
+    a = np.cumsum(rng.integers(0, 5, n))
+    lines = [H3.decode()] + [f"{a[i]},{rng.integers(1, 4000)},{rng.integers(1, 900)}"
+                             for i in range(n)]
+    data = ("\n".join(lines) + "\n").encode()
+    dev = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+
+    def call(cap, buf=None):
+        guard = 64
+        arr = torch.full((cap + guard,), -7, dtype=torch.int64, device="cuda")
+        prm = torch.full((cap + guard,), -7, dtype=torch.int32, device="cuda")
+        out = torch.full((cap + guard,), -7, dtype=torch.int32, device="cuda")
+        cls = torch.full((cap + guard,), 7, dtype=torch.uint8, device="cuda")
+        res = L.CTraceResult()
+        b = dev if buf is None else buf
+        rc = gsb.lib.gsb_trace_parse(gsb.ctx, C.c_void_p(b.data_ptr()), b.numel(), 1024, cap,
+                                     C.c_void_p(arr.data_ptr()), C.c_void_p(prm.data_ptr()),
+                                     C.c_void_p(out.data_ptr()), C.c_void_p(cls.data_ptr()),
+                                     C.byref(res), None)
+        torch.cuda.synchronize()
+        return rc, res, arr, prm, out, cls
+
+    rc, res, arr, prm, out, cls = call(1000)
+    assert rc == L.INVALID_ARGUMENT and res.n_rows == n
+    assert (arr[1000:] == -7).all() and (prm[1000:] == -7).all() and (cls[1000:] == 7).all()
+    rc, res, arr, prm, out, cls = call(n)
+    assert rc == L.OK and res.n_rows == n and res.max_arrival_ms == a[-1]
+    want = restate.trace_parse(data, 1024)
+    for got, w in zip((arr, prm, out, cls), want[:4]):
+        np.testing.assert_array_equal(got[:n].cpu().numpy(), w)
+    bad = torch.frombuffer(bytearray(b"arrival,prompt\n" + data[len(H3) + 1:]), dtype=torch.uint8).cuda()
+    rc, res, *_ = call(10, bad)
+    assert rc == L.TRACE_ERROR and L.TRACE_KINDS[res.kind] == "BadHeader" and res.row == 1
