@@ -243,6 +243,7 @@ k_csv_parse(TraceParams tp, const unsigned long long* __restrict__ tile_pref,
   __shared__ int64_t s_st[kMaxLines];  // the tile's non-empty lines: start, end (tile-relative),
   __shared__ int32_t s_b[kMaxLines];   // line index (tile-relative)
   __shared__ int32_t s_ln[kMaxLines];
+  __shared__ unsigned long long s_cm[(kTile + kPre) / 64 + 1];  // comma bitmap of the stage
   const int64_t t = blockIdx.x;
   stage_tile(tp, t, sm);
   __syncthreads();
@@ -256,6 +257,28 @@ k_csv_parse(TraceParams tp, const unsigned long long* __restrict__ tile_pref,
     line_ends16(sm, s0, tp.n, b0 + 16 * h, last_is_nl, &e, &ne16);
     ends |= static_cast<unsigned long long>(e) << (16 * h);
     nonempty |= static_cast<unsigned long long>(ne16) << (16 * h);
+  }
+  // the comma bitmap of the staged bytes (bit i <-> byte s0 + i), for the line fast path
+  {
+    const unsigned char* mine = sm + kPre + kPerThread * threadIdx.x;
+    unsigned long long cw = 0;
+#pragma unroll
+    for (int h = 0; h < kPerThread / 16; ++h)
+      cw |= static_cast<unsigned long long>(
+                eq_mask16(*reinterpret_cast<const uint4*>(mine + 16 * h), 0x2c2c2c2cu))
+            << (16 * h);
+    s_cm[kPre / 64 + threadIdx.x] = cw;
+    if (threadIdx.x < kPre / 64) {
+      const unsigned char* pre_b = sm + 64 * threadIdx.x;
+      unsigned long long cp = 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        cp |= static_cast<unsigned long long>(
+                  eq_mask16(*reinterpret_cast<const uint4*>(pre_b + 16 * h), 0x2c2c2c2cu))
+              << (16 * h);
+      s_cm[threadIdx.x] = cp;
+    }
+    if (threadIdx.x == 0) s_cm[(kTile + kPre) / 64] = 0;
   }
   const unsigned nl = __popcll(ends), ne = __popcll(nonempty);
   unsigned long long pre, agg;
@@ -298,21 +321,15 @@ k_csv_parse(TraceParams tp, const unsigned long long* __restrict__ tile_pref,
     unsigned char c0 = 0, c1 = 0;
     int clen = 0, ncols;
     const int len = static_cast<int>(min(en - st, static_cast<int64_t>(INT32_MAX)));
-    bool general = !(in_sm && len <= 64);
+    bool general = !(in_sm && len <= 64 && st - s0 >= 16);
     if (!general) {
-      // fast path: the line's comma mask from 4-byte SIMD compares, then one tight digit loop
-      // per column (no per-byte branching)
-      const unsigned char* q = sm + (st - s0);
-      const int o = static_cast<int>(reinterpret_cast<uintptr_t>(q) & 3);
-      const uint32_t* w = reinterpret_cast<const uint32_t*>(q - o);
-      unsigned long long cm = 0;
-      const int nw = (len + o + 3) >> 2;
-      for (int k = 0; k < nw; ++k) {
-        const uint32_t e = __vcmpeq4(w[k], 0x2c2c2c2cu) & 0x80808080u;
-        const unsigned long long bits = (e * 0x00204081u) >> 28;  // bit j: byte j is ','
-        const int sh = 4 * k - o;
-        cm |= sh >= 64 ? 0ull : (sh >= 0 ? (bits << sh) : (bits >> -sh));
-      }
+      // fast path: the line's comma mask from the tile's comma bitmap (s_cm), then each
+      // numeric column as at most two 8-digit SWAR words (unaligned 8-byte smem reads)
+      const int qo = static_cast<int>(st - s0);
+      const unsigned char* q = sm + qo;
+      const int cw = qo >> 6, cb = qo & 63;
+      unsigned long long cm = s_cm[cw] >> cb;
+      if (cb) cm |= s_cm[cw + 1] << (64 - cb);
       if (len < 64) cm &= (1ull << len) - 1ull;
       const bool trailing = (cm >> (len - 1)) & 1ull;
       ncols = __popcll(cm) + (trailing ? 0 : 1);  // a final ',' adds no column
@@ -327,21 +344,46 @@ k_csv_parse(TraceParams tp, const unsigned long long* __restrict__ tile_pref,
         fe[k] = e;
         f0 = min(e + 1, len);
       }
-      // <= 18 digits cannot overflow int64, so the digit loop is a plain multiply-add; longer
-      // columns (leading zeros, overflow candidates) send the line to the general path
+      // the 8 bytes q[end-8, end) as a little-endian word (qo >= 16 keeps them staged)
+      auto ld8 = [&](int end) -> unsigned long long {
+        const int off = qo + end - 8;
+        const int sh = (off & 7) * 8;
+        const unsigned long long* w = reinterpret_cast<const unsigned long long*>(sm + (off & ~7));
+        return sh ? (w[0] >> sh) | (w[1] << (64 - sh)) : w[0];
+      };
+      // n (1..8) digits in the top n bytes of x: their value, and whether all are '0'..'9'
+      auto parse8 = [](unsigned long long x, int n, bool& dig) -> unsigned long long {
+        const unsigned long long keep = ~0ull << (8 * (8 - n));
+        x = (x & keep) | (0x3030303030303030ull & ~keep);  // leading '0's
+        dig = ((x & 0xF0F0F0F0F0F0F0F0ull) == 0x3030303030303030ull) &&
+              (((x + 0x0606060606060606ull) & 0xF0F0F0F0F0F0F0F0ull) == 0x3030303030303030ull);
+        x -= 0x3030303030303030ull;
+        x = x * 10 + (x >> 8);
+        return (((x & 0x000000FF000000FFull) * (100 + (1000000ull << 32))) +
+                (((x >> 16) & 0x000000FF000000FFull) * (1 + (10000ull << 32)))) >> 32;
+      };
+      // from_chars<int64> on the whole column: >= 1 digit; a sign or more than 16 digits
+      // (possible overflow) goes to the general path
       auto num = [&](int a0, int a1, unsigned long long& v, bool& ok) {
-        const bool neg = a1 > a0 && q[a0] == '-';
-        const int d0 = a0 + (neg ? 1 : 0);
-        if (a1 - d0 > 18) general = true;
-        bool good = a1 > d0;
-        unsigned long long val = 0;
-        for (int i = d0; i < a1; ++i) {
-          const unsigned d = static_cast<unsigned>(q[i]) - '0';
-          good = good && d <= 9;
-          val = val * 10ull + d;
+        const int n = a1 - a0;
+        if (n > 16 || (n > 0 && q[a0] == '-')) {
+          general = true;
+          return;
         }
-        ok = good;
-        v = neg ? 0ull - val : val;
+        ok = false;
+        v = 0;
+        if (n == 0) return;
+        bool d_lo;
+        const unsigned long long lo = parse8(ld8(a1), n > 8 ? 8 : n, d_lo);
+        if (n > 8) {
+          bool d_hi;
+          const unsigned long long hi = parse8(ld8(a1 - 8), n - 8, d_hi);
+          v = hi * 100000000ull + lo;
+          ok = d_lo && d_hi;
+        } else {
+          v = lo;
+          ok = d_lo;
+        }
       };
       if (ncols == expect) {
         num(fs[0], fe[0], v0, ok0);
