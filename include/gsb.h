@@ -396,9 +396,17 @@ int gsb_prefill_commands_csv(gsb_ctx* ctx, int64_t n, const double* d_tick_ms,
                              const double* d_f_mhz, const double* d_window_ms,
                              const uint8_t* d_infeasible, char* d_out, int64_t cap_bytes,
                              int64_t* h_bytes, void* stream);
+/* greensim::decision_log_csv (decode_ctl.cpp:231-247) of K3b / K5 decision records: header +
+ * one line per record, numbers as snprintf("%.6g"), worker / bucket as std::to_string, the
+ * action by name. d_out == NULL: size query; *h_bytes = bytes. Synchronous. */
+int gsb_decision_log_csv(gsb_ctx* ctx, int64_t n, const gsb_decision* d_records, char* d_out,
+                         int64_t cap_bytes, int64_t* h_bytes, void* stream);
 /* snprintf("%.10g") of n values: value i's text at d_out32 + 32*i, its length in d_len[i]. */
 int gsb_format_g10(gsb_ctx* ctx, int64_t n, const double* d_values, char* d_out32,
                    int32_t* d_len, void* stream);
+/* the same for snprintf("%.<precision>g"), precision 6 or 10 */
+int gsb_format_g(gsb_ctx* ctx, int precision, int64_t n, const double* d_values, char* d_out32,
+                 int32_t* d_len, void* stream);
 
 /* ---------------------------------------------------------------- K3/K4: decode control */
 /* Raw decode telemetry of S streams (one decode worker each), CSR layout:

@@ -629,6 +629,8 @@ class Reference:
         L.ref_freq_timeline_csv.restype = _i64
         L.ref_prefill_commands_csv.argtypes = [_i64, _p, _p, _p, _p, _p, _p, _p, _i64]
         L.ref_prefill_commands_csv.restype = _i64
+        L.ref_decision_log_csv.argtypes = [_i64, _p, _p, _i64]
+        L.ref_decision_log_csv.restype = _i64
         L.ref_prefill_pass_ex.argtypes = [C.c_int, C.c_int, _p, C.c_int, C.c_int, _p, _i64, _p,
                                           _p, _i64, _i64, _i64, _d, C.POINTER(QoptCfg), _d, _d,
                                           C.c_int, _p, _p, _p]
@@ -752,6 +754,23 @@ class Reference:
         buf = C.create_string_buffer(cap)
         k = self.lib.ref_prefill_commands_csv(n, *(ptr(x) for x in a), buf, cap)
         return buf.raw[:k]
+
+    def decision_log_csv(self, records) -> bytes:
+        """greensim::decision_log_csv over records in the gsb_decision layout (a structured or
+        raw uint8 array of 64-byte records, action as its index), run by
+        oracle/_ref/ref_save_trace --decisions in its own process."""
+        import subprocess
+        import tempfile
+        raw = np.ascontiguousarray(records).view(np.uint8).reshape(-1)
+        n = raw.size // 64
+        with tempfile.TemporaryDirectory() as d:
+            src, dst = os.path.join(d, "rec.bin"), os.path.join(d, "log.csv")
+            with open(src, "wb") as f:
+                f.write(np.int64(n).tobytes() + raw.tobytes())
+            subprocess.run([os.path.join(os.path.dirname(REF_SO), "ref_save_trace"),
+                            "--decisions", src, dst], check=True)
+            with open(dst, "rb") as f:
+                return f.read()
 
     def prefill_pass(self, profs, thresholds, arrival, prompt, window_ms, w0, n_windows, D,
                      threads=1, outputs=True, enabled=True):

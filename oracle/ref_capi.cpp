@@ -453,6 +453,37 @@ int64_t ref_prefill_commands_csv(int64_t n, const double* tick, const int32_t* c
   return static_cast<int64_t>(s.size());
 }
 
+// decision_log_csv (decode_ctl.cpp:237-247) over records in the gsb_decision layout (6 doubles:
+// tick, tps, p95, band_lo, band_hi, command; then worker, bucket, action index, pad). Its
+// ostringstream does not survive the Python interpreter's libstdc++ once numpy is loaded: call
+// it through oracle/_ref/ref_save_trace --decisions (Reference.decision_log_csv does).
+struct RefDecisionIn {
+  double tick_ms, tps, p95_tbt_ms, band_lo, band_hi, command_mhz;
+  int32_t worker, bucket, action, pad_;
+};
+int64_t ref_decision_log_csv(int64_t n, const RefDecisionIn* rec, char* out, int64_t cap) {
+  static const char* const kNames[8] = {"hold",           "up",            "down",
+                                        "coarse_hold",    "coarse_pending", "coarse_commit",
+                                        "adapt_up",       "adapt_down"};
+  std::vector<DecisionRecord> r(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    const RefDecisionIn& d = rec[i];
+    DecisionRecord& x = r[static_cast<size_t>(i)];
+    x.tick_ms = d.tick_ms;
+    x.worker = d.worker;
+    x.tps = d.tps;
+    x.p95_tbt_ms = d.p95_tbt_ms;
+    x.bucket = d.bucket;
+    x.band_lo = d.band_lo;
+    x.band_hi = d.band_hi;
+    x.command_mhz = d.command_mhz;
+    x.action = kNames[d.action & 7];
+  }
+  const std::string s = decision_log_csv(r);
+  if (out) std::memcpy(out, s.data(), static_cast<size_t>(std::min<int64_t>(cap, s.size())));
+  return static_cast<int64_t>(s.size());
+}
+
 // queue_optimizer_tick over n_queues snapshots at one instant; returns #commands.
 int ref_queue_optimizer_tick(const gso_profile* c, const gso_qopt_cfg* qc, int n_queues,
                              const int32_t* class_ids, const int64_t* off, const int32_t* prompt,

@@ -2,13 +2,37 @@
 // in its own process (the reference's ofstream path does not survive being dlopen'ed into the
 // Python interpreter). Input: a raw file of  n (i64) | arrival i64[n] | prompt i32[n] |
 // output i32[n] | has_cls (u8) | cls u8[n];  output: the CSV written by the reference.
+// `--decisions IN OUT`: IN = n (i64) | n decision records in the gsb_decision layout (64 B);
+// OUT = the reference's decision_log_csv of them (its ostringstream path, same reason).
 #include <cstdint>
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "greensim/trace.hpp"
 
+extern "C" int64_t ref_decision_log_csv(int64_t n, const void* rec, char* out, int64_t cap);
+
+static int decisions(const char* in, const char* out) {
+  FILE* f = std::fopen(in, "rb");
+  if (!f) return 3;
+  int64_t n = 0;
+  if (std::fread(&n, 8, 1, f) != 1) return 4;
+  std::vector<unsigned char> rec(static_cast<size_t>(n) * 64);
+  if (std::fread(rec.data(), 1, rec.size(), f) != rec.size()) return 5;
+  std::fclose(f);
+  const int64_t k = ref_decision_log_csv(n, rec.data(), nullptr, 0);
+  std::vector<char> buf(static_cast<size_t>(k));
+  ref_decision_log_csv(n, rec.data(), buf.data(), k);
+  FILE* o = std::fopen(out, "wb");
+  if (!o) return 6;
+  std::fwrite(buf.data(), 1, buf.size(), o);
+  std::fclose(o);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 4 && std::string(argv[1]) == "--decisions") return decisions(argv[2], argv[3]);
   if (argc != 3) return 2;
   FILE* f = std::fopen(argv[1], "rb");
   if (!f) return 3;

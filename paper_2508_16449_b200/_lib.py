@@ -148,6 +148,7 @@ EXPORTS = (
     "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
     "gsb_prefill_pass", "gsb_select_batches_running", "gsb_freq_timeline_csv",
     "gsb_prefill_commands_csv", "gsb_format_g10", "gsb_mg1_side_output",
+    "gsb_decision_log_csv", "gsb_format_g",
     "gsb_combine_summaries", "gsb_reduce_summaries", "gsb_tally_pool", "gsb_combine_tallies",
     "gsb_reduce_tallies",
 )
@@ -203,6 +204,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_prefill_commands_csv.argtypes = [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i64, P(_i64),
                                            _p]
     L.gsb_format_g10.argtypes = [_p, _i64, _p, _p, _p, _p]
+    L.gsb_format_g.argtypes = [_p, _i32, _i64, _p, _p, _p, _p]
+    L.gsb_decision_log_csv.argtypes = [_p, _i64, _p, _p, _i64, P(_i64), _p]
     L.gsb_combine_summaries.argtypes = [C.c_int, C.c_int, _p, _p, _p]
     L.gsb_reduce_summaries.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, ALLGATHER_FN, _p,
                                        _p, _p]

@@ -691,14 +691,29 @@ class Engine:
              self._dev(window_ms, torch.float64), self._dev(infeasible, torch.uint8)]
         return self._render(self.lib.gsb_prefill_commands_csv, a[0].numel(), a)
 
+    def decision_log_csv(self, records) -> bytes:
+        """decision_log_csv (decode_ctl.cpp:231-247) of decision records in the gsb_decision
+        layout (DECISION_DTYPE, host or device; e.g. a K3b / K5 records slice), rendered on the
+        GPU: '%.6g' numbers, byte-identical."""
+        if isinstance(records, torch.Tensor):
+            r = records.to(self.device).contiguous().view(torch.uint8).reshape(-1)
+        else:
+            raw = np.ascontiguousarray(records).view(np.uint8).reshape(-1)
+            r = torch.from_numpy(raw.copy()).to(self.device)
+        return self._render(self.lib.gsb_decision_log_csv, r.numel() // 64, [r])
+
     def format_g10(self, values) -> list:
         """snprintf("%.10g") of every value, on the GPU (the reference's fmt_g)."""
+        return self.format_g(values, 10)
+
+    def format_g(self, values, precision: int = 10) -> list:
+        """snprintf("%.<precision>g") (6 or 10) of every value, on the GPU."""
         v = self._dev(values, torch.float64)
         n = v.numel()
         out = self._empty((max(n, 1), 32), torch.uint8)
         ln = self._empty(max(n, 1), torch.int32)
-        self._check(self.lib.gsb_format_g10(self.ctx, n, _ptr(v), _ptr(out), _ptr(ln),
-                                            self.stream()))
+        self._check(self.lib.gsb_format_g(self.ctx, int(precision), n, _ptr(v), _ptr(out),
+                                          _ptr(ln), self.stream()))
         o, l = out.cpu().numpy(), ln.cpu().numpy()
         return [bytes(o[i, :l[i]]).decode() for i in range(n)]
 

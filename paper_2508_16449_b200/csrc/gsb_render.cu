@@ -1,5 +1,6 @@
 // gsb_render.cu — the simulator's CSV wire formats rendered on the GPU from device-resident
-// records: freq_timeline_csv and prefill_commands_csv (simkernel.cpp:686-714), byte for byte.
+// records: freq_timeline_csv and prefill_commands_csv (simkernel.cpp:686-714) and the
+// controllers' decision_log_csv (decode_ctl.cpp:231-247, '%.6g'), byte for byte.
 //
 // Numbers go through the reference's fmt_g = snprintf("%.10g") (simkernel.cpp:679-683): ten
 // significant digits, correctly rounded from the double's EXACT binary value (ties to even, as
@@ -112,8 +113,16 @@ __device__ __forceinline__ double pow10_d(int s) {  // 10^s: exact for |s| <= 22
   return exp10(static_cast<double>(s));
 }
 
-// snprintf(buf, 40, "%.10g", v); returns the length (<= 17)
-__device__ int fmt_g10(double v, char* out) {
+__host__ __device__ constexpr unsigned long long pow10_u(int k) {
+  return k == 0 ? 1ull : 10ull * pow10_u(k - 1);
+}
+
+// snprintf(buf, 40, "%.<PR>g", v) for PR = 10 (fmt_g, simkernel.cpp:679-683) or 6 (fmt_num,
+// decode_ctl.cpp:231-235); returns the length (<= PR + 7)
+template <int PR>
+__device__ int fmt_g(double v, char* out) {
+  constexpr unsigned long long kLo = pow10_u(PR - 1), kHi = pow10_u(PR);
+  constexpr double kHiD = static_cast<double>(kHi), kLoD = static_cast<double>(kLo);
   int n = 0;
   const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
   const bool neg = bits >> 63;
@@ -141,15 +150,15 @@ __device__ int fmt_g10(double v, char* out) {
   int X = static_cast<int>(floor(log10(av)));
   unsigned long long D = 0;
   for (int iter = 0; iter < 8; ++iter) {
-    const int s = 9 - X;
+    const int s = (PR - 1) - X;
     // estimate (relative error ~1e-15), in two factors so neither overflows at the range ends
     const double x = (av * pow10_d(s / 2)) * pow10_d(s - s / 2);
     // the estimate only moves X when clearly off; the exact floor below settles the boundary
-    if (x >= 1.01e10) {
+    if (x >= 1.01 * kHiD) {
       ++X;
       continue;
     }
-    if (x < 0.99e9) {
+    if (x < 0.99 * kLoD) {
       --X;
       continue;
     }
@@ -157,31 +166,31 @@ __device__ int fmt_g10(double v, char* out) {
     // exact floor: D <= value * 10^s < D + 1
     for (int k = 0; k < 8 && D > 0 && cmp_scaled(mant, e, s, 2 * D) < 0; ++k) --D;
     for (int k = 0; k < 8 && cmp_scaled(mant, e, s, 2 * D + 2) >= 0; ++k) ++D;
-    if (D < 1000000000ull) {  // exactly below the decade: one digit too few
+    if (D < kLo) {  // exactly below the decade: one digit too few
       --X;
       continue;
     }
-    if (D >= 10000000000ull) {  // exactly at or above the next decade
+    if (D >= kHi) {  // exactly at or above the next decade
       ++X;
       continue;
     }
     // round half to even on the exact value
     const int c = cmp_scaled(mant, e, s, 2 * D + 1);
     if (c > 0 || (c == 0 && (D & 1))) ++D;
-    if (D == 10000000000ull) {  // 9999999999.5.. rounds up to the next decade: exactly 1e9 there
-      D = 1000000000ull;
+    if (D == kHi) {  // 99..9.5.. rounds up to the next decade: exactly 10^(PR-1) there
+      D = kLo;
       ++X;
     }
     break;
   }
-  char dg[10];
-  for (int i = 9; i >= 0; --i) {
+  char dg[PR];
+  for (int i = PR - 1; i >= 0; --i) {
     dg[i] = static_cast<char>('0' + D % 10);
     D /= 10;
   }
-  int last = 9;  // last significant digit after stripping trailing zeros
+  int last = PR - 1;  // last significant digit after stripping trailing zeros
   while (last > 0 && dg[last] == '0') --last;
-  if (X < -4 || X >= 10) {
+  if (X < -4 || X >= PR) {
     out[n++] = dg[0];
     if (last > 0) {
       out[n++] = '.';
@@ -207,6 +216,8 @@ __device__ int fmt_g10(double v, char* out) {
   }
   return n;
 }
+
+__device__ __forceinline__ int fmt_g10(double v, char* out) { return fmt_g<10>(v, out); }
 
 __device__ __forceinline__ int fmt_int(long long v, char* out) {  // std::to_string
   int n = 0;
@@ -269,7 +280,41 @@ __device__ int line_of(const CommandRecords& r, int64_t i, char* b) {
   return n;
 }
 
-constexpr int kLineMax = 96;  // longest line: 3 x 17 (%.10g) + 2 x 11 (int) + separators
+struct DecisionRecords {  // gsb_decision (K3b / K5 decision logs) = DecisionRecord
+  const gsb_decision* r;   // (decode_ctl.hpp:95-105) with the action as its index
+};
+
+__constant__ char c_actions[8][16] = {"hold",           "up",          "down",
+                                      "coarse_hold",    "coarse_pending", "coarse_commit",
+                                      "adapt_up",       "adapt_down"};
+
+// decision_log_csv's line for record i (decode_ctl.cpp:237-246), '%.6g' numbers
+__device__ int line_of(const DecisionRecords& d, int64_t i, char* b) {
+  const gsb_decision r = d.r[i];
+  int n = fmt_g<6>(r.tick_ms, b);
+  b[n++] = ',';
+  n += fmt_int(r.worker, b + n);
+  b[n++] = ',';
+  n += fmt_g<6>(r.tps, b + n);
+  b[n++] = ',';
+  n += fmt_g<6>(r.p95_tbt_ms, b + n);
+  b[n++] = ',';
+  n += fmt_int(r.bucket, b + n);
+  b[n++] = ',';
+  n += fmt_g<6>(r.band_lo, b + n);
+  b[n++] = ',';
+  n += fmt_g<6>(r.band_hi, b + n);
+  b[n++] = ',';
+  n += fmt_g<6>(r.command_mhz, b + n);
+  b[n++] = ',';
+  const char* a = c_actions[static_cast<unsigned>(r.action) & 7u];
+  for (int k = 0; a[k]; ++k) b[n++] = a[k];
+  b[n++] = '\n';
+  return n;
+}
+
+// longest line: decisions, 6 x 13 (%.6g) + 2 x 11 (int) + 14 (action) + separators
+constexpr int kLineMax = 128;
 
 template <class R>
 __global__ void k_render_len(R r, int64_t n, unsigned long long* __restrict__ len) {
@@ -326,12 +371,13 @@ int render(gsb_ctx* ctx, const char* what, const char* header, R r, int64_t n, c
 }
 
 // single values (tests, and any host that wants the reference's fmt_g on the device)
-__global__ void k_fmt_g10(int64_t n, const double* __restrict__ v, char* __restrict__ out,
-                          int32_t* __restrict__ len) {
+template <int PR>
+__global__ void k_fmt_g(int64_t n, const double* __restrict__ v, char* __restrict__ out,
+                        int32_t* __restrict__ len) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   char b[32];
-  const int k = fmt_g10(v[i], b);
+  const int k = fmt_g<PR>(v[i], b);
   for (int j = 0; j < k; ++j) out[i * 32 + j] = b[j];
   len[i] = k;
 }
@@ -359,13 +405,29 @@ int gsb_prefill_commands_csv(gsb_ctx* ctx, int64_t n, const double* d_tick_ms,
                 n, d_out, cap_bytes, h_bytes, stream);
 }
 
+int gsb_decision_log_csv(gsb_ctx* ctx, int64_t n, const gsb_decision* d_records, char* d_out,
+                         int64_t cap_bytes, int64_t* h_bytes, void* stream) {
+  return render(ctx, "decision_log_csv",
+                "tick_ms,worker,tps,p95_tbt_ms,bucket,band_lo,band_hi,command_mhz,action\n",
+                DecisionRecords{d_records}, n, d_out, cap_bytes, h_bytes, stream);
+}
+
+int gsb_format_g(gsb_ctx* ctx, int precision, int64_t n, const double* d_values, char* d_out32,
+                 int32_t* d_len, void* stream) {
+  if (!ctx || n < 0 || (precision != 6 && precision != 10)) return GSB_INVALID_ARGUMENT;
+  if (n == 0) return GSB_OK;
+  const unsigned g = static_cast<unsigned>((n + 127) / 128);
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  if (precision == 6)
+    k_fmt_g<6><<<g, 128, 0, s>>>(n, d_values, d_out32, d_len);
+  else
+    k_fmt_g<10><<<g, 128, 0, s>>>(n, d_values, d_out32, d_len);
+  return gsb_check_launch(ctx, "format_g");
+}
+
 int gsb_format_g10(gsb_ctx* ctx, int64_t n, const double* d_values, char* d_out32,
                    int32_t* d_len, void* stream) {
-  if (!ctx || n < 0) return GSB_INVALID_ARGUMENT;
-  if (n == 0) return GSB_OK;
-  k_fmt_g10<<<static_cast<unsigned>((n + 127) / 128), 128, 0, gsb_pick_stream(ctx, stream)>>>(
-      n, d_values, d_out32, d_len);
-  return gsb_check_launch(ctx, "format_g10");
+  return gsb_format_g(ctx, 10, n, d_values, d_out32, d_len, stream);
 }
 
 }  // extern "C"

@@ -87,3 +87,60 @@ def test_prefill_commands_csv_from_k2(gsb, ref):
     assert inf.sum() > 0 and (inf == 0).sum() > 0
     assert gsb.prefill_commands_csv([], [], [], [], [], []) == ref.prefill_commands_csv(
         [], [], [], [], [], [])
+
+
+def _edge_values6(rng):
+    v = [0.0, -0.0, 1.0, 0.1, 1.5, 2.5, 1e-5, 0.0001, 0.000123456789, 9.999995e-5, 999999.0,
+         999999.5, 9999995.0, 999999.4999, 1234565.0, 1234575.0, 123456.5, 123457.5, 1e6, 1e15,
+         5e-324, 1.7976931348623157e308, math.inf, -math.inf, math.nan, 1410.0, 25.125, 0.95,
+         60000.0 * 0.95, 1 / 3, 2 / 3, 123.4565, 100.0 / 7]
+    v += list(rng.uniform(-1e6, 1e6, 300)) + list(10.0 ** rng.uniform(-30, 30, 300))
+    # exact ties at the 6th significant digit: d.dddd5 x 10^k with short binary forms
+    v += [int(x) / 2 ** 3 for x in rng.integers(10 ** 6, 10 ** 8, 300)]
+    v += list(np.round(rng.uniform(0, 1e4, 300), 2))
+    return np.array(v, np.float64)
+
+
+def test_format_g6_matches_reference(gsb, ref):
+    """'%.6g' (decode_ctl.cpp fmt_num) on the GPU against the reference's own decision_log_csv
+    rendering the same values (tick_ms column)."""
+    from paper_2508_16449_b200 import api
+    rng = np.random.default_rng(6)
+    vals = _edge_values6(rng)
+    got = gsb.format_g(vals, 6)
+    rec = np.zeros(len(vals), api.DECISION_DTYPE)
+    rec["tick_ms"] = vals
+    want = [w.split(",")[0] for w in ref.decision_log_csv(rec).decode().splitlines()[1:]]
+    bad = [(x, g, w) for x, g, w in zip(vals, got, want) if g != w]
+    assert not bad, bad[:10]
+
+
+def test_decision_log_csv_from_the_decode_pool(gsb, ref):
+    """K5's per-worker controller decision logs (every action kind), rendered on the GPU as the
+    reference's decision_log_csv, byte for byte; plus random records over every field."""
+    from paper_2508_16449_b200 import api, workloads as wl
+    pa, pp, po = wl.sinusoid_decode_trace(1500.0, 1000.0, 120_000.0, 60_000, seed=11)
+    stream = wl.decode_stream(pa, pp, po)
+    cfgs = wl.pool_sweep(3)
+    plan = gsb.decode_pool(cfgs, stream, api.GpuProfile.default_profile(), api.SimConfig(),
+                           api.SloConfig(), rec_cap=6000, launch=False)
+    plan["out"]["records"].zero_()
+    gsb.run_pool(plan)
+    torch.cuda.synchronize()
+    rec = plan["out"]["records"].cpu().numpy().view(api.DECISION_DTYPE)[..., 0]  # [N][W][cap]
+    r = rec[0].reshape(-1)
+    r = r[r["tick_ms"] > 0]
+    assert len(r) > 100 and len(set(r["action"].tolist())) >= 4
+    assert gsb.decision_log_csv(r) == ref.decision_log_csv(r)
+    # the device tensor path gives the same bytes
+    dev = torch.from_numpy(r.view(np.uint8).copy()).cuda()
+    assert gsb.decision_log_csv(dev) == ref.decision_log_csv(r)
+    rng = np.random.default_rng(2)
+    x = np.zeros(400, api.DECISION_DTYPE)
+    for f in ("tick_ms", "tps", "p95_tbt_ms", "band_lo", "band_hi", "command_mhz"):
+        x[f] = 10.0 ** rng.uniform(-6, 9, 400) * rng.choice([-1, 1], 400)
+    x["worker"] = rng.integers(-5, 1 << 30, 400)
+    x["bucket"] = rng.integers(-1, 40, 400)
+    x["action"] = rng.integers(0, 8, 400)
+    assert gsb.decision_log_csv(x) == ref.decision_log_csv(x)
+    assert gsb.decision_log_csv(x[:0]) == ref.decision_log_csv(x[:0])
