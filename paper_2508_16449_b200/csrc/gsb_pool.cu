@@ -76,17 +76,29 @@ struct Smem {
   int32_t* bc;     // [W][MB] worker's (gap <= SLO) prefix count at the first token; bit 31: TTFT met
   int32_t* ttok;   // [W][TC]
   uint16_t* rc;    // [W][RC] TBT run counts
+  // the controllers (cold: touched on ticks only), out of registers: lanes >= W share row W
+  CtlK* k;         // [1]
+  Ctl<false>* ctl; // [W + 1]
+  double* fo;      // [W + 1][NB] each controller's f_opt table
 };
 
-__host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC) {
-  int64_t b = 16ll * W * MB + 8ll * W * RC + 8ll * W * TC + 16ll * W * kFQ + 12ll * W * MB +
-              4ll * W * TC + 2ll * W * RC;
+__host__ __device__ inline int64_t ctl_bytes(int W, int NB) {
+  return ((static_cast<int64_t>(sizeof(CtlK)) + 15) & ~15ll) +
+         ((static_cast<int64_t>(sizeof(Ctl<false>)) * (W + 1) + 15) & ~15ll) + 8ll * (W + 1) * NB;
+}
+
+__host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC, int NB) {
+  int64_t b = ctl_bytes(W, NB) + 16ll * W * MB + 8ll * W * RC + 8ll * W * TC + 16ll * W * kFQ +
+              12ll * W * MB + 4ll * W * TC + 2ll * W * RC;
   return (b + 15) & ~15ll;
 }
 
-__device__ __forceinline__ Smem carve(char* base, int W, int MB, int RC, int TC) {
+__device__ __forceinline__ Smem carve(char* base, int W, int MB, int RC, int TC, int NB) {
   Smem s;
   char* p = base;
+  s.k = reinterpret_cast<CtlK*>(p); p += (sizeof(CtlK) + 15) & ~size_t{15};
+  s.ctl = reinterpret_cast<Ctl<false>*>(p); p += (sizeof(Ctl<false>) * (W + 1) + 15) & ~size_t{15};
+  s.fo = reinterpret_cast<double*>(p); p += 8ll * (W + 1) * NB;
   s.bp = reinterpret_cast<uint64_t*>(p); p += 8ll * W * MB;
   s.first = reinterpret_cast<double*>(p); p += 8ll * W * MB;
   s.rv = reinterpret_cast<double*>(p); p += 8ll * W * RC;
@@ -211,16 +223,22 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   bool runs_full = false;  // lane ww: the run ring (RC < RC_full) could not take a new run
 
   // controller (lane w), DecodeController ctor (decode_ctl.cpp:130-140)
-  double f_opt[GSB_MAX_BUCKETS];
-  const CtlK k = make_k(ccfg, NB, a.d_tps_hi + tb * NB, prof.f_min_mhz, prof.f_max_mhz);
-  Ctl<false> c;
+  // controller state in shared memory (ticks only); lanes >= W work on the shared row W
+  double* f_opt = s.fo + (is_w ? w : W) * NB;
+  if (lane == 0) *s.k = make_k(ccfg, NB, a.d_tps_hi + tb * NB, prof.f_min_mhz, prof.f_max_mhz);
+  __syncwarp();
+  const CtlK& k = *s.k;
+  Ctl<false>& c = s.ctl[is_w ? w : W];
   if (ctl_on) {
-    for (int b = 0; b < NB; ++b) f_opt[b] = a.d_f_opt[tb * NB + b];
-    ctl_init(c, f_opt, k);
-  } else {
+    if (is_w || lane == W) {
+      for (int b = 0; b < NB; ++b) f_opt[b] = a.d_f_opt[tb * NB + b];
+      ctl_init(c, f_opt, k);
+    }
+  } else if (is_w || lane == W) {
     c.n_rec = 0;
     c.digest = kFnv0;
   }
+  __syncwarp();
   gsb_decision* rec = (a.d_records && a.rec_cap > 0 && is_w)
                           ? a.d_records + (n * W + w) * a.rec_cap : nullptr;
   double* fout = (a.d_freq && a.freq_cap > 0 && is_w) ? a.d_freq + (n * W + w) * a.freq_cap * 2
@@ -696,7 +714,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_decode_pool(const __
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const Smem s = carve(smem + wib * P.warp_bytes, P.W, P.MB, P.RC, P.TC);
+  const Smem s = carve(smem + wib * P.warp_bytes, P.W, P.MB, P.RC, P.TC, P.a.n_buckets);
   const int64_t slot = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
   int32_t* pend = P.ws_pending + slot * P.W * P.cfg.pending_cap;
   for (;;) {
@@ -773,8 +791,8 @@ int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* c
   const int RC2 = P.RC_full;
   int per_sm[2] = {0, 0};
   int64_t warp_bytes[2];
-  warp_bytes[0] = smem_bytes(W, MB, RC1, P.TC);
-  warp_bytes[1] = smem_bytes(W, MB, RC2, P.TC);
+  warp_bytes[0] = smem_bytes(W, MB, RC1, P.TC, a->n_buckets);
+  warp_bytes[1] = smem_bytes(W, MB, RC2, P.TC, a->n_buckets);
   if (warp_bytes[1] * kWarpsPerBlock > 227 * 1024)
     return gsb_set_error(ctx, GSB_MODEL_ERROR, "decode pool: per-scenario state exceeds shared memory");
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
