@@ -63,6 +63,18 @@ struct PoolParams {
   const unsigned* list_n;
 };
 
+// Worker state touched only at step starts and clock applications: shared memory, one row per
+// decode worker (lanes >= W share row W), so the event loop's registers stay for the hot state.
+struct WorkerCold {
+  double ps_last, ps_power;      // PowerState (simkernel.cpp:53-57)
+  double act_j, idle_j;          // WorkerLedger sums
+  double last_applied;
+  uint64_t fdig;                 // applied-clock digest
+  int64_t n_freq;
+  int ps_phase;
+  int pad_;
+};
+
 // shared-memory carve-up of one warp's region
 struct Smem {
   uint64_t* bp;    // [W][MB] worker's gap-bits prefix sum at the stream's first token
@@ -80,11 +92,13 @@ struct Smem {
   CtlK* k;         // [1]
   Ctl<false>* ctl; // [W + 1]
   double* fo;      // [W + 1][NB] each controller's f_opt table
+  WorkerCold* wc;  // [W + 1]
 };
 
 __host__ __device__ inline int64_t ctl_bytes(int W, int NB) {
   return ((static_cast<int64_t>(sizeof(CtlK)) + 15) & ~15ll) +
-         ((static_cast<int64_t>(sizeof(Ctl<false>)) * (W + 1) + 15) & ~15ll) + 8ll * (W + 1) * NB;
+         ((static_cast<int64_t>(sizeof(Ctl<false>)) * (W + 1) + 15) & ~15ll) + 8ll * (W + 1) * NB +
+         static_cast<int64_t>(sizeof(WorkerCold)) * (W + 1);
 }
 
 __host__ __device__ inline int64_t smem_bytes(int W, int MB, int RC, int TC, int NB) {
@@ -99,6 +113,7 @@ __device__ __forceinline__ Smem carve(char* base, int W, int MB, int RC, int TC,
   s.k = reinterpret_cast<CtlK*>(p); p += (sizeof(CtlK) + 15) & ~size_t{15};
   s.ctl = reinterpret_cast<Ctl<false>*>(p); p += (sizeof(Ctl<false>) * (W + 1) + 15) & ~size_t{15};
   s.fo = reinterpret_cast<double*>(p); p += 8ll * (W + 1) * NB;
+  s.wc = reinterpret_cast<WorkerCold*>(p); p += sizeof(WorkerCold) * (W + 1);
   s.bp = reinterpret_cast<uint64_t*>(p); p += 8ll * W * MB;
   s.first = reinterpret_cast<double*>(p); p += 8ll * W * MB;
   s.rv = reinterpret_cast<double*>(p); p += 8ll * W * RC;
@@ -129,20 +144,14 @@ struct Worker {
   uint64_t p_bits;               // prefix sum of gap bit patterns
   int64_t p_head, p_tail;        // FIFO [head, tail) in the workspace ring
   int fq_head, fq_n;             // pending clock applications
-  double ps_last, ps_power;      // PowerState (simkernel.cpp:53-57)
-  int ps_phase;
-  double act_j, idle_j;          // WorkerLedger sums
   int r_head, r_n, r_total;      // TBT runs ring
   bool p95_valid;
   double p95;
   int t_head, t_n;               // TPS ring
-  uint64_t fdig;                 // applied-clock digest
-  int64_t n_freq;
-  double last_applied;
 };
 
 // ledger_close / ledger_set (simkernel.cpp:60-79)
-__device__ __forceinline__ void ledger_close(Worker& wk, double now) {
+__device__ __forceinline__ void ledger_close(WorkerCold& wk, double now) {
   if (now > wk.ps_last) {
     const double joules = wk.ps_power * (now - wk.ps_last) / 1000.0;
     if (wk.ps_phase == PH_DECODE)
@@ -152,7 +161,7 @@ __device__ __forceinline__ void ledger_close(Worker& wk, double now) {
   }
   wk.ps_last = now;
 }
-__device__ __forceinline__ void ledger_set(Worker& wk, double now, int phase, double power) {
+__device__ __forceinline__ void ledger_set(WorkerCold& wk, double now, int phase, double power) {
   if (phase == wk.ps_phase && power == wk.ps_power) return;
   ledger_close(wk, now);
   wk.ps_phase = phase;
@@ -249,6 +258,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   // Sim::init (simkernel.cpp:195-233): decode clocks start at controllers_[0].command()
   const double f0 = ctl_on ? shfl_d(c.sp, 0) : fixed;
   Worker wk;
+  WorkerCold& wc = s.wc[is_w ? w : W];
   wk.freq = wk.target = f0;
   wk.P = power_at(prof, f0);
   wk.t_end = INFINITY;
@@ -259,17 +269,17 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   wk.p_bits = 0;
   wk.p_head = wk.p_tail = 0;
   wk.fq_head = wk.fq_n = 0;
-  wk.ps_last = 0.0;
-  wk.ps_power = prof.p_idle_w;
-  wk.ps_phase = PH_IDLE;
-  wk.act_j = wk.idle_j = 0.0;
+  wc.ps_last = 0.0;
+  wc.ps_power = prof.p_idle_w;
+  wc.ps_phase = PH_IDLE;
+  wc.act_j = wc.idle_j = 0.0;
   wk.r_head = wk.r_n = wk.r_total = 0;
   wk.p95_valid = false;
   wk.p95 = 0.0;
   wk.t_head = wk.t_n = 0;
-  wk.fdig = kFnv0;
-  wk.n_freq = 0;
-  wk.last_applied = 0.0;
+  wc.fdig = kFnv0;
+  wc.n_freq = 0;
+  wc.last_applied = 0.0;
 
   // uniform state
   double tf = ccfg.fine_period_ms, tc = ccfg.coarse_period_ms, ta = ccfg.adapt_period_s * 1000.0;
@@ -310,7 +320,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
       wk.n_active = na + take;
       wk.n_new = take;
       if (wk.n_active == 0) {
-        ledger_set(wk, now, PH_IDLE, prof.p_idle_w);
+        ledger_set(wc, now, PH_IDLE, prof.p_idle_w);
       } else {
         const double B = static_cast<double>(wk.n_active);
         // decode_step_raw_ms, gpu_model.cpp:99-103
@@ -318,7 +328,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
                             (prof.dec_beta0_ms + prof.dec_beta1_ms * B) * prof.dec_f_ref_mhz / wk.freq;
         wk.t_start = now;
         wk.t_end = now + step;
-        ledger_set(wk, now, PH_DECODE, wk.P);
+        ledger_set(wc, now, PH_DECODE, wk.P);
       }
     }
   };
@@ -558,14 +568,14 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
         if (f != wk.freq) {
           wk.freq = f;
           wk.P = power_at(prof, f);
-          if (wk.t_end != INFINITY) ledger_set(wk, now, PH_DECODE, wk.P);
-          wk.fdig = mix(mix(wk.fdig, dbits(now)), dbits(f));
-          if (fout && wk.n_freq < a.freq_cap) {
-            fout[2 * wk.n_freq] = now;
-            fout[2 * wk.n_freq + 1] = f;
+          if (wk.t_end != INFINITY) ledger_set(wc, now, PH_DECODE, wk.P);
+          wc.fdig = mix(mix(wc.fdig, dbits(now)), dbits(f));
+          if (fout && wc.n_freq < a.freq_cap) {
+            fout[2 * wc.n_freq] = now;
+            fout[2 * wc.n_freq + 1] = f;
           }
-          ++wk.n_freq;
-          wk.last_applied = now;
+          ++wc.n_freq;
+          wc.last_applied = now;
         }
       }
     } else {
@@ -647,12 +657,12 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   }
   // ---- finalize (simkernel.cpp:503-520) and the summary
   double end = std_max(end_floor, max_finish);
-  end = std_max(end, is_w ? wk.last_applied : 0.0);
+  end = std_max(end, is_w ? wc.last_applied : 0.0);
   for (int off = 16; off > 0; off >>= 1) end = std_max(end, __shfl_xor_sync(kFull, end, off));
-  if (is_w) ledger_close(wk, end);
+  if (is_w) ledger_close(wc, end);
   if (a.d_ledger && is_w) {
-    a.d_ledger[(n * W + w) * 2] = wk.act_j;
-    a.d_ledger[(n * W + w) * 2 + 1] = wk.idle_j;
+    a.d_ledger[(n * W + w) * 2] = wc.act_j;
+    a.d_ledger[(n * W + w) * 2 + 1] = wc.idle_j;
   }
   auto sum64 = [&](int64_t v) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
@@ -670,20 +680,20 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
   samples_ok = sum64(samples_ok);
   rdig = sumu64(rdig);
   const int64_t n_dec = sum64(is_w ? c.n_rec : 0);
-  const int64_t n_fc = sum64(is_w ? wk.n_freq : 0);
+  const int64_t n_fc = sum64(is_w ? wc.n_freq : 0);
   n_steps = sum64(is_w ? n_steps : 0);
   status = static_cast<int>(__reduce_or_sync(kFull, static_cast<unsigned>(status)));
   // RunResult::decode_pool_j (simkernel.cpp:617-621), worker order
   double e_sum = 0.0, act = 0.0, idle = 0.0;
   uint64_t dd = kFnv0, fd = kFnv0;
   for (int ww = 0; ww < W; ++ww) {
-    const double aj = shfl_d(wk.act_j, ww);
-    const double ij = shfl_d(wk.idle_j, ww);
+    const double aj = shfl_d(wc.act_j, ww);
+    const double ij = shfl_d(wc.idle_j, ww);
     e_sum += 0.0 + aj + ij;
     act += aj;
     idle += ij;
     dd = mix(dd, __shfl_sync(kFull, c.digest, ww));
-    fd = mix(fd, __shfl_sync(kFull, wk.fdig, ww));
+    fd = mix(fd, __shfl_sync(kFull, wc.fdig, ww));
   }
   if (lane == 0) {
     gsb_pool_summary o;
@@ -710,7 +720,7 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
 }
 
 template <bool REQ_OUT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) k_decode_pool(const __grid_constant__ PoolParams P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) k_decode_pool(const __grid_constant__ PoolParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
