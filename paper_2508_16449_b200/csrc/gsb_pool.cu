@@ -788,8 +788,8 @@ int gsb_decode_pool(gsb_ctx* ctx, const gsb_profile* prof, const gsb_pool_cfg* c
   auto kern = req_out ? k_decode_pool<true> : k_decode_pool<false>;
   // First launch: a TBT run ring of at most 32 runs per worker (a run is the equal gaps of
   // consecutive steps with the same gap, so a 256-token window rarely holds more than a few),
-  // which keeps four 4-scenario CTAs resident per SM (the 128-register bound; 5 or 6 CTAs
-  // spill 0.5-0.8 KB and ran 27-42% slower) with the smallest shared-memory carve-out; the
+  // which keeps five 4-scenario CTAs resident per SM (44 KB each; 102 registers since the
+  // controllers and the cold worker fields live in shared memory) with the smallest carve-out; the
   // scenarios whose ring fills are replayed by a second launch with the full capacity
   // (runs <= tokens <= tbt_cap). Both launches are always enqueued (graph-capturable); the
   // second exits at once when nothing overflowed. Pool rate by first-launch ring (runs merged):
