@@ -477,10 +477,16 @@ struct ListIn {
   int64_t cap;
 };
 
-constexpr int kListCta = 128;
+#ifndef GSB_K2_CTA
+#define GSB_K2_CTA 64
+#endif
+// 2-warp CTAs: a one-wave K2 is FP64-pipe bound per SM, and its warps of work split over the
+// SMs in CTA-sized lumps, so 2-warp CTAs (up to 20 per SM) leave at most 2 warps of imbalance
+// per SM where 4-warp CTAs left 4 (36 vs 40 warps at C4)
+constexpr int kListCta = GSB_K2_CTA;
 
 template <int G>
-__global__ void __launch_bounds__(kListCta, 10)
+__global__ void __launch_bounds__(kListCta, 1280 / kListCta)
 k_prefill_select_list(const __grid_constant__ SelectParams sp, const __grid_constant__ ClockSet<G> cs,
                       int P, ListIn li, const double* __restrict__ t_ref,
                       const double* __restrict__ min_deadline, double* __restrict__ window,

@@ -54,6 +54,8 @@ def main():
         "K1nolist": lambda: eng.route_bin(da, dp, routing, wms, 0, nW, out=rn),
         "K1a": lambda: eng.window_bounds(da, routing, wms, 0, nW),
         "K1": lambda: eng.route_bin(da, dp, routing, wms, 0, nW, out=rr),
+        "K1+K2k": lambda: (eng.route_bin(da, dp, routing, wms, 0, nW, out=rr),
+                           eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel)),
         "K1+K2": lambda: (eng.route_bin(da, dp, routing, wms, 0, nW, out=rr),
                           eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel,
                                              summary_out=summ)),
