@@ -292,19 +292,21 @@ __device__ __forceinline__ void route_bin_tile(
         const int key = g * C + cl;
         const unsigned m = __match_any_sync(kFull, valid ? key : 0x10000);
         const unsigned below = m & lt;
-        const int base = hist_w[valid ? key : 0];
-        __syncwarp();
+        // the key group's leader takes the group's slots with one shared-memory atomic and
+        // hands the base to the group (no read-modify-write of the histogram across the warp)
+        const int leader = __ffs(static_cast<int>(m)) - 1;
+        int base = 0;
+        if (valid && below == 0) base = atomicAdd(&hist_w[key], __popc(m));
+        base = __shfl_sync(kFull, base, leader);
         if (valid) {
           *cls_p = static_cast<uint8_t>(cl);
           s.kr[j] = static_cast<typename S::KR>(key | ((base + __popc(below)) << S::kKeyBits));
-          if (below == 0) hist_w[key] = base + __popc(m);
           if (DL) {
             const double ttft = L <= rp.slo_boundary ? rp.ttft_sm : rp.ttft_l;
             const double dl = static_cast<double>(__ldg(arrival + c0 + j)) + ttft - rp.allowance;
             if (dl == dl) atomicMin(&s.mdl[key], ord_f64(dl));
           }
         }
-        __syncwarp();
       }
     }
     __syncthreads();
