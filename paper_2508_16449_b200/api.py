@@ -571,8 +571,16 @@ class Engine:
                   want_fifo: bool = False, slo: SloConfig = SloConfig(),
                   allowance_ms: float = 100.0, out: Optional[RouteResult] = None) -> RouteResult:
         """K1: classify every request (router.cpp:26-31) and bin the trace into
-        (window, class) cells with the reference-order T_ref per profile."""
-        arrival = self._dev(arrival, torch.int64)
+        (window, class) cells with the reference-order T_ref per profile.
+
+        A PINNED host int64 `arrival` tensor is read in place (zero copy): with unified
+        addressing the kernels dereference pinned host memory directly, and K1 reads only one
+        arrival per 32 requests plus the 32-request tiles that hold a window start (the FIXED /
+        PER_CELL modes; the deadline mode reads every arrival once)."""
+        if not (isinstance(arrival, torch.Tensor) and arrival.device.type == "cpu"
+                and arrival.is_pinned() and arrival.dtype == torch.int64
+                and arrival.is_contiguous()):
+            arrival = self._dev(arrival, torch.int64)
         prompt = self._dev(prompt, torch.int32)
         n = arrival.numel()
         if n_windows is None:

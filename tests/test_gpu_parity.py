@@ -626,3 +626,30 @@ def test_summary_is_deterministic_and_exact_counts(eng, restate):
         e = en[fi[:, c] >= 0, c]
         assert abs(s1[0, c]["sum_energy_j"] - e.sum()) <= 1e-9 * abs(e.sum())
         assert s1[0, c]["min_energy_j"] == e.min()
+
+
+@pytest.mark.parametrize("want_deadline", [False, True])
+def test_route_bin_reads_pinned_host_arrivals_in_place(eng, restate, want_deadline):
+    """A pinned host arrival tensor is read in place by K1 (zero copy over PCIe): every output
+    equals the device-resident path's, bit for bit."""
+    api = _api()
+    profs = synth_profiles(api)[:4]
+    eng.set_profiles(profs)
+    a, p, _ = restate.gen_poisson_trace(6.0, 3_600_000, 768.0, 3072.0, 0.15, 128.0, seed=8)
+    thr = [128, 256, 512, 768, 1024, 2048, 4096]
+    rc = api.RoutingConfig(True, thr, list(range(len(thr) + 1)))
+    nw = int(a[-1] // 60_000) + 1
+    h = torch.as_tensor(a).pin_memory()
+    assert h.is_pinned()
+    r_dev = eng.route_bin(torch.as_tensor(a, device="cuda"), p, rc, 60_000, 0, nw,
+                          want_deadline=want_deadline)
+    r_host = eng.route_bin(h, p, rc, 60_000, 0, nw, want_deadline=want_deadline)
+    torch.cuda.synchronize()
+    for f in ("bounds", "cls", "count", "t_ref", "n_nonempty"):
+        assert torch.equal(getattr(r_dev, f), getattr(r_host, f)), f
+    n = int(r_dev.n_nonempty.item())  # list entries past n are not written
+    assert torch.equal(r_dev.nonempty[:n], r_host.nonempty[:n])
+    assert torch.equal(r_dev.t_ref_list[:, :n], r_host.t_ref_list[:, :n])
+    if want_deadline:
+        assert torch.equal(r_dev.min_deadline.view(torch.int64), r_host.min_deadline.view(torch.int64))
+    eng.set_profiles([api.GpuProfile.default_profile()])
