@@ -371,9 +371,18 @@ def run_gsb(args, rank, world, dist):
     h2d = h_prm.numel() * 4 + arr_bytes
     d2h = h_fidx.numel() * 2 + h_en.numel() * 8
 
+    up_stream = torch.cuda.Stream()
+    fork, prm_ready = torch.cuda.Event(), torch.cuda.Event()
+
     def e2e_step():
-        d_prm.copy_(h_prm, non_blocking=True)
-        eng.route_bin(h_arr, d_prm, routing, wms, w0, nW, out=rr)
+        # the prompt upload runs beside K1a (which reads the pinned arrivals in place); K1b
+        # waits for it
+        fork.record()
+        with torch.cuda.stream(up_stream):
+            up_stream.wait_event(fork)
+            d_prm.copy_(h_prm, non_blocking=True)
+            prm_ready.record()
+        eng.route_bin(h_arr, d_prm, routing, wms, w0, nW, out=rr, prompt_ready=prm_ready)
         eng.prefill_select(rr, api.L.FIXED_WINDOW, fixed_window_ms=D, out=sel, summary_out=summ)
         h_fidx.copy_(sel.f_idx, non_blocking=True)
         h_en.copy_(sel.energy_j, non_blocking=True)

@@ -569,9 +569,13 @@ class Engine:
     def route_bin(self, arrival, prompt, routing: RoutingConfig, window_ms: int, w0: int = 0,
                   n_windows: Optional[int] = None, want_deadline: bool = False,
                   want_fifo: bool = False, slo: SloConfig = SloConfig(),
-                  allowance_ms: float = 100.0, out: Optional[RouteResult] = None) -> RouteResult:
+                  allowance_ms: float = 100.0, out: Optional[RouteResult] = None,
+                  prompt_ready: Optional[torch.cuda.Event] = None) -> RouteResult:
         """K1: classify every request (router.cpp:26-31) and bin the trace into
         (window, class) cells with the reference-order T_ref per profile.
+
+        prompt_ready: an event after which `prompt` is complete (e.g. its upload on another
+        stream); only K1b waits for it, so the window-bounds pass (arrivals only) overlaps it.
 
         A PINNED host int64 `arrival` tensor is read in place (zero copy): with unified
         addressing the kernels dereference pinned host memory directly, and K1 reads only one
@@ -604,6 +608,8 @@ class Engine:
         s = self.stream()
         self._check(self.lib.gsb_window_bounds(self.ctx, C.byref(cfg), n, _ptr(arrival),
                                                _ptr(out.bounds), s))
+        if prompt_ready is not None:
+            torch.cuda.current_stream(self.device).wait_event(prompt_ready)
         cl = out.cell_list()
         self._check(self.lib.gsb_route_bin_list(self.ctx, C.byref(cfg), n, _ptr(arrival),
                                                 _ptr(prompt), _ptr(out.bounds), _ptr(out.cls),
