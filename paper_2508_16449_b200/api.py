@@ -483,6 +483,12 @@ class TraceArrays:
     nominal_qps: float
 
 
+def _pinned(t, dtype) -> bool:
+    """a contiguous pinned host tensor of dtype (read in place by the kernels)"""
+    return (isinstance(t, torch.Tensor) and t.device.type == "cpu" and t.is_pinned()
+            and t.dtype == dtype and t.is_contiguous())
+
+
 class Engine:
     """One libgsb context on one CUDA device (single owner, like the reference's objects)."""
 
@@ -578,14 +584,15 @@ class Engine:
         stream); only K1b waits for it, so the window-bounds pass (arrivals only) overlaps it.
 
         A PINNED host int64 `arrival` tensor is read in place (zero copy): with unified
-        addressing the kernels dereference pinned host memory directly, and K1 reads only one
-        arrival per 32 requests plus the 32-request tiles that hold a window start (the FIXED /
-        PER_CELL modes; the deadline mode reads every arrival once)."""
-        if not (isinstance(arrival, torch.Tensor) and arrival.device.type == "cpu"
-                and arrival.is_pinned() and arrival.dtype == torch.int64
-                and arrival.is_contiguous()):
+        addressing the kernels dereference pinned host memory directly, and K1a reads only one
+        arrival per 256 requests plus two 128-byte lines per window edge (dense traces; else one
+        arrival per 32 requests plus the 32-request tiles that hold a window start; the deadline
+        mode reads every arrival once). A pinned int32 `prompt` tensor is read in place by K1b
+        (plain loads instead of its TMA stage)."""
+        if not _pinned(arrival, torch.int64):
             arrival = self._dev(arrival, torch.int64)
-        prompt = self._dev(prompt, torch.int32)
+        if not _pinned(prompt, torch.int32):
+            prompt = self._dev(prompt, torch.int32)
         n = arrival.numel()
         if n_windows is None:
             last = int(arrival[-1].item()) if n else 0

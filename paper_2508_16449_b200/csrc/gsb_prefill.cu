@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 
 #include "gsb_common.cuh"
 #include "gsb_scan.cuh"
@@ -31,6 +32,7 @@ struct RouteParams {
   int32_t C;
   int32_t slo_boundary;
   int32_t want_deadline;
+  int32_t prompt_host;  // prompts in pinned host memory: plain loads instead of the TMA stage
   int64_t window_ms, w0, n_windows;
   double ttft_sm, ttft_l, allowance;
   double lat_a[GSB_MAX_PROFILES], lat_b[GSB_MAX_PROFILES], lat_c[GSB_MAX_PROFILES];
@@ -110,6 +112,137 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
       }
     }
   }
+}
+
+// K1a for dense traces (>= kSearchDense requests per window on average): an interpolation
+// search that touches ~1 sector per 256 requests plus two 128-byte lines per window edge
+// (round 2: 13.3 MB of DRAM traffic at C4 from the sampled pass above, whose one sector per 32
+// requests the L2 fetches as whole lines, and 198 us when the arrivals are pinned host memory
+// read over PCIe as 32-byte requests).
+// bounds[k] = #{i : arrival[i] < T_k}, T_k = (w0 + k) * W, because win(a) < k <=> a < T_k for
+// integer a and W > 0 (the same values the sampled pass writes). Block j = requests
+// [jS, e_j], e_j = min((j + 1)S, n) - 1; it owns the edges k in (win(e_{j-1}), win(e_j)]
+// (win(e_{-1}) = -1), whose answers lie in [jS, e_j]: arrival[e_{j-1}] < T_k <= arrival[e_j].
+// One warp per block: the CTA's 8 warps share the 9 bracket samples (one load each), then each
+// warp probes 32 consecutive arrivals (two aligned 128-byte lines) around the interpolated
+// position until the probe holds the edge; each probe that misses shrinks the bracket past
+// it, so the loop terminates. All edges k..win(arrival[q]) share the answer q (empty windows)
+// and are written at once. The warp after the last block writes n for the tail edges.
+constexpr int kSearchS = 256;      // requests per block
+constexpr int kSearchWarps = 8;    // blocks per CTA
+constexpr int kSearchDense = 64;   // launch rule: n >= kSearchDense * (n_windows + 1)
+
+__global__ void __launch_bounds__(kSearchWarps * 32)
+k_window_bounds_search(const int64_t* __restrict__ arrival, int64_t n, int64_t window_ms,
+                       int64_t w0, int64_t n_windows, int64_t* __restrict__ bounds,
+                       unsigned* __restrict__ zero_words, int64_t n_zero) {
+  gsb::grid_dep_wait();
+  gsb::grid_dep_launch();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_zero;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    zero_words[i] = 0;
+  __shared__ int64_t s_a[kSearchWarps + 1];  // arrival[e_{j-1}] for the CTA's blocks and the last
+  const double rd = 1.0 / static_cast<double>(window_ms);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t m = (n + kSearchS - 1) / kSearchS;  // blocks; block m = the tail
+  const int64_t jb = static_cast<int64_t>(blockIdx.x) * kSearchWarps;
+  auto last_of = [&](int64_t j) -> int64_t { return min((j + 1) * kSearchS, n) - 1; };
+  if (threadIdx.x <= kSearchWarps) {
+    const int64_t j = jb + threadIdx.x - 1;  // the sample ending block j
+    s_a[threadIdx.x] = (j >= 0 && j < m) ? __ldg(arrival + last_of(j)) : 0;
+  }
+  __syncthreads();
+  const int64_t j = jb + wib;
+  if (j > m) return;  // warp-uniform
+  auto win = [&](int64_t a) -> int64_t { return div_floor(a, window_ms, rd) - w0; };
+  const int64_t w_lo = j == 0 ? -1 : win(s_a[wib]);
+  if (j == m) {  // tail: edges past the last request's window
+    for (int64_t k = max(w_lo + 1, int64_t{0}) + lane; k <= n_windows; k += 32) bounds[k] = n;
+    return;
+  }
+  const int64_t e = last_of(j), a_e = s_a[wib + 1];
+  const int64_t ke = min(win(a_e), n_windows);
+  int64_t lo = j * kSearchS - 1, a_lo = j == 0 ? 0 : s_a[wib];
+  for (int64_t k = max(w_lo + 1, int64_t{0}); k <= ke;) {
+    const int64_t T = (w0 + k) * window_ms;
+    int64_t hi = e, a_hi = a_e;  // answer in (lo, hi]
+    int64_t q, v;                // answer and arrival[q]
+    for (;;) {     // arrival[lo] < T <= arrival[hi] (lo may be -1)
+      if (hi - lo == 1) {
+        q = hi;
+        v = a_hi;
+        break;
+      }
+      int64_t g = lo + 1;
+      if (lo >= 0) {
+        const double frac = static_cast<double>(T - a_lo) / static_cast<double>(a_hi - a_lo);
+        g = lo + static_cast<int64_t>(ceil(frac * static_cast<double>(hi - lo)));
+        g = min(max(g, lo + 1), hi);
+      }
+      const int64_t p0 = max(min(g - 16, hi - 31), lo + 1) & ~int64_t{15};
+      const int64_t i = p0 + lane;
+      const int64_t x = i < n ? __ldg(arrival + i) : INT64_MAX;
+      const unsigned below = __ballot_sync(kFull, x < T);  // a prefix of the lanes (sorted)
+      const int c = __popc(below);
+      if (c == 0) {
+        hi = min(hi, p0);
+        a_hi = __shfl_sync(kFull, x, 0);
+      } else if (c == 32) {
+        lo = max(lo, p0 + 31);
+        a_lo = __shfl_sync(kFull, x, 31);
+      } else {
+        q = p0 + c;
+        v = __shfl_sync(kFull, x, c);
+        break;
+      }
+    }
+    const int64_t kend = min(win(v), ke);  // T_k' <= v for every k' in [k, kend]
+    for (int64_t k2 = k + lane; k2 <= kend; k2 += 32) bounds[k2] = q;
+    k = kend + 1;  // T_k > v: the next answer is past q
+    lo = q;
+    a_lo = v;
+  }
+}
+
+// Pinned host memory (cudaHostAlloc / cudaHostRegister), which the kernels read in place over
+// PCIe. (cudaPointerGetAttributes enqueues nothing, so it is legal inside a graph capture.)
+bool is_host_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// K1a launch: the interpolation search when the arrivals are pinned HOST memory read over PCIe
+// (dense traces whose thresholds (w0 + k) * W fit in int64): 3x fewer bytes than the sampled
+// pass, in 128-byte requests instead of 32-byte ones (C4 e2e: 0.51 -> 0.42 ms per step). From
+// device memory the sampled pass stays: two dependent DRAM round trips instead of the search's
+// two or three (6.7 vs 8.7 us at C4, graph-timed).
+void launch_window_bounds(const int64_t* d_arrival, int64_t n, int64_t window_ms, int64_t w0,
+                          int64_t n_windows, int64_t* d_bounds, unsigned* zero_words,
+                          int64_t n_zero, cudaStream_t s) {
+  const int64_t lim = INT64_MAX / window_ms - 1;
+  const bool fits = w0 > -lim && w0 < lim - n_windows - 1;
+  // GSB_BOUNDS=sampled / search forces one kernel (tests compare both with a host search)
+  const char* force = std::getenv("GSB_BOUNDS");
+  const bool host = !force && is_host_ptr(d_arrival);
+  const bool search = force && force[0] == 's' && force[1] == 'e'
+                          ? fits
+                          : (force && force[0] == 's'
+                                 ? false
+                                 : host && fits && n >= kSearchDense * (n_windows + 1));
+  if (search) {
+    const int64_t blocks = ((n + kSearchS - 1) / kSearchS + 1 + kSearchWarps - 1) / kSearchWarps;
+    k_window_bounds_search<<<static_cast<unsigned>(blocks), kSearchWarps * 32, 0, s>>>(
+        d_arrival, n, window_ms, w0, n_windows, d_bounds, zero_words, n_zero);
+    return;
+  }
+  const int64_t warps = n / (32 * kBoundsTile) + 1;
+  const int64_t blocks = (warps + 7) / 8;
+  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, s>>>(
+      d_arrival, n, window_ms, w0, n_windows, d_bounds, zero_words, n_zero);
 }
 
 // classify(), router.cpp:26-31: number of thresholds strictly below the prompt. The thresholds
@@ -232,7 +365,7 @@ __device__ __forceinline__ void route_bin_tile(
   if (tid == 0 && lo.list) epoch = __ldcg(&lo.hdr->epoch);
   __syncthreads();
   const int64_t b0 = s.bnd[0], bG = s.bnd[G];
-  const bool tma = (reinterpret_cast<uintptr_t>(prompt) & 15) == 0;
+  const bool tma = !rp.prompt_host && (reinterpret_cast<uintptr_t>(prompt) & 15) == 0;
   // fold role: lane (fg, fp) = (window, profile)
   const int fg = lane / P, fp = lane - (lane / P) * P;
   const bool folder = lane < G * P;
@@ -254,6 +387,7 @@ __device__ __forceinline__ void route_bin_tile(
       gsb::mbar_expect_tx(&s.bar, bytes);
       gsb::bulk_g2s(s.stage, prompt + a0, bytes, &s.bar);
     }
+#pragma unroll 8
     for (int64_t i = max(a1, c0) + tid; i < c1; i += NW * 32) s.stage[i - a0] = __ldg(prompt + i);
     for (int k = tid; k < NW * K; k += NW * 32) (&s.hist[0][0])[k] = 0;
     if (tid <= G)
@@ -805,11 +939,8 @@ int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
   if (!ctx) return GSB_INVALID_ARGUMENT;
   int rc = check_route_cfg(ctx, cfg);
   if (rc) return rc;
-  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
-  const int64_t blocks = (warps + 7) / 8;
-  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0,
-                    gsb_pick_stream(ctx, stream)>>>(d_arrival, n_req, cfg->window_ms, cfg->w0,
-                                                    cfg->n_windows, d_bounds, nullptr, 0);
+  launch_window_bounds(d_arrival, n_req, cfg->window_ms, cfg->w0, cfg->n_windows, d_bounds,
+                       nullptr, 0, gsb_pick_stream(ctx, stream));
   return gsb_check_launch(ctx, "window_bounds");
 }
 
@@ -845,6 +976,7 @@ int gsb_route_bin_list(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,
                  reinterpret_cast<unsigned long long*>(sy + 256), nullptr, nullptr};
   }
   RouteParams rp = make_route_params(ctx, cfg);
+  rp.prompt_host = is_host_ptr(d_prompt) ? 1 : 0;
   rp.want_deadline = d_min_deadline != nullptr;
   const int P = ctx->n_profiles;
   cudaStream_t s = gsb_pick_stream(ctx, stream);
@@ -917,12 +1049,11 @@ int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
   PassHdr* ph = reinterpret_cast<PassHdr*>(sy + 256);
   unsigned* ready = reinterpret_cast<unsigned*>(sy + o_rd);
   // K1a (window bounds), which also zeroes the pass header and the readiness counters
-  const int64_t warps = n_req / (32 * kBoundsTile) + 1;
-  const int64_t blocks = (warps + 7) / 8;
-  k_window_bounds<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, 0, s>>>(
-      d_arrival, n_req, rcfg->window_ms, rcfg->w0, rcfg->n_windows, d_bounds,
-      reinterpret_cast<unsigned*>(ph), static_cast<int64_t>((o_st - 256) / sizeof(unsigned)));
+  launch_window_bounds(d_arrival, n_req, rcfg->window_ms, rcfg->w0, rcfg->n_windows, d_bounds,
+                       reinterpret_cast<unsigned*>(ph),
+                       static_cast<int64_t>((o_st - 256) / sizeof(unsigned)), s);
   RouteParams rp = make_route_params(ctx, rcfg);
+  rp.prompt_host = is_host_ptr(d_prompt) ? 1 : 0;
   rp.want_deadline = dl ? 1 : 0;
   const ListOut lo{list->d_cells, list->d_n, list->d_t_ref, dl ? list->d_min_deadline : nullptr,
                    list->capacity, reinterpret_cast<gsb::CompactHdr*>(sy),
