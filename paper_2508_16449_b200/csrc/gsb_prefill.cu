@@ -371,6 +371,8 @@ __device__ __forceinline__ void route_bin_tile(
   const bool folder = lane < G * P;
   const double la = rp.lat_a[fp], lb = rp.lat_b[fp], lc = rp.lat_c[fp];
   constexpr int CPW = (C + NW - 1) / NW;  // classes per warp in the fold: c = wib + k * NW
+  // (a class -> warp map rotated by tile, to spread a skewed mix's populated classes over the
+  // SM sub-partitions, measured 4 us slower at C4: 33.3 vs 29.3 us)
   double acc[CPW];
 #pragma unroll
   for (int k = 0; k < CPW; ++k) acc[k] = 0.0;
