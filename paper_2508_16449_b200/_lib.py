@@ -146,7 +146,7 @@ EXPORTS = (
     "gsb_t_ref_batches", "gsb_energy_closed_form_batches",
     "gsb_decode_pool", "gsb_decode_pool_tps_cap", "gsb_prefill_select_summary",
     "gsb_trace_parse", "gsb_trace_format", "gsb_route_bin_list", "gsb_prefill_select_list",
-    "gsb_prefill_pass", "gsb_select_batches_running", "gsb_freq_timeline_csv",
+    "gsb_prefill_pass", "gsb_prefill_pass_host", "gsb_select_batches_running", "gsb_freq_timeline_csv",
     "gsb_prefill_commands_csv", "gsb_format_g10", "gsb_mg1_side_output",
     "gsb_decision_log_csv", "gsb_format_g",
     "gsb_combine_summaries", "gsb_reduce_summaries", "gsb_tally_pool", "gsb_combine_tallies",
@@ -215,6 +215,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     L.gsb_mg1_side_output.argtypes = [_p, C.c_int, _i64, _d, _p, _p, _p, _p, _p, _p, _p, _p, _p]
     L.gsb_prefill_pass.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, _p, _p, _p, _p, _p,
                                    P(CCellList), P(CSelectCfg), _p, _p, _p, _p, _p]
+    L.gsb_prefill_pass_host.argtypes = [_p, P(CRouteCfg), _i64, _p, _p, P(CSelectCfg), C.c_int,
+                                        _p, _p, _p, _p]
     L.gsb_n_ticks.argtypes = [_d, _d]
     L.gsb_n_ticks.restype = _i64
     L.gsb_window_series.argtypes = [_p, P(CTelemetry), C.c_int, _d, _d, _d, _p, _p, _p, _p]

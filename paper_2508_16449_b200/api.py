@@ -448,6 +448,29 @@ class SelectResult:
 
 
 @dataclass
+class HostPassResult:
+    """prefill_pass_host output: host f_idx / energy [P, cells] and the per-chunk summary
+    records (pinned bytes [chunks, P*C*48]; argmin cells relative to the chunk)."""
+    f_idx: torch.Tensor
+    energy_j: torch.Tensor
+    chunk_summaries: Optional[torch.Tensor]
+    chunks: int
+    n_windows: int
+    n_classes: int
+
+    def chunk_records(self) -> np.ndarray:
+        """[chunks, P*C] gsb_class_summary records"""
+        from .distributed import SUMMARY_DTYPE
+        return self.chunk_summaries.numpy().view(SUMMARY_DTYPE).reshape(self.chunks, -1)
+
+    def summary(self) -> np.ndarray:
+        """the chunks' summaries combined in window order (gsb_combine_summaries)"""
+        from .distributed import combine_summaries_c
+        offs = [self.n_windows * k // self.chunks * self.n_classes for k in range(self.chunks)]
+        return combine_summaries_c(self.chunk_records(), offs)
+
+
+@dataclass
 class Telemetry:
     """Raw decode telemetry of S streams, CSR (include/gsb.h gsb_telemetry)."""
     ev_off: np.ndarray   # i64 [S+1]
@@ -672,6 +695,44 @@ class Engine:
             self.stream()))
         rr.profile_gen = self.profile_gen
         return rr, sel
+
+    def prefill_pass_host(self, arrival: torch.Tensor, prompt: torch.Tensor,
+                          routing: RoutingConfig, window_ms: int, w0: int, n_windows: int,
+                          mode: int = L.FIXED_WINDOW, fixed_window_ms: float = 0.0,
+                          qopt: QueueOptimizerConfig = QueueOptimizerConfig(),
+                          slo: SloConfig = SloConfig(), allowance_ms: float = 100.0,
+                          chunks: int = 4, out: Optional["HostPassResult"] = None,
+                          want_summary: bool = True) -> "HostPassResult":
+        """The whole pass from PINNED host arrays to host arrays (gsb_prefill_pass_host): the
+        windows split into `chunks` ranges whose prompt upload, kernels and read-back overlap
+        each other's (PCIe is full duplex). f_idx / energy equal prefill_pass's bit for bit;
+        the per-chunk summaries combine like ranks (HostPassResult.summary()). Stream-ordered:
+        synchronize the engine's stream before reading the result."""
+        if not (_pinned(arrival, torch.int64) and _pinned(prompt, torch.int32)):
+            raise ValueError("prefill_pass_host: arrival (int64) and prompt (int32) must be "
+                             "contiguous pinned host tensors")
+        Cn = routing.n_classes() if routing.enabled else 1
+        cells = n_windows * Cn
+        P = len(self.profiles)
+        chunks = max(1, min(int(chunks), 64, int(n_windows)))
+        if out is None:
+            # every host output pinned: a read-back into pageable memory would block the host
+            # until its chunk is done, serializing the pipeline
+            summ = None
+            if want_summary:
+                summ = torch.zeros((chunks, P * Cn * self.SUMMARY_DTYPE.itemsize),
+                                   dtype=torch.uint8).pin_memory()
+            out = HostPassResult(torch.empty((P, cells), dtype=torch.int16).pin_memory(),
+                                 torch.empty((P, cells), dtype=torch.float64).pin_memory(),
+                                 summ, chunks, n_windows, Cn)
+        rcfg = _route_cfg(routing, window_ms, w0, n_windows, slo, allowance_ms)
+        scfg = L.CSelectCfg(mode, Cn, fixed_window_ms, w0, window_ms, qopt.to_c())
+        self._check(self.lib.gsb_prefill_pass_host(
+            self.ctx, C.byref(rcfg), arrival.numel(), _ptr(arrival), _ptr(prompt), C.byref(scfg),
+            out.chunks, _ptr(out.f_idx), _ptr(out.energy_j),
+            _ptr(out.chunk_summaries) if out.chunk_summaries is not None else None,
+            self.stream()))
+        return out
 
     def mg1_side_output(self, rr: RouteResult, sel: "SelectResult", prompt):
         """M/G/1 side output beside the decisions (gsb_mg1_side_output): dict of [P, cells]

@@ -1123,4 +1123,162 @@ int gsb_fifo_order(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const 
   return gsb_check_launch(ctx, "fifo_order");
 }
 
+
+// The offline pass from HOST buffers, pipelined over window chunks (include/gsb.h). PCIe is
+// full duplex and the copy engines are separate from the SMs, so chunk k's prompt upload (up
+// stream), its K1b / K2 / finish / summary (the caller's stream) and its read-back (down
+// stream) overlap the neighbouring chunks' work. Every chunk's K1a' (latency-bound probes of
+// the pinned arrivals over PCIe) is issued up front on a fourth stream, beside the uploads,
+// so that no chunk's search sits on the compute stream (measured: 4 chunks with in-line
+// searches took 0.64 ms against 0.44 ms for one). Every chunk is an independent pass over
+// windows [a_k, a_k+1) and their requests [r_k, r_k+1) (found by a host lower_bound over the
+// pinned arrivals, the same values as the device bounds), with its own device buffers.
+int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
+                          const int64_t* h_arrival, const int32_t* h_prompt,
+                          const gsb_select_cfg* scfg, int n_chunks, int16_t* h_f_idx,
+                          double* h_energy, gsb_class_summary* h_summary, void* stream) {
+  if (!ctx || !scfg || !h_f_idx || !h_energy || n_req < 0 || (n_req > 0 && (!h_arrival || !h_prompt)))
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass_host: null or negative argument");
+  int rc = check_route_cfg(ctx, rcfg);
+  if (rc) return rc;
+  if (scfg->mode != GSB_FIXED_WINDOW && scfg->mode != GSB_DEADLINE_SLACK)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass_host: mode must be FIXED_WINDOW or DEADLINE_SLACK");
+  if (n_chunks < 1 || n_chunks > 64 || n_chunks > rcfg->n_windows)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT,
+                         "pass_host: n_chunks must be in [1, min(64, n_windows)]");
+  if (ctx->n_profiles < 1) return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass_host: no profiles set");
+  const int64_t nW = rcfg->n_windows, W = rcfg->window_ms;
+  const int C = rcfg->enabled ? rcfg->n_thresholds + 1 : 1, P = ctx->n_profiles;
+  const int64_t cells = nW * C;
+  const int K = n_chunks;
+  if (scfg->n_classes != C)
+    return gsb_set_error(ctx, GSB_INVALID_ARGUMENT, "pass_host: scfg->n_classes != classes of rcfg");
+  const bool dl = scfg->mode == GSB_DEADLINE_SLACK;
+  // chunk k: windows [a[k], a[k+1]), requests [r[k], r[k+1]) = those with arrival in
+  // [(w0 + a[k]) W, (w0 + a[k+1]) W): lower_bound over the sorted host arrivals
+  std::vector<int64_t> a(K + 1), r(K + 1);
+  for (int k = 0; k <= K; ++k) {
+    a[k] = nW * k / K;
+    const int64_t T = (rcfg->w0 + a[k]) * W;
+    r[k] = std::lower_bound(h_arrival, h_arrival + n_req, T) - h_arrival;
+  }
+  // device layout: the prompts, then per chunk its own buffers (256-byte aligned)
+  auto al = [](size_t b) { return (b + 255) & ~size_t{255}; };
+  std::vector<size_t> off(K + 1);
+  size_t bytes = al(sizeof(int32_t) * std::max<int64_t>(n_req, 1));
+  const size_t summ_b = sizeof(gsb_class_summary) * P * C;
+  for (int k = 0; k < K; ++k) {
+    off[k] = bytes;
+    const int64_t nk = r[k + 1] - r[k], wk = a[k + 1] - a[k], ck = wk * C;
+    bytes += al(8 * (wk + 1)) + al(std::max<int64_t>(nk, 1)) + al(4 * ck) + 2 * al(8 * P * ck) +
+             al(4 * ck) + al(8) + al(2 * P * ck) + al(8 * P * ck) + al(summ_b) +
+             (dl ? 2 * al(8 * ck) : 0);
+  }
+  cudaStream_t s = gsb_pick_stream(ctx, stream);
+  if (bytes > ctx->hostpass_bytes) {  // grow: nothing of an earlier call may still use the old one
+    if (ctx->d_hostpass) {
+      cudaStreamSynchronize(s);
+      if (ctx->up_stream) cudaStreamSynchronize(ctx->up_stream);
+      if (ctx->down_stream) cudaStreamSynchronize(ctx->down_stream);
+      cudaFree(ctx->d_hostpass);
+      ctx->d_hostpass = nullptr;
+      ctx->hostpass_bytes = 0;
+    }
+    if (cudaMalloc(&ctx->d_hostpass, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_hostpass = nullptr;
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: device allocation failed");
+    }
+    ctx->hostpass_bytes = bytes;
+  }
+  if ((!ctx->up_stream && cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking) != cudaSuccess) ||
+      (!ctx->down_stream && cudaStreamCreateWithFlags(&ctx->down_stream, cudaStreamNonBlocking) != cudaSuccess) ||
+      (!ctx->search_stream && cudaStreamCreateWithFlags(&ctx->search_stream, cudaStreamNonBlocking) != cudaSuccess))
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: stream creation failed");
+  const size_t n_ev = 2 + 3 * static_cast<size_t>(K);
+  while (ctx->hp_events.size() < n_ev) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event creation failed");
+    ctx->hp_events.push_back(e);
+  }
+  cudaEvent_t ev_start = ctx->hp_events[0], ev_end = ctx->hp_events[1];
+  char* base = static_cast<char*>(ctx->d_hostpass);
+  int32_t* d_prompt = reinterpret_cast<int32_t*>(base);
+  // the copies start after everything queued before this call on the caller's stream (an
+  // earlier call's kernels may still read the same device buffers)
+  if (cudaEventRecord(ev_start, s) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx->up_stream, ev_start, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx->down_stream, ev_start, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx->search_stream, ev_start, 0) != cudaSuccess)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event ordering failed");
+  // chunk k's bounds live at the start of its region (see take() below)
+  for (int k = 0; k < K; ++k) {
+    const int64_t nk = r[k + 1] - r[k];
+    gsb_route_cfg cfg_k = *rcfg;
+    cfg_k.w0 = rcfg->w0 + a[k];
+    cfg_k.n_windows = a[k + 1] - a[k];
+    rc = gsb_window_bounds(ctx, &cfg_k, nk, h_arrival + r[k],
+                           reinterpret_cast<int64_t*>(base + off[k]), ctx->search_stream);
+    if (rc) return rc;
+    if (cudaEventRecord(ctx->hp_events[2 + 2 * K + k], ctx->search_stream) != cudaSuccess)
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
+  }
+  for (int k = 0; k < K; ++k) {
+    const int64_t nk = r[k + 1] - r[k], wk = a[k + 1] - a[k], ck = wk * C;
+    cudaEvent_t ev_up = ctx->hp_events[2 + 2 * k], ev_done = ctx->hp_events[3 + 2 * k];
+    if (nk > 0 && cudaMemcpyAsync(d_prompt + r[k], h_prompt + r[k], sizeof(int32_t) * nk,
+                                  cudaMemcpyHostToDevice, ctx->up_stream) != cudaSuccess)
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: prompt upload failed");
+    if (cudaEventRecord(ev_up, ctx->up_stream) != cudaSuccess)
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
+    char* q = base + off[k];
+    auto take = [&](size_t b) { char* p0 = q; q += al(b); return p0; };
+    int64_t* d_bounds = reinterpret_cast<int64_t*>(take(8 * (wk + 1)));
+    uint8_t* d_class = reinterpret_cast<uint8_t*>(take(std::max<int64_t>(nk, 1)));
+    uint32_t* d_count = reinterpret_cast<uint32_t*>(take(4 * ck));
+    double* d_t_ref = reinterpret_cast<double*>(take(8 * P * ck));
+    double* d_t_list = reinterpret_cast<double*>(take(8 * P * ck));
+    uint32_t* d_list = reinterpret_cast<uint32_t*>(take(4 * ck));
+    int64_t* d_nl = reinterpret_cast<int64_t*>(take(8));
+    int16_t* d_fi = reinterpret_cast<int16_t*>(take(2 * P * ck));
+    double* d_en = reinterpret_cast<double*>(take(8 * P * ck));
+    gsb_class_summary* d_sm = reinterpret_cast<gsb_class_summary*>(take(summ_b));
+    double* d_mdl = dl ? reinterpret_cast<double*>(take(8 * ck)) : nullptr;
+    double* d_mdl_list = dl ? reinterpret_cast<double*>(take(8 * ck)) : nullptr;
+    gsb_route_cfg cfg_k = *rcfg;
+    cfg_k.w0 = rcfg->w0 + a[k];
+    cfg_k.n_windows = wk;
+    gsb_select_cfg sc_k = *scfg;
+    sc_k.w0 = scfg->w0 + a[k];
+    const gsb_cell_list list{d_list, d_nl, d_t_list, d_mdl_list, ck};
+    if (cudaStreamWaitEvent(s, ctx->hp_events[2 + 2 * K + k], 0) != cudaSuccess ||
+        cudaStreamWaitEvent(s, ev_up, 0) != cudaSuccess)
+      rc = gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event wait failed");
+    if (!rc)
+      rc = gsb_route_bin_list(ctx, &cfg_k, nk, h_arrival + r[k], d_prompt + r[k], d_bounds,
+                              d_class, d_count, d_t_ref, d_mdl, &list, s);
+    if (!rc)
+      rc = gsb_prefill_select_list(ctx, &sc_k, ck, d_t_ref, d_count, &list, d_mdl, nullptr, d_fi,
+                                   d_en, h_summary ? d_sm : nullptr, s);
+    if (rc) return rc;
+    // the read-back of chunk k (its P rows into the [P][cells] host arrays) runs beside the
+    // next chunk's upload and kernels
+    if (cudaEventRecord(ev_done, s) != cudaSuccess ||
+        cudaStreamWaitEvent(ctx->down_stream, ev_done, 0) != cudaSuccess ||
+        cudaMemcpy2DAsync(h_f_idx + a[k] * C, sizeof(int16_t) * cells, d_fi, sizeof(int16_t) * ck,
+                          sizeof(int16_t) * ck, P, cudaMemcpyDeviceToHost, ctx->down_stream) != cudaSuccess ||
+        cudaMemcpy2DAsync(h_energy + a[k] * C, sizeof(double) * cells, d_en, sizeof(double) * ck,
+                          sizeof(double) * ck, P, cudaMemcpyDeviceToHost, ctx->down_stream) != cudaSuccess ||
+        (h_summary && cudaMemcpyAsync(h_summary + static_cast<size_t>(k) * P * C, d_sm, summ_b,
+                                      cudaMemcpyDeviceToHost, ctx->down_stream) != cudaSuccess))
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: read-back failed");
+  }
+  // the caller's stream covers the read-backs (the host outputs are valid after it syncs)
+  if (cudaEventRecord(ev_end, ctx->down_stream) != cudaSuccess ||
+      cudaStreamWaitEvent(s, ev_end, 0) != cudaSuccess)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: final join failed");
+  return GSB_OK;
+}
+
 }  // extern "C"

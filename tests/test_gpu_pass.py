@@ -103,3 +103,51 @@ def test_pass_c4_matches_reference_and_replays_in_a_graph(gsb, ref):
         assert torch.equal(sel.f_idx, f0)
         assert torch.equal(sel.energy_j.view(torch.int64), e0.view(torch.int64))
         assert torch.equal(summ, s0)
+
+
+def _cmp_host_pass(gsb, a, p, routing, wms, w0, nW, mode, chunks, **kw):
+    """prefill_pass_host (pinned host in, host out, chunked pipeline) against the device pass:
+    f_idx / energy bit for bit; the combined chunk summaries: counts and argmin exact, the
+    energy sum (folded chunk by chunk instead of one tree) to 1e-12."""
+    from paper_2508_16449_b200 import api
+    C = routing.n_classes() if routing.enabled else 1
+    da, dp = torch.as_tensor(a, device="cuda"), torch.as_tensor(p, device="cuda")
+    s1 = gsb.summary_buffer(C)
+    _, sel = gsb.prefill_pass(da, dp, routing, wms, w0, nW, mode, summary_out=s1, **kw)
+    ha, hp = torch.as_tensor(a).pin_memory(), torch.as_tensor(p).pin_memory()
+    res = gsb.prefill_pass_host(ha, hp, routing, wms, w0, nW, mode, chunks=chunks, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(sel.f_idx.cpu(), res.f_idx)
+    assert torch.equal(sel.energy_j.cpu().view(torch.int64), res.energy_j.view(torch.int64))
+    want = np.frombuffer(s1.cpu().numpy().tobytes(), gsb.SUMMARY_DTYPE)
+    got = res.summary().reshape(-1)
+    for f in ("n_cmd", "n_infeasible", "n_empty", "argmin_cell"):
+        assert np.array_equal(want[f], got[f]), f
+    assert np.array_equal(u64(want["min_energy_j"]), u64(got["min_energy_j"]))
+    np.testing.assert_allclose(got["sum_energy_j"], want["sum_energy_j"], rtol=1e-12, atol=0)
+    return res
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 4, 7])
+def test_host_pass_equals_device_pass(gsb, chunks):
+    from paper_2508_16449_b200 import api, workloads as wl
+    gsb.set_profiles(wl.synth_profiles(4))
+    a, p, _ = wl.poisson_trace(5.0, 1000 * 60_000, "alibaba_chat", seed=21)
+    routing = api.RoutingConfig(True, wl.THRESHOLDS[8], list(range(8)))
+    for _ in range(2):  # repeated calls reuse the context's buffers, streams and events
+        _cmp_host_pass(gsb, a, p, routing, 60_000, 0, 1000, api.L.FIXED_WINDOW, chunks,
+                       fixed_window_ms=0.95 * 60_000)
+
+
+def test_host_pass_deadline_offset_windows_and_sparse(gsb):
+    from paper_2508_16449_b200 import api, workloads as wl
+    gsb.set_profiles(wl.synth_profiles(3))
+    a, p, _ = wl.poisson_trace(5.0, 700 * 60_000, "alibaba_chat", seed=22)
+    routing = api.RoutingConfig(True, wl.THRESHOLDS[5], list(range(5)))
+    # requests before window 0 (w0 = 100) and after the last window (n_windows = 450)
+    _cmp_host_pass(gsb, a, p, routing, 60_000, 100, 450, api.L.DEADLINE_SLACK, 4,
+                   qopt=api.QueueOptimizerConfig())
+    # sparse (most windows empty; the sampled K1a path), chunks with no requests
+    b, q, _ = wl.poisson_trace(0.02, 3000 * 60_000, "alibaba_chat", seed=23)
+    _cmp_host_pass(gsb, b, q, routing, 60_000, 0, 3000, api.L.FIXED_WINDOW, 16,
+                   fixed_window_ms=0.95 * 60_000)

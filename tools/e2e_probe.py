@@ -4,6 +4,7 @@ flushed before each.  python tools/e2e_probe.py  (one GPU)"""
 import os
 import statistics
 import sys
+import time
 
 import torch
 
@@ -198,6 +199,29 @@ def main():
         t = statistics.median(res[name])
         print(f"{name:32s} {t:9.1f} us  (minus flush-only graph: {t - base:8.1f})  "
               f"[{min(res[name]):.1f} .. {max(res[name]):.1f}]", flush=True)
+    # the pipelined host-buffer pass (eager: its chunk split reads the arrivals on the host)
+    for chunks in (1, 2, 4, 8, 16):
+        res = eng.prefill_pass_host(h_arr, h_prm, routing, wms, 0, nW, api.L.FIXED_WINDOW,
+                                    fixed_window_ms=D, chunks=chunks)
+        torch.cuda.synchronize()
+        ts, hs = [], []
+        for i in range(23):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            h0 = time.perf_counter()
+            eng.prefill_pass_host(h_arr, h_prm, routing, wms, 0, nW, api.L.FIXED_WINDOW,
+                                  fixed_window_ms=D, chunks=chunks, out=res)
+            h1 = time.perf_counter()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+                hs.append((h1 - h0) * 1e6)
+        ok = torch.equal(res.f_idx, sel.f_idx.cpu())
+        print(f"prefill_pass_host chunks={chunks:2d}     {statistics.median(ts):9.1f} us  "
+              f"[{min(ts):.1f} .. {max(ts):.1f}]  host enqueue {statistics.median(hs):.1f} us  "
+              f"equal={ok}", flush=True)
     print("bytes: prompts", h_prm.numel() * 4, "arrivals", h_arr.numel() * 8,
           "d2h", h_fidx.numel() * 2 + h_en.numel() * 8)
 
