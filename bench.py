@@ -596,20 +596,23 @@ def run_gsb(args, rank, world, dist):
                    "l2": "flushed between timed steps (256 MB write, outside the events)",
                    "cuda_graphs": use_graph},
         "grid_value": world * evals / (ms_pre / 1e3),
-        "e2e": {"value": evaluated_all / (ms_e2e_graph / 1e3),
-                "unit": "window x class x clock evals/s",
-                "ms_per_step": ms_e2e_graph, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "Engine.route_bin / prefill_select from pinned host buffers in one CUDA "
-                        "graph: the prompt upload beside K1a' (which reads the pinned arrivals "
-                        "in place; h2d counts the sectors / lines it reads), then K1b, K2, the "
-                        "finish and summary, and the read-back of every cell's clock and energy",
-                "pipelined": {"ms_per_step": ms_e2e, "value": evaluated_all / (ms_e2e / 1e3),
-                              "d2h_bytes_per_step": d2h_host, "chunks": e2e_chunks,
-                              "mismatches_vs_device_pass": e2e_host_mismatch,
-                              "path": "Engine.prefill_pass_host (gsb_prefill_pass_host): window "
-                                      "chunks whose prompt upload, kernels and read-back "
-                                      "overlap; launched eagerly (its chunk split reads the "
-                                      "arrivals on the host)"}},
+        "e2e": {"value": evaluated_all / (ms_e2e / 1e3), "unit": "window x class x clock evals/s",
+                "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h_host,
+                "path": f"Engine.prefill_pass_host (gsb_prefill_pass_host), the public call for a "
+                        f"host-resident trace: pinned arrivals / prompts in, host f_idx / energy "
+                        f"(+ per-chunk summaries) out; {e2e_chunks} window chunks of decreasing "
+                        f"size whose prompt upload, kernels and read-back overlap; K1a' reads the "
+                        f"pinned arrivals in place (h2d counts the sectors / lines it reads); "
+                        f"launched eagerly (its chunk split reads the arrivals on the host)",
+                "chunks": e2e_chunks,
+                "mismatches_vs_device_pass": e2e_host_mismatch,
+                "graph_step": {"ms_per_step": ms_e2e_graph,
+                               "value": evaluated_all / (ms_e2e_graph / 1e3),
+                               "d2h_bytes_per_step": d2h,
+                               "path": "Engine.route_bin / prefill_select in one CUDA graph: the "
+                                       "prompt upload beside K1a', then K1b, K2, the finish and "
+                                       "summary, and the read-back of every cell's clock and "
+                                       "energy"}},
         "roofline": {"bound": "fp64", "kernel": "k_prefill_select_list (K2)",
                      "achieved": k2_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                      "frac": k2_tflops / peak_tflops,

@@ -329,18 +329,19 @@ int gsb_prefill_pass(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
                      const gsb_select_cfg* scfg, double* d_window, int16_t* d_f_idx,
                      double* d_energy, gsb_class_summary* d_summary, void* stream);
 
-/* The same pass from HOST buffers, pipelined: the windows are split into n_chunks consecutive
- * ranges (chunk k = windows [k*nW/n_chunks, (k+1)*nW/n_chunks) and their requests, found by a
- * host lower_bound over h_arrival), and per chunk the prompt upload (a copy engine, its own
- * stream), K1a' reading the PINNED h_arrival in place, K1b, K2 with the finish and the summary
- * (on `stream`) and the read-back of the chunk's rows of h_f_idx / h_energy (another copy
- * engine) overlap the neighbouring chunks' work. h_arrival and h_prompt must be pinned (cudaHostAlloc
+/* The same pass from HOST buffers, pipelined: the windows are split into K = n_chunks
+ * consecutive ranges of decreasing size (chunk k = windows [a_k, a_k+1), a_k = nW * S_k /
+ * (K (K+1) / 2) with S_k = K + (K-1) + ... + (K-k+1), integer division), their requests found
+ * by a host lower_bound over h_arrival. K1a' reads the PINNED h_arrival in place once; per
+ * chunk the prompt upload (a copy engine, its own stream), K1b, K2 with the finish and the
+ * summary (two alternating compute streams) and the read-back of the chunk's rows of h_f_idx /
+ * h_energy (another copy engine) overlap the neighbouring chunks' work. h_arrival and h_prompt must be pinned (cudaHostAlloc
  * / cudaHostRegister); h_f_idx [P][cells] and h_energy [P][cells] are host arrays (pinned for an
  * asynchronous read-back: a pageable one blocks the call until its chunk is done) receiving
  * exactly gsb_prefill_pass's d_f_idx / d_energy. h_summary (optional, pinned host
  * [n_chunks][P*C]) receives each chunk's gsb_class_summary records, argmin
  * cells relative to the chunk: combine them with gsb_combine_summaries and cell offsets
- * k*nW/n_chunks*C (as ranks). mode FIXED_WINDOW or DEADLINE_SLACK; 1 <= n_chunks <=
+ * a_k * C (as ranks). mode FIXED_WINDOW or DEADLINE_SLACK; 1 <= n_chunks <=
  * min(64, n_windows). Stream-ordered: the outputs are valid once `stream` has synchronized. The
  * chunk split reads h_arrival on the host at call time, so the call is not for graph capture. */
 int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,

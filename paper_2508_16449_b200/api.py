@@ -466,8 +466,19 @@ class HostPassResult:
     def summary(self) -> np.ndarray:
         """the chunks' summaries combined in window order (gsb_combine_summaries)"""
         from .distributed import combine_summaries_c
-        offs = [self.n_windows * k // self.chunks * self.n_classes for k in range(self.chunks)]
-        return combine_summaries_c(self.chunk_records(), offs)
+        return combine_summaries_c(self.chunk_records(),
+                                   [a * self.n_classes for a in self.chunk_windows()[:-1]])
+
+    def chunk_windows(self) -> list:
+        """chunk k = windows [a_k, a_k+1): decreasing sizes, weights K, K-1, ..., 1
+        (gsb_prefill_pass_host)"""
+        K = self.chunks
+        wsum, acc, out = K * (K + 1) // 2, 0, []
+        for k in range(K + 1):
+            out.append(self.n_windows * acc // wsum)
+            if k < K:
+                acc += K - k
+        return out
 
 
 @dataclass

@@ -211,11 +211,13 @@ void gsb_ctx_destroy(gsb_ctx* c) {
   if (c->up_stream) cudaStreamSynchronize(c->up_stream);
   if (c->down_stream) cudaStreamSynchronize(c->down_stream);
   if (c->search_stream) cudaStreamSynchronize(c->search_stream);
+  if (c->compute2) cudaStreamSynchronize(c->compute2);
   cudaFree(c->d_hostpass);
   for (cudaEvent_t e : c->hp_events) cudaEventDestroy(e);
   if (c->up_stream) cudaStreamDestroy(c->up_stream);
   if (c->down_stream) cudaStreamDestroy(c->down_stream);
   if (c->search_stream) cudaStreamDestroy(c->search_stream);
+  if (c->compute2) cudaStreamDestroy(c->compute2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -12,6 +12,8 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
+#include <string>
 
 #include "gsb_common.cuh"
 #include "gsb_scan.cuh"
@@ -1126,11 +1128,12 @@ int gsb_fifo_order(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req, const 
 
 // The offline pass from HOST buffers, pipelined over window chunks (include/gsb.h). PCIe is
 // full duplex and the copy engines are separate from the SMs, so chunk k's prompt upload (up
-// stream), its K1b / K2 / finish / summary (the caller's stream) and its read-back (down
-// stream) overlap the neighbouring chunks' work. Every chunk's K1a' (latency-bound probes of
-// the pinned arrivals over PCIe) is issued up front on a fourth stream, beside the uploads,
-// so that no chunk's search sits on the compute stream (measured: 4 chunks with in-line
-// searches took 0.64 ms against 0.44 ms for one). Every chunk is an independent pass over
+// stream), its K1b / K2 / finish / summary (a compute stream) and its read-back (down stream)
+// overlap the neighbouring chunks' work. K1a' (latency-bound probes of the pinned arrivals over
+// PCIe) runs once, up front, on a fourth stream beside the first uploads. A chunk's small K1b / K2 grids are
+// latency-bound and fill a fraction of the GPU, so consecutive chunks run on two alternating
+// compute streams, each chunk with its own look-back sync words and summary scratch (swapped
+// into the context while its kernels are enqueued; the context's own are untouched). Every chunk is an independent pass over
 // windows [a_k, a_k+1) and their requests [r_k, r_k+1) (found by a host lower_bound over the
 // pinned arrivals, the same values as the device bounds), with its own device buffers.
 int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req,
@@ -1157,23 +1160,48 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
   // chunk k: windows [a[k], a[k+1]), requests [r[k], r[k+1]) = those with arrival in
   // [(w0 + a[k]) W, (w0 + a[k+1]) W): lower_bound over the sorted host arrivals
   std::vector<int64_t> a(K + 1), r(K + 1);
+  // decreasing chunk sizes (weights K, K-1, ..., 1): the last chunk's kernels and read-back,
+  // which nothing overlaps, are the smallest
+  const int64_t wsum = static_cast<int64_t>(K) * (K + 1) / 2;
+  int64_t acc = 0;
   for (int k = 0; k <= K; ++k) {
-    a[k] = nW * k / K;
+    a[k] = nW * acc / wsum;
+    if (k < K) acc += K - k;
     const int64_t T = (rcfg->w0 + a[k]) * W;
     r[k] = std::lower_bound(h_arrival, h_arrival + n_req, T) - h_arrival;
   }
-  // device layout: the prompts, then per chunk its own buffers (256-byte aligned)
+  // device layout: the per-chunk sync words (zeroed once, at allocation), the prompts, then
+  // per chunk its own buffers (256-byte aligned)
   auto al = [](size_t b) { return (b + 255) & ~size_t{255}; };
-  std::vector<size_t> off(K + 1);
-  size_t bytes = al(sizeof(int32_t) * std::max<int64_t>(n_req, 1));
+  std::vector<size_t> off(K + 1), sync_off(K), scr_off(K);
+  std::vector<size_t> sync_b(K), scr_b(K);
+  size_t bytes = 0;
+  for (int k = 0; k < K; ++k) {
+    const int64_t wk = a[k + 1] - a[k];
+    sync_b[k] = al(256 + sizeof(unsigned long long) * static_cast<size_t>(wk / 8 + 2));
+    sync_off[k] = bytes;
+    bytes += sync_b[k];
+  }
+  const size_t sync_total = bytes;
+  bytes += al(sizeof(int32_t) * std::max<int64_t>(n_req, 1));
+  const size_t bounds_off = bytes;
+  bytes += al(sizeof(int64_t) * (nW + 1));
+  const size_t class_off = bytes;
+  bytes += al(std::max<int64_t>(n_req, 1));
   const size_t summ_b = sizeof(gsb_class_summary) * P * C;
   for (int k = 0; k < K; ++k) {
     off[k] = bytes;
     const int64_t nk = r[k + 1] - r[k], wk = a[k + 1] - a[k], ck = wk * C;
-    bytes += al(8 * (wk + 1)) + al(std::max<int64_t>(nk, 1)) + al(4 * ck) + 2 * al(8 * P * ck) +
-             al(4 * ck) + al(8) + al(2 * P * ck) + al(8 * P * ck) + al(summ_b) +
-             (dl ? 2 * al(8 * ck) : 0);
+    (void)nk;
+    bytes += al(4 * ck) + 2 * al(8 * P * ck) + al(4 * ck) + al(8) + al(2 * P * ck) +
+             al(8 * P * ck) + al(summ_b) + (dl ? 2 * al(8 * ck) : 0);
+    scr_b[k] = al(gsb_finish_scratch_bytes(P, C, std::max<int64_t>(ck, 1)));
+    scr_off[k] = bytes;
+    bytes += scr_b[k];
   }
+  // the sync words' layout depends on the chunk split: a call with another split re-zeroes
+  const bool new_split = ctx->hostpass_bytes < bytes || ctx->hp_sync_total != sync_total ||
+                         ctx->hp_chunks != K;
   cudaStream_t s = gsb_pick_stream(ctx, stream);
   if (bytes > ctx->hostpass_bytes) {  // grow: nothing of an earlier call may still use the old one
     if (ctx->d_hostpass) {
@@ -1191,11 +1219,18 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
     }
     ctx->hostpass_bytes = bytes;
   }
+  if (new_split) {  // zero state for every chunk's look-back words (then stream-ordered reuse)
+    if (cudaMemsetAsync(ctx->d_hostpass, 0, sync_total, s) != cudaSuccess)
+      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: sync-word reset failed");
+    ctx->hp_sync_total = sync_total;
+    ctx->hp_chunks = K;
+  }
   if ((!ctx->up_stream && cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking) != cudaSuccess) ||
       (!ctx->down_stream && cudaStreamCreateWithFlags(&ctx->down_stream, cudaStreamNonBlocking) != cudaSuccess) ||
-      (!ctx->search_stream && cudaStreamCreateWithFlags(&ctx->search_stream, cudaStreamNonBlocking) != cudaSuccess))
+      (!ctx->search_stream && cudaStreamCreateWithFlags(&ctx->search_stream, cudaStreamNonBlocking) != cudaSuccess) ||
+      (!ctx->compute2 && cudaStreamCreateWithFlags(&ctx->compute2, cudaStreamNonBlocking) != cudaSuccess))
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: stream creation failed");
-  const size_t n_ev = 2 + 3 * static_cast<size_t>(K);
+  const size_t n_ev = 3 + 2 * static_cast<size_t>(K);
   while (ctx->hp_events.size() < n_ev) {
     cudaEvent_t e;
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
@@ -1204,26 +1239,37 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
   }
   cudaEvent_t ev_start = ctx->hp_events[0], ev_end = ctx->hp_events[1];
   char* base = static_cast<char*>(ctx->d_hostpass);
-  int32_t* d_prompt = reinterpret_cast<int32_t*>(base);
+  int32_t* d_prompt = reinterpret_cast<int32_t*>(base + sync_total);
   // the copies start after everything queued before this call on the caller's stream (an
   // earlier call's kernels may still read the same device buffers)
   if (cudaEventRecord(ev_start, s) != cudaSuccess ||
       cudaStreamWaitEvent(ctx->up_stream, ev_start, 0) != cudaSuccess ||
       cudaStreamWaitEvent(ctx->down_stream, ev_start, 0) != cudaSuccess ||
-      cudaStreamWaitEvent(ctx->search_stream, ev_start, 0) != cudaSuccess)
+      cudaStreamWaitEvent(ctx->search_stream, ev_start, 0) != cudaSuccess ||
+      cudaStreamWaitEvent(ctx->compute2, ev_start, 0) != cudaSuccess)
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event ordering failed");
-  // chunk k's bounds live at the start of its region (see take() below)
-  for (int k = 0; k < K; ++k) {
-    const int64_t nk = r[k + 1] - r[k];
-    gsb_route_cfg cfg_k = *rcfg;
-    cfg_k.w0 = rcfg->w0 + a[k];
-    cfg_k.n_windows = a[k + 1] - a[k];
-    rc = gsb_window_bounds(ctx, &cfg_k, nk, h_arrival + r[k],
-                           reinterpret_cast<int64_t*>(base + off[k]), ctx->search_stream);
-    if (rc) return rc;
-    if (cudaEventRecord(ctx->hp_events[2 + 2 * K + k], ctx->search_stream) != cudaSuccess)
-      return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
-  }
+  // diagnostics (GSB_HP_TRACE=1): timing events per stage, printed after a synchronize
+  const bool trace = std::getenv("GSB_HP_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tev;
+  auto mark = [&](const std::string& name, cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.emplace_back(name, e);
+  };
+  mark("start", s);
+  // K1a' once over the whole window range (the chunks use slices of one bounds array): a
+  // search per chunk would keep its PCIe-latency-bound CTAs resident across the whole upload,
+  // and K2's one-wave grid of a chunk cannot become resident beside them
+  int64_t* d_bounds_all = reinterpret_cast<int64_t*>(base + bounds_off);
+  uint8_t* d_class_all = reinterpret_cast<uint8_t*>(base + class_off);
+  rc = gsb_window_bounds(ctx, rcfg, n_req, h_arrival, d_bounds_all, ctx->search_stream);
+  if (rc) return rc;
+  cudaEvent_t ev_search = ctx->hp_events[2 + 2 * K];
+  if (cudaEventRecord(ev_search, ctx->search_stream) != cudaSuccess)
+    return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
+  mark("search", ctx->search_stream);
   for (int k = 0; k < K; ++k) {
     const int64_t nk = r[k + 1] - r[k], wk = a[k + 1] - a[k], ck = wk * C;
     cudaEvent_t ev_up = ctx->hp_events[2 + 2 * k], ev_done = ctx->hp_events[3 + 2 * k];
@@ -1232,10 +1278,9 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
       return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: prompt upload failed");
     if (cudaEventRecord(ev_up, ctx->up_stream) != cudaSuccess)
       return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
+    mark("upload" + std::to_string(k), ctx->up_stream);
     char* q = base + off[k];
     auto take = [&](size_t b) { char* p0 = q; q += al(b); return p0; };
-    int64_t* d_bounds = reinterpret_cast<int64_t*>(take(8 * (wk + 1)));
-    uint8_t* d_class = reinterpret_cast<uint8_t*>(take(std::max<int64_t>(nk, 1)));
     uint32_t* d_count = reinterpret_cast<uint32_t*>(take(4 * ck));
     double* d_t_ref = reinterpret_cast<double*>(take(8 * P * ck));
     double* d_t_list = reinterpret_cast<double*>(take(8 * P * ck));
@@ -1252,19 +1297,47 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
     gsb_select_cfg sc_k = *scfg;
     sc_k.w0 = scfg->w0 + a[k];
     const gsb_cell_list list{d_list, d_nl, d_t_list, d_mdl_list, ck};
-    if (cudaStreamWaitEvent(s, ctx->hp_events[2 + 2 * K + k], 0) != cudaSuccess ||
-        cudaStreamWaitEvent(s, ev_up, 0) != cudaSuccess)
+    cudaStream_t cs = (k & 1) ? ctx->compute2 : s;
+    if (cudaStreamWaitEvent(cs, ev_search, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(cs, ev_up, 0) != cudaSuccess)
       rc = gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event wait failed");
+    mark("compute_begin" + std::to_string(k), cs);
+    // the chunk's own look-back words and summary scratch, in place of the context's
+    void* const sv_sync = ctx->d_sync;
+    void* const sv_scr = ctx->d_scratch;
+    const size_t sv_sync_b = ctx->sync_bytes, sv_scr_b = ctx->scratch_bytes;
+    ctx->d_sync = base + sync_off[k];
+    ctx->sync_bytes = sync_b[k];
+    ctx->d_scratch = base + scr_off[k];
+    ctx->scratch_bytes = scr_b[k];
     if (!rc)
-      rc = gsb_route_bin_list(ctx, &cfg_k, nk, h_arrival + r[k], d_prompt + r[k], d_bounds,
-                              d_class, d_count, d_t_ref, d_mdl, &list, s);
+      // absolute request indices: the full arrays and the chunk's slice of the bounds
+      rc = gsb_route_bin_list(ctx, &cfg_k, n_req, h_arrival, d_prompt, d_bounds_all + a[k],
+                              d_class_all, d_count, d_t_ref, d_mdl, &list, cs);
     if (!rc)
       rc = gsb_prefill_select_list(ctx, &sc_k, ck, d_t_ref, d_count, &list, d_mdl, nullptr, d_fi,
-                                   d_en, h_summary ? d_sm : nullptr, s);
+                                   d_en, h_summary ? d_sm : nullptr, cs);
+    const bool swapped_ok = ctx->d_sync == base + sync_off[k] && ctx->d_scratch == base + scr_off[k];
+    if (!swapped_ok) {  // a callee grew a buffer: keep the new one for gsb_ctx_destroy to free,
+                        // and drop the chunk regions it retired (they belong to d_hostpass)
+      auto& rs = ctx->retired_scratch;
+      rs.erase(std::remove_if(rs.begin(), rs.end(), [&](void* v) {
+                 return static_cast<char*>(v) >= base && static_cast<char*>(v) < base + bytes;
+               }), rs.end());
+      if (ctx->d_sync != base + sync_off[k]) rs.push_back(ctx->d_sync);
+      if (ctx->d_scratch != base + scr_off[k]) rs.push_back(ctx->d_scratch);
+    }
+    ctx->d_sync = sv_sync;
+    ctx->sync_bytes = sv_sync_b;
+    ctx->d_scratch = sv_scr;
+    ctx->scratch_bytes = sv_scr_b;
+    if (!rc && !swapped_ok)  // a callee outgrew the chunk's workspace (sizing bug): fail loudly
+      rc = gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: chunk workspace outgrown");
     if (rc) return rc;
     // the read-back of chunk k (its P rows into the [P][cells] host arrays) runs beside the
     // next chunk's upload and kernels
-    if (cudaEventRecord(ev_done, s) != cudaSuccess ||
+    mark("compute_end" + std::to_string(k), cs);
+    if (cudaEventRecord(ev_done, cs) != cudaSuccess ||
         cudaStreamWaitEvent(ctx->down_stream, ev_done, 0) != cudaSuccess ||
         cudaMemcpy2DAsync(h_f_idx + a[k] * C, sizeof(int16_t) * cells, d_fi, sizeof(int16_t) * ck,
                           sizeof(int16_t) * ck, P, cudaMemcpyDeviceToHost, ctx->down_stream) != cudaSuccess ||
@@ -1275,9 +1348,19 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
       return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: read-back failed");
   }
   // the caller's stream covers the read-backs (the host outputs are valid after it syncs)
+  mark("readback_end", ctx->down_stream);
   if (cudaEventRecord(ev_end, ctx->down_stream) != cudaSuccess ||
       cudaStreamWaitEvent(s, ev_end, 0) != cudaSuccess)
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: final join failed");
+  if (trace) {
+    cudaStreamSynchronize(s);
+    for (auto& [name, e] : tev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0].second, e);
+      std::fprintf(stderr, "gsb_hp %-16s %8.1f us\n", name.c_str(), ms * 1e3);
+    }
+    for (auto& te : tev) cudaEventDestroy(te.second);
+  }
   return GSB_OK;
 }
 

@@ -896,6 +896,10 @@ int resident_ctas(gsb_ctx* ctx, K kernel, int threads) {
 
 }  // namespace
 
+size_t gsb_finish_scratch_bytes(int P, int C, int64_t n_cells) {
+  return finish_scratch_bytes(P, C, n_cells);
+}
+
 // for the fused pass (gsb_prefill.cu): the empty cells' outputs and the summary
 int gsb_internal_finish(gsb_ctx* ctx, int P, int C, int64_t n_cells, const uint32_t* count,
                         int16_t* f_idx, double* energy, gsb_class_summary* out, cudaStream_t s) {
