@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4,
-                    help="window chunks of the pipelined host-buffer e2e pass")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="window chunks of the pipelined host-buffer e2e pass (0: 4 for >= 1e6 "
+                         "requests per rank, else 1)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: ONE global trace of the config's windows, sliced per "
                          "rank (distributed.window_shard / trace_slice), scenarios split too")
@@ -421,7 +422,8 @@ def run_gsb(args, rank, world, dist):
     # the headline e2e: Engine.prefill_pass_host (gsb_prefill_pass_host), the public call for a
     # host-resident trace. Pinned arrivals / prompts in, host f_idx / energy out, the windows
     # split into chunks whose prompt upload, kernels and read-back overlap (PCIe is full duplex)
-    e2e_chunks = args.e2e_chunks
+    # chunks: 4 for a large trace; a small one (C2) is latency-bound and takes one
+    e2e_chunks = args.e2e_chunks or (4 if len(arrival) >= 1_000_000 else 1)
     hres = eng.prefill_pass_host(h_arr, h_prm, routing, wms, w0, nW, api.L.FIXED_WINDOW,
                                  fixed_window_ms=D, chunks=e2e_chunks)
     torch.cuda.synchronize()
