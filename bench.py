@@ -424,12 +424,15 @@ def run_gsb(args, rank, world, dist):
     # split into chunks whose prompt upload, kernels and read-back overlap (PCIe is full duplex)
     # chunks: 4 for a large trace; a small one (C2) is latency-bound and takes one
     e2e_chunks = args.e2e_chunks or (4 if len(arrival) >= 1_000_000 else 1)
-    hres = eng.prefill_pass_host(h_arr, h_prm, routing, wms, w0, nW, api.L.FIXED_WINDOW,
-                                 fixed_window_ms=D, chunks=e2e_chunks)
-    torch.cuda.synchronize()
-    d2h_host = hres.f_idx.numel() * 2 + hres.energy_j.numel() * 8 + hres.chunk_summaries.numel()
+    # (set up when its leg runs, so the launch order before it, which the committed ncu
+    # captures select by count, is the same as without it)
+    hres = None
 
     def run_e2e_host(timed_steps, warm):
+        nonlocal hres
+        hres = eng.prefill_pass_host(h_arr, h_prm, routing, wms, w0, nW, api.L.FIXED_WINDOW,
+                                     fixed_window_ms=D, chunks=e2e_chunks)
+        torch.cuda.synchronize()
         ts = []
         for i in range(warm + timed_steps):
             flush.zero_()
@@ -494,6 +497,7 @@ def run_gsb(args, rank, world, dist):
     ms_dec = max_over_ranks(statistics.mean(dec_ms))
     ms_e2e_graph = max_over_ranks(statistics.mean(e2e_ms))
     ms_e2e = max_over_ranks(statistics.mean(e2e_host_ms))
+    d2h_host = hres.f_idx.numel() * 2 + hres.energy_j.numel() * 8 + hres.chunk_summaries.numel()
     e2e_host_mismatch = int((hres.f_idx != sel.f_idx.cpu()).sum().item()) + int(
         (hres.energy_j.view(torch.int64) != sel.energy_j.cpu().view(torch.int64)).sum().item())
     ms_pool = max_over_ranks(statistics.mean(pool_ms))

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <chrono>
 
 #include "gsb_common.cuh"
 #include "gsb_scan.cuh"
@@ -1259,6 +1260,13 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
     tev.emplace_back(name, e);
   };
   mark("start", s);
+  // host-side cost of each call group (diagnostics: the host issues ~35 us of calls per chunk)
+  using hclock = std::chrono::steady_clock;
+  std::vector<std::pair<std::string, double>> hts;
+  auto hmark = [&, t0 = hclock::now()](const std::string& name) {
+    if (trace)
+      hts.emplace_back(name, std::chrono::duration<double, std::micro>(hclock::now() - t0).count());
+  };
   // K1a' once over the whole window range (the chunks use slices of one bounds array): a
   // search per chunk would keep its PCIe-latency-bound CTAs resident across the whole upload,
   // and K2's one-wave grid of a chunk cannot become resident beside them
@@ -1270,6 +1278,7 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
   if (cudaEventRecord(ev_search, ctx->search_stream) != cudaSuccess)
     return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
   mark("search", ctx->search_stream);
+  hmark("search issued");
   for (int k = 0; k < K; ++k) {
     const int64_t nk = r[k + 1] - r[k], wk = a[k + 1] - a[k], ck = wk * C;
     cudaEvent_t ev_up = ctx->hp_events[2 + 2 * k], ev_done = ctx->hp_events[3 + 2 * k];
@@ -1279,6 +1288,7 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
     if (cudaEventRecord(ev_up, ctx->up_stream) != cudaSuccess)
       return gsb_set_error(ctx, GSB_CUDA_ERROR, "pass_host: event record failed");
     mark("upload" + std::to_string(k), ctx->up_stream);
+    hmark("upload" + std::to_string(k) + " issued");
     char* q = base + off[k];
     auto take = [&](size_t b) { char* p0 = q; q += al(b); return p0; };
     uint32_t* d_count = reinterpret_cast<uint32_t*>(take(4 * ck));
@@ -1314,9 +1324,11 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
       // absolute request indices: the full arrays and the chunk's slice of the bounds
       rc = gsb_route_bin_list(ctx, &cfg_k, n_req, h_arrival, d_prompt, d_bounds_all + a[k],
                               d_class_all, d_count, d_t_ref, d_mdl, &list, cs);
+    hmark("route" + std::to_string(k) + " issued");
     if (!rc)
       rc = gsb_prefill_select_list(ctx, &sc_k, ck, d_t_ref, d_count, &list, d_mdl, nullptr, d_fi,
                                    d_en, h_summary ? d_sm : nullptr, cs);
+    hmark("select" + std::to_string(k) + " issued");
     const bool swapped_ok = ctx->d_sync == base + sync_off[k] && ctx->d_scratch == base + scr_off[k];
     if (!swapped_ok) {  // a callee grew a buffer: keep the new one for gsb_ctx_destroy to free,
                         // and drop the chunk regions it retired (they belong to d_hostpass)
@@ -1360,6 +1372,7 @@ int gsb_prefill_pass_host(gsb_ctx* ctx, const gsb_route_cfg* rcfg, int64_t n_req
       std::fprintf(stderr, "gsb_hp %-16s %8.1f us\n", name.c_str(), ms * 1e3);
     }
     for (auto& te : tev) cudaEventDestroy(te.second);
+    for (auto& [name, us] : hts) std::fprintf(stderr, "gsb_hp host %-18s %8.1f us\n", name.c_str(), us);
   }
   return GSB_OK;
 }
