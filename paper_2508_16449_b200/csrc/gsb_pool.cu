@@ -720,7 +720,10 @@ __device__ void run_scenario(const PoolParams& P, const Smem& s, int32_t* pend, 
 }
 
 template <bool REQ_OUT>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) k_decode_pool(const __grid_constant__ PoolParams P) {
+#ifndef GSB_POOL_MINB
+#define GSB_POOL_MINB 5
+#endif
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, GSB_POOL_MINB) k_decode_pool(const __grid_constant__ PoolParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
