@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=0,
-                    help="window chunks of the pipelined host-buffer e2e pass (0: 4 for >= 1e6 "
+                    help="window chunks of the pipelined host-buffer e2e pass (0: 3 for >= 1e6 "
                          "requests per rank, else 1)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: ONE global trace of the config's windows, sliced per "
@@ -422,8 +422,9 @@ def run_gsb(args, rank, world, dist):
     # the headline e2e: Engine.prefill_pass_host (gsb_prefill_pass_host), the public call for a
     # host-resident trace. Pinned arrivals / prompts in, host f_idx / energy out, the windows
     # split into chunks whose prompt upload, kernels and read-back overlap (PCIe is full duplex)
-    # chunks: 4 for a large trace; a small one (C2) is latency-bound and takes one
-    e2e_chunks = args.e2e_chunks or (4 if len(arrival) >= 1_000_000 else 1)
+    # chunks: 3 for a large trace (2 / 3 / 4 measured 0.383 / 0.381 / 0.386 ms at C4); a small
+    # one (C2) is latency-bound and takes one
+    e2e_chunks = args.e2e_chunks or (3 if len(arrival) >= 1_000_000 else 1)
     # (set up when its leg runs, so the launch order before it, which the committed ncu
     # captures select by count, is the same as without it)
     hres = None
