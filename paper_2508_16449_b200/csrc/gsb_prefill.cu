@@ -131,7 +131,10 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
 // position until the probe holds the edge; each probe that misses shrinks the bracket past
 // it, so the loop terminates. All edges k..win(arrival[q]) share the answer q (empty windows)
 // and are written at once. The warp after the last block writes n for the tail edges.
-constexpr int kSearchS = 256;      // requests per block
+#ifndef GSB_SEARCH_S
+#define GSB_SEARCH_S 256
+#endif
+constexpr int kSearchS = GSB_SEARCH_S;  // requests per block
 constexpr int kSearchWarps = 8;    // blocks per CTA
 constexpr int kSearchDense = 64;   // launch rule: n >= kSearchDense * (n_windows + 1)
 

@@ -200,7 +200,7 @@ def main():
         print(f"{name:32s} {t:9.1f} us  (minus flush-only graph: {t - base:8.1f})  "
               f"[{min(res[name]):.1f} .. {max(res[name]):.1f}]", flush=True)
     # the pipelined host-buffer pass (eager: its chunk split reads the arrivals on the host)
-    for chunks in (1, 2, 4, 8, 16):
+    for chunks in (1, 2, 3, 4, 8, 16):
         res = eng.prefill_pass_host(h_arr, h_prm, routing, wms, 0, nW, api.L.FIXED_WINDOW,
                                     fixed_window_ms=D, chunks=chunks)
         torch.cuda.synchronize()
