@@ -199,3 +199,33 @@ def test_c_abi_reductions_equal_the_python_combine():
     assert D.tally_pool_c(sm, 17).tobytes() == D.tally_pool(sm, 17).tobytes()
     parts = np.array([D.tally_pool(sm[i::3], 100 * i) for i in range(3)], D.DECODE_TALLY_DTYPE)
     assert D.combine_tallies_c(parts).tobytes() == D.combine_tallies(parts).tobytes()
+
+
+def test_host_pass_chunk_split_and_summary_combine():
+    """gsb_prefill_pass_host's window chunks (decreasing sizes, weights K..1, gsb.h) cover every
+    window once, and its per-chunk summary records combine like ranks (argmin cells offset by the
+    chunk starts): the C combine equals the Python rank-order combine."""
+    import torch
+    from paper_2508_16449_b200 import api
+    from paper_2508_16449_b200.distributed import SUMMARY_DTYPE, combine_summaries
+    rng = np.random.default_rng(5)
+    for nW, K in [(10_000, 3), (7, 7), (1440, 4), (1_000_000, 16), (5, 1)]:
+        C, P = 8, 4
+        r = api.HostPassResult(None, None, None, K, nW, C)
+        a = r.chunk_windows()
+        assert a[0] == 0 and a[-1] == nW and len(a) == K + 1
+        sizes = np.diff(a)
+        assert (sizes >= 0).all() and sizes.sum() == nW
+        if nW >= 10 * K:
+            assert (np.diff(sizes) <= 1).all()  # non-increasing (up to rounding)
+        recs = np.zeros((K, P * C), SUMMARY_DTYPE)
+        recs["n_cmd"] = rng.integers(0, 50, recs.shape)
+        recs["n_infeasible"] = rng.integers(0, 5, recs.shape)
+        recs["n_empty"] = rng.integers(0, 50, recs.shape)
+        recs["sum_energy_j"] = rng.random(recs.shape) * 1e3
+        recs["min_energy_j"] = rng.random(recs.shape)
+        recs["argmin_cell"] = rng.integers(0, max(1, nW // K) * C, recs.shape)
+        r.chunk_summaries = torch.from_numpy(recs.view(np.uint8).reshape(K, -1).copy())
+        got = r.summary()
+        want = combine_summaries(recs.reshape(K, P, C), [x * C for x in a[:-1]]).reshape(-1)
+        assert got.tobytes() == want.tobytes()
