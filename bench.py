@@ -369,11 +369,11 @@ def run_gsb(args, rank, world, dist):
     # the prompts are copied (K1b stages every one); the arrivals stay in pinned host memory
     # and K1a reads them in place over PCIe. For a dense trace (>= 64 requests per window) it
     # is the interpolation search: one 32-byte sector per 256-request block plus one probe of
-    # two 128-byte lines per window edge (a probe that misses adds 256 bytes; not counted);
+    # one 64-byte probe per window edge (a probe that misses adds 64 bytes; not counted);
     # otherwise one sector per 32-request tile plus the 256 bytes of every tile holding an edge
     n_req_h = h_arr.numel()
     if n_req_h >= 64 * (nW + 1):
-        arr_bytes = 32 * ((n_req_h + 255) // 256) + 256 * (nW + 1)
+        arr_bytes = 32 * ((n_req_h + 255) // 256) + 64 * (nW + 1)
     else:
         n_tiles32 = (n_req_h + 31) // 32
         arr_bytes = 32 * n_tiles32 + 256 * min(nW + 1, n_tiles32)

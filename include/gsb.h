@@ -153,7 +153,8 @@ int gsb_classify(gsb_ctx* ctx, int n_thresholds, const int32_t* thresholds, int6
  * d_arrival_ms (here and in gsb_route_bin*) may be PINNED HOST memory (cudaHostAlloc /
  * cudaHostRegister): with unified addressing the kernels read it in place over PCIe. From pinned
  * host memory a dense trace (>= 64 requests per window) takes an interpolation search: one
- * arrival per 256 requests plus two 128-byte lines per window edge; otherwise the pass reads
+ * arrival per 256 requests plus a 64-byte probe per window edge (more where a probe misses);
+ * otherwise the pass reads
  * one 32-byte sector per 32 requests plus the 32-request tiles holding a window start. Either
  * way a host-resident trace needs no arrival upload (K1b reads arrivals only in deadline mode). */
 int gsb_window_bounds(gsb_ctx* ctx, const gsb_route_cfg* cfg, int64_t n_req,

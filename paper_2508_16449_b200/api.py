@@ -619,7 +619,7 @@ class Engine:
 
         A PINNED host int64 `arrival` tensor is read in place (zero copy): with unified
         addressing the kernels dereference pinned host memory directly, and K1a reads only one
-        arrival per 256 requests plus two 128-byte lines per window edge (dense traces; else one
+        arrival per 256 requests plus a 64-byte probe per window edge (dense traces; else one
         arrival per 32 requests plus the 32-request tiles that hold a window start; the deadline
         mode reads every arrival once). A pinned int32 `prompt` tensor is read in place by K1b
         (plain loads instead of its TMA stage)."""

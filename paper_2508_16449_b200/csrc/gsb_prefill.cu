@@ -118,7 +118,7 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
 }
 
 // K1a for dense traces (>= kSearchDense requests per window on average): an interpolation
-// search that touches ~1 sector per 256 requests plus two 128-byte lines per window edge
+// search that touches ~1 sector per 256 requests plus one 64-byte half line per probe
 // (round 2: 13.3 MB of DRAM traffic at C4 from the sampled pass above, whose one sector per 32
 // requests the L2 fetches as whole lines, and 198 us when the arrivals are pinned host memory
 // read over PCIe as 32-byte requests).
@@ -127,7 +127,7 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
 // [jS, e_j], e_j = min((j + 1)S, n) - 1; it owns the edges k in (win(e_{j-1}), win(e_j)]
 // (win(e_{-1}) = -1), whose answers lie in [jS, e_j]: arrival[e_{j-1}] < T_k <= arrival[e_j].
 // One warp per block: the CTA's 8 warps share the 9 bracket samples (one load each), then each
-// warp probes 32 consecutive arrivals (two aligned 128-byte lines) around the interpolated
+// warp probes kProbe consecutive arrivals (an aligned 64-byte half line) around the interpolated
 // position until the probe holds the edge; each probe that misses shrinks the bracket past
 // it, so the loop terminates. All edges k..win(arrival[q]) share the answer q (empty windows)
 // and are written at once. The warp after the last block writes n for the tail edges.
@@ -136,6 +136,15 @@ k_window_bounds(const int64_t* __restrict__ arrival, int64_t n, int64_t window_m
 #endif
 constexpr int kSearchS = GSB_SEARCH_S;  // requests per block
 constexpr int kSearchWarps = 8;    // blocks per CTA
+#ifndef GSB_SEARCH_PROBE
+#define GSB_SEARCH_PROBE 8
+#endif
+// arrivals per probe: 8 = an aligned 64-byte half line. Over PCIe at C4, K1a' and the
+// host-buffer pass measured 73-75 us / 0.364 ms (8), 75-77 us / 0.37 ms (16) and 88 us / 0.385 ms
+// (32): the misses' extra round trips cost less than the bytes saved on the shared H2D link
+constexpr int kProbe = GSB_SEARCH_PROBE;
+static_assert(kProbe == 8 || kProbe == 16 || kProbe == 32, "probe of 8, 16 or 32 arrivals");
+constexpr int64_t kProbeAlign = kProbe >= 16 ? 16 : kProbe;
 constexpr int kSearchDense = 64;   // launch rule: n >= kSearchDense * (n_windows + 1)
 
 __global__ void __launch_bounds__(kSearchWarps * 32)
@@ -185,17 +194,18 @@ k_window_bounds_search(const int64_t* __restrict__ arrival, int64_t n, int64_t w
         g = lo + static_cast<int64_t>(ceil(frac * static_cast<double>(hi - lo)));
         g = min(max(g, lo + 1), hi);
       }
-      const int64_t p0 = max(min(g - 16, hi - 31), lo + 1) & ~int64_t{15};
+      const int64_t p0 =
+          max(min(g - kProbe / 2, hi - (kProbe - 1)), lo + 1) & ~(kProbeAlign - 1);
       const int64_t i = p0 + lane;
-      const int64_t x = i < n ? __ldg(arrival + i) : INT64_MAX;
+      const int64_t x = (lane < kProbe && i < n) ? __ldg(arrival + i) : INT64_MAX;
       const unsigned below = __ballot_sync(kFull, x < T);  // a prefix of the lanes (sorted)
       const int c = __popc(below);
       if (c == 0) {
         hi = min(hi, p0);
         a_hi = __shfl_sync(kFull, x, 0);
-      } else if (c == 32) {
-        lo = max(lo, p0 + 31);
-        a_lo = __shfl_sync(kFull, x, 31);
+      } else if (c == kProbe) {
+        lo = max(lo, p0 + kProbe - 1);
+        a_lo = __shfl_sync(kFull, x, kProbe - 1);
       } else {
         q = p0 + c;
         v = __shfl_sync(kFull, x, c);
@@ -223,7 +233,7 @@ bool is_host_ptr(const void* p) {
 
 // K1a launch: the interpolation search when the arrivals are pinned HOST memory read over PCIe
 // (dense traces whose thresholds (w0 + k) * W fit in int64): 3x fewer bytes than the sampled
-// pass, in 128-byte requests instead of 32-byte ones (C4 e2e: 0.51 -> 0.42 ms per step). From
+// pass (C4 e2e: 0.51 -> 0.42 ms per step with two-line probes, then 0.41 with 64-byte ones). From
 // device memory the sampled pass stays: two dependent DRAM round trips instead of the search's
 // two or three (6.7 vs 8.7 us at C4, graph-timed).
 void launch_window_bounds(const int64_t* d_arrival, int64_t n, int64_t window_ms, int64_t w0,
