@@ -141,9 +141,10 @@ constexpr int kSearchWarps = 8;    // blocks per CTA
 #endif
 // arrivals per probe: 8 = an aligned 64-byte half line. Over PCIe at C4, K1a' and the
 // host-buffer pass measured 73-75 us / 0.364 ms (8), 75-77 us / 0.37 ms (16) and 88 us / 0.385 ms
-// (32): the misses' extra round trips cost less than the bytes saved on the shared H2D link
+// (32): the misses' extra round trips cost less than the bytes saved on the shared H2D link.
+// 4 (one sector) measured 82 us alone and the same e2e as 8.
 constexpr int kProbe = GSB_SEARCH_PROBE;
-static_assert(kProbe == 8 || kProbe == 16 || kProbe == 32, "probe of 8, 16 or 32 arrivals");
+static_assert(kProbe == 4 || kProbe == 8 || kProbe == 16 || kProbe == 32, "probe of 4-32 arrivals");
 constexpr int64_t kProbeAlign = kProbe >= 16 ? 16 : kProbe;
 constexpr int kSearchDense = 64;   // launch rule: n >= kSearchDense * (n_windows + 1)
 
